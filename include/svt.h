@@ -1,0 +1,319 @@
+/*
+ * svt.h — C-ABI of the B200-native tailored LM-head path (VocabTailor,
+ * arXiv 2508.15229). Implemented by paper_2508_15229_b200/lib/libsvt.so
+ * (hand-written sm_100a CUDA; no CPU fallback — every compute entry point
+ * fails with SVT_ERR_RUNTIME when no CUDA device is usable).
+ *
+ * The reference has no FFI: its boundary is the C++ API in
+ * /root/reference/proj/include/subvocab/{selector,head,token_set,error}.hpp.
+ * Each entry point below names the reference function it replaces. The C++
+ * drop-in (include/subvocab/ headers, libsubvocab_b200.so) is a thin layer over
+ * these calls; INTEGRATION.md shows the bindings a maintainer would add.
+ *
+ * Conventions
+ *  - Status codes mirror subvocab::Error::exit_code() (error.hpp:10-38):
+ *    0 ok, 1 runtime (CUDA/NCCL/internal), 2 ConfigError, 3 ParseError,
+ *    4 IntegrityError. svt_last_error() returns the message of the last
+ *    failing call on this thread (same wording as the reference's throws).
+ *  - `d_` pointers are device memory (caller-allocated), `h_` pointers are
+ *    host memory. Device entry points are stream-ordered and never
+ *    synchronise; data-dependent errors (an input id >= V) are written to
+ *    caller-provided device status words instead of being returned.
+ *  - Ids are uint32 (TokenId, token_set.hpp:12); sizes are size_t/int64.
+ *  - Arithmetic: logits are computed in the reference's exact order
+ *    (head.cpp:194-199: acc=+0.0f, ascending column, product rounded then
+ *    sum rounded), so logits, argmax ids and remapped ids are bit-identical
+ *    to the CPU reference for f32, f16 and bf16 weights.
+ */
+#ifndef SVT_H
+#define SVT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int svt_status;
+#define SVT_OK 0
+#define SVT_ERR_RUNTIME 1
+#define SVT_ERR_CONFIG 2
+#define SVT_ERR_PARSE 3
+#define SVT_ERR_INTEGRITY 4
+
+/* Storage element type of a head. The reference stores f32 and, for
+ * dtype_bytes==2, IEEE binary16 (head.cpp:39-82); bf16 is this build's
+ * addition (values widen exactly to f32 before the reference arithmetic). */
+typedef enum { SVT_F32 = 0, SVT_F16 = 1, SVT_BF16 = 2 } svt_dtype;
+
+typedef void* svt_stream; /* cudaStream_t; NULL = legacy default stream */
+
+#define SVT_ABI_VERSION 1
+#define SVT_GROUP_ROWS 32 /* rows per lane-interleaved row group */
+
+int svt_abi_version(void);
+const char* svt_last_error(void);
+/* Number of usable CUDA devices (0 when none; compute calls then fail). */
+int svt_device_count(void);
+size_t svt_dtype_size(svt_dtype dt);
+
+/* ------------------------------------------------------------------------
+ * HeadMatrix::random (head.cpp:89-107) regenerated on device.
+ * Element i of the row-major rows x dim matrix = splitmix64(seed+(i+1)*γ)
+ * mapped to r*2^-23-1; `round_through` SVT_F16 applies the reference's
+ * binary16 round trip (dtype_bytes==2, head.cpp:104), SVT_BF16 rounds to
+ * bf16 (RNE), SVT_F32 none. The result is stored as `store` (f32 values,
+ * f16 bits or bf16 bits). `first_elem` offsets the counter (row slices).
+ * ---------------------------------------------------------------------- */
+svt_status svt_head_random(void* d_out, svt_dtype store, svt_dtype round_through,
+                           uint64_t first_elem, uint64_t n_elems, uint64_t seed,
+                           svt_stream stream);
+
+/* f32 -> storage conversion (reference float_to_half for SVT_F16, RNE for
+ * SVT_BF16, copy for SVT_F32). */
+svt_status svt_convert_from_f32(const float* d_in, void* d_out, svt_dtype store, uint64_t n,
+                                svt_stream stream);
+/* storage -> f32 widening (exact). */
+svt_status svt_convert_to_f32(const void* d_in, svt_dtype store, float* d_out, uint64_t n,
+                              svt_stream stream);
+
+/* ------------------------------------------------------------------------
+ * (a) Hybrid static-dynamic vocabulary builder.
+ * Replaces: select(std::span<const TokenId>, const TokenSet&, size_t)
+ *           selector.cpp:16-43 (selector.hpp:28-31), batched over requests.
+ *
+ * d_static_words: TokenSet bitmap of T, ceil(V/64) u64 words (bit id%64 of
+ *   word id/64, token_set.hpp:17-64). static_universe must equal V
+ *   (selector.cpp:18-22 -> SVT_ERR_INTEGRITY, checked on the host).
+ * Request b's prompt is d_input_ids[d_input_offsets[b] .. d_input_offsets[b+1]).
+ * Request b's plan (strictly increasing active ids) is written to
+ *   d_active_ids[d_active_offsets[b] ..], capacity d_active_offsets[b+1]-
+ *   d_active_offsets[b] (must be >= |T| + prompt length).
+ * Per request: d_n_active[b] = |S|, d_n_dynamic[b] = |S \ T|, d_n_static[b] = |T|,
+ *   d_first_bad[b] = -1 on success, the position of the first input id >= V
+ *   (the reference throws IntegrityError naming it, selector.cpp:27-30),
+ *   or -2 when the capacity is too small. Any non-(-1) leaves n_active = 0.
+ * ---------------------------------------------------------------------- */
+svt_status svt_select_batched(const uint64_t* d_static_words, size_t static_universe,
+                              size_t full_vocab_size, const uint32_t* d_input_ids,
+                              const int64_t* d_input_offsets, int32_t batch,
+                              uint32_t* d_active_ids, const int64_t* d_active_offsets,
+                              int64_t* d_n_active, int64_t* d_n_static, int64_t* d_n_dynamic,
+                              int64_t* d_first_bad, svt_stream stream);
+
+/* TokenSet::from_ids (token_set.cpp:13-16) on device: OR the ids into
+ * d_words (ceil(universe/64) words, caller zeroes them). Ids >= universe set
+ * *d_bad = 1 (TokenSet::insert throws IntegrityError, token_set.cpp:24-27). */
+svt_status svt_bitset_insert(const uint32_t* d_ids, size_t n, size_t universe,
+                             uint64_t* d_words, int32_t* d_bad, svt_stream stream);
+
+/* union_plans (selector.cpp:58-77) of `n_plans` device plans into one
+ * strictly increasing id list. d_words is a zeroed scratch bitmap of
+ * ceil(full/64) words; *d_n_out receives |∪|. Ids >= full set *d_bad = 1.
+ * (The empty-batch ConfigError and the full/n_static mismatch checks are
+ * host-side metadata checks done by the caller, selector.cpp:59,65-67.) */
+svt_status svt_union_plans(const uint32_t* d_ids, const int64_t* d_offsets, int32_t n_plans,
+                           size_t full_vocab_size, uint64_t* d_words, uint32_t* d_out_ids,
+                           int64_t* d_n_out, int32_t* d_bad, svt_stream stream);
+
+/* Row-group layout of a micro-batch of plans: group g covers rows
+ * [32k, 32k+32) of one request. d_group_begin[b] = first group of request b
+ * (exclusive prefix sum of ceil(n_active/32)); d_group_begin[batch] = total.
+ * d_group_req[g] = owning request of group g, for g < total <= max_groups. */
+svt_status svt_plan_layout(const int64_t* d_n_active, int32_t batch, int64_t* d_group_begin,
+                           int32_t* d_group_req, int64_t max_groups, svt_stream stream);
+
+/* ------------------------------------------------------------------------
+ * (b) LM-head row gather.
+ * Replaces: gather(const HeadMatrix&, const SelectionPlan&) head.cpp:176-187.
+ * Row-major: d_out[k, :] = d_head[d_ids[k], :], bit copy. The reference
+ * bounds-checks only the last id (head.cpp:177-180); here every id is
+ * checked and *d_bad (optional) is set to 1 on any id >= rows.
+ * ---------------------------------------------------------------------- */
+svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                           const uint32_t* d_ids, size_t n, void* d_out, int32_t* d_bad,
+                           svt_stream stream);
+
+/* Gather into the lane-interleaved sub-head layout consumed by the decode
+ * kernel: for group g, 16-byte chunk c, lane l (row 32k+l of the request):
+ *   d_sub + ((g * nchunks + c) * 32 + l) * 16,  nchunks = ceil(dim*esize/16),
+ * rows past n_active and bytes past dim*esize are zero.
+ * d_sub must hold svt_subhead_bytes(dt, dim, groups) bytes. */
+size_t svt_subhead_bytes(svt_dtype dt, size_t dim, int64_t groups);
+svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                                  const uint32_t* d_active_ids, const int64_t* d_active_offsets,
+                                  const int64_t* d_n_active, const int64_t* d_group_begin,
+                                  const int32_t* d_group_req, int32_t batch, int64_t max_groups,
+                                  void* d_sub, int32_t* d_bad, svt_stream stream);
+
+/* ------------------------------------------------------------------------
+ * (c) Tailored logits contraction h·W_subᵀ in the reference order.
+ * Replaces: logits(const HeadMatrix&, std::span<const float>) head.cpp:189-201.
+ * d_head is row-major rows x dim; d_hidden is `dim` floats; d_out `rows`.
+ * ---------------------------------------------------------------------- */
+svt_status svt_logits(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                      const float* d_hidden, float* d_out, svt_stream stream);
+
+/* Batched forms over a plan layout (svt_plan_layout): request b scores its
+ * rows k < d_n_rows[b] against d_hidden + b*hidden_ld and writes
+ * d_out[d_out_offsets[b] + k].
+ *   _rows        : row k is head row d_ids[d_id_offsets[b] + k] (fused gather;
+ *                  with d_ids == NULL, head row k).
+ *   _interleaved : row k of request b's lane-interleaved sub-head. */
+svt_status svt_logits_rows(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                           const int64_t* d_group_begin, const int32_t* d_group_req,
+                           const int64_t* d_n_rows, const uint32_t* d_ids,
+                           const int64_t* d_id_offsets, int32_t batch, int64_t max_groups,
+                           const float* d_hidden, size_t hidden_ld, float* d_out,
+                           const int64_t* d_out_offsets, svt_stream stream);
+svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
+                                  const int64_t* d_group_begin, const int32_t* d_group_req,
+                                  const int64_t* d_n_rows, int32_t batch, int64_t max_groups,
+                                  const float* d_hidden, size_t hidden_ld, float* d_out,
+                                  const int64_t* d_out_offsets, svt_stream stream);
+
+/* Single-plan greedy over a row-major sub-head (the exact greedy_step
+ * signature shape: sub-head rows are the plan's rows in order, d_plan_ids
+ * remaps the winner). d_out_id/d_out_max are single elements. */
+svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, size_t dim,
+                           const float* d_hidden, const uint32_t* d_plan_ids,
+                           uint32_t* d_out_id, float* d_out_max, void* d_workspace,
+                           svt_stream stream);
+
+/* Kernel tuning (0 = automatic): warps per CTA and ring stages per warp of
+ * the exact-order GEMV. Used by bench sweeps; not needed for correctness. */
+void svt_set_tuning(int warps, int stages);
+
+/* ------------------------------------------------------------------------
+ * (d) Fused greedy decode: logits + strict-'>' argmax (ties -> lowest local
+ * row; s[0]=NaN -> row 0; NaN elsewhere skipped; -0.0 == +0.0) + remap_out.
+ * Replaces: greedy_step(const HeadMatrix&, std::span<const float>,
+ *           const SelectionPlan&) head.cpp:203-217 and remap_out
+ *           selector.cpp:50-56, for a micro-batch with one plan per request.
+ *
+ * Source layouts:
+ *   svt_greedy_interleaved — sub-heads produced by svt_gather_interleaved.
+ *   svt_greedy_fused       — no materialised sub-head: rows are streamed
+ *                            from the full row-major head through the plan
+ *                            ids (gather fused into the GEMV).
+ * d_hidden: request b's hidden state at d_hidden + b*hidden_ld (f32; hidden_ld
+ *   % 4 == 0 and hidden_ld >= dim). Outputs per request: d_out_ids[b] (global
+ *   id), d_out_max[b] (the winning logit, optional), d_out_keys[b] (optional
+ *   packed (orderable max << 32 | ~global_row) key for cross-shard combines).
+ * row_base/plan_start: for vocab-sharded use (a contiguous slice of a larger
+ *   plan); pass 0 / 1 for a whole plan.
+ * d_workspace: svt_greedy_workspace_bytes(batch) bytes, zeroed ONCE by the
+ *   caller; every launch leaves it zeroed again (graph-replayable).
+ * Requests with n_active == 0 are skipped (the reference throws
+ *   IntegrityError "greedy step over an empty sub-head", head.cpp:205-206).
+ * ---------------------------------------------------------------------- */
+size_t svt_greedy_workspace_bytes(int32_t batch);
+svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
+                                  const int64_t* d_group_begin, const int32_t* d_group_req,
+                                  const int64_t* d_n_active, const uint32_t* d_active_ids,
+                                  const int64_t* d_active_offsets, int32_t batch,
+                                  int64_t max_groups, const float* d_hidden, size_t hidden_ld,
+                                  uint32_t row_base, int32_t plan_start, uint32_t* d_out_ids,
+                                  float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
+                                  svt_stream stream);
+svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                            const int64_t* d_group_begin, const int32_t* d_group_req,
+                            const int64_t* d_n_active, const uint32_t* d_active_ids,
+                            const int64_t* d_active_offsets, int32_t batch, int64_t max_groups,
+                            const float* d_hidden, size_t hidden_ld, uint32_t row_base,
+                            int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
+                            uint64_t* d_out_keys, void* d_workspace, svt_stream stream);
+
+/* Cross-shard combine for the vocab-sharded head: given the
+ * all-gathered keys of G shards ([G][batch], packed as d_out_keys above) and
+ * matching ids/max, pick per request the largest key (max value, ties to the
+ * lowest global row == lowest id since shards are contiguous and ascending). */
+svt_status svt_shard_combine(const uint64_t* d_keys, const uint32_t* d_ids,
+                             const float* d_max, int32_t shards, int32_t batch,
+                             uint32_t* d_out_ids, float* d_out_max, svt_stream stream);
+
+/* ------------------------------------------------------------------------
+ * (e) Offloaded embedding lookup (the reference only models it:
+ * offload_sim.cpp:44-60 "embedding = L * lookup_latency"; memory_report keeps
+ * the full embedding on the host, head.cpp:219-237).
+ *   _zero_copy: a kernel reads rows straight from PINNED host memory
+ *               (cudaHostAlloc'd/registered, mapped) over the host link.
+ *   _staged   : the host gathers rows into pinned staging memory and one
+ *               cudaMemcpyAsync moves them on `stream` (a side stream).
+ * ---------------------------------------------------------------------- */
+svt_status svt_embed_lookup_zero_copy(const void* h_table, svt_dtype dt, size_t rows,
+                                      size_t dim, const uint32_t* d_ids, size_t n, void* d_out,
+                                      int32_t* d_bad, svt_stream stream);
+svt_status svt_embed_lookup_staged(const void* h_table, svt_dtype dt, size_t rows, size_t dim,
+                                   const uint32_t* h_ids, size_t n, void* h_staging,
+                                   void* d_out, svt_stream stream);
+
+/* ------------------------------------------------------------------------
+ * Host-side accounting that travels with the path (no device work).
+ * memory_report: head.cpp:219-237 (MemoryReport, head.hpp:63-74).
+ * simulate / breakeven_rows: offload_sim.cpp:44-87 (the reference's analytic
+ * transfer/prefill overlap model; measured overlap is reported against it).
+ * dtype_bytes is the reference's storage width (2 or 4; else ConfigError).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    uint64_t full_head_bytes;
+    uint64_t sub_head_bytes;
+    uint64_t embedding_bytes_gpu;
+    uint64_t embedding_bytes_host;
+    double saved_fraction;
+} svt_memory_report_t;
+
+typedef struct {
+    double transfer_time;
+    double prefill_time;
+    double embedding_time;
+    double exposed_latency;
+    int32_t hidden;
+} svt_overlap_timeline_t;
+
+svt_status svt_memory_report(size_t full_size, size_t dim, int dtype_bytes, size_t plan_size,
+                             svt_memory_report_t* out);
+svt_status svt_simulate(double link_bandwidth, double device_flops, double host_lookup_latency,
+                        size_t plan_size, size_t dim, int dtype_bytes, size_t prompt_len,
+                        double model_flops_per_token, svt_overlap_timeline_t* out);
+svt_status svt_breakeven_rows(double link_bandwidth, double device_flops,
+                              double host_lookup_latency, size_t dim, int dtype_bytes,
+                              size_t prompt_len, double model_flops_per_token, size_t* out_rows);
+
+/* ------------------------------------------------------------------------
+ * Session: device-resident tailored head for a micro-batch, driven with HOST
+ * buffers (the reference-facing call an external runtime makes; used by the
+ * C++ drop-in and by bench.py's e2e measurement). A session owns device
+ * copies of the plans, interleaved sub-heads and workspaces; the full head
+ * stays caller-owned on the device.
+ * ---------------------------------------------------------------------- */
+typedef struct svt_session svt_session;
+
+svt_status svt_session_create(svt_session** out, const void* d_head, svt_dtype dt,
+                              size_t rows, size_t dim, int32_t max_batch,
+                              int64_t max_plan_rows, svt_stream stream);
+svt_status svt_session_destroy(svt_session* s);
+/* H2D of the static bitmap + prompts, then select + layout + gather on the
+ * session stream; synchronises and reports the first per-request error
+ * (IntegrityError with the reference's message). */
+svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_words,
+                                    size_t static_universe, const uint32_t* h_input_ids,
+                                    const int64_t* h_input_offsets, int32_t batch);
+/* Copy the prepared plans back: per request n_active/n_static/n_dynamic
+ * (each batch-long, optional) and ids in CSR order (optional). */
+svt_status svt_session_plans_host(svt_session* s, int64_t* h_n_active, int64_t* h_n_static,
+                                  int64_t* h_n_dynamic, uint32_t* h_ids, int64_t* h_offsets);
+/* One decode step: H2D hidden [batch x dim] f32 (host_ld floats apart),
+ * fused greedy on the device, D2H ids (and max), synchronise. */
+svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t host_ld,
+                                   uint32_t* h_out_ids, float* h_out_max);
+/* Same step with the hidden state already on the device (no sync). */
+svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size_t hidden_ld,
+                                     uint32_t* d_out_ids, float* d_out_max);
+svt_stream svt_session_stream(svt_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVT_H */

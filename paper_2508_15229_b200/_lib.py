@@ -1,0 +1,116 @@
+"""ctypes binding of the C-ABI in include/svt.h (libsvt.so, sm_100a CUDA).
+
+There is no CPU fallback: importing this module fails loudly when the
+shared library is missing, and every compute call raises ``Error`` when no
+CUDA device is usable. Status codes map onto the reference's exception
+taxonomy (/root/reference/proj/include/subvocab/error.hpp:10-38).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(HERE, "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libsvt.so")
+
+SVT_F32, SVT_F16, SVT_BF16 = 0, 1, 2
+GROUP_ROWS = 32
+
+
+class Error(RuntimeError):
+    """subvocab::Error (exit code 1) — also CUDA/runtime failures."""
+
+    exit_code = 1
+
+
+class ConfigError(Error):
+    exit_code = 2
+
+
+class ParseError(Error):
+    exit_code = 3
+
+
+class IntegrityError(Error):
+    exit_code = 4
+
+
+_ERRORS = {1: Error, 2: ConfigError, 3: ParseError, 4: IntegrityError}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA extension first "
+        "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+
+lib = C.CDLL(LIB_PATH)
+
+_vp, _sz, _i32, _i64, _u32, _u64 = C.c_void_p, C.c_size_t, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
+
+_SIGS = {
+    "svt_abi_version": ([], C.c_int),
+    "svt_last_error": ([], C.c_char_p),
+    "svt_device_count": ([], C.c_int),
+    "svt_dtype_size": ([C.c_int], _sz),
+    "svt_set_tuning": ([C.c_int, C.c_int], None),
+    "svt_head_random": ([_vp, C.c_int, C.c_int, _u64, _u64, _u64, _vp], C.c_int),
+    "svt_convert_from_f32": ([_vp, _vp, C.c_int, _u64, _vp], C.c_int),
+    "svt_convert_to_f32": ([_vp, C.c_int, _vp, _u64, _vp], C.c_int),
+    "svt_select_batched": ([_vp, _sz, _sz, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                           C.c_int),
+    "svt_bitset_insert": ([_vp, _sz, _sz, _vp, _vp, _vp], C.c_int),
+    "svt_union_plans": ([_vp, _vp, _i32, _sz, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_plan_layout": ([_vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
+    "svt_gather_rows": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
+    "svt_subhead_bytes": ([C.c_int, _sz, _i64], _sz),
+    "svt_gather_interleaved": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp,
+                                _vp, _vp], C.c_int),
+    "svt_logits": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp], C.c_int),
+    "svt_logits_rows": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _sz,
+                         _vp, _vp, _vp], C.c_int),
+    "svt_logits_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp,
+                                _vp], C.c_int),
+    "svt_greedy_step": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_greedy_workspace_bytes": ([_i32], _sz),
+    "svt_greedy_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _sz,
+                                _u32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_greedy_fused": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _sz,
+                          _u32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_shard_combine": ([_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
+    "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
+    "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
+    "svt_session_create": ([C.POINTER(_vp), _vp, C.c_int, _sz, _sz, _i32, _i64, _vp], C.c_int),
+    "svt_session_destroy": ([_vp], C.c_int),
+    "svt_session_prepare_host": ([_vp, _vp, _sz, _vp, _vp, _i32], C.c_int),
+    "svt_session_plans_host": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_session_greedy_host": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
+    "svt_session_greedy_device": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
+    "svt_session_stream": ([_vp], _vp),
+    "svt_memory_report": ([_sz, _sz, C.c_int, _sz, _vp], C.c_int),
+    "svt_simulate": ([C.c_double, C.c_double, C.c_double, _sz, _sz, C.c_int, _sz, C.c_double,
+                      _vp], C.c_int),
+    "svt_breakeven_rows": ([C.c_double, C.c_double, C.c_double, _sz, C.c_int, _sz, C.c_double,
+                            _vp], C.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_args, _res) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+
+
+def last_error() -> str:
+    m = lib.svt_last_error()
+    return m.decode() if m else ""
+
+
+def check(status: int, what: str = "") -> None:
+    if status:
+        cls = _ERRORS.get(status, Error)
+        raise cls(f"{what}: {last_error()}" if what else last_error())
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib, name)(*args), name)

@@ -1,0 +1,181 @@
+// svt_gather.cu — (b) LM-head row gather (gather(), head.cpp:176-187).
+//
+//  * gather_rows_kernel: the reference layout (row-major W_sub[k,:] =
+//    W[S[k],:]); one warp per row, 16-byte vector copies when rows are
+//    16-byte multiples, byte copies otherwise.
+//  * gather_interleaved_kernel: the decode layout. One warp owns a 32-row x
+//    32-chunk tile (16 KB): it reads the 32 selected rows with coalesced
+//    16-byte loads (one row per load instruction, 512 B contiguous), stages
+//    the tile in shared memory with an XOR swizzle (conflict-free both ways),
+//    and writes it back chunk-major so that the decode kernel's bulk copies
+//    and lane reads are contiguous. Both directions are fully coalesced;
+//    HBM traffic = 2 * |S| * d * b (read + write).
+#include "svt_common.cuh"
+
+namespace svt {
+namespace {
+
+constexpr int kGatherWarps = 4;
+
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ head, int64_t rows,
+                                   int64_t row_bytes, const uint32_t* __restrict__ ids,
+                                   int64_t n, uint8_t* __restrict__ out, int32_t* bad,
+                                   bool vec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         k < n; k += nwarps) {
+        const uint32_t id = ids[k];
+        uint8_t* dst = out + k * row_bytes;
+        if (static_cast<int64_t>(id) >= rows) {
+            if (bad && lane == 0) *bad = 1;
+            for (int64_t i = lane; i < row_bytes; i += 32) dst[i] = 0;
+            continue;
+        }
+        const uint8_t* src = head + static_cast<int64_t>(id) * row_bytes;
+        if (vec) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            const int64_t n4 = row_bytes >> 4;
+            for (int64_t i = lane; i < n4; i += 32) d4[i] = ld_stream_u4(s4 + i);
+        } else {
+            for (int64_t i = lane; i < row_bytes; i += 32) dst[i] = src[i];
+        }
+    }
+}
+
+// one 16-byte chunk of a row, zero past the row's end (unaligned rows)
+__device__ inline uint4 load_chunk_bytes(const uint8_t* row, int64_t row_bytes, int64_t c) {
+    uint8_t buf[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int64_t off = c * 16 + i;
+        buf[i] = off < row_bytes ? row[off] : 0;
+    }
+    uint4 v;
+    memcpy(&v, buf, 16);
+    return v;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kGatherWarps * 32)
+gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_t row_bytes,
+                          int32_t nchunks, const uint32_t* __restrict__ active_ids,
+                          const int64_t* __restrict__ active_off,
+                          const int64_t* __restrict__ n_active,
+                          const int64_t* __restrict__ group_begin,
+                          const int32_t* __restrict__ group_req, int32_t B, int64_t max_groups,
+                          uint4* __restrict__ out, int32_t* bad) {
+    extern __shared__ __align__(16) uint4 tiles[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint4* tile = tiles + wid * 32 * 32;
+    const int nblk = (nchunks + 31) >> 5;
+    const int64_t total = min(group_begin[B], max_groups);
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kGatherWarps;
+    for (int64_t wg = static_cast<int64_t>(blockIdx.x) * kGatherWarps + wid; wg < total * nblk;
+         wg += nwarps) {
+        const int64_t g = wg / nblk;
+        const int cb = static_cast<int>(wg - g * nblk);
+        const int b = group_req[g];
+        const int64_t row0 = (g - group_begin[b]) * kGroupRows;
+        const int64_t n = n_active[b];
+        // lane r fetches the plan id of row r; broadcast per row below
+        int64_t my_row = row0 + lane;
+        uint32_t my_id = my_row < n ? active_ids[active_off[b] + my_row] : 0xFFFFFFFFu;
+        const bool my_ok = my_row < n && static_cast<int64_t>(my_id) < rows;
+        if (my_row < n && !my_ok && bad) *bad = 1;
+        const unsigned ok_mask = __ballot_sync(0xFFFFFFFFu, my_ok);
+        const int64_t c = static_cast<int64_t>(cb) * 32 + lane;
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+            const uint32_t id = __shfl_sync(0xFFFFFFFFu, my_id, r);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (((ok_mask >> r) & 1u) && c < nchunks) {
+                const uint8_t* src = head + static_cast<int64_t>(id) * row_bytes;
+                if constexpr (VEC)
+                    v = ld_stream_u4(reinterpret_cast<const uint4*>(src) + c);
+                else
+                    v = load_chunk_bytes(src, row_bytes, c);
+            }
+            tile[r * 32 + (lane ^ (r & 7))] = v;
+        }
+        __syncwarp();
+        uint4* dst = out + g * static_cast<int64_t>(nchunks) * kGroupRows;
+#pragma unroll 8
+        for (int cc = 0; cc < 32; ++cc) {
+            const int64_t ch = static_cast<int64_t>(cb) * 32 + cc;
+            if (ch < nchunks) dst[ch * kGroupRows + lane] = tile[lane * 32 + (cc ^ (lane & 7))];
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+}  // namespace svt
+
+extern "C" size_t svt_subhead_bytes(svt_dtype dt, size_t dim, int64_t groups) {
+    const size_t nchunks = (dim * static_cast<size_t>(svt::esize_of(dt)) + 15) / 16;
+    return static_cast<size_t>(groups < 0 ? 0 : groups) * nchunks * svt::kChunkRowBytes;
+}
+
+extern "C" svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                                      const uint32_t* d_ids, size_t n, void* d_out,
+                                      int32_t* d_bad, svt_stream stream) {
+    using namespace svt;
+    if (dt != SVT_F32 && dt != SVT_F16 && dt != SVT_BF16) {
+        set_error("dtype must be SVT_F32, SVT_F16 or SVT_BF16");
+        return SVT_ERR_CONFIG;
+    }
+    if (n == 0 || dim == 0) return SVT_OK;
+    const int64_t row_bytes = static_cast<int64_t>(dim) * esize_of(dt);
+    const bool vec = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(d_head) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
+    const int64_t blocks = (static_cast<int64_t>(n) + 7) / 8;
+    const int grid = static_cast<int>(blocks < sm_count() * 8 ? blocks : sm_count() * 8);
+    gather_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, d_ids,
+        static_cast<int64_t>(n), static_cast<uint8_t*>(d_out), d_bad, vec);
+    SVT_LAUNCH_CHECK("gather_rows_kernel");
+    return SVT_OK;
+}
+
+extern "C" svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, size_t rows,
+                                             size_t dim, const uint32_t* d_active_ids,
+                                             const int64_t* d_active_offsets,
+                                             const int64_t* d_n_active,
+                                             const int64_t* d_group_begin,
+                                             const int32_t* d_group_req, int32_t batch,
+                                             int64_t max_groups, void* d_sub, int32_t* d_bad,
+                                             svt_stream stream) {
+    using namespace svt;
+    if (dt != SVT_F32 && dt != SVT_F16 && dt != SVT_BF16) {
+        set_error("dtype must be SVT_F32, SVT_F16 or SVT_BF16");
+        return SVT_ERR_CONFIG;
+    }
+    if (max_groups <= 0 || dim == 0) return SVT_OK;
+    const int64_t row_bytes = static_cast<int64_t>(dim) * esize_of(dt);
+    const int32_t nchunks = static_cast<int32_t>((row_bytes + 15) / 16);
+    const bool vec = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(d_head) & 15u) == 0;
+    const int64_t work = max_groups * ((nchunks + 31) / 32);
+    const int64_t blocks = (work + kGatherWarps - 1) / kGatherWarps;
+    const int grid = static_cast<int>(blocks < sm_count() * 6 ? blocks : sm_count() * 6);
+    const int smem = kGatherWarps * 32 * 32 * 16;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (vec) {
+        SVT_CUDA_TRY(cudaFuncSetAttribute(gather_interleaved_kernel<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        gather_interleaved_kernel<true><<<grid, kGatherWarps * 32, smem, st>>>(
+            static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
+            d_active_ids, d_active_offsets, d_n_active, d_group_begin, d_group_req, batch,
+            max_groups, static_cast<uint4*>(d_sub), d_bad);
+    } else {
+        SVT_CUDA_TRY(cudaFuncSetAttribute(gather_interleaved_kernel<false>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        gather_interleaved_kernel<false><<<grid, kGatherWarps * 32, smem, st>>>(
+            static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
+            d_active_ids, d_active_offsets, d_n_active, d_group_begin, d_group_req, batch,
+            max_groups, static_cast<uint4*>(d_sub), d_bad);
+    }
+    SVT_LAUNCH_CHECK("gather_interleaved_kernel");
+    return SVT_OK;
+}

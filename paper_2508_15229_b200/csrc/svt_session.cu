@@ -1,0 +1,370 @@
+// svt_session.cu — host-buffer session over the device path: the call an
+// external inference runtime makes (and the C++ drop-in's engine).
+//
+// prepare: static bitmap + prompts (host) -> H2D -> select (a) -> plan layout
+//          -> interleaved gather (b), all stream-ordered, one sync at the end
+//          to surface the reference's IntegrityError for an id >= V.
+// greedy : hidden [batch x dim] (host) -> H2D -> fused logits + argmax +
+//          remap (c, d) -> D2H ids -> sync.
+// Buffers grow monotonically and are reused, so a steady decode loop does no
+// allocation; the greedy workspace is zeroed once and left zeroed by every
+// launch.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "svt_common.cuh"
+
+struct svt_session {
+    const void* head = nullptr;
+    svt_dtype dt = SVT_F32;
+    size_t rows = 0, dim = 0, ld = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+
+    int32_t batch = 0;
+    int64_t max_groups = 0;
+    std::vector<int64_t> n_active, n_static, n_dynamic, act_off;
+
+    // device buffers (capacity in elements)
+    uint64_t* d_words = nullptr;
+    size_t cap_words = 0;
+    uint32_t* d_inputs = nullptr;
+    size_t cap_inputs = 0;
+    int64_t* d_in_off = nullptr;
+    int64_t* d_act_off = nullptr;
+    int64_t* d_meta = nullptr;  // n_active | n_static | n_dynamic | first_bad | group_begin
+    size_t cap_batch = 0;
+    uint32_t* d_active = nullptr;
+    size_t cap_active = 0;
+    int32_t* d_group_req = nullptr;
+    uint8_t* d_sub = nullptr;
+    size_t cap_groups = 0;
+    float* d_hidden = nullptr;
+    uint32_t* d_out_ids = nullptr;
+    float* d_out_max = nullptr;
+    void* d_ws = nullptr;
+    int32_t* d_bad = nullptr;
+    // pinned host mirrors
+    float* h_hidden = nullptr;
+    uint32_t* h_ids = nullptr;
+    float* h_max = nullptr;
+
+    int64_t* n_active_d() { return d_meta; }
+    int64_t* n_static_d() { return d_meta + cap_batch; }
+    int64_t* n_dynamic_d() { return d_meta + 2 * cap_batch; }
+    int64_t* first_bad_d() { return d_meta + 3 * cap_batch; }
+    int64_t* group_begin_d() { return d_meta + 4 * cap_batch; }
+};
+
+namespace {
+using svt::set_error;
+
+template <typename T>
+svt_status grow(T** p, size_t* cap, size_t need) {
+    if (need <= *cap && *p) return SVT_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    size_t n = need ? need : 1;
+    n += n / 4;
+    SVT_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+    *cap = n;
+    return SVT_OK;
+}
+
+void free_all(svt_session* s) {
+    void* dev[] = {s->d_words, s->d_inputs, s->d_in_off, s->d_act_off, s->d_meta, s->d_active,
+                   s->d_group_req, s->d_sub, s->d_hidden, s->d_out_ids, s->d_out_max, s->d_ws,
+                   s->d_bad};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    void* host[] = {s->h_hidden, s->h_ids, s->h_max};
+    for (void* p : host)
+        if (p) cudaFreeHost(p);
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+svt_status ensure_batch(svt_session* s, size_t B) {
+    if (B <= s->cap_batch && s->d_meta) return SVT_OK;
+    const size_t nb = B + B / 4 + 1;
+    void* old[] = {s->d_in_off, s->d_act_off, s->d_meta, s->d_hidden, s->d_out_ids,
+                   s->d_out_max, s->d_ws};
+    for (void* p : old)
+        if (p) cudaFree(p);
+    if (s->h_hidden) cudaFreeHost(s->h_hidden);
+    if (s->h_ids) cudaFreeHost(s->h_ids);
+    if (s->h_max) cudaFreeHost(s->h_max);
+    SVT_CUDA_TRY(cudaMalloc(&s->d_in_off, (nb + 1) * sizeof(int64_t)));
+    SVT_CUDA_TRY(cudaMalloc(&s->d_act_off, (nb + 1) * sizeof(int64_t)));
+    SVT_CUDA_TRY(cudaMalloc(&s->d_meta, (5 * nb + 1) * sizeof(int64_t)));
+    SVT_CUDA_TRY(cudaMalloc(&s->d_hidden, nb * s->ld * sizeof(float)));
+    SVT_CUDA_TRY(cudaMemset(s->d_hidden, 0, nb * s->ld * sizeof(float)));
+    SVT_CUDA_TRY(cudaMalloc(&s->d_out_ids, nb * sizeof(uint32_t)));
+    SVT_CUDA_TRY(cudaMalloc(&s->d_out_max, nb * sizeof(float)));
+    const size_t ws = svt_greedy_workspace_bytes(static_cast<int32_t>(nb));
+    SVT_CUDA_TRY(cudaMalloc(&s->d_ws, ws));
+    SVT_CUDA_TRY(cudaMemset(s->d_ws, 0, ws));
+    SVT_CUDA_TRY(cudaMallocHost(&s->h_hidden, nb * s->ld * sizeof(float)));
+    SVT_CUDA_TRY(cudaMallocHost(&s->h_ids, nb * sizeof(uint32_t)));
+    SVT_CUDA_TRY(cudaMallocHost(&s->h_max, nb * sizeof(float)));
+    s->cap_batch = nb;
+    return SVT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+svt_status svt_session_create(svt_session** out, const void* d_head, svt_dtype dt, size_t rows,
+                              size_t dim, int32_t max_batch, int64_t max_plan_rows,
+                              svt_stream stream) {
+    if (dt != SVT_F32 && dt != SVT_F16 && dt != SVT_BF16) {
+        set_error("dtype must be SVT_F32, SVT_F16 or SVT_BF16");
+        return SVT_ERR_CONFIG;
+    }
+    if (svt_device_count() == 0) {
+        set_error("no CUDA device available: the tailored-head path has no CPU fallback");
+        return SVT_ERR_RUNTIME;
+    }
+    auto* s = new svt_session();
+    s->head = d_head;
+    s->dt = dt;
+    s->rows = rows;
+    s->dim = dim;
+    s->ld = ((dim + 3) / 4) * 4;
+    if (stream) {
+        s->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete s;
+            return svt::cuda_status(cudaGetLastError(), "cudaStreamCreate");
+        }
+        s->own_stream = true;
+    }
+    svt_status st = ensure_batch(s, max_batch > 0 ? static_cast<size_t>(max_batch) : 1);
+    if (!st && max_plan_rows > 0 && max_batch > 0) {
+        const size_t groups = static_cast<size_t>(max_batch) *
+                              ((static_cast<size_t>(max_plan_rows) + 31) / 32);
+        st = grow(&s->d_active, &s->cap_active,
+                  static_cast<size_t>(max_batch) * static_cast<size_t>(max_plan_rows));
+        if (!st) {
+            size_t cap = 0;
+            st = grow(&s->d_group_req, &cap, groups);
+            if (!st) {
+                size_t bytes = svt_subhead_bytes(dt, dim, static_cast<int64_t>(cap));
+                size_t capb = 0;
+                st = grow(&s->d_sub, &capb, bytes);
+                s->cap_groups = cap;
+            }
+        }
+    }
+    if (!st) {
+        size_t c = 0;
+        st = grow(&s->d_bad, &c, 1);
+    }
+    if (st) {
+        free_all(s);
+        delete s;
+        return st;
+    }
+    *out = s;
+    return SVT_OK;
+}
+
+svt_status svt_session_destroy(svt_session* s) {
+    if (!s) return SVT_OK;
+    cudaStreamSynchronize(s->stream);
+    free_all(s);
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return SVT_OK;
+}
+
+svt_stream svt_session_stream(svt_session* s) { return s ? s->stream : nullptr; }
+
+svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_words,
+                                    size_t static_universe, const uint32_t* h_input_ids,
+                                    const int64_t* h_input_offsets, int32_t batch) {
+    if (!s) {
+        set_error("null session");
+        return SVT_ERR_CONFIG;
+    }
+    if (static_universe != s->rows) {
+        set_error("static vocabulary universe %zu does not match full vocabulary size %zu",
+                  static_universe, s->rows);
+        return SVT_ERR_INTEGRITY;
+    }
+    if (batch < 0) {
+        set_error("negative batch");
+        return SVT_ERR_CONFIG;
+    }
+    const size_t B = static_cast<size_t>(batch);
+    const size_t nw = (s->rows + 63) / 64;
+    int64_t n_static = 0;
+    for (size_t i = 0; i < nw; ++i) n_static += __builtin_popcountll(h_static_words[i]);
+    // capacities: |S_b| <= |T| + len_b
+    s->act_off.assign(B + 1, 0);
+    int64_t groups = 0;
+    for (size_t b = 0; b < B; ++b) {
+        const int64_t cap = n_static + (h_input_offsets[b + 1] - h_input_offsets[b]);
+        s->act_off[b + 1] = s->act_off[b] + cap;
+        groups += (cap + 31) / 32;
+    }
+    const size_t n_inputs = static_cast<size_t>(B ? h_input_offsets[B] - h_input_offsets[0] : 0);
+    svt_status st = ensure_batch(s, B ? B : 1);
+    if (!st) st = grow(&s->d_words, &s->cap_words, nw);
+    if (!st) st = grow(&s->d_inputs, &s->cap_inputs, n_inputs);
+    if (!st) st = grow(&s->d_active, &s->cap_active, static_cast<size_t>(s->act_off[B]));
+    if (!st && static_cast<size_t>(groups) > s->cap_groups) {
+        size_t cap = 0;
+        st = grow(&s->d_group_req, &cap, static_cast<size_t>(groups));
+        if (!st) {
+            if (s->d_sub) cudaFree(s->d_sub);
+            s->d_sub = nullptr;
+            size_t capb = 0;
+            st = grow(&s->d_sub, &capb, svt_subhead_bytes(s->dt, s->dim, static_cast<int64_t>(cap)));
+            s->cap_groups = cap;
+        }
+    }
+    if (st) return st;
+    s->batch = batch;
+    s->max_groups = groups;
+    if (B == 0) return SVT_OK;
+
+    cudaStream_t q = s->stream;
+    std::vector<int64_t> in_off(B + 1);
+    for (size_t b = 0; b <= B; ++b) in_off[b] = h_input_offsets[b] - h_input_offsets[0];
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_words, h_static_words, nw * sizeof(uint64_t),
+                                 cudaMemcpyHostToDevice, q));
+    if (n_inputs)
+        SVT_CUDA_TRY(cudaMemcpyAsync(s->d_inputs, h_input_ids + h_input_offsets[0],
+                                     n_inputs * sizeof(uint32_t), cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_in_off, in_off.data(), (B + 1) * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_act_off, s->act_off.data(), (B + 1) * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaMemsetAsync(s->d_bad, 0, sizeof(int32_t), q));
+    st = svt_select_batched(s->d_words, static_universe, s->rows, s->d_inputs, s->d_in_off, batch,
+                            s->d_active, s->d_act_off, s->n_active_d(), s->n_static_d(),
+                            s->n_dynamic_d(), s->first_bad_d(), q);
+    if (!st)
+        st = svt_plan_layout(s->n_active_d(), batch, s->group_begin_d(), s->d_group_req,
+                             s->max_groups, q);
+    if (!st)
+        st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim, s->d_active, s->d_act_off,
+                                    s->n_active_d(), s->group_begin_d(), s->d_group_req, batch,
+                                    s->max_groups, s->d_sub, s->d_bad, q);
+    if (st) return st;
+    std::vector<int64_t> meta(4 * B);
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data(), s->n_active_d(), B * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data() + B, s->n_static_d(), B * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data() + 2 * B, s->n_dynamic_d(), B * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data() + 3 * B, s->first_bad_d(), B * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, q));
+    SVT_CUDA_TRY(cudaStreamSynchronize(q));
+    s->n_active.assign(meta.begin(), meta.begin() + B);
+    s->n_static.assign(meta.begin() + B, meta.begin() + 2 * B);
+    s->n_dynamic.assign(meta.begin() + 2 * B, meta.begin() + 3 * B);
+    for (size_t b = 0; b < B; ++b) {
+        const int64_t bad = meta[3 * B + b];
+        if (bad >= 0) {
+            const uint32_t id = h_input_ids[h_input_offsets[b] + bad];
+            set_error("input token id %u out of range for vocabulary of size %zu", id, s->rows);
+            s->batch = 0;
+            return SVT_ERR_INTEGRITY;
+        }
+        if (bad == -2) {
+            set_error("internal: plan capacity exceeded for request %zu", b);
+            s->batch = 0;
+            return SVT_ERR_RUNTIME;
+        }
+    }
+    return SVT_OK;
+}
+
+svt_status svt_session_plans_host(svt_session* s, int64_t* h_n_active, int64_t* h_n_static,
+                                  int64_t* h_n_dynamic, uint32_t* h_ids, int64_t* h_offsets) {
+    if (!s) {
+        set_error("null session");
+        return SVT_ERR_CONFIG;
+    }
+    const size_t B = static_cast<size_t>(s->batch);
+    int64_t off = 0;
+    for (size_t b = 0; b < B; ++b) {
+        if (h_n_active) h_n_active[b] = s->n_active[b];
+        if (h_n_static) h_n_static[b] = s->n_static[b];
+        if (h_n_dynamic) h_n_dynamic[b] = s->n_dynamic[b];
+        if (h_offsets) h_offsets[b] = off;
+        if (h_ids && s->n_active[b])
+            SVT_CUDA_TRY(cudaMemcpyAsync(h_ids + off, s->d_active + s->act_off[b],
+                                         s->n_active[b] * sizeof(uint32_t),
+                                         cudaMemcpyDeviceToHost, s->stream));
+        off += s->n_active[b];
+    }
+    if (h_offsets) h_offsets[B] = off;
+    SVT_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return SVT_OK;
+}
+
+svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size_t hidden_ld,
+                                     uint32_t* d_out_ids, float* d_out_max) {
+    if (!s) {
+        set_error("null session");
+        return SVT_ERR_CONFIG;
+    }
+    for (int32_t b = 0; b < s->batch; ++b)
+        if (s->n_active[b] == 0) {
+            set_error("greedy step over an empty sub-head");
+            return SVT_ERR_INTEGRITY;
+        }
+    return svt_greedy_interleaved(s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req,
+                                  s->n_active_d(), s->d_active, s->d_act_off, s->batch,
+                                  s->max_groups, d_hidden, hidden_ld, 0, 1, d_out_ids, d_out_max,
+                                  nullptr, s->d_ws, s->stream);
+}
+
+svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t host_ld,
+                                   uint32_t* h_out_ids, float* h_out_max) {
+    if (!s) {
+        set_error("null session");
+        return SVT_ERR_CONFIG;
+    }
+    const size_t B = static_cast<size_t>(s->batch);
+    if (B == 0) return SVT_OK;
+    cudaStream_t q = s->stream;
+    if (is_pinned(h_hidden)) {
+        SVT_CUDA_TRY(cudaMemcpy2DAsync(s->d_hidden, s->ld * sizeof(float), h_hidden,
+                                       host_ld * sizeof(float), s->dim * sizeof(float), B,
+                                       cudaMemcpyHostToDevice, q));
+    } else {
+        for (size_t b = 0; b < B; ++b)
+            std::memcpy(s->h_hidden + b * s->ld, h_hidden + b * host_ld, s->dim * sizeof(float));
+        SVT_CUDA_TRY(cudaMemcpyAsync(s->d_hidden, s->h_hidden, B * s->ld * sizeof(float),
+                                     cudaMemcpyHostToDevice, q));
+    }
+    svt_status st = svt_session_greedy_device(s, s->d_hidden, s->ld, s->d_out_ids, s->d_out_max);
+    if (st) return st;
+    const bool direct = is_pinned(h_out_ids);
+    SVT_CUDA_TRY(cudaMemcpyAsync(direct ? h_out_ids : s->h_ids, s->d_out_ids, B * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, q));
+    if (h_out_max)
+        SVT_CUDA_TRY(cudaMemcpyAsync(s->h_max, s->d_out_max, B * sizeof(float),
+                                     cudaMemcpyDeviceToHost, q));
+    SVT_CUDA_TRY(cudaStreamSynchronize(q));
+    if (!direct) std::memcpy(h_out_ids, s->h_ids, B * sizeof(uint32_t));
+    if (h_out_max) std::memcpy(h_out_max, s->h_max, B * sizeof(float));
+    return SVT_OK;
+}
+
+}  // extern "C"

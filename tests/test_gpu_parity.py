@@ -1,0 +1,377 @@
+"""GPU parity: the sm_100a path (libsvt.so, through the C-ABI) against the
+oracle and the reference goldens. Bit-exact for ids, plans AND logits — the
+kernels keep the reference's accumulation order (head.cpp:194-199)."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_cases
+from oracle.oracle import c_oracle, words_from_ids
+
+pytestmark = pytest.mark.gpu
+
+orc = c_oracle()
+
+
+@pytest.fixture(scope="module")
+def th():
+    from paper_2508_15229_b200 import tailored_head
+
+    torch.cuda.set_device(0)
+    return tailored_head
+
+
+def bits(x):
+    return np.ascontiguousarray(x, np.float32).view(np.uint32)
+
+
+def bf16_np(x):
+    from paper_2508_15229_b200.synth import round_bf16
+
+    return round_bf16(np.asarray(x, np.float32))
+
+
+# ---- generator -------------------------------------------------------------------
+def test_head_random_matches_reference_generator(th):
+    for db, st in [(4, th.SVT_F32), (2, th.SVT_F16), (2, th.SVT_F32)]:
+        rt = th.SVT_F16 if db == 2 else th.SVT_F32
+        m = th.HeadMatrix.random(61, 37, 0xC0FFEE, dtype_bytes=db, storage=st, round_through=rt)
+        assert np.array_equal(bits(m.to_host()), bits(orc.head_random(61, 37, 0xC0FFEE, db)))
+    m = th.HeadMatrix.random(33, 50, 0x5EED, storage=th.SVT_BF16)
+    assert np.array_equal(bits(m.to_host()), bits(bf16_np(orc.head_random(33, 50, 0x5EED))))
+
+
+# ---- (a) select ----------------------------------------------------------------
+def test_select_known_answers(th):
+    plan = th.select([0, 2, 0], th.TokenSet.from_ids(8, [3, 4]), 8)
+    assert plan.active_ids.tolist() == [0, 2, 3, 4]
+    assert (plan.n_static, plan.n_dynamic, plan.full_vocab_size) == (2, 2, 8)
+    again = th.select([0, 2, 0], th.TokenSet.from_ids(8, [3, 4]), 8)
+    assert again.active_ids.tolist() == plan.active_ids.tolist()
+    p = th.select([7, 3, 3], th.TokenSet(16), 16)
+    assert p.active_ids.tolist() == [3, 7] and (p.n_static, p.n_dynamic) == (0, 2)
+    p = th.select([2, 1, 2], th.TokenSet.from_ids(8, [1, 2, 5]), 8)
+    assert p.active_ids.tolist() == [1, 2, 5] and p.n_dynamic == 0
+
+
+def test_select_errors(th):
+    with pytest.raises(th.IntegrityError, match="input token id 8 out of range"):
+        th.select([8], th.TokenSet(8), 8)
+    with pytest.raises(th.IntegrityError):
+        th.select([0], th.TokenSet(4), 8)
+    # first offending id in input order is the one named
+    with pytest.raises(th.IntegrityError, match="input token id 12 "):
+        th.select([1, 12, 3, 9, 15], th.TokenSet(9), 9)
+
+
+def test_select_randomised_against_oracle(th):
+    rng = np.random.default_rng(11)
+    for V in [1, 63, 64, 65, 1000, 4097, 128256, 151936, 256000]:
+        for _ in range(3):
+            t = np.unique(rng.integers(0, V, int(rng.integers(0, min(V, 3000) + 1))))
+            ids = rng.integers(0, V, int(rng.integers(0, 2500))).astype(np.uint32)
+            got = th.select(ids, th.TokenSet.from_ids(V, t) if t.size < 400 else _fast_set(th, V, t), V)
+            want = orc.select(ids, words_from_ids(t, V), V, V)
+            assert np.array_equal(got.active_ids, want.active_ids)
+            assert (got.n_static, got.n_dynamic) == (want.n_static, want.n_dynamic)
+
+
+def _fast_set(th, V, ids):
+    s = th.TokenSet(V)
+    s.words = words_from_ids(ids, V)
+    return s
+
+
+def test_union_plans(th):
+    t = th.TokenSet.from_ids(8, [5])
+    u = th.union_plans([th.select([0], t, 8), th.select([2, 3], t, 8)])
+    assert u.active_ids.tolist() == [0, 2, 3, 5] and (u.n_static, u.n_dynamic) == (1, 3)
+    with pytest.raises(th.ConfigError):
+        th.union_plans([])
+    rng = np.random.default_rng(3)
+    V = 151936
+    T = _fast_set(th, V, rng.integers(0, V, 2048))
+    plans = [th.select(rng.integers(0, V, 512).astype(np.uint32), T, V) for _ in range(8)]
+    want = orc.union_plans([_oplan(p) for p in plans])
+    got = th.union_plans(plans)
+    assert np.array_equal(got.active_ids, want.active_ids) and got.n_dynamic == want.n_dynamic
+
+
+def _oplan(p):
+    from oracle.oracle import Plan
+
+    return Plan(p.active_ids, p.n_static, p.n_dynamic, p.full_vocab_size)
+
+
+# ---- (b) gather, (c) logits, (d) greedy_step: reference-shaped calls ------------
+def test_gather_copies_rows_exactly(th):
+    head = th.HeadMatrix.random(8, 4, 1234)
+    sub = th.gather(head, th.SelectionPlan(np.array([0, 2, 3, 4], np.uint32), 0, 4, 8))
+    assert np.array_equal(bits(sub.to_host()), bits(head.to_host()[[0, 2, 3, 4]]))
+    h6 = th.HeadMatrix.random(6, 3, 9)
+    ident = th.gather(h6, th.SelectionPlan(np.arange(6, dtype=np.uint32), 0, 6, 6))
+    assert np.array_equal(bits(ident.to_host()), bits(h6.to_host()))
+    assert th.gather(h6, th.SelectionPlan(np.zeros(0, np.uint32), 0, 0, 6)).rows() == 0
+    with pytest.raises(th.IntegrityError):
+        th.gather(h6, th.SelectionPlan(np.array([6], np.uint32), 0, 1, 8))
+
+
+def test_logits_basics(th):
+    head = th.HeadMatrix.from_host(np.array([[2.0], [3.0]], np.float32))
+    assert th.logits(head, [5.0]).tolist() == [10.0, 15.0]
+    r = th.HeadMatrix.random(4, 8, 7)
+    assert (th.logits(r, np.zeros(8, np.float32)) == 0).all()
+    with pytest.raises(th.IntegrityError):
+        th.logits(r, [1.0])
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16", "bf16"])
+def test_logits_bitwise_against_oracle(th, storage):
+    st = {"f32": th.SVT_F32, "f16": th.SVT_F16, "bf16": th.SVT_BF16}[storage]
+    rng = np.random.default_rng(17)
+    # odd dims take the generic kernel, multiples of 8 the bulk-copy ring kernel
+    for rows, dim in [(1, 1), (5, 3), (33, 7), (100, 16), (257, 64), (1000, 896), (70, 2048),
+                      (64, 2304), (40, 3072), (31, 1000)]:
+        db = 2 if st == th.SVT_F16 else 4
+        head = th.HeadMatrix.random(rows, dim, int(rng.integers(0, 2**62)), dtype_bytes=db,
+                                    storage=st)
+        hv = rng.uniform(-2, 2, dim).astype(np.float32)
+        if st == th.SVT_BF16:
+            hv = bf16_np(hv)
+        got = th.logits(head, hv)
+        want = orc.logits(head.to_host(), hv)
+        assert np.array_equal(bits(got), bits(want)), (rows, dim)
+
+
+def test_sub_head_logits_equal_full_head_bitwise(th):
+    # test_head.cpp:73-93 on the GPU: logits(gather(head, plan)) == logits(head)[plan]
+    rng = np.random.default_rng(0x10617)
+    for _ in range(150):
+        rows, dim = int(rng.integers(1, 33)), int(rng.integers(1, 17))
+        head = th.HeadMatrix.random(rows, dim, int(rng.integers(0, 2**62)))
+        picked = np.flatnonzero(rng.integers(0, 2, rows)).astype(np.uint32)
+        plan = th.SelectionPlan(picked, 0, picked.size, rows)
+        h = rng.uniform(-1, 1, dim).astype(np.float32)
+        full = th.logits(head, h)
+        sub = th.logits(th.gather(head, plan), h)
+        assert np.array_equal(bits(sub), bits(full[picked]))
+        assert np.array_equal(bits(full), bits(orc.logits(head.to_host(), h)))
+
+
+def test_greedy_step_known_answers(th):
+    plan = th.SelectionPlan(np.array([0, 2, 4], np.uint32), 0, 3, 8)
+    sub = th.HeadMatrix.from_host(np.array([[1.0], [3.0], [2.0]], np.float32))
+    assert th.greedy_step(sub, [1.0], plan) == 2
+    flat = th.HeadMatrix.from_host(np.ones((3, 1), np.float32))
+    assert th.greedy_step(flat, [1.0], plan) == 0
+    with pytest.raises(th.IntegrityError, match="empty sub-head"):
+        th.greedy_step(th.HeadMatrix(0, 1), [1.0], th.SelectionPlan())
+    with pytest.raises(th.IntegrityError):
+        th.greedy_step(sub, [1.0], th.SelectionPlan(np.array([0, 2], np.uint32), 0, 2, 8))
+
+
+def test_greedy_special_values(th):
+    nan, inf = np.float32("nan"), np.float32("inf")
+    ids = np.array([3, 5, 9, 11], np.uint32)
+    plan = th.SelectionPlan(ids, 0, 4, 16)
+    for scores, want in [([nan, 5, 7, 1], 3), ([1, nan, 7, 7], 9), ([-0.0, 0.0, -1, -2], 3),
+                         ([0.0, -0.0, -1, -2], 3), ([-inf, inf, inf, 0], 5),
+                         ([-inf, -inf, -inf, -inf], 3), ([1, nan, nan, nan], 3)]:
+        sub = th.HeadMatrix.from_host(np.array(scores, np.float32).reshape(4, 1))
+        assert th.greedy_step(sub, [1.0], plan) == want, scores
+
+
+def test_greedy_agrees_with_full_argmax_when_in_plan(th):
+    rng = np.random.default_rng(0xA26A)
+    for _ in range(100):
+        head = th.HeadMatrix.random(16, 8, int(rng.integers(0, 2**62)))
+        picked = np.flatnonzero(rng.integers(0, 2, 16)).astype(np.uint32)
+        if picked.size == 0:
+            continue
+        plan = th.SelectionPlan(picked, 0, picked.size, 16)
+        h = rng.uniform(-1, 1, 8).astype(np.float32)
+        full = th.logits(head, h)
+        arg = orc.argmax_first(full)
+        got = th.greedy_step(th.gather(head, plan), h, plan)
+        if plan.global_to_local(arg) is not None:
+            assert got == arg
+        ohead = head.to_host()
+        assert got == orc.greedy_step(ohead[picked], h, picked)[0]
+
+
+# ---- golden fixtures from the real reference ---------------------------------
+@pytest.mark.parametrize("name,case", golden_cases(), ids=[n for n, _ in golden_cases()])
+@pytest.mark.parametrize("fused", [False, True])
+def test_batched_engine_reproduces_reference_goldens(th, name, case, fused):
+    V, d, db = int(case["V"]), int(case["d"]), int(case["dtype_bytes"])
+    st = th.SVT_BF16 if bool(case["bf16"]) else (th.SVT_F16 if db == 2 else th.SVT_F32)
+    head = th.HeadMatrix.random(V, d, int(case["W_seed"]), dtype_bytes=db, storage=st)
+    assert hashlib.sha256(bits(head.to_host()).tobytes()).hexdigest() == str(case["W_sha256"])
+    words = words_from_ids(case["static_ids"], V)
+    poff = case["prompt_off"]
+    B = len(poff) - 1
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(),
+                                len(case["static_ids"]), V,
+                                torch.from_numpy(np.concatenate([case["prompts"], [0]]).astype(
+                                    np.uint32).view(np.int32)).cuda(), poff)
+    off = case["plan_off"]
+    for b in range(B):
+        p = tb.plan(b)
+        assert np.array_equal(p.active_ids, case["plan_ids"][off[b]:off[b + 1]])
+        assert (p.n_static, p.n_dynamic) == (int(case["n_static"][b]), int(case["n_dynamic"][b]))
+    tb.gather(head)
+    ld = (d + 3) // 4 * 4
+    hid = torch.zeros((B, ld), dtype=torch.float32, device="cuda")
+    hid[:, :d] = torch.from_numpy(case["hidden_bits"].view(np.float32).reshape(B, d)).cuda()
+    lg = tb.logits(hid, fused=fused).cpu().numpy()
+    out = torch.full((B,), -1, dtype=torch.int32, device="cuda")
+    tb.greedy(hid, out, fused=fused)
+    got = out.cpu().numpy().view(np.uint32)
+    lo = 0
+    for b in range(B):
+        n = off[b + 1] - off[b]
+        o = int(tb.act_off_h[b])
+        assert np.array_equal(bits(lg[o:o + n]), case["logit_bits"][lo:lo + n])
+        lo += n
+        if n:
+            assert got[b] == case["greedy"][b]
+
+
+# ---- the BASELINE shapes ---------------------------------------------------------
+def _build_workload(th, V, d, st, B, L, nT, steps, seed_off=0):
+    from paper_2508_15229_b200 import synth
+
+    head = th.HeadMatrix.random(V, d, synth.SEED_W, storage=st,
+                                round_through=st if st != th.SVT_F16 else th.SVT_F16)
+    t_ids = synth.static_ids(V, nT)
+    words = synth.words_of(t_ids, V)
+    prompts = [synth.prompt_ids(V, L, seed_off + r) for r in range(B)]
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in prompts])
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), nT, V,
+                                torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda(),
+                                off)
+    tb.gather(head)
+    hid = synth.head_random(steps * B, d, synth.SEED_H).reshape(steps, B, d)
+    if st == th.SVT_BF16:
+        hid = synth.round_bf16(hid)
+    return head, words, prompts, tb, hid
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_cfg1_llama1b_shape_bit_exact(th, fused):
+    """cfg1: V=128256, d=2048, fp32, one 512-token prompt + 2048 static."""
+    V, d = 128256, 2048
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_F32, 1, 512, 2048, 4)
+    W = head.to_host()
+    plan = orc.select(prompts[0], words, V, V)
+    assert np.array_equal(tb.plan(0).active_ids, plan.active_ids)
+    sub = orc.gather(W, plan.active_ids)
+    out = torch.empty(1, dtype=torch.int32, device="cuda")
+    for t in range(hid.shape[0]):
+        h = torch.from_numpy(hid[t]).cuda()
+        tb.greedy(h, out, fused=fused)
+        assert int(out.item()) == orc.greedy_step(sub, hid[t][0], plan.active_ids)[0]
+    lg = tb.logits(torch.from_numpy(hid[0]).cuda(), fused=fused).cpu().numpy()
+    assert np.array_equal(bits(lg[: plan.active_ids.size]), bits(orc.logits(sub, hid[0][0])))
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_cfg2_qwen05b_shape_bit_exact(th, fused):
+    """cfg2: V=151936, d=896, bf16, 64 requests with their own plans."""
+    V, d, B = 151936, 896, 64
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_BF16, B, 512, 2048, 2)
+    W = head.to_host()
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    mx = torch.empty(B, dtype=torch.float32, device="cuda")
+    for t in range(hid.shape[0]):
+        tb.greedy(torch.from_numpy(hid[t]).cuda(), out, mx, fused=fused)
+        got = out.cpu().numpy().view(np.uint32)
+        for b in range(0, B, 7 if t else 1):
+            plan = orc.select(prompts[b], words, V, V)
+            if t == 0:
+                gp = tb.plan(b)
+                assert np.array_equal(gp.active_ids, plan.active_ids)
+                assert gp.n_static + gp.n_dynamic == gp.size()
+            want, wmax = orc.greedy_step(orc.gather(W, plan.active_ids), hid[t][b],
+                                         plan.active_ids)
+            assert got[b] == want
+            assert bits(mx.cpu().numpy()[b]) == bits(np.float32(wmax))
+
+
+def test_decode_is_replayable_and_workspace_self_cleaning(th):
+    V, d, B = 151936, 896, 16
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_BF16, B, 512, 2048, 1)
+    h = torch.from_numpy(hid[0]).cuda()
+    outs = []
+    for _ in range(5):
+        o = torch.empty(B, dtype=torch.int32, device="cuda")
+        tb.greedy(h, o)
+        outs.append(o.cpu().numpy())
+    assert all(np.array_equal(outs[0], o) for o in outs)
+    assert int(tb.ws.sum().item()) == 0
+    # CUDA-graph capture of the decode step replays bit-identically
+    o = torch.empty(B, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    tb.stream = s
+    with torch.cuda.stream(s):
+        tb.greedy(h, o)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tb.greedy(h, o)
+    o.fill_(-1)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(o.cpu().numpy(), outs[0])
+
+
+def test_vocab_sharded_combine(th):
+    """Contiguous row shards of one plan + per-shard greedy with row_base +
+    svt_shard_combine == whole-plan greedy."""
+    from paper_2508_15229_b200 import sharded
+
+    V, d = 20000, 256
+    head = th.HeadMatrix.random(V, d, 77, storage=th.SVT_BF16)
+    rng = np.random.default_rng(9)
+    hid = bf16_np(rng.uniform(-1, 1, (3, d)).astype(np.float32))
+    full_ids = np.arange(V, dtype=np.uint32)
+    want = [orc.greedy_step(head.to_host(), hid[b], full_ids)[0] for b in range(3)]
+    for G in (1, 2, 3, 8):
+        got = sharded.sharded_greedy_local(head, hid, G)
+        assert got.tolist() == want, G
+
+
+def test_embedding_lookup_paths(th):
+    from paper_2508_15229_b200 import offload
+
+    rows, dim = 5000, 896
+    table = np.random.default_rng(1).standard_normal((rows, dim)).astype(np.float32)
+    ids = np.random.default_rng(2).integers(0, rows, 700).astype(np.uint32)
+    emb = offload.HostEmbedding(table, th.SVT_BF16)
+    want = bf16_np(table[ids])
+    for mode in ("zero_copy", "staged"):
+        got = emb.lookup(ids, mode=mode).float().cpu().numpy()
+        assert np.array_equal(bits(got), bits(want)), mode
+    with pytest.raises(th.IntegrityError):
+        emb.lookup(np.array([rows], np.uint32), mode="staged")
+
+
+def test_session_host_api_matches_batched_engine(th):
+    from paper_2508_15229_b200 import session
+
+    V, d, B = 151936, 896, 8
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_BF16, B, 512, 2048, 2)
+    with session.Session(head, max_batch=B) as s:
+        off = np.zeros(B + 1, np.int64)
+        off[1:] = np.cumsum([len(p) for p in prompts])
+        s.prepare(words, V, np.concatenate(prompts), off)
+        for t in range(2):
+            ids = s.greedy(hid[t])
+            o = torch.empty(B, dtype=torch.int32, device="cuda")
+            tb.greedy(torch.from_numpy(hid[t]).cuda(), o)
+            assert np.array_equal(ids, o.cpu().numpy().view(np.uint32))
+        with pytest.raises(th.IntegrityError, match="out of range"):
+            s.prepare(words, V, np.array([V + 5], np.uint32), np.array([0, 1], np.int64))
