@@ -1,0 +1,478 @@
+#!/usr/bin/env python
+"""Benchmark of the tailored LM-head path (BASELINE.json metric:
+"tailored LM-head tokens/s ... ; HBM GB/s vs roofline").
+
+Workload (BASELINE.json configs[1], the single-GPU throughput config):
+  Qwen2.5-0.5B-shaped head, V=151936, d=896, bf16 weights, B=64 requests per
+  GPU, each with its own plan S_b = T ∪ prompt_b (|T|=2048 static ids, 512-
+  token synthetic prompt), 64 greedy decode steps per request.
+One bench STEP = one full pass of the hot path over one request batch:
+  (a) select  -> plan layout -> (b) interleaved gather -> 64 x (c+d) fused
+  exact-order logits + argmax + remap.   tokens per step = B * 64.
+Inputs (head, static bitmap, prompts, 64 x B hidden states) are resident in
+HBM before the timed region. The per-step decode working set (Σ|S_b|·d·2 ≈
+293 MB) exceeds the 126 MB L2, so no explicit flush is needed ("inputs larger
+than L2").
+
+N>1 (torchrun): batch-shard weak scaling — every rank runs its own 64
+requests (request seeds offset by rank); no collective on the data path.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified reference TUs) on the host cores, same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tailored LM-head tokens/s (Llama-3.2-1B shape); HBM GB/s vs roofline"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="interleaved", choices=["interleaved", "fused"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--decode-steps", type=int, default=64)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+CFG2 = dict(workload="cfg2: Qwen2.5-0.5B-shaped tailored head, per-request plans",
+            V=151936, d=896, static=2048, prompt_len=512, dtype="bf16")
+CFG1 = dict(workload="cfg1: Llama-3.2-1B-shaped tailored head, batch 1", V=128256, d=2048,
+            static=2048, prompt_len=512, dtype="f32")
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(kernel_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    j = json.load(open(p))
+    return j.get(kernel_key)
+
+
+# --------------------------------------------------------------------------
+# clocks: NVML sampled in a thread during the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        r = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": r, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+class Job:
+    """Device-resident inputs + the engine for one request batch."""
+
+    def __init__(self, cfg, B, steps, rank, torch, th, synth):
+        self.cfg, self.B, self.steps = cfg, B, steps
+        V, d = cfg["V"], cfg["d"]
+        st = th.SVT_BF16 if cfg["dtype"] == "bf16" else th.SVT_F32
+        self.esize = 2 if st == th.SVT_BF16 else 4
+        self.head = th.HeadMatrix.random(V, d, synth.SEED_W, storage=st)
+        t_ids = synth.static_ids(V, cfg["static"])
+        self.words_h = synth.words_of(t_ids, V)
+        self.prompts_h = [synth.prompt_ids(V, cfg["prompt_len"], rank * B + r) for r in range(B)]
+        self.off_h = np.zeros(B + 1, np.int64)
+        self.off_h[1:] = np.cumsum([len(p) for p in self.prompts_h])
+        self.flat_h = np.concatenate(self.prompts_h)
+        self.ld = (d + 3) // 4 * 4
+        # hidden states for every decode step (device), bf16-rounded for bf16
+        n = steps * B * d
+        hid = torch.empty(n, dtype=torch.float32, device="cuda")
+        th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_F32,
+                     th.SVT_BF16 if st == th.SVT_BF16 else th.SVT_F32, 0, n, synth.SEED_H, None)
+        self.hidden = torch.zeros((steps, B, self.ld), dtype=torch.float32, device="cuda")
+        self.hidden[:, :, :d] = hid.view(steps, B, d)
+        self.words = torch.from_numpy(self.words_h.view(np.int64)).cuda()
+        self.prompts = torch.from_numpy(self.flat_h.view(np.int32)).cuda()
+        self.tb = th.TailoredBatch.build(self.words, cfg["static"], V, self.prompts, self.off_h)
+        self.tb.gather(self.head)
+        self.out = torch.empty((steps, B), dtype=torch.int32, device="cuda")
+        self.torch = torch
+
+    def run(self, mode, dec_events=None):
+        tb = self.tb
+        tb.run_select()
+        if mode == "interleaved":
+            tb.gather(self.head)
+        for t in range(self.steps):
+            if dec_events is not None:
+                dec_events[t][0].record()
+            tb.greedy(self.hidden[t], self.out[t], fused=(mode == "fused"))
+            if dec_events is not None:
+                dec_events[t][1].record()
+
+    def launches_per_step(self, mode):
+        return 2 + (1 if mode == "interleaved" else 0) + self.steps
+
+    def decode_bytes(self):
+        return self.tb.algorithmic_decode_bytes(self.esize, self.cfg["d"])
+
+
+def time_job(job, mode, K, W, torch, dist, world):
+    for _ in range(W):
+        job.run(mode)
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(job.steps)] for _ in range(K)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        start.record()
+        for k in range(K):
+            job.run(mode, ev[k])
+        end.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    dec_ms = [a.elapsed_time(b) for row in ev for (a, b) in row]
+    if dist is not None and world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, dec_ms, clk.summary()
+
+
+def e2e_session(job, K, W, th, torch, session_mod):
+    """Same workload through the host-buffer C-ABI session: per step H2D of
+    the static bitmap + prompts (select+gather inside), then per decode step
+    H2D of the hidden states from pinned memory and D2H of the ids."""
+    B, steps, d = job.B, job.steps, job.cfg["d"]
+    hid_h = job.hidden[:, :, :d].cpu().pin_memory()
+    ids_h = torch.empty((steps, B), dtype=torch.int32).pin_memory()
+    with session_mod.Session(job.head, max_batch=B) as s:
+        def one():
+            s.prepare(job.words_h, job.cfg["V"], job.flat_h, job.off_h)
+            for t in range(steps):
+                s.greedy(hid_h[t], ids_h[t])
+        for _ in range(W):
+            one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            one()
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+    h2d = job.words_h.nbytes + job.flat_h.nbytes + job.off_h.nbytes + steps * B * d * 4
+    d2h = steps * B * 4 + 3 * B * 8 + B * 8  # ids + plan counters + status words
+    ok = np.array_equal(ids_h.numpy(), job.out.cpu().numpy())
+    return B * steps * K / sec, h2d, d2h, ok
+
+
+# --------------------------------------------------------------------------
+# the reference on the host cores
+# --------------------------------------------------------------------------
+class CpuRef:
+    """The reference (oracle/_ref: the unmodified reference TUs select /
+    gather / greedy_step, HeadMatrix::random for the weights) on the host
+    cores, requests batch-sharded over std::thread (each thread calls the
+    reference functions). Falls back to the C restatement (single thread,
+    kind "port") when oracle/_ref was not built."""
+
+    def __init__(self, cfg, B, rank=0):
+        from oracle import oracle as O
+        from paper_2508_15229_b200 import synth
+
+        self.cfg, self.B = cfg, B
+        V, d = cfg["V"], cfg["d"]
+        self.kind = "reference" if O.ref_available() else "port"
+        bf16 = cfg["dtype"] == "bf16"
+        t_ids = synth.static_ids(V, cfg["static"])
+        self.words = synth.words_of(t_ids, V)
+        self.prompts = [synth.prompt_ids(V, cfg["prompt_len"], rank * B + r) for r in range(B)]
+        self.off = np.zeros(B + 1, np.int64)
+        self.off[1:] = np.cumsum([len(p) for p in self.prompts])
+        self.flat = np.concatenate(self.prompts)
+        if self.kind == "reference":
+            self.R = O.ref_lib()
+            L = self.R.L
+            self.h = L.ref_head_new_random(V, d, synth.SEED_W, 4)
+            if bf16:
+                buf = np.empty(V * d, np.float32)
+                L.ref_head_copy_out(self.h, buf)
+                L.ref_head_assign(self.h, synth.round_bf16(buf))
+                del buf
+        else:
+            self.orc = O.c_oracle()
+            W = self.orc.head_random(V, d, synth.SEED_W)
+            self.W = synth.round_bf16(W) if bf16 else W
+        self.synth, self.bf16 = synth, bf16
+
+    def hidden(self, n_steps):
+        d, B = self.cfg["d"], self.B
+        hid = self.synth.head_random(n_steps * B, d, self.synth.SEED_H).reshape(n_steps, B, d)
+        return self.synth.round_bf16(hid) if self.bf16 else hid
+
+    def step(self, decode_sample, threads):
+        """select+gather for B requests, then `decode_sample` decode steps.
+        Returns (t_select_gather, mean t_decode_step, threads used)."""
+        V, d, B = self.cfg["V"], self.cfg["d"], self.B
+        hid = self.hidden(decode_sample)
+        dec = []
+        if self.kind == "reference":
+            L = self.R.L
+            bt = L.ref_batch_new()
+            t0 = time.perf_counter()
+            self.R._chk(L.ref_batch_prepare(bt, self.h, self.words, V, self.flat, self.off, B,
+                                            threads))
+            t_prep = time.perf_counter() - t0
+            ids = np.zeros(B, np.uint32)
+            for t in range(decode_sample):
+                h = np.ascontiguousarray(hid[t].reshape(-1))
+                t0 = time.perf_counter()
+                self.R._chk(L.ref_batch_greedy(bt, h, d, B, threads, ids))
+                dec.append(time.perf_counter() - t0)
+            L.ref_batch_free(bt)
+            return t_prep, sum(dec) / len(dec), threads
+        orc = self.orc
+        t0 = time.perf_counter()
+        plans = [orc.select(self.prompts[b], self.words, V, V).active_ids for b in range(B)]
+        subs = [orc.gather(self.W, p) for p in plans]
+        t_prep = time.perf_counter() - t0
+        for t in range(decode_sample):
+            t0 = time.perf_counter()
+            for b in range(B):
+                orc.greedy_step(subs[b], hid[t][b], plans[b])
+            dec.append(time.perf_counter() - t0)
+        return t_prep, sum(dec) / len(dec), 1
+
+    def close(self):
+        if self.kind == "reference":
+            self.R.L.ref_head_free(self.h)
+
+    def describe(self, value, used, decode_sample):
+        B = self.B
+        return {"value": value, "unit": UNIT, "cores": used, "kind": self.kind,
+                "sample": f"{self.cfg['workload']}: select+gather for {B} requests + "
+                          f"{decode_sample} of 64 decode steps ({B} request-tokens each) on "
+                          f"{used} host threads ({_cpu_model()}); tokens/s = {B}*64 / "
+                          f"(t_select_gather + 64 * mean t_decode_step)"}
+
+
+def cpu_reference(cfg, B, decode_sample, threads, rank=0):
+    ref = CpuRef(cfg, B, rank)
+    t_prep, t_dec, used = ref.step(decode_sample, threads)
+    ref.close()
+    v = B * 64 / (t_prep + 64 * t_dec)
+    return ref.describe(v, used, decode_sample)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    cfg = CFG2
+    ref = CpuRef(cfg, args.batch, 0)
+    sample = 2
+    vals, used = [], threads
+    for k in range(args.warmup + args.steps):
+        t_prep, t_dec, used = ref.step(sample, threads)
+        if k >= args.warmup:
+            vals.append(args.batch * 64 / (t_prep + 64 * t_dec))
+    ref.close()
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * args.batch * 64 / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (bf16-rounded values)",
+        "data": "synthetic (seeded splitmix64 streams, SURVEY §8d)",
+        "config": {"workload": cfg["workload"], "V": cfg["V"], "d": cfg["d"],
+                   "requests": args.batch, "prompt_len": cfg["prompt_len"],
+                   "static_vocab": cfg["static"], "decode_steps": 64},
+        "cpu_baseline": ref.describe(v, used, sample),
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    world, rank, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2508_15229_b200 import session as session_mod
+    from paper_2508_15229_b200 import synth
+    from paper_2508_15229_b200 import tailored_head as th
+
+    B, steps = args.batch, args.decode_steps
+    job = Job(CFG2, B, steps, rank, torch, th, synth)
+    ms, dec_ms, clocks = time_job(job, args.mode, args.steps, args.warmup, torch, dist, world)
+    tokens = B * steps * args.steps * world
+    value = tokens / (ms / 1000.0)
+    dec_bytes = job.decode_bytes()
+    dec_avg_ms = sum(dec_ms) / len(dec_ms)
+    peak, peak_kind = load_peaks()
+    achieved = dec_bytes / (dec_avg_ms / 1000.0) / 1e9
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": load_traffic(f"decode_{args.mode}_cfg2"),
+        "kernel": "gemv_ring_kernel<bf16,%s,argmax>" % (
+            "INTERLEAVED" if args.mode == "interleaved" else "ROWS"),
+        "bytes_per_launch": dec_bytes, "avg_launch_us": dec_avg_ms * 1000.0,
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "decode_share_of_step": sum(dec_ms) / ms if world == 1 else None,
+    }
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded splitmix64 streams, SURVEY §8d); random-init head",
+        "config": {"workload": CFG2["workload"], "V": CFG2["V"], "d": CFG2["d"],
+                   "requests_per_gpu": B, "prompt_len": CFG2["prompt_len"],
+                   "static_vocab": CFG2["static"], "decode_steps": steps,
+                   "step": "select + layout + gather + 64 fused greedy decode steps",
+                   "mode": args.mode, "parallelism": f"batch-shard x{world}",
+                   "l2": "decode working set > L2 (inputs larger than L2), no flush"},
+        "roofline": roofline,
+        "gpu_launches": job.launches_per_step(args.mode) * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_e2e:
+        e2e_v, h2d, d2h, ok = e2e_session(job, max(2, args.steps // 4), 1, th, torch, session_mod)
+        result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                         "d2h_bytes_per_step": d2h, "api": "svt_session_* (host buffers)",
+                         "ids_match_device_path": ok}
+    if rank == 0 and world == 1 and not args.no_secondary:
+        result["secondary"] = secondary(args, torch, th, synth)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_reference(CFG2, B, 2, os.cpu_count() or 1)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def secondary(args, torch, th, synth):
+    """cfg1 (Llama-3.2-1B shape, batch 1, fp32) and the fused variant of cfg2."""
+    out = {}
+    job = Job(CFG1, 1, 64, 0, torch, th, synth)
+    for mode in ("interleaved",):
+        ms, dec_ms, _ = time_job(job, mode, 10, 3, torch, None, 1)
+        dec_avg = sum(dec_ms) / len(dec_ms)
+        peak, _ = load_peaks()
+        gbs = job.decode_bytes() / (dec_avg / 1e3) / 1e9
+        out["cfg1_" + mode] = {"tokens_per_s": 64 * 10 / (ms / 1e3),
+                               "decode_us_per_token": dec_avg * 1e3,
+                               "decode_tokens_per_s": 1e3 / dec_avg,
+                               "decode_gbs": gbs, "frac": gbs / peak,
+                               "plan_rows": int(job.tb.n_active[0].item())}
+    del job
+    torch.cuda.empty_cache()
+    job = Job(CFG2, args.batch, args.decode_steps, 0, torch, th, synth)
+    ms, dec_ms, _ = time_job(job, "fused", 5, 2, torch, None, 1)
+    dec_avg = sum(dec_ms) / len(dec_ms)
+    peak, _ = load_peaks()
+    gbs = job.decode_bytes() / (dec_avg / 1e3) / 1e9
+    out["cfg2_fused"] = {"tokens_per_s": args.batch * args.decode_steps * 5 / (ms / 1e3),
+                         "decode_us": dec_avg * 1e3, "decode_gbs": gbs, "frac": gbs / peak}
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -466,17 +466,36 @@ class TailoredBatch:
 
     # ---- (b) interleaved gather ------------------------------------------
     def gather(self, head: HeadMatrix):
-        self.head = head
-        nbytes = _lib.lib.svt_subhead_bytes(head.storage, head.dim(), self.max_groups)
-        if self.sub is None or self.sub.numel() < nbytes:
-            self.sub = torch.empty(max(16, nbytes), dtype=torch.uint8, device="cuda")
-        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if self.head is not head or self.sub is None:
+            self.head = head
+            nbytes = _lib.lib.svt_subhead_bytes(head.storage, head.dim(), self.max_groups)
+            if self.sub is None or self.sub.numel() < nbytes:
+                self.sub = torch.empty(max(16, nbytes), dtype=torch.uint8, device="cuda")
+            # sticky error flag: set by the kernel when a plan id is >= rows
+            self.gather_bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+            self._fast = None
         call("svt_gather_interleaved", head.data.data_ptr(), head.storage, head.rows(),
              head.dim(), self.active.data_ptr(), self.act_off.data_ptr(),
              self.n_active.data_ptr(), self.group_begin.data_ptr(), self.group_req.data_ptr(),
-             self.B, self.max_groups, self.sub.data_ptr(), bad.data_ptr(), _stream(self.stream))
-        self._gather_bad = bad
+             self.B, self.max_groups, self.sub.data_ptr(), self.gather_bad.data_ptr(),
+             _stream(self.stream))
         return self
+
+    def _fast_args(self):
+        """Pointer tuples for the per-step decode call, resolved once so the
+        host side of a decode step is a single ctypes call."""
+        if getattr(self, "_fast", None) is None:
+            h = self.head
+            common = (self.group_begin.data_ptr(), self.group_req.data_ptr(),
+                      self.n_active.data_ptr(), self.active.data_ptr(), self.act_off.data_ptr(),
+                      self.B, self.max_groups)
+            self._fast = {
+                False: (_lib.lib.svt_greedy_interleaved,
+                        (self.sub.data_ptr(), h.storage, h.dim()) + common),
+                True: (_lib.lib.svt_greedy_fused,
+                       (h.data.data_ptr(), h.storage, h.rows(), h.dim()) + common),
+            }
+        return self._fast
 
     # ---- (c)+(d) fused greedy ----------------------------------------------
     def greedy(self, hidden: torch.Tensor, out_ids: torch.Tensor,
@@ -484,6 +503,13 @@ class TailoredBatch:
                out_keys: Optional[torch.Tensor] = None, row_base: int = 0,
                plan_start: int = 1) -> torch.Tensor:
         """hidden: [B, ld] float32 on the device (ld % 4 == 0, ld >= dim)."""
+        if out_max is None and out_keys is None and row_base == 0 and plan_start == 1 and (
+                fused or self.sub is not None):
+            fn, pre = self._fast_args()[bool(fused)]
+            st = fn(*pre, hidden.data_ptr(), hidden.stride(0), 0, 1, out_ids.data_ptr(), None,
+                    None, self.ws.data_ptr(), _stream(self.stream))
+            _lib.check(st, "greedy")
+            return out_ids
         head = self.head
         if fused:
             call("svt_greedy_fused", head.data.data_ptr(), head.storage, head.rows(), head.dim(),
