@@ -166,6 +166,28 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 
+// gpu-scope atomics with explicit ordering (no full MEMBAR.GPU round trip)
+__device__ __forceinline__ void atom_max_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "l"(p), "r"(v)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long atom_exch_relaxed_u64(unsigned long long* p,
+                                                                    unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.relaxed.gpu.global.exch.b64 %0, [%1], %2;"
+                 : "=l"(old)
+                 : "l"(p), "l"(v)
+                 : "memory");
+    return old;
+}
+
 __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

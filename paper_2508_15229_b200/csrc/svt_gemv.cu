@@ -18,14 +18,17 @@
 //       - ROWS source (fused gather from the full row-major head through the
 //         plan ids, or a plain row-major head): 32 row-slice copies, padded by
 //         16 B per row in shared memory so lane reads are conflict-free.
-//     The ring runs across group boundaries (no pipeline drain per group).
+//     The ring runs across group boundaries (no pipeline drain per group);
+//     all ring bookkeeping is incremental (no integer division in the loop).
 //   * compute: lane l reads chunk (c, l) with one LDS.128, widens it exactly
-//     to f32 and applies __fadd_rn(acc, __fmul_rn(w, h)) E times.
+//     to f32 and applies __fadd_rn(acc, __fmul_rn(w, h)) E times. Full stages
+//     take a branch-free, fully unrolled path; only a row's tail stage is
+//     guarded.
 //   * epilogue: either the logits are stored, or a (value, row) key is
 //     max-reduced across the warp and across the request's groups with a u64
-//     atomicMax; the last group of a request (completion counter) decodes the
-//     winner, remaps it through the plan ids (remap_out, selector.cpp:50-56)
-//     and resets the workspace.
+//     red.max; the last group of a request (acq_rel completion counter)
+//     decodes the winner, remaps it through the plan ids (remap_out,
+//     selector.cpp:50-56) and resets the workspace.
 // The grid is persistent: gridDim.x <= #SMs CTAs of `nwa` warps; warp w takes
 // groups w, w + TW, ... with w = warp * gridDim.x + block so that small
 // batches spread across SMs first.
@@ -58,13 +61,13 @@ __device__ __forceinline__ void group_epilogue(const GemvParams& p, int b, int64
             acc, p.row_base + static_cast<uint32_t>(row), valid, p.plan_start != 0 && row == 0);
         const unsigned long long kmax = warp_max_u64(key);
         if (lane == 0) {
-            if (kmax) atomicMax(&p.keys[b], kmax);
-            __threadfence();
+            if (kmax) atom_max_relaxed_u64(&p.keys[b], kmax);
             const unsigned int ngroups = static_cast<unsigned int>(p.ngroups(b));
-            const unsigned int prev = atomicAdd(&p.counters[b], 1u);
+            // release: our max is visible before the count; acquire (last
+            // arriver): every other group's max is visible to us
+            const unsigned int prev = atom_add_acq_rel_u32(&p.counters[b], 1u);
             if (prev == ngroups - 1u) {
-                __threadfence();
-                const unsigned long long k = atomicExch(&p.keys[b], 0ull);
+                const unsigned long long k = atom_exch_relaxed_u64(&p.keys[b], 0ull);
                 p.counters[b] = 0u;
                 uint32_t id = 0xFFFFFFFFu;
                 float mx = __int_as_float(0x7FC00000);
@@ -90,6 +93,28 @@ __device__ __forceinline__ bool row_valid(const GemvParams& p, int b, int64_t ro
     return true;
 }
 
+// one chunk-row: E exact-order multiply-adds
+template <int DT, int SRC>
+__device__ __forceinline__ void load_chunk(const uint8_t* wsl, const float* hsl, int cr, int lane,
+                                           float (&wv)[Chunk<DT>::E],
+                                           float (&hv)[Chunk<DT>::E]) {
+    constexpr int E = Chunk<DT>::E;
+    uint4 v;
+    if constexpr (SRC == SRC_INTERLEAVED)
+        v = reinterpret_cast<const uint4*>(wsl)[cr * kGroupRows + lane];
+    else
+        v = reinterpret_cast<const uint4*>(wsl)[lane * (kCR + 1) + cr];
+    Chunk<DT>::widen(v, wv);
+#pragma unroll
+    for (int e = 0; e < E; e += 4) {
+        const float4 h4 = *reinterpret_cast<const float4*>(hsl + cr * E + e);
+        hv[e] = h4.x;
+        hv[e + 1] = h4.y;
+        hv[e + 2] = h4.z;
+        hv[e + 3] = h4.w;
+    }
+}
+
 // ---- pipelined kernel -------------------------------------------------------
 template <int DT, int SRC, int MODE>
 __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
@@ -112,6 +137,7 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
     const int64_t w = static_cast<int64_t>(wid) * gridDim.x + blockIdx.x;
     const int64_t ng = total_groups > w ? (total_groups - w + TW - 1) / TW : 0;
     const int ns = (p.nchunks + kCR - 1) / kCR;
+    const int full_stages = p.dim / (kCR * E);  // stages with no element past dim
     const int64_t nq = ng * ns;
     if (nq == 0) return;
 
@@ -124,115 +150,112 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
     const uint64_t pol_w = policy_evict_first();
     const int dim4 = (p.dim + 3) & ~3;
 
-    // issue-side state (the producer runs S stages ahead of the consumer)
-    int64_t is_k = -1;
-    int is_b = 0;
-    const uint8_t* is_src = nullptr;  // ROWS: this lane's source row
-    unsigned is_mask = 0;
+    // ---- producer (issue) state: runs S stages ahead of the consumer ----
+    int64_t iq = 0, ik = 0, ig = w;
+    int is = 0, islot = 0, ib = 0;
+    const uint8_t* isrc = nullptr;  // ROWS: this lane's source row
+    unsigned imask = 0;
 
-    auto issue = [&](int64_t q) {
-        const int64_t k = q / ns;
-        const int s = static_cast<int>(q - k * ns);
-        const int64_t g = w + k * TW;
-        if (k != is_k) {
-            is_k = k;
-            is_b = p.req(g);
+    auto issue_next = [&]() {
+        if (is == 0) {  // entering a new group on the issue side
+            ib = p.req(ig);
             if constexpr (SRC == SRC_ROWS) {
-                const int64_t row = (g - p.gbegin(is_b)) * kGroupRows + lane;
-                const bool ok = row_valid<SRC>(p, is_b, row);
-                is_src = p.W + (ok ? p.src_row(is_b, row) : 0) * p.row_bytes;
-                is_mask = __ballot_sync(0xFFFFFFFFu, ok);
+                const int64_t row = (ig - p.gbegin(ib)) * kGroupRows + lane;
+                const bool ok = row_valid<SRC>(p, ib, row);
+                isrc = p.W + (ok ? p.src_row(ib, row) : 0) * p.row_bytes;
+                imask = __ballot_sync(0xFFFFFFFFu, ok);
             }
         }
-        const int slot = static_cast<int>(q % S);
-        uint8_t* wdst = ring + slot * kSlot;
+        uint8_t* wdst = ring + islot * kSlot;
         uint8_t* hdst = wdst + kSlotW;
-        const int c0 = s * kCR;
+        const int c0 = is * kCR;
         const int cc = min(kCR, p.nchunks - c0);
         const int e0 = c0 * E;
         const int hb = min(cc * E, dim4 - e0) * 4;
-        const float* hsrc = p.hidden + static_cast<int64_t>(is_b) * p.hidden_ld + e0;
+        const float* hsrc = p.hidden + static_cast<int64_t>(ib) * p.hidden_ld + e0;
         if constexpr (SRC == SRC_INTERLEAVED) {
             if (lane == 0) {
                 const uint32_t wb = static_cast<uint32_t>(cc) * kChunkRowBytes;
-                mbar_arrive_expect_tx(&bars[slot], wb + hb);
-                bulk_g2s(wdst, p.W + (g * p.nchunks + c0) * static_cast<int64_t>(kChunkRowBytes),
-                         wb, &bars[slot], pol_w);
-                bulk_g2s(hdst, hsrc, hb, &bars[slot], pol_w);
+                mbar_arrive_expect_tx(&bars[islot], wb + hb);
+                bulk_g2s(wdst, p.W + (ig * p.nchunks + c0) * static_cast<int64_t>(kChunkRowBytes),
+                         wb, &bars[islot], pol_w);
+                bulk_g2s(hdst, hsrc, hb, &bars[islot], pol_w);
             }
         } else {
             const uint32_t slice = static_cast<uint32_t>(cc) * kChunkBytes;
             if (lane == 0) {
-                mbar_arrive_expect_tx(&bars[slot], __popc(is_mask) * slice + hb);
-                bulk_g2s(hdst, hsrc, hb, &bars[slot], pol_w);
+                mbar_arrive_expect_tx(&bars[islot], __popc(imask) * slice + hb);
+                bulk_g2s(hdst, hsrc, hb, &bars[islot], pol_w);
             }
             __syncwarp();
-            if ((is_mask >> lane) & 1u)
-                bulk_g2s(wdst + lane * (kCR + 1) * kChunkBytes, is_src + c0 * kChunkBytes, slice,
-                         &bars[slot], pol_w);
+            if ((imask >> lane) & 1u)
+                bulk_g2s(wdst + lane * (kCR + 1) * kChunkBytes, isrc + c0 * kChunkBytes, slice,
+                         &bars[islot], pol_w);
         }
+        ++iq;
+        if (++is == ns) {
+            is = 0;
+            ++ik;
+            ig += TW;
+        }
+        if (++islot == S) islot = 0;
     };
 
-    const int64_t pre = nq < S ? nq : S;
-    for (int64_t q = 0; q < pre; ++q) issue(q);
+    while (iq < nq && iq < S) issue_next();
 
+    // ---- consumer state ----
+    int64_t g = w;
+    int s = 0, slot = 0;
+    uint32_t phase = 0;
     float acc = 0.0f;
     int b = 0;
     int64_t row = 0;
     bool valid = false;
     for (int64_t q = 0; q < nq; ++q) {
-        const int64_t k = q / ns;
-        const int s = static_cast<int>(q - k * ns);
         if (s == 0) {
-            const int64_t g = w + k * TW;
             acc = 0.0f;
             b = p.req(g);
             row = (g - p.gbegin(b)) * kGroupRows + lane;
             valid = row_valid<SRC>(p, b, row);
         }
-        const int slot = static_cast<int>(q % S);
-        mbar_wait_parity(&bars[slot], static_cast<uint32_t>((q / S) & 1));
+        mbar_wait_parity(&bars[slot], phase);
         const uint8_t* wsl = ring + slot * kSlot;
         const float* hsl = reinterpret_cast<const float*>(wsl + kSlotW);
-        const int c0 = s * kCR;
-        const int cc = min(kCR, p.nchunks - c0);
+        if (s < full_stages) {
+            // branch-free: kCR chunk-rows, all elements below dim
 #pragma unroll
-        for (int cr = 0; cr < kCR; ++cr) {
-            if (cr < cc) {
-                uint4 v;
-                if constexpr (SRC == SRC_INTERLEAVED)
-                    v = reinterpret_cast<const uint4*>(wsl)[cr * kGroupRows + lane];
-                else
-                    v = reinterpret_cast<const uint4*>(wsl)[lane * (kCR + 1) + cr];
-                float wv[E];
-                CK::widen(v, wv);
-                const float* h = hsl + cr * E;
-                float hv[E];
+            for (int cr = 0; cr < kCR; ++cr) {
+                float wv[E], hv[E];
+                load_chunk<DT, SRC>(wsl, hsl, cr, lane, wv, hv);
 #pragma unroll
-                for (int e = 0; e < E; e += 4) {
-                    const float4 h4 = *reinterpret_cast<const float4*>(h + e);
-                    hv[e] = h4.x;
-                    hv[e + 1] = h4.y;
-                    hv[e + 2] = h4.z;
-                    hv[e + 3] = h4.w;
-                }
+                for (int e = 0; e < E; ++e) acc = ref_mac(acc, wv[e], hv[e]);
+            }
+        } else {
+            const int c0 = s * kCR;
+            const int cc = min(kCR, p.nchunks - c0);
+            for (int cr = 0; cr < cc; ++cr) {
+                float wv[E], hv[E];
+                load_chunk<DT, SRC>(wsl, hsl, cr, lane, wv, hv);
                 const int ebase = (c0 + cr) * E;
-                if (ebase + E <= p.dim) {
 #pragma unroll
-                    for (int e = 0; e < E; ++e) acc = ref_mac(acc, wv[e], hv[e]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < E; ++e)
-                        if (ebase + e < p.dim) acc = ref_mac(acc, wv[e], hv[e]);
-                }
+                for (int e = 0; e < E; ++e)
+                    if (ebase + e < p.dim) acc = ref_mac(acc, wv[e], hv[e]);
             }
         }
         __syncwarp();
-        if (q + S < nq) {
+        if (iq < nq) {
             fence_proxy_async_smem();
-            issue(q + S);
+            issue_next();
         }
-        if (s == ns - 1) group_epilogue<MODE>(p, b, row, valid, acc, lane);
+        if (++slot == S) {
+            slot = 0;
+            phase ^= 1u;
+        }
+        if (++s == ns) {
+            group_epilogue<MODE>(p, b, row, valid, acc, lane);
+            s = 0;
+            g += TW;
+        }
     }
 }
 
@@ -266,6 +289,7 @@ __global__ void __launch_bounds__(128) gemv_generic_kernel(const GemvParams p) {
         group_epilogue<MODE>(p, b, row, valid, acc, lane);
     }
 }
+
 
 // ---- host-side launch ----------------------------------------------------
 namespace {
