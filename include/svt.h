@@ -117,12 +117,18 @@ svt_status svt_union_plans(const uint32_t* d_ids, const int64_t* d_offsets, int3
                            size_t full_vocab_size, uint64_t* d_words, uint32_t* d_out_ids,
                            int64_t* d_n_out, int32_t* d_bad, svt_stream stream);
 
-/* Row-group layout of a micro-batch of plans: group g covers rows
+/* Row-group layout of a micro-batch of plans: group g covers plan rows
  * [32k, 32k+32) of one request. d_group_begin[b] = first group of request b
  * (exclusive prefix sum of ceil(n_active/32)); d_group_begin[batch] = total.
- * d_group_req[g] = owning request of group g, for g < total <= max_groups. */
-svt_status svt_plan_layout(const int64_t* d_n_active, int32_t batch, int64_t* d_group_begin,
-                           int32_t* d_group_req, int64_t max_groups, svt_stream stream);
+ * d_group_meta: one SVT_GROUP_META_BYTES record per group (g < total <=
+ * max_groups): { int32 request, int32 valid rows (1..32), int32 groups of
+ * the request, int32 0, int64 plan row of lane 0, int64 index of that row's
+ * id in the plan-id array = d_id_offsets[request] + row }. d_id_offsets may
+ * be NULL (identity plans: the id index is the row itself). */
+#define SVT_GROUP_META_BYTES 32
+svt_status svt_plan_layout(const int64_t* d_n_active, const int64_t* d_id_offsets, int32_t batch,
+                           int64_t* d_group_begin, void* d_group_meta, int64_t max_groups,
+                           svt_stream stream);
 
 /* ------------------------------------------------------------------------
  * (b) LM-head row gather.
@@ -136,15 +142,14 @@ svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t rows, size_t
                            svt_stream stream);
 
 /* Gather into the lane-interleaved sub-head layout consumed by the decode
- * kernel: for group g, 16-byte chunk c, lane l (row 32k+l of the request):
+ * kernel: for group g, 16-byte chunk c, lane l (plan row row0(g)+l):
  *   d_sub + ((g * nchunks + c) * 32 + l) * 16,  nchunks = ceil(dim*esize/16),
- * rows past n_active and bytes past dim*esize are zero.
- * d_sub must hold svt_subhead_bytes(dt, dim, groups) bytes. */
+ * rows past the plan and bytes past dim*esize are zero. Group records come
+ * from svt_plan_layout. d_sub must hold svt_subhead_bytes(dt, dim, groups). */
 size_t svt_subhead_bytes(svt_dtype dt, size_t dim, int64_t groups);
 svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
-                                  const uint32_t* d_active_ids, const int64_t* d_active_offsets,
-                                  const int64_t* d_n_active, const int64_t* d_group_begin,
-                                  const int32_t* d_group_req, int32_t batch, int64_t max_groups,
+                                  const uint32_t* d_active_ids, const int64_t* d_group_begin,
+                                  const void* d_group_meta, int32_t batch, int64_t max_groups,
                                   void* d_sub, int32_t* d_bad, svt_stream stream);
 
 /* ------------------------------------------------------------------------
@@ -156,22 +161,22 @@ svt_status svt_logits(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
                       const float* d_hidden, float* d_out, svt_stream stream);
 
 /* Batched forms over a plan layout (svt_plan_layout): request b scores its
- * rows k < d_n_rows[b] against d_hidden + b*hidden_ld and writes
+ * plan rows against d_hidden + b*hidden_ld (f32, hidden_ld % 4 == 0 and
+ * hidden_ld >= dim for the bulk-copy path) and writes row k to
  * d_out[d_out_offsets[b] + k].
- *   _rows        : row k is head row d_ids[d_id_offsets[b] + k] (fused gather;
- *                  with d_ids == NULL, head row k).
- *   _interleaved : row k of request b's lane-interleaved sub-head. */
+ *   _rows        : plan row k is head row d_ids[idx(k)] (fused gather; with
+ *                  d_ids == NULL, head row k).
+ *   _interleaved : plan row k of request b's lane-interleaved sub-head. */
 svt_status svt_logits_rows(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
-                           const int64_t* d_group_begin, const int32_t* d_group_req,
-                           const int64_t* d_n_rows, const uint32_t* d_ids,
-                           const int64_t* d_id_offsets, int32_t batch, int64_t max_groups,
+                           const int64_t* d_group_begin, const void* d_group_meta,
+                           const uint32_t* d_ids, int32_t batch, int64_t max_groups,
                            const float* d_hidden, size_t hidden_ld, float* d_out,
                            const int64_t* d_out_offsets, svt_stream stream);
 svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
-                                  const int64_t* d_group_begin, const int32_t* d_group_req,
-                                  const int64_t* d_n_rows, int32_t batch, int64_t max_groups,
-                                  const float* d_hidden, size_t hidden_ld, float* d_out,
-                                  const int64_t* d_out_offsets, svt_stream stream);
+                                  const int64_t* d_group_begin, const void* d_group_meta,
+                                  int32_t batch, int64_t max_groups, const float* d_hidden,
+                                  size_t hidden_ld, float* d_out, const int64_t* d_out_offsets,
+                                  svt_stream stream);
 
 /* Single-plan greedy over a row-major sub-head (the exact greedy_step
  * signature shape: sub-head rows are the plan's rows in order, d_plan_ids
@@ -196,7 +201,10 @@ void svt_set_tuning(int warps, int stages);
  *   svt_greedy_interleaved — sub-heads produced by svt_gather_interleaved.
  *   svt_greedy_fused       — no materialised sub-head: rows are streamed
  *                            from the full row-major head through the plan
- *                            ids (gather fused into the GEMV).
+ *                            ids (gather fused into the GEMV); d_active_ids
+ *                            == NULL streams head rows 0..n-1 (identity plan).
+ * d_active_ids (the plan ids, indexed through the group records) remap the
+ *   winner; NULL returns row_base + winning row.
  * d_hidden: request b's hidden state at d_hidden + b*hidden_ld (f32; hidden_ld
  *   % 4 == 0 and hidden_ld >= dim). Outputs per request: d_out_ids[b] (global
  *   id), d_out_max[b] (the winning logit, optional), d_out_keys[b] (optional
@@ -205,22 +213,21 @@ void svt_set_tuning(int warps, int stages);
  *   plan); pass 0 / 1 for a whole plan.
  * d_workspace: svt_greedy_workspace_bytes(batch) bytes, zeroed ONCE by the
  *   caller; every launch leaves it zeroed again (graph-replayable).
- * Requests with n_active == 0 are skipped (the reference throws
- *   IntegrityError "greedy step over an empty sub-head", head.cpp:205-206).
+ * Requests with an empty plan have no group and are left untouched (the
+ *   reference throws IntegrityError "greedy step over an empty sub-head",
+ *   head.cpp:205-206; the host-buffer APIs raise it).
  * ---------------------------------------------------------------------- */
 size_t svt_greedy_workspace_bytes(int32_t batch);
 svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
-                                  const int64_t* d_group_begin, const int32_t* d_group_req,
-                                  const int64_t* d_n_active, const uint32_t* d_active_ids,
-                                  const int64_t* d_active_offsets, int32_t batch,
+                                  const int64_t* d_group_begin, const void* d_group_meta,
+                                  const uint32_t* d_active_ids, int32_t batch,
                                   int64_t max_groups, const float* d_hidden, size_t hidden_ld,
                                   uint32_t row_base, int32_t plan_start, uint32_t* d_out_ids,
                                   float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
                                   svt_stream stream);
 svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
-                            const int64_t* d_group_begin, const int32_t* d_group_req,
-                            const int64_t* d_n_active, const uint32_t* d_active_ids,
-                            const int64_t* d_active_offsets, int32_t batch, int64_t max_groups,
+                            const int64_t* d_group_begin, const void* d_group_meta,
+                            const uint32_t* d_active_ids, int32_t batch, int64_t max_groups,
                             const float* d_hidden, size_t hidden_ld, uint32_t row_base,
                             int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
                             uint64_t* d_out_keys, void* d_workspace, svt_stream stream);

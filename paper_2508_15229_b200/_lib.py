@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(LIB_DIR, "libsvt.so")
 
 SVT_F32, SVT_F16, SVT_BF16 = 0, 1, 2
 GROUP_ROWS = 32
+GROUP_META_BYTES = 32
 
 
 class Error(RuntimeError):
@@ -60,22 +61,22 @@ _SIGS = {
                            C.c_int),
     "svt_bitset_insert": ([_vp, _sz, _sz, _vp, _vp, _vp], C.c_int),
     "svt_union_plans": ([_vp, _vp, _i32, _sz, _vp, _vp, _vp, _vp, _vp], C.c_int),
-    "svt_plan_layout": ([_vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
+    "svt_plan_layout": ([_vp, _vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
     "svt_gather_rows": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_subhead_bytes": ([C.c_int, _sz, _i64], _sz),
-    "svt_gather_interleaved": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp,
-                                _vp, _vp], C.c_int),
+    "svt_gather_interleaved": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp],
+                               C.c_int),
     "svt_logits": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp], C.c_int),
-    "svt_logits_rows": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _sz,
-                         _vp, _vp, _vp], C.c_int),
-    "svt_logits_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp,
-                                _vp], C.c_int),
+    "svt_logits_rows": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp,
+                         _vp], C.c_int),
+    "svt_logits_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp, _vp],
+                               C.c_int),
     "svt_greedy_step": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_greedy_workspace_bytes": ([_i32], _sz),
-    "svt_greedy_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _sz,
-                                _u32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
-    "svt_greedy_fused": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _sz,
-                          _u32, _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_greedy_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,
+                                _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_greedy_fused": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,
+                          _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_shard_combine": ([_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),

@@ -119,9 +119,8 @@ svt_status svt_logits(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
 }
 
 svt_status svt_logits_rows(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
-                           const int64_t* d_group_begin, const int32_t* d_group_req,
-                           const int64_t* d_n_rows, const uint32_t* d_ids,
-                           const int64_t* d_id_offsets, int32_t batch, int64_t max_groups,
+                           const int64_t* d_group_begin, const void* d_group_meta,
+                           const uint32_t* d_ids, int32_t batch, int64_t max_groups,
                            const float* d_hidden, size_t hidden_ld, float* d_out,
                            const int64_t* d_out_offsets, svt_stream stream) {
     if (svt_status s = check_dtype(dt)) return s;
@@ -129,10 +128,8 @@ svt_status svt_logits_rows(const void* d_head, svt_dtype dt, size_t rows, size_t
     if (batch <= 0) return SVT_OK;
     GemvParams p = base_params(d_head, dt, rows, dim);
     p.group_begin = d_group_begin;
-    p.group_req = d_group_req;
-    p.n_rows = d_n_rows;
+    p.meta = static_cast<const GroupMeta*>(d_group_meta);
     p.src_ids = d_ids;
-    p.id_off = d_id_offsets;
     p.B = batch;
     p.max_groups = max_groups;
     p.hidden = d_hidden;
@@ -143,17 +140,16 @@ svt_status svt_logits_rows(const void* d_head, svt_dtype dt, size_t rows, size_t
 }
 
 svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
-                                  const int64_t* d_group_begin, const int32_t* d_group_req,
-                                  const int64_t* d_n_rows, int32_t batch, int64_t max_groups,
-                                  const float* d_hidden, size_t hidden_ld, float* d_out,
-                                  const int64_t* d_out_offsets, svt_stream stream) {
+                                  const int64_t* d_group_begin, const void* d_group_meta,
+                                  int32_t batch, int64_t max_groups, const float* d_hidden,
+                                  size_t hidden_ld, float* d_out, const int64_t* d_out_offsets,
+                                  svt_stream stream) {
     if (svt_status s = check_dtype(dt)) return s;
     if (svt_status s = need_device()) return s;
     if (batch <= 0) return SVT_OK;
     GemvParams p = base_params(d_sub, dt, 0, dim);
     p.group_begin = d_group_begin;
-    p.group_req = d_group_req;
-    p.n_rows = d_n_rows;
+    p.meta = static_cast<const GroupMeta*>(d_group_meta);
     p.B = batch;
     p.max_groups = max_groups;
     p.hidden = d_hidden;
@@ -164,11 +160,10 @@ svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
 }
 
 static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t rows, size_t dim,
-                                const int64_t* gb, const int32_t* gr, const int64_t* n_active,
-                                const uint32_t* ids, const int64_t* id_off, int32_t batch,
-                                int64_t max_groups, const float* hidden, size_t ld,
-                                uint32_t row_base, int32_t plan_start, uint32_t* out_ids,
-                                float* out_max, uint64_t* out_keys, void* ws,
+                                const int64_t* gb, const void* meta, const uint32_t* ids,
+                                int32_t batch, int64_t max_groups, const float* hidden,
+                                size_t ld, uint32_t row_base, int32_t plan_start,
+                                uint32_t* out_ids, float* out_max, uint64_t* out_keys, void* ws,
                                 svt_stream stream) {
     if (svt_status s = check_dtype(dt)) return s;
     if (svt_status s = need_device()) return s;
@@ -179,11 +174,9 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
     }
     GemvParams p = base_params(W, dt, rows, dim);
     p.group_begin = gb;
-    p.group_req = gr;
-    p.n_rows = n_active;
+    p.meta = static_cast<const GroupMeta*>(meta);
     p.src_ids = src == SRC_ROWS ? ids : nullptr;
     p.ids = ids;
-    p.id_off = id_off;
     p.B = batch;
     p.max_groups = max_groups;
     p.hidden = hidden;
@@ -201,30 +194,26 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
 }
 
 svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
-                                  const int64_t* d_group_begin, const int32_t* d_group_req,
-                                  const int64_t* d_n_active, const uint32_t* d_active_ids,
-                                  const int64_t* d_active_offsets, int32_t batch,
+                                  const int64_t* d_group_begin, const void* d_group_meta,
+                                  const uint32_t* d_active_ids, int32_t batch,
                                   int64_t max_groups, const float* d_hidden, size_t hidden_ld,
                                   uint32_t row_base, int32_t plan_start, uint32_t* d_out_ids,
                                   float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
                                   svt_stream stream) {
-    return greedy_common(SRC_INTERLEAVED, d_sub, dt, 0, dim, d_group_begin, d_group_req,
-                         d_n_active, d_active_ids, d_active_offsets, batch, max_groups, d_hidden,
-                         hidden_ld, row_base, plan_start, d_out_ids, d_out_max, d_out_keys,
-                         d_workspace, stream);
+    return greedy_common(SRC_INTERLEAVED, d_sub, dt, 0, dim, d_group_begin, d_group_meta,
+                         d_active_ids, batch, max_groups, d_hidden, hidden_ld, row_base,
+                         plan_start, d_out_ids, d_out_max, d_out_keys, d_workspace, stream);
 }
 
 svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
-                            const int64_t* d_group_begin, const int32_t* d_group_req,
-                            const int64_t* d_n_active, const uint32_t* d_active_ids,
-                            const int64_t* d_active_offsets, int32_t batch, int64_t max_groups,
+                            const int64_t* d_group_begin, const void* d_group_meta,
+                            const uint32_t* d_active_ids, int32_t batch, int64_t max_groups,
                             const float* d_hidden, size_t hidden_ld, uint32_t row_base,
                             int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
                             uint64_t* d_out_keys, void* d_workspace, svt_stream stream) {
-    return greedy_common(SRC_ROWS, d_head, dt, rows, dim, d_group_begin, d_group_req, d_n_active,
-                         d_active_ids, d_active_offsets, batch, max_groups, d_hidden, hidden_ld,
-                         row_base, plan_start, d_out_ids, d_out_max, d_out_keys, d_workspace,
-                         stream);
+    return greedy_common(SRC_ROWS, d_head, dt, rows, dim, d_group_begin, d_group_meta,
+                         d_active_ids, batch, max_groups, d_hidden, hidden_ld, row_base,
+                         plan_start, d_out_ids, d_out_max, d_out_keys, d_workspace, stream);
 }
 
 svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, size_t dim,

@@ -10,7 +10,7 @@
 //    and writes it back chunk-major so that the decode kernel's bulk copies
 //    and lane reads are contiguous. Both directions are fully coalesced;
 //    HBM traffic = 2 * |S| * d * b (read + write).
-#include "svt_common.cuh"
+#include "svt_gemv.cuh"
 
 namespace svt {
 namespace {
@@ -61,10 +61,8 @@ template <bool VEC>
 __global__ void __launch_bounds__(kGatherWarps * 32)
 gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_t row_bytes,
                           int32_t nchunks, const uint32_t* __restrict__ active_ids,
-                          const int64_t* __restrict__ active_off,
-                          const int64_t* __restrict__ n_active,
                           const int64_t* __restrict__ group_begin,
-                          const int32_t* __restrict__ group_req, int32_t B, int64_t max_groups,
+                          const GroupMeta* __restrict__ meta, int32_t B, int64_t max_groups,
                           uint4* __restrict__ out, int32_t* bad) {
     extern __shared__ __align__(16) uint4 tiles[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -76,14 +74,12 @@ gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_
          wg += nwarps) {
         const int64_t g = wg / nblk;
         const int cb = static_cast<int>(wg - g * nblk);
-        const int b = group_req[g];
-        const int64_t row0 = (g - group_begin[b]) * kGroupRows;
-        const int64_t n = n_active[b];
+        const GroupMeta m = meta[g];
         // lane r fetches the plan id of row r; broadcast per row below
-        int64_t my_row = row0 + lane;
-        uint32_t my_id = my_row < n ? active_ids[active_off[b] + my_row] : 0xFFFFFFFFu;
-        const bool my_ok = my_row < n && static_cast<int64_t>(my_id) < rows;
-        if (my_row < n && !my_ok && bad) *bad = 1;
+        const bool in_plan = lane < m.nvalid;
+        const uint32_t my_id = in_plan ? active_ids[m.idbase + lane] : 0xFFFFFFFFu;
+        const bool my_ok = in_plan && static_cast<int64_t>(my_id) < rows;
+        if (in_plan && !my_ok && bad) *bad = 1;
         const unsigned ok_mask = __ballot_sync(0xFFFFFFFFu, my_ok);
         const int64_t c = static_cast<int64_t>(cb) * 32 + lane;
 #pragma unroll 8
@@ -141,10 +137,8 @@ extern "C" svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t r
 
 extern "C" svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, size_t rows,
                                              size_t dim, const uint32_t* d_active_ids,
-                                             const int64_t* d_active_offsets,
-                                             const int64_t* d_n_active,
                                              const int64_t* d_group_begin,
-                                             const int32_t* d_group_req, int32_t batch,
+                                             const void* d_group_meta, int32_t batch,
                                              int64_t max_groups, void* d_sub, int32_t* d_bad,
                                              svt_stream stream) {
     using namespace svt;
@@ -166,14 +160,14 @@ extern "C" svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, s
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         gather_interleaved_kernel<true><<<grid, kGatherWarps * 32, smem, st>>>(
             static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
-            d_active_ids, d_active_offsets, d_n_active, d_group_begin, d_group_req, batch,
+            d_active_ids, d_group_begin, static_cast<const GroupMeta*>(d_group_meta), batch,
             max_groups, static_cast<uint4*>(d_sub), d_bad);
     } else {
         SVT_CUDA_TRY(cudaFuncSetAttribute(gather_interleaved_kernel<false>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         gather_interleaved_kernel<false><<<grid, kGatherWarps * 32, smem, st>>>(
             static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
-            d_active_ids, d_active_offsets, d_n_active, d_group_begin, d_group_req, batch,
+            d_active_ids, d_group_begin, static_cast<const GroupMeta*>(d_group_meta), batch,
             max_groups, static_cast<uint4*>(d_sub), d_bad);
     }
     SVT_LAUNCH_CHECK("gather_interleaved_kernel");

@@ -19,11 +19,13 @@
 //         plan ids, or a plain row-major head): 32 row-slice copies, padded by
 //         16 B per row in shared memory so lane reads are conflict-free.
 //     The ring runs across group boundaries (no pipeline drain per group);
-//     all ring bookkeeping is incremental (no integer division in the loop).
+//     all ring bookkeeping is incremental, and each group's metadata (one
+//     32-byte GroupMeta record) is prefetched a group ahead on both the
+//     producer and the consumer side.
 //   * compute: lane l reads chunk (c, l) with one LDS.128, widens it exactly
 //     to f32 and applies __fadd_rn(acc, __fmul_rn(w, h)) E times. Full stages
-//     take a branch-free, fully unrolled path; only a row's tail stage is
-//     guarded.
+//     take a branch-free, fully unrolled path with products formed a chunk
+//     ahead of the serial FADD chain; only a row's tail stage is guarded.
 //   * epilogue: either the logits are stored, or a (value, row) key is
 //     max-reduced across the warp and across the request's groups with a u64
 //     red.max; the last group of a request (acq_rel completion counter)
@@ -52,48 +54,53 @@ __host__ __device__ constexpr int slot_bytes(int E) {
 
 // ---- shared epilogue ------------------------------------------------------
 template <int MODE>
-__device__ __forceinline__ void group_epilogue(const GemvParams& p, int b, int64_t row,
-                                               bool valid, float acc, int lane) {
+__device__ __forceinline__ void group_epilogue(const GemvParams& p, const GroupMeta& m,
+                                               int64_t lbase, bool valid, float acc, int lane) {
+    const int64_t row = m.row0 + lane;
     if constexpr (MODE == MODE_LOGITS) {
-        if (valid) p.logits[p.loff(b) + row] = acc;
+        if (valid) p.logits[lbase + row] = acc;
     } else {
         const unsigned long long key = make_key(
             acc, p.row_base + static_cast<uint32_t>(row), valid, p.plan_start != 0 && row == 0);
         const unsigned long long kmax = warp_max_u64(key);
         if (lane == 0) {
-            if (kmax) atom_max_relaxed_u64(&p.keys[b], kmax);
-            const unsigned int ngroups = static_cast<unsigned int>(p.ngroups(b));
+            if (kmax) atom_max_relaxed_u64(&p.keys[m.b], kmax);
             // release: our max is visible before the count; acquire (last
             // arriver): every other group's max is visible to us
-            const unsigned int prev = atom_add_acq_rel_u32(&p.counters[b], 1u);
-            if (prev == ngroups - 1u) {
-                const unsigned long long k = atom_exch_relaxed_u64(&p.keys[b], 0ull);
-                p.counters[b] = 0u;
+            const unsigned int prev = atom_add_acq_rel_u32(&p.counters[m.b], 1u);
+            if (prev == static_cast<unsigned int>(m.ngroups) - 1u) {
+                const unsigned long long k = atom_exch_relaxed_u64(&p.keys[m.b], 0ull);
+                p.counters[m.b] = 0u;
                 uint32_t id = 0xFFFFFFFFu;
                 float mx = __int_as_float(0x7FC00000);
                 if (k) {
                     const uint32_t hi = static_cast<uint32_t>(k >> 32);
                     const uint32_t grow = 0xFFFFFFFFu - static_cast<uint32_t>(k);
-                    const uint32_t local = grow - p.row_base;
-                    id = p.ids ? p.ids[p.idoff(b) + local] : grow;
+                    const int64_t local = static_cast<int64_t>(grow - p.row_base);
+                    id = p.ids ? p.ids[m.idbase - m.row0 + local] : grow;
                     mx = hi == 0xFFFFFFFFu ? __int_as_float(0x7FC00000) : float_of_ord(hi);
                 }
-                p.out_ids[b] = id;
-                if (p.out_max) p.out_max[b] = mx;
-                if (p.out_keys) p.out_keys[b] = k;
+                p.out_ids[m.b] = id;
+                if (p.out_max) p.out_max[m.b] = mx;
+                if (p.out_keys) p.out_keys[m.b] = k;
             }
         }
     }
 }
 
 template <int SRC>
-__device__ __forceinline__ bool row_valid(const GemvParams& p, int b, int64_t row) {
-    if (row >= p.nrows(b)) return false;
-    if constexpr (SRC == SRC_ROWS) return p.src_row(b, row) < p.head_rows;
+__device__ __forceinline__ bool lane_valid(const GemvParams& p, const GroupMeta& m, int lane,
+                                           int64_t* srow) {
+    if (lane >= m.nvalid) return false;
+    if constexpr (SRC == SRC_ROWS) {
+        const int64_t r = p.src_ids ? static_cast<int64_t>(p.src_ids[m.idbase + lane])
+                                    : m.row0 + lane;
+        *srow = r;
+        return r < p.head_rows;
+    }
     return true;
 }
 
-// one chunk-row: E exact-order multiply-adds
 template <int DT, int SRC>
 __device__ __forceinline__ void load_chunk(const uint8_t* wsl, const float* hsl, int cr, int lane,
                                            float (&wv)[Chunk<DT>::E],
@@ -149,22 +156,22 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
 
     const uint64_t pol_w = policy_evict_first();
     const int dim4 = (p.dim + 3) & ~3;
+    const GroupMeta dummy{};
 
     // ---- producer (issue) state: runs S stages ahead of the consumer ----
-    int64_t iq = 0, ik = 0, ig = w;
-    int is = 0, islot = 0, ib = 0;
+    int64_t iq = 0, ig = w;
+    int is = 0, islot = 0;
+    GroupMeta im = p.group(w);
+    GroupMeta im_next = (w + TW < total_groups) ? p.group(w + TW) : dummy;
     const uint8_t* isrc = nullptr;  // ROWS: this lane's source row
     unsigned imask = 0;
 
     auto issue_next = [&]() {
-        if (is == 0) {  // entering a new group on the issue side
-            ib = p.req(ig);
-            if constexpr (SRC == SRC_ROWS) {
-                const int64_t row = (ig - p.gbegin(ib)) * kGroupRows + lane;
-                const bool ok = row_valid<SRC>(p, ib, row);
-                isrc = p.W + (ok ? p.src_row(ib, row) : 0) * p.row_bytes;
-                imask = __ballot_sync(0xFFFFFFFFu, ok);
-            }
+        if (is == 0 && SRC == SRC_ROWS) {  // entering a new group on the issue side
+            int64_t srow = 0;
+            const bool ok = lane_valid<SRC>(p, im, lane, &srow);
+            isrc = p.W + (ok ? srow : 0) * p.row_bytes;
+            imask = __ballot_sync(0xFFFFFFFFu, ok);
         }
         uint8_t* wdst = ring + islot * kSlot;
         uint8_t* hdst = wdst + kSlotW;
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
         const int cc = min(kCR, p.nchunks - c0);
         const int e0 = c0 * E;
         const int hb = min(cc * E, dim4 - e0) * 4;
-        const float* hsrc = p.hidden + static_cast<int64_t>(ib) * p.hidden_ld + e0;
+        const float* hsrc = p.hidden + static_cast<int64_t>(im.b) * p.hidden_ld + e0;
         if constexpr (SRC == SRC_INTERLEAVED) {
             if (lane == 0) {
                 const uint32_t wb = static_cast<uint32_t>(cc) * kChunkRowBytes;
@@ -195,8 +202,9 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
         ++iq;
         if (++is == ns) {
             is = 0;
-            ++ik;
             ig += TW;
+            im = im_next;
+            if (ig + TW < total_groups) im_next = p.group(ig + TW);
         }
         if (++islot == S) islot = 0;
     };
@@ -208,27 +216,47 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
     int s = 0, slot = 0;
     uint32_t phase = 0;
     float acc = 0.0f;
-    int b = 0;
-    int64_t row = 0;
+    GroupMeta cm = p.group(w);
+    GroupMeta cm_next = (w + TW < total_groups) ? p.group(w + TW) : dummy;
     bool valid = false;
+    int64_t lbase = 0;
     for (int64_t q = 0; q < nq; ++q) {
         if (s == 0) {
             acc = 0.0f;
-            b = p.req(g);
-            row = (g - p.gbegin(b)) * kGroupRows + lane;
-            valid = row_valid<SRC>(p, b, row);
+            int64_t srow = 0;
+            valid = lane_valid<SRC>(p, cm, lane, &srow);
+            if constexpr (MODE == MODE_LOGITS) lbase = p.loff(cm.b);
         }
         mbar_wait_parity(&bars[slot], phase);
         const uint8_t* wsl = ring + slot * kSlot;
         const float* hsl = reinterpret_cast<const float*>(wsl + kSlotW);
         if (s < full_stages) {
-            // branch-free: kCR chunk-rows, all elements below dim
+            // branch-free: kCR chunk-rows, all elements below dim. Products
+            // are formed one chunk ahead of the dependent FADD chain (the
+            // only serial part: acc = acc + p, 4-cycle latency), so the
+            // LDS + widen + FMUL of chunk cr+1 fill the chain's latency.
+            float pr[E];
+            {
+                float wv[E], hv[E];
+                load_chunk<DT, SRC>(wsl, hsl, 0, lane, wv, hv);
+#pragma unroll
+                for (int e = 0; e < E; ++e) pr[e] = __fmul_rn(wv[e], hv[e]);
+            }
 #pragma unroll
             for (int cr = 0; cr < kCR; ++cr) {
-                float wv[E], hv[E];
-                load_chunk<DT, SRC>(wsl, hsl, cr, lane, wv, hv);
+                float pn[E];
+                if (cr + 1 < kCR) {
+                    float wv[E], hv[E];
+                    load_chunk<DT, SRC>(wsl, hsl, cr + 1, lane, wv, hv);
 #pragma unroll
-                for (int e = 0; e < E; ++e) acc = ref_mac(acc, wv[e], hv[e]);
+                    for (int e = 0; e < E; ++e) pn[e] = __fmul_rn(wv[e], hv[e]);
+                }
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc = __fadd_rn(acc, pr[e]);
+                if (cr + 1 < kCR) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) pr[e] = pn[e];
+                }
             }
         } else {
             const int c0 = s * kCR;
@@ -242,19 +270,22 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
                     if (ebase + e < p.dim) acc = ref_mac(acc, wv[e], hv[e]);
             }
         }
+        // WAR on the slot: every lane's LDS results have been consumed by the
+        // FADD chain above, so after the warp barrier the bulk engine may
+        // overwrite it (the same-warp analogue of an empty-barrier release;
+        // no cross-proxy fence — that costs a MEMBAR.CTA per stage).
         __syncwarp();
-        if (iq < nq) {
-            fence_proxy_async_smem();
-            issue_next();
-        }
+        if (iq < nq) issue_next();
         if (++slot == S) {
             slot = 0;
             phase ^= 1u;
         }
         if (++s == ns) {
-            group_epilogue<MODE>(p, b, row, valid, acc, lane);
+            group_epilogue<MODE>(p, cm, lbase, valid, acc, lane);
             s = 0;
             g += TW;
+            cm = cm_next;
+            if (g + TW < total_groups) cm_next = p.group(g + TW);
         }
     }
 }
@@ -268,10 +299,10 @@ __global__ void __launch_bounds__(128) gemv_generic_kernel(const GemvParams p) {
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
          g < total_groups; g += nwarps) {
-        const int b = p.req(g);
-        const int64_t row = (g - p.gbegin(b)) * kGroupRows + lane;
-        const bool valid = row_valid<SRC>(p, b, row);
-        const float* h = p.hidden + static_cast<int64_t>(b) * p.hidden_ld;
+        const GroupMeta m = p.group(g);
+        int64_t srow = 0;
+        const bool valid = lane_valid<SRC>(p, m, lane, &srow);
+        const float* h = p.hidden + static_cast<int64_t>(m.b) * p.hidden_ld;
         float acc = 0.0f;
         if constexpr (SRC == SRC_INTERLEAVED) {
             const uint4* base = reinterpret_cast<const uint4*>(p.W) + g * p.nchunks * kGroupRows;
@@ -283,13 +314,12 @@ __global__ void __launch_bounds__(128) gemv_generic_kernel(const GemvParams p) {
                     if (c * E + e < p.dim) acc = ref_mac(acc, wv[e], h[c * E + e]);
             }
         } else if (valid) {
-            const uint8_t* rp = p.W + p.src_row(b, row) * p.row_bytes;
+            const uint8_t* rp = p.W + srow * p.row_bytes;
             for (int c = 0; c < p.dim; ++c) acc = ref_mac(acc, load_elem<DT>(rp, c), h[c]);
         }
-        group_epilogue<MODE>(p, b, row, valid, acc, lane);
+        group_epilogue<MODE>(p, m, MODE == MODE_LOGITS ? p.loff(m.b) : 0, valid, acc, lane);
     }
 }
-
 
 // ---- host-side launch ----------------------------------------------------
 namespace {

@@ -9,6 +9,19 @@ namespace svt {
 enum { SRC_INTERLEAVED = 0, SRC_ROWS = 1 };
 enum { MODE_LOGITS = 0, MODE_ARGMAX = 1 };
 
+// One record per 32-row group, written by svt_plan_layout: everything a warp
+// needs to start a group in one (prefetchable) 32-byte load instead of a
+// chain of dependent lookups.
+struct alignas(16) GroupMeta {
+    int32_t b;        // owning request
+    int32_t nvalid;   // rows of this group inside the plan (1..32)
+    int32_t ngroups;  // groups of request b (completion-counter target)
+    int32_t pad;
+    int64_t row0;     // plan-local row of lane 0
+    int64_t idbase;   // index of row0's id in the plan-id array
+};
+static_assert(sizeof(GroupMeta) == SVT_GROUP_META_BYTES, "GroupMeta layout");
+
 struct GemvParams {
     const uint8_t* W;
     int64_t row_bytes;  // row-major source stride (dim * esize)
@@ -16,13 +29,11 @@ struct GemvParams {
     int32_t nchunks;    // 16-byte chunks per row
     int32_t dim;
     const int64_t* group_begin;  // nullptr: single request of `single_rows` rows
-    const int32_t* group_req;
+    const GroupMeta* meta;
     int64_t max_groups;
     int32_t B;
-    const int64_t* n_rows;
-    const uint32_t* src_ids;  // ROWS source: row k of request b is head row src_ids[idoff(b)+k]
-    const uint32_t* ids;      // argmax remap: winner local row k -> ids[idoff(b)+k]
-    const int64_t* id_off;
+    const uint32_t* src_ids;  // ROWS source: row k of the group is head row src_ids[idbase+k]
+    const uint32_t* ids;      // argmax remap: winner plan row r -> ids[idbase - row0 + r]
     const float* hidden;
     int64_t hidden_ld;
     float* logits;
@@ -41,23 +52,20 @@ struct GemvParams {
         return group_begin ? min(group_begin[B], max_groups)
                            : (single_rows + kGroupRows - 1) / kGroupRows;
     }
-    __device__ __forceinline__ int req(int64_t g) const { return group_req ? group_req[g] : 0; }
-    __device__ __forceinline__ int64_t gbegin(int b) const {
-        return group_begin ? group_begin[b] : 0;
+    __device__ __forceinline__ GroupMeta group(int64_t g) const {
+        if (meta) return meta[g];
+        GroupMeta m;
+        m.b = 0;
+        m.row0 = g * kGroupRows;
+        const int64_t left = single_rows - m.row0;
+        m.nvalid = static_cast<int32_t>(left < kGroupRows ? left : kGroupRows);
+        m.ngroups = static_cast<int32_t>((single_rows + kGroupRows - 1) / kGroupRows);
+        m.pad = 0;
+        m.idbase = m.row0;
+        return m;
     }
-    __device__ __forceinline__ int64_t ngroups(int b) const {
-        return group_begin ? group_begin[b + 1] - group_begin[b] : total();
-    }
-    __device__ __forceinline__ int64_t nrows(int b) const {
-        return n_rows ? n_rows[b] : single_rows;
-    }
-    __device__ __forceinline__ int64_t idoff(int b) const { return id_off ? id_off[b] : 0; }
     __device__ __forceinline__ int64_t loff(int b) const {
         return logits_off ? logits_off[b] : 0;
-    }
-    // head row backing local row `row` of request b (ROWS source)
-    __device__ __forceinline__ int64_t src_row(int b, int64_t row) const {
-        return src_ids ? static_cast<int64_t>(src_ids[idoff(b) + row]) : row;
     }
 };
 

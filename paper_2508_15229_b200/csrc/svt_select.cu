@@ -14,7 +14,7 @@
 //      (TokenSet::to_ids, token_set.cpp:46-51).
 // An id >= V leaves the plan empty and reports the FIRST offending position
 // (the reference throws on the first one in input order, selector.cpp:27-30).
-#include "svt_common.cuh"
+#include "svt_gemv.cuh"
 
 namespace svt {
 namespace {
@@ -209,10 +209,11 @@ bitmap_compact_kernel(const unsigned long long* __restrict__ words, int64_t nw,
     if (threadIdx.x == 0) *n_out = s_total;
 }
 
-// exclusive scan of ceil(n_active/32) -> group_begin, then group -> request map
+// exclusive scan of ceil(n_active/32) -> group_begin, then one GroupMeta
+// record per group (request, valid rows, group count, first row, id index)
 __global__ void __launch_bounds__(kSelectThreads)
-plan_layout_kernel(const int64_t* __restrict__ n_active, int32_t B,
-                   int64_t* __restrict__ group_begin, int32_t* __restrict__ group_req,
+plan_layout_kernel(const int64_t* __restrict__ n_active, const int64_t* __restrict__ id_off,
+                   int32_t B, int64_t* __restrict__ group_begin, GroupMeta* __restrict__ meta,
                    int64_t max_groups) {
     __shared__ int64_t warp_tot[32];
     __shared__ int64_t s_total;
@@ -231,11 +232,22 @@ plan_layout_kernel(const int64_t* __restrict__ n_active, int32_t B,
     }
     if (threadIdx.x == 0) group_begin[B] = s_carry;
     __syncthreads();
-    // fill the map: one warp per request
+    // fill the records: one warp per request
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (int32_t b = wid; b < B; b += nwarps) {
         const int64_t g0 = group_begin[b], g1 = group_begin[b + 1];
-        for (int64_t g = g0 + lane; g < g1 && g < max_groups; g += 32) group_req[g] = b;
+        const int64_t n = n_active[b];
+        const int64_t base = id_off ? id_off[b] : 0;
+        for (int64_t g = g0 + lane; g < g1 && g < max_groups; g += 32) {
+            GroupMeta m;
+            m.b = b;
+            m.row0 = (g - g0) * kGroupRows;
+            m.nvalid = static_cast<int32_t>(min(n - m.row0, static_cast<int64_t>(kGroupRows)));
+            m.ngroups = static_cast<int32_t>(g1 - g0);
+            m.pad = 0;
+            m.idbase = base + m.row0;
+            meta[g] = m;
+        }
     }
 }
 
@@ -307,8 +319,8 @@ extern "C" svt_status svt_union_plans(const uint32_t* d_ids, const int64_t* d_of
     return SVT_OK;
 }
 
-extern "C" svt_status svt_plan_layout(const int64_t* d_n_active, int32_t batch,
-                                      int64_t* d_group_begin, int32_t* d_group_req,
+extern "C" svt_status svt_plan_layout(const int64_t* d_n_active, const int64_t* d_id_offsets,
+                                      int32_t batch, int64_t* d_group_begin, void* d_group_meta,
                                       int64_t max_groups, svt_stream stream) {
     using namespace svt;
     if (batch < 0) {
@@ -316,7 +328,8 @@ extern "C" svt_status svt_plan_layout(const int64_t* d_n_active, int32_t batch,
         return SVT_ERR_CONFIG;
     }
     plan_layout_kernel<<<1, kSelectThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        d_n_active, batch, d_group_begin, d_group_req, max_groups);
+        d_n_active, d_id_offsets, batch, d_group_begin, static_cast<GroupMeta*>(d_group_meta),
+        max_groups);
     SVT_LAUNCH_CHECK("plan_layout_kernel");
     return SVT_OK;
 }

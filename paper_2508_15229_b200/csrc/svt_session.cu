@@ -13,7 +13,7 @@
 #include <string>
 #include <vector>
 
-#include "svt_common.cuh"
+#include "svt_gemv.cuh"
 
 struct svt_session {
     const void* head = nullptr;
@@ -37,7 +37,7 @@ struct svt_session {
     size_t cap_batch = 0;
     uint32_t* d_active = nullptr;
     size_t cap_active = 0;
-    int32_t* d_group_req = nullptr;
+    svt::GroupMeta* d_group_req = nullptr;  // one record per row group
     uint8_t* d_sub = nullptr;
     size_t cap_groups = 0;
     float* d_hidden = nullptr;
@@ -256,11 +256,11 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
                             s->d_active, s->d_act_off, s->n_active_d(), s->n_static_d(),
                             s->n_dynamic_d(), s->first_bad_d(), q);
     if (!st)
-        st = svt_plan_layout(s->n_active_d(), batch, s->group_begin_d(), s->d_group_req,
+        st = svt_plan_layout(s->n_active_d(), s->d_act_off, batch, s->group_begin_d(), s->d_group_req,
                              s->max_groups, q);
     if (!st)
-        st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim, s->d_active, s->d_act_off,
-                                    s->n_active_d(), s->group_begin_d(), s->d_group_req, batch,
+        st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim, s->d_active,
+                                    s->group_begin_d(), s->d_group_req, batch,
                                     s->max_groups, s->d_sub, s->d_bad, q);
     if (st) return st;
     std::vector<int64_t> meta(4 * B);
@@ -329,7 +329,7 @@ svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size
             return SVT_ERR_INTEGRITY;
         }
     return svt_greedy_interleaved(s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req,
-                                  s->n_active_d(), s->d_active, s->d_act_off, s->batch,
+                                  s->d_active, s->batch,
                                   s->max_groups, d_hidden, hidden_ld, 0, 1, d_out_ids, d_out_max,
                                   nullptr, s->d_ws, s->stream);
 }

@@ -46,11 +46,12 @@ class RowShard:
         g = (self.n + 31) // 32
         self.max_groups = g * B
         dev = "cuda"
-        self.n_active = torch.full((B,), self.n, dtype=torch.int64, device=dev)
-        gb = np.arange(B + 1, dtype=np.int64) * g
-        self.group_begin = torch.from_numpy(gb).to(dev)
-        self.group_req = torch.from_numpy(np.repeat(np.arange(B, dtype=np.int32), g)).to(dev) \
-            if self.max_groups else torch.zeros(1, dtype=torch.int32, device=dev)
+        n_active = torch.full((max(B, 1),), self.n, dtype=torch.int64, device=dev)
+        self.group_begin = torch.zeros(B + 1, dtype=torch.int64, device=dev)
+        self.group_meta = torch.zeros((max(1, self.max_groups), 8), dtype=torch.int32, device=dev)
+        # identity plan over the slice: no id offsets (row == id index)
+        call("svt_plan_layout", n_active.data_ptr(), None, B, self.group_begin.data_ptr(),
+             self.group_meta.data_ptr(), self.max_groups, _stream(None))
         self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_workspace_bytes(B)), dtype=torch.uint8,
                               device=dev)
         self.keys = torch.zeros(B, dtype=torch.int64, device=dev)
@@ -63,8 +64,8 @@ class RowShard:
             self.keys.zero_()
             return self.keys, self.ids, self.max
         call("svt_greedy_fused", self.rows.data_ptr(), self.storage, self.n, self.dim,
-             self.group_begin.data_ptr(), self.group_req.data_ptr(), self.n_active.data_ptr(),
-             None, None, self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), self.r0,
+             self.group_begin.data_ptr(), self.group_meta.data_ptr(), None, self.B,
+             self.max_groups, hidden.data_ptr(), hidden.stride(0), self.r0,
              self.plan_start, self.ids.data_ptr(), self.max.data_ptr(), self.keys.data_ptr(),
              self.ws.data_ptr(), _stream(stream))
         return self.keys, self.ids, self.max

@@ -407,7 +407,8 @@ class TailoredBatch:
         self.meta = torch.zeros((4, max(B, 1)), dtype=torch.int64, device=dev)
         self.n_active, self.n_static, self.n_dynamic, self.first_bad_d = self.meta
         self.group_begin = torch.zeros(B + 1, dtype=torch.int64, device=dev)
-        self.group_req = torch.zeros(max(1, self.max_groups), dtype=torch.int32, device=dev)
+        # one 32-byte GroupMeta record per 32-row group (svt_plan_layout)
+        self.group_meta = torch.zeros((max(1, self.max_groups), 8), dtype=torch.int32, device=dev)
         self.sub: Optional[torch.Tensor] = None
         self.head: Optional[HeadMatrix] = None
         self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_workspace_bytes(B)), dtype=torch.uint8,
@@ -433,8 +434,9 @@ class TailoredBatch:
              self.active.data_ptr(), self.act_off.data_ptr(), self.n_active.data_ptr(),
              self.n_static.data_ptr(), self.n_dynamic.data_ptr(), self.first_bad_d.data_ptr(),
              _stream(self.stream))
-        call("svt_plan_layout", self.n_active.data_ptr(), self.B, self.group_begin.data_ptr(),
-             self.group_req.data_ptr(), self.max_groups, _stream(self.stream))
+        call("svt_plan_layout", self.n_active.data_ptr(), self.act_off.data_ptr(), self.B,
+             self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.max_groups,
+             _stream(self.stream))
         self._first_bad_h = None
 
     @classmethod
@@ -475,10 +477,9 @@ class TailoredBatch:
             self.gather_bad = torch.zeros(1, dtype=torch.int32, device="cuda")
             self._fast = None
         call("svt_gather_interleaved", head.data.data_ptr(), head.storage, head.rows(),
-             head.dim(), self.active.data_ptr(), self.act_off.data_ptr(),
-             self.n_active.data_ptr(), self.group_begin.data_ptr(), self.group_req.data_ptr(),
-             self.B, self.max_groups, self.sub.data_ptr(), self.gather_bad.data_ptr(),
-             _stream(self.stream))
+             head.dim(), self.active.data_ptr(), self.group_begin.data_ptr(),
+             self.group_meta.data_ptr(), self.B, self.max_groups, self.sub.data_ptr(),
+             self.gather_bad.data_ptr(), _stream(self.stream))
         return self
 
     def _fast_args(self):
@@ -486,9 +487,8 @@ class TailoredBatch:
         host side of a decode step is a single ctypes call."""
         if getattr(self, "_fast", None) is None:
             h = self.head
-            common = (self.group_begin.data_ptr(), self.group_req.data_ptr(),
-                      self.n_active.data_ptr(), self.active.data_ptr(), self.act_off.data_ptr(),
-                      self.B, self.max_groups)
+            common = (self.group_begin.data_ptr(), self.group_meta.data_ptr(),
+                      self.active.data_ptr(), self.B, self.max_groups)
             self._fast = {
                 False: (_lib.lib.svt_greedy_interleaved,
                         (self.sub.data_ptr(), h.storage, h.dim()) + common),
@@ -513,15 +513,13 @@ class TailoredBatch:
         head = self.head
         if fused:
             call("svt_greedy_fused", head.data.data_ptr(), head.storage, head.rows(), head.dim(),
-                 self.group_begin.data_ptr(), self.group_req.data_ptr(),
-                 self.n_active.data_ptr(), self.active.data_ptr(), self.act_off.data_ptr(),
+                 self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.active.data_ptr(),
                  self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), row_base,
                  plan_start, out_ids.data_ptr(), _ptr(out_max), _ptr(out_keys),
                  self.ws.data_ptr(), _stream(self.stream))
         else:
             call("svt_greedy_interleaved", self.sub.data_ptr(), head.storage, head.dim(),
-                 self.group_begin.data_ptr(), self.group_req.data_ptr(),
-                 self.n_active.data_ptr(), self.active.data_ptr(), self.act_off.data_ptr(),
+                 self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.active.data_ptr(),
                  self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), row_base,
                  plan_start, out_ids.data_ptr(), _ptr(out_max), _ptr(out_keys),
                  self.ws.data_ptr(), _stream(self.stream))
@@ -533,16 +531,14 @@ class TailoredBatch:
         out = torch.empty(max(1, int(self.act_off_h[-1])), dtype=torch.float32, device="cuda")
         if fused:
             call("svt_logits_rows", head.data.data_ptr(), head.storage, head.rows(), head.dim(),
-                 self.group_begin.data_ptr(), self.group_req.data_ptr(),
-                 self.n_active.data_ptr(), self.active.data_ptr(), self.act_off.data_ptr(),
+                 self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.active.data_ptr(),
                  self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), out.data_ptr(),
                  self.act_off.data_ptr(), _stream(self.stream))
         else:
             call("svt_logits_interleaved", self.sub.data_ptr(), head.storage, head.dim(),
-                 self.group_begin.data_ptr(), self.group_req.data_ptr(),
-                 self.n_active.data_ptr(), self.B, self.max_groups, hidden.data_ptr(),
-                 hidden.stride(0), out.data_ptr(), self.act_off.data_ptr(),
-                 _stream(self.stream))
+                 self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.B,
+                 self.max_groups, hidden.data_ptr(), hidden.stride(0), out.data_ptr(),
+                 self.act_off.data_ptr(), _stream(self.stream))
         return out
 
     def algorithmic_decode_bytes(self, esize: int, dim: int) -> int:
