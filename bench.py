@@ -183,7 +183,9 @@ class Job:
                 dec_events[t][1].record()
 
     def launches_per_step(self, mode):
-        return 2 + (1 if mode == "interleaved" else 0) + self.steps
+        # select + plan layout (+ interleaved gather) + per decode step the
+        # exact-order GEMV and its programmatic-dependent argmax finalize
+        return 2 + (1 if mode == "interleaved" else 0) + 2 * self.steps
 
     def decode_bytes(self):
         return self.tb.algorithmic_decode_bytes(self.esize, self.cfg["d"])

@@ -122,8 +122,10 @@ svt_status svt_union_plans(const uint32_t* d_ids, const int64_t* d_offsets, int3
  * (exclusive prefix sum of ceil(n_active/32)); d_group_begin[batch] = total.
  * d_group_meta: one SVT_GROUP_META_BYTES record per group (g < total <=
  * max_groups): { int32 request, int32 valid rows (1..32), int32 groups of
- * the request, int32 0, int64 plan row of lane 0, int64 index of that row's
- * id in the plan-id array = d_id_offsets[request] + row }. d_id_offsets may
+ * the request, int32 flags (bit 0: every gathered weight of the group lies
+ * in the exact-FMA range; set to 1 here and cleared by
+ * svt_gather_interleaved), int64 plan row of lane 0, int64 index of that
+ * row's id in the plan-id array = d_id_offsets[request] + row }. d_id_offsets may
  * be NULL (identity plans: the id index is the row itself). */
 #define SVT_GROUP_META_BYTES 32
 svt_status svt_plan_layout(const int64_t* d_n_active, const int64_t* d_id_offsets, int32_t batch,
@@ -180,7 +182,8 @@ svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
 
 /* Single-plan greedy over a row-major sub-head (the exact greedy_step
  * signature shape: sub-head rows are the plan's rows in order, d_plan_ids
- * remaps the winner). d_out_id/d_out_max are single elements. */
+ * remaps the winner). d_out_id/d_out_max are single elements; d_workspace
+ * holds svt_greedy_workspace_bytes(1, ceil(rows/32)) bytes. */
 svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, size_t dim,
                            const float* d_hidden, const uint32_t* d_plan_ids,
                            uint32_t* d_out_id, float* d_out_max, void* d_workspace,
@@ -189,6 +192,10 @@ svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, siz
 /* Kernel tuning (0 = automatic): warps per CTA and ring stages per warp of
  * the exact-order GEMV. Used by bench sweeps; not needed for correctness. */
 void svt_set_tuning(int warps, int stages);
+/* Instrumentation: when d_counters != NULL, every pipelined GEMV launch
+ * writes 4 u64 cycle counters per (CTA, warp pair): producer total, producer
+ * wait-for-empty, consumer total, consumer wait-for-full. NULL disables. */
+void svt_set_debug(void* d_counters);
 
 /* ------------------------------------------------------------------------
  * (d) Fused greedy decode: logits + strict-'>' argmax (ties -> lowest local
@@ -211,13 +218,16 @@ void svt_set_tuning(int warps, int stages);
  *   packed (orderable max << 32 | ~global_row) key for cross-shard combines).
  * row_base/plan_start: for vocab-sharded use (a contiguous slice of a larger
  *   plan); pass 0 / 1 for a whole plan.
- * d_workspace: svt_greedy_workspace_bytes(batch) bytes, zeroed ONCE by the
- *   caller; every launch leaves it zeroed again (graph-replayable).
+ * d_workspace: svt_greedy_workspace_bytes(batch, max_groups) bytes of scratch
+ *   (one key per row group; no initialisation needed, graph-replayable).
+ *   Each call is two stream-ordered launches: the exact-order GEMV, which
+ *   stores one (max, row) key per group, and a programmatic-dependent
+ *   finalize grid that reduces each request's keys and remaps the winner.
  * Requests with an empty plan have no group and are left untouched (the
  *   reference throws IntegrityError "greedy step over an empty sub-head",
  *   head.cpp:205-206; the host-buffer APIs raise it).
  * ---------------------------------------------------------------------- */
-size_t svt_greedy_workspace_bytes(int32_t batch);
+size_t svt_greedy_workspace_bytes(int32_t batch, int64_t max_groups);
 svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
                                   const int64_t* d_group_begin, const void* d_group_meta,
                                   const uint32_t* d_active_ids, int32_t batch,

@@ -54,6 +54,7 @@ _SIGS = {
     "svt_device_count": ([], C.c_int),
     "svt_dtype_size": ([C.c_int], _sz),
     "svt_set_tuning": ([C.c_int, C.c_int], None),
+    "svt_set_debug": ([_vp], None),
     "svt_head_random": ([_vp, C.c_int, C.c_int, _u64, _u64, _u64, _vp], C.c_int),
     "svt_convert_from_f32": ([_vp, _vp, C.c_int, _u64, _vp], C.c_int),
     "svt_convert_to_f32": ([_vp, C.c_int, _vp, _u64, _vp], C.c_int),
@@ -72,7 +73,7 @@ _SIGS = {
     "svt_logits_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp, _vp],
                                C.c_int),
     "svt_greedy_step": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
-    "svt_greedy_workspace_bytes": ([_i32], _sz),
+    "svt_greedy_workspace_bytes": ([_i32, _i64], _sz),
     "svt_greedy_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,
                                 _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_greedy_fused": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,

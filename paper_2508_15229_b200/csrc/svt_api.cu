@@ -96,11 +96,15 @@ int svt_device_count(void) {
 }
 size_t svt_dtype_size(svt_dtype dt) { return valid_dtype(dt) ? esize_of(dt) : 0; }
 void svt_set_tuning(int warps, int stages) { gemv_set_tuning(warps, stages); }
+void svt_set_debug(void* d_counters) {
+    gemv_set_debug(static_cast<unsigned long long*>(d_counters));
+}
 
-size_t svt_greedy_workspace_bytes(int32_t batch) {
-    // keys (u64) + counters (u32), padded
-    const size_t b = batch > 0 ? static_cast<size_t>(batch) : 0;
-    return ((b * 8 + 255) & ~size_t(255)) + ((b * 4 + 255) & ~size_t(255));
+size_t svt_greedy_workspace_bytes(int32_t batch, int64_t max_groups) {
+    // one u64 key per row group (batch kept for ABI symmetry)
+    (void)batch;
+    const size_t g = max_groups > 0 ? static_cast<size_t>(max_groups) : 1;
+    return (g * 8 + 255) & ~size_t(255);
 }
 
 svt_status svt_logits(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
@@ -181,10 +185,7 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
     p.max_groups = max_groups;
     p.hidden = hidden;
     p.hidden_ld = static_cast<int64_t>(ld);
-    p.keys = static_cast<unsigned long long*>(ws);
-    p.counters = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(ws) +
-                                                 ((static_cast<size_t>(batch) * 8 + 255) &
-                                                  ~size_t(255)));
+    p.gkeys = static_cast<unsigned long long*>(ws);
     p.out_ids = out_ids;
     p.out_max = out_max;
     p.out_keys = reinterpret_cast<unsigned long long*>(out_keys);
@@ -231,8 +232,7 @@ svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, siz
     p.B = 1;
     p.hidden = d_hidden;
     p.hidden_ld = static_cast<int64_t>(dim);
-    p.keys = static_cast<unsigned long long*>(d_workspace);
-    p.counters = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(d_workspace) + 256);
+    p.gkeys = static_cast<unsigned long long*>(d_workspace);
     p.out_ids = d_out_id;
     p.out_max = d_out_max;
     // rows of the sub-head are the plan's rows in order; the winner's local

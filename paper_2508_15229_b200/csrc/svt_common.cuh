@@ -34,15 +34,48 @@ struct Chunk<SVT_F32> {
 template <>
 struct Chunk<SVT_BF16> {
     static constexpr int E = 8;
+    // PRMT + LOP3 (ALU pipe) rather than an IMAD shift (FMA pipe)
     __device__ static inline void widen(const uint4& v, float (&w)[E]) {
         const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            w[2 * i] = __uint_as_float(u[i] << 16);
+            w[2 * i] = __uint_as_float(__byte_perm(u[i], 0u, 0x1044));
             w[2 * i + 1] = __uint_as_float(u[i] & 0xFFFF0000u);
         }
     }
 };
+
+// ---- exact-FMA eligibility -------------------------------------------------
+// fma(w, h, acc) == acc + (w * h) bit for bit whenever w*h is exactly
+// representable in f32: both operands zero or normal with exponents in
+// [2^-60, 2^60] (no overflow/underflow of the product) and the two
+// significands together at most 24 bits wide. Weights: bf16 (8 bits) or
+// f16 (11 bits); hidden values are checked for <= 16 (bf16 W) / <= 13
+// (f16 W) significant bits.
+__device__ __forceinline__ bool exp_in_range(uint32_t bits) {
+    const uint32_t e = (bits >> 23) & 0xFFu;
+    return (bits & 0x7FFFFFFFu) == 0u || (e >= 127u - 60u && e <= 127u + 60u);
+}
+template <int DT>
+__device__ __forceinline__ bool hidden_fma_safe(float h) {
+    const uint32_t b = __float_as_uint(h);
+    constexpr uint32_t low = DT == SVT_BF16 ? 0xFFu : 0x3FFu;
+    return exp_in_range(b) && (b & low) == 0u;
+}
+// weight element of a 16-byte chunk (storage bits) inside the safe range
+__device__ __forceinline__ bool bf16_fma_safe(uint32_t two) {
+    return exp_in_range(two << 16) && exp_in_range(two & 0xFFFF0000u);
+}
+__device__ __forceinline__ bool f16_fma_safe(uint32_t two) {
+    // f16 normals span 2^-14..2^15 (inside the range); subnormals and
+    // inf/nan are excluded
+    const uint32_t lo = two & 0xFFFFu, hi = two >> 16;
+    auto ok = [](uint32_t h) {
+        const uint32_t e = (h >> 10) & 0x1Fu;
+        return (h & 0x7FFFu) == 0u || (e != 0u && e != 0x1Fu);
+    };
+    return ok(lo) && ok(hi);
+}
 
 template <>
 struct Chunk<SVT_F16> {
@@ -130,6 +163,9 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),

@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(kGatherWarps * 32)
 gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_t row_bytes,
                           int32_t nchunks, const uint32_t* __restrict__ active_ids,
                           const int64_t* __restrict__ group_begin,
-                          const GroupMeta* __restrict__ meta, int32_t B, int64_t max_groups,
-                          uint4* __restrict__ out, int32_t* bad) {
+                          GroupMeta* __restrict__ meta, int32_t B, int64_t max_groups,
+                          uint4* __restrict__ out, int32_t* bad, int dt) {
     extern __shared__ __align__(16) uint4 tiles[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint4* tile = tiles + wid * 32 * 32;
@@ -75,6 +75,7 @@ gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_
         const int64_t g = wg / nblk;
         const int cb = static_cast<int>(wg - g * nblk);
         const GroupMeta m = meta[g];
+        bool safe = true;
         // lane r fetches the plan id of row r; broadcast per row below
         const bool in_plan = lane < m.nvalid;
         const uint32_t my_id = in_plan ? active_ids[m.idbase + lane] : 0xFFFFFFFFu;
@@ -94,7 +95,17 @@ gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_
                     v = load_chunk_bytes(src, row_bytes, c);
             }
             tile[r * 32 + (lane ^ (r & 7))] = v;
+            // exact-FMA eligibility of the gathered weights (GroupMeta.pad)
+            if (dt == SVT_BF16)
+                safe = safe && bf16_fma_safe(v.x) && bf16_fma_safe(v.y) && bf16_fma_safe(v.z) &&
+                       bf16_fma_safe(v.w);
+            else if (dt == SVT_F16)
+                safe = safe && f16_fma_safe(v.x) && f16_fma_safe(v.y) && f16_fma_safe(v.z) &&
+                       f16_fma_safe(v.w);
+            else
+                safe = false;
         }
+        if (!__all_sync(0xFFFFFFFFu, safe) && lane == 0) atomicAnd(&meta[g].pad, 0);
         __syncwarp();
         uint4* dst = out + g * static_cast<int64_t>(nchunks) * kGroupRows;
 #pragma unroll 8
@@ -160,15 +171,15 @@ extern "C" svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, s
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         gather_interleaved_kernel<true><<<grid, kGatherWarps * 32, smem, st>>>(
             static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
-            d_active_ids, d_group_begin, static_cast<const GroupMeta*>(d_group_meta), batch,
-            max_groups, static_cast<uint4*>(d_sub), d_bad);
+            d_active_ids, d_group_begin, static_cast<GroupMeta*>(const_cast<void*>(d_group_meta)),
+            batch, max_groups, static_cast<uint4*>(d_sub), d_bad, static_cast<int>(dt));
     } else {
         SVT_CUDA_TRY(cudaFuncSetAttribute(gather_interleaved_kernel<false>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         gather_interleaved_kernel<false><<<grid, kGatherWarps * 32, smem, st>>>(
             static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
-            d_active_ids, d_group_begin, static_cast<const GroupMeta*>(d_group_meta), batch,
-            max_groups, static_cast<uint4*>(d_sub), d_bad);
+            d_active_ids, d_group_begin, static_cast<GroupMeta*>(const_cast<void*>(d_group_meta)),
+            batch, max_groups, static_cast<uint4*>(d_sub), d_bad, static_cast<int>(dt));
     }
     SVT_LAUNCH_CHECK("gather_interleaved_kernel");
     return SVT_OK;

@@ -53,8 +53,11 @@ __host__ __device__ constexpr int slot_bytes(int E) {
 }
 
 // ---- shared epilogue ------------------------------------------------------
+// Argmax: the warp's best (value, row) key goes to gkeys[g] with a plain
+// store — no atomics, no fences; argmax_finalize_kernel (launched as a
+// programmatic dependent of this grid) reduces each request's groups.
 template <int MODE>
-__device__ __forceinline__ void group_epilogue(const GemvParams& p, const GroupMeta& m,
+__device__ __forceinline__ void group_epilogue(const GemvParams& p, const GroupMeta& m, int64_t g,
                                                int64_t lbase, bool valid, float acc, int lane) {
     const int64_t row = m.row0 + lane;
     if constexpr (MODE == MODE_LOGITS) {
@@ -63,27 +66,49 @@ __device__ __forceinline__ void group_epilogue(const GemvParams& p, const GroupM
         const unsigned long long key = make_key(
             acc, p.row_base + static_cast<uint32_t>(row), valid, p.plan_start != 0 && row == 0);
         const unsigned long long kmax = warp_max_u64(key);
+        if (lane == 0) p.gkeys[g] = kmax;
+    }
+}
+
+// one warp per request: max over the request's group keys, decode, remap
+// through the plan ids (remap_out, selector.cpp:50-56)
+__global__ void __launch_bounds__(256) argmax_finalize_kernel(const GemvParams p) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int lane = threadIdx.x & 31;
+    const int nreq = p.group_begin ? p.B : 1;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         b < nreq; b += nw) {
+        int64_t g0 = 0, g1 = p.total();
+        if (p.group_begin) {
+            g0 = min(p.group_begin[b], p.max_groups);
+            g1 = min(p.group_begin[b + 1], p.max_groups);
+        }
+        if (g1 <= g0) continue;  // empty plan: nothing to decode
+        unsigned long long k = 0;
+        for (int64_t g = g0 + lane; g < g1; g += 32) {
+            const unsigned long long v = p.gkeys[g];
+            k = v > k ? v : k;
+        }
+        k = warp_max_u64(k);
         if (lane == 0) {
-            if (kmax) atom_max_relaxed_u64(&p.keys[m.b], kmax);
-            // release: our max is visible before the count; acquire (last
-            // arriver): every other group's max is visible to us
-            const unsigned int prev = atom_add_acq_rel_u32(&p.counters[m.b], 1u);
-            if (prev == static_cast<unsigned int>(m.ngroups) - 1u) {
-                const unsigned long long k = atom_exch_relaxed_u64(&p.keys[m.b], 0ull);
-                p.counters[m.b] = 0u;
-                uint32_t id = 0xFFFFFFFFu;
-                float mx = __int_as_float(0x7FC00000);
-                if (k) {
-                    const uint32_t hi = static_cast<uint32_t>(k >> 32);
-                    const uint32_t grow = 0xFFFFFFFFu - static_cast<uint32_t>(k);
-                    const int64_t local = static_cast<int64_t>(grow - p.row_base);
-                    id = p.ids ? p.ids[m.idbase - m.row0 + local] : grow;
-                    mx = hi == 0xFFFFFFFFu ? __int_as_float(0x7FC00000) : float_of_ord(hi);
+            uint32_t id = 0xFFFFFFFFu;
+            float mx = __int_as_float(0x7FC00000);
+            if (k) {
+                const uint32_t hi = static_cast<uint32_t>(k >> 32);
+                const uint32_t grow = 0xFFFFFFFFu - static_cast<uint32_t>(k);
+                const int64_t local = static_cast<int64_t>(grow - p.row_base);
+                if (p.ids) {
+                    const GroupMeta m0 = p.group(g0);
+                    id = p.ids[m0.idbase - m0.row0 + local];
+                } else {
+                    id = grow;
                 }
-                p.out_ids[m.b] = id;
-                if (p.out_max) p.out_max[m.b] = mx;
-                if (p.out_keys) p.out_keys[m.b] = k;
+                mx = hi == 0xFFFFFFFFu ? __int_as_float(0x7FC00000) : float_of_ord(hi);
             }
+            p.out_ids[b] = id;
+            if (p.out_max) p.out_max[b] = mx;
+            if (p.out_keys) p.out_keys[b] = k;
         }
     }
 }
@@ -122,96 +147,130 @@ __device__ __forceinline__ void load_chunk(const uint8_t* wsl, const float* hsl,
     }
 }
 
-// ---- pipelined kernel -------------------------------------------------------
+// ---- pipelined, warp-specialised kernel ----------------------------------
+// Warps come in (producer, consumer) pairs sharing one ring of S slots with a
+// "full" and an "empty" mbarrier per slot. The producer walks the pair's
+// (group, stage) sequence issuing bulk copies; the consumer only waits,
+// computes and releases, so the per-stage address/bookkeeping work never sits
+// in front of the serial FADD chain.
 template <int DT, int SRC, int MODE>
-__global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
     using CK = Chunk<DT>;
     constexpr int E = CK::E;
     constexpr int kSlot = slot_bytes<SRC>(E);
     constexpr int kSlotW = stage_w_bytes<SRC>();
 
+    // let the (tiny) argmax finalize grid get scheduled now; it waits for
+    // this grid's completion in griddepcontrol.wait
+    asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
-    const int nwa = blockDim.x >> 5;
+    const int npairs = blockDim.x >> 6;
+    const int pair = wid >> 1;
+    const bool producer = (wid & 1) == 0;
     const int S = p.stages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + wid * S;
-    const int bar_bytes = (nwa * S * 8 + 127) & ~127;
-    uint8_t* ring = smem + bar_bytes + static_cast<int64_t>(wid) * S * kSlot;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem) + pair * 2 * S;
+    uint64_t* empty = full + S;
+    const int bar_bytes = (npairs * 2 * S * 8 + 127) & ~127;
+    uint8_t* ring = smem + bar_bytes + static_cast<int64_t>(pair) * S * kSlot;
 
     const int64_t total_groups = p.total();
-    const int64_t TW = static_cast<int64_t>(gridDim.x) * nwa;
-    const int64_t w = static_cast<int64_t>(wid) * gridDim.x + blockIdx.x;
+    const int64_t TW = static_cast<int64_t>(gridDim.x) * npairs;
+    const int64_t w = static_cast<int64_t>(pair) * gridDim.x + blockIdx.x;
     const int64_t ng = total_groups > w ? (total_groups - w + TW - 1) / TW : 0;
     const int ns = (p.nchunks + kCR - 1) / kCR;
-    const int full_stages = p.dim / (kCR * E);  // stages with no element past dim
     const int64_t nq = ng * ns;
-    if (nq == 0) return;
 
-    if (lane == 0) {
-        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+    if (producer && lane == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
         fence_mbar_init();
     }
-    __syncwarp();
-
-    const uint64_t pol_w = policy_evict_first();
-    const int dim4 = (p.dim + 3) & ~3;
+    __syncthreads();
+    if (nq == 0) return;
     const GroupMeta dummy{};
-
-    // ---- producer (issue) state: runs S stages ahead of the consumer ----
-    int64_t iq = 0, ig = w;
-    int is = 0, islot = 0;
-    GroupMeta im = p.group(w);
-    GroupMeta im_next = (w + TW < total_groups) ? p.group(w + TW) : dummy;
-    const uint8_t* isrc = nullptr;  // ROWS: this lane's source row
-    unsigned imask = 0;
-
-    auto issue_next = [&]() {
-        if (is == 0 && SRC == SRC_ROWS) {  // entering a new group on the issue side
-            int64_t srow = 0;
-            const bool ok = lane_valid<SRC>(p, im, lane, &srow);
-            isrc = p.W + (ok ? srow : 0) * p.row_bytes;
-            imask = __ballot_sync(0xFFFFFFFFu, ok);
+    const long long t_start = p.dbg ? clock64() : 0;
+    long long dbg_wait = 0, dbg_epi = 0;
+    auto dbg_flush = [&](int which) {
+        if (p.dbg && lane == 0) {
+            unsigned long long* d = p.dbg + (static_cast<int64_t>(blockIdx.x) * npairs + pair) * 6;
+            d[4 + which] += static_cast<unsigned long long>(dbg_epi);
+            d[which * 2] = static_cast<unsigned long long>(clock64() - t_start);
+            d[which * 2 + 1] = static_cast<unsigned long long>(dbg_wait);
         }
-        uint8_t* wdst = ring + islot * kSlot;
-        uint8_t* hdst = wdst + kSlotW;
-        const int c0 = is * kCR;
-        const int cc = min(kCR, p.nchunks - c0);
-        const int e0 = c0 * E;
-        const int hb = min(cc * E, dim4 - e0) * 4;
-        const float* hsrc = p.hidden + static_cast<int64_t>(im.b) * p.hidden_ld + e0;
-        if constexpr (SRC == SRC_INTERLEAVED) {
-            if (lane == 0) {
-                const uint32_t wb = static_cast<uint32_t>(cc) * kChunkRowBytes;
-                mbar_arrive_expect_tx(&bars[islot], wb + hb);
-                bulk_g2s(wdst, p.W + (ig * p.nchunks + c0) * static_cast<int64_t>(kChunkRowBytes),
-                         wb, &bars[islot], pol_w);
-                bulk_g2s(hdst, hsrc, hb, &bars[islot], pol_w);
-            }
-        } else {
-            const uint32_t slice = static_cast<uint32_t>(cc) * kChunkBytes;
-            if (lane == 0) {
-                mbar_arrive_expect_tx(&bars[islot], __popc(imask) * slice + hb);
-                bulk_g2s(hdst, hsrc, hb, &bars[islot], pol_w);
-            }
-            __syncwarp();
-            if ((imask >> lane) & 1u)
-                bulk_g2s(wdst + lane * (kCR + 1) * kChunkBytes, isrc + c0 * kChunkBytes, slice,
-                         &bars[islot], pol_w);
-        }
-        ++iq;
-        if (++is == ns) {
-            is = 0;
-            ig += TW;
-            im = im_next;
-            if (ig + TW < total_groups) im_next = p.group(ig + TW);
-        }
-        if (++islot == S) islot = 0;
     };
 
-    while (iq < nq && iq < S) issue_next();
+    if (producer) {
+        const uint64_t pol_w = policy_evict_first();
+        const int dim4 = (p.dim + 3) & ~3;
+        int64_t ig = w;
+        int is = 0, islot = 0;
+        uint32_t ephase = 0;
+        GroupMeta im = p.group(w);
+        GroupMeta im_next = (w + TW < total_groups) ? p.group(w + TW) : dummy;
+        const uint8_t* isrc = nullptr;  // ROWS: this lane's source row
+        unsigned imask = 0;
+        for (int64_t q = 0; q < nq; ++q) {
+            // use k = q / S of this slot needs the consumer's release of use
+            // k-1, i.e. completion of empty-phase k-1 (parity = ephase ^ 1)
+            if (q >= S) {
+                const long long tw = p.dbg ? clock64() : 0;
+                mbar_wait_parity(&empty[islot], ephase ^ 1u);
+                if (p.dbg) dbg_wait += clock64() - tw;
+            }
+            if (is == 0 && SRC == SRC_ROWS) {
+                int64_t srow = 0;
+                const bool ok = lane_valid<SRC>(p, im, lane, &srow);
+                isrc = p.W + (ok ? srow : 0) * p.row_bytes;
+                imask = __ballot_sync(0xFFFFFFFFu, ok);
+            }
+            uint8_t* wdst = ring + islot * kSlot;
+            uint8_t* hdst = wdst + kSlotW;
+            const int c0 = is * kCR;
+            const int cc = min(kCR, p.nchunks - c0);
+            const int e0 = c0 * E;
+            const int hb = min(cc * E, dim4 - e0) * 4;
+            const float* hsrc = p.hidden + static_cast<int64_t>(im.b) * p.hidden_ld + e0;
+            if constexpr (SRC == SRC_INTERLEAVED) {
+                if (lane == 0) {
+                    const uint32_t wb = static_cast<uint32_t>(cc) * kChunkRowBytes;
+                    mbar_arrive_expect_tx(&full[islot], wb + hb);
+                    bulk_g2s(wdst,
+                             p.W + (ig * p.nchunks + c0) * static_cast<int64_t>(kChunkRowBytes),
+                             wb, &full[islot], pol_w);
+                    bulk_g2s(hdst, hsrc, hb, &full[islot], pol_w);
+                }
+            } else {
+                const uint32_t slice = static_cast<uint32_t>(cc) * kChunkBytes;
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[islot], __popc(imask) * slice + hb);
+                    bulk_g2s(hdst, hsrc, hb, &full[islot], pol_w);
+                }
+                __syncwarp();
+                if ((imask >> lane) & 1u)
+                    bulk_g2s(wdst + lane * (kCR + 1) * kChunkBytes, isrc + c0 * kChunkBytes,
+                             slice, &full[islot], pol_w);
+            }
+            if (++is == ns) {
+                is = 0;
+                ig += TW;
+                im = im_next;
+                if (ig + TW < total_groups) im_next = p.group(ig + TW);
+            }
+            if (++islot == S) {
+                islot = 0;
+                ephase ^= 1u;
+            }
+        }
+        dbg_flush(0);
+        return;
+    }
 
-    // ---- consumer state ----
+    // ---- consumer ----
+    const int full_stages = p.dim / (kCR * E);  // stages with no element past dim
     int64_t g = w;
     int s = 0, slot = 0;
     uint32_t phase = 0;
@@ -227,10 +286,37 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
             valid = lane_valid<SRC>(p, cm, lane, &srow);
             if constexpr (MODE == MODE_LOGITS) lbase = p.loff(cm.b);
         }
-        mbar_wait_parity(&bars[slot], phase);
+        if (p.dbg) {
+            const long long tw = clock64();
+            mbar_wait_parity(&full[slot], phase);
+            dbg_wait += clock64() - tw;
+        } else {
+            mbar_wait_parity(&full[slot], phase);
+        }
         const uint8_t* wsl = ring + slot * kSlot;
         const float* hsl = reinterpret_cast<const float*>(wsl + kSlotW);
-        if (s < full_stages) {
+        bool exact_fma = false;
+        if constexpr (DT != SVT_F32 && SRC == SRC_INTERLEAVED && kCR * E == 128) {
+            // weights of this group vetted by the gather (GroupMeta.pad);
+            // the stage's 128 hidden values: one float4 per lane + a vote
+            if (cm.pad & 1) {
+                const float4 hq = reinterpret_cast<const float4*>(hsl)[lane];
+                const bool ok = hidden_fma_safe<DT>(hq.x) && hidden_fma_safe<DT>(hq.y) &&
+                                hidden_fma_safe<DT>(hq.z) && hidden_fma_safe<DT>(hq.w);
+                exact_fma = __all_sync(0xFFFFFFFFu, ok);
+            }
+        }
+        if (exact_fma && s < full_stages) {
+            // every product is exact in f32, so fma(w, h, acc) rounds once
+            // exactly like acc + fl(w * h): one FFMA per element.
+#pragma unroll
+            for (int cr = 0; cr < kCR; ++cr) {
+                float wv[E], hv[E];
+                load_chunk<DT, SRC>(wsl, hsl, cr, lane, wv, hv);
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc = __fmaf_rn(wv[e], hv[e], acc);
+            }
+        } else if (s < full_stages) {
             // branch-free: kCR chunk-rows, all elements below dim. Products
             // are formed one chunk ahead of the dependent FADD chain (the
             // only serial part: acc = acc + p, 4-cycle latency), so the
@@ -270,24 +356,24 @@ __global__ void __launch_bounds__(256, 1) gemv_ring_kernel(const GemvParams p) {
                     if (ebase + e < p.dim) acc = ref_mac(acc, wv[e], hv[e]);
             }
         }
-        // WAR on the slot: every lane's LDS results have been consumed by the
-        // FADD chain above, so after the warp barrier the bulk engine may
-        // overwrite it (the same-warp analogue of an empty-barrier release;
-        // no cross-proxy fence — that costs a MEMBAR.CTA per stage).
+        // release the slot: all lanes' LDS results are consumed above
         __syncwarp();
-        if (iq < nq) issue_next();
+        if (lane == 0) mbar_arrive(&empty[slot]);
         if (++slot == S) {
             slot = 0;
             phase ^= 1u;
         }
         if (++s == ns) {
-            group_epilogue<MODE>(p, cm, lbase, valid, acc, lane);
+            const long long te = p.dbg ? clock64() : 0;
+            group_epilogue<MODE>(p, cm, g, lbase, valid, acc, lane);
+            if (p.dbg) dbg_epi += clock64() - te;
             s = 0;
             g += TW;
             cm = cm_next;
             if (g + TW < total_groups) cm_next = p.group(g + TW);
         }
     }
+    dbg_flush(1);
 }
 
 // ---- generic (unaligned / dim 0) kernel: direct loads, same order/epilogue --
@@ -317,7 +403,7 @@ __global__ void __launch_bounds__(128) gemv_generic_kernel(const GemvParams p) {
             const uint8_t* rp = p.W + srow * p.row_bytes;
             for (int c = 0; c < p.dim; ++c) acc = ref_mac(acc, load_elem<DT>(rp, c), h[c]);
         }
-        group_epilogue<MODE>(p, m, MODE == MODE_LOGITS ? p.loff(m.b) : 0, valid, acc, lane);
+        group_epilogue<MODE>(p, m, g, MODE == MODE_LOGITS ? p.loff(m.b) : 0, valid, acc, lane);
     }
 }
 
@@ -327,6 +413,7 @@ namespace {
 struct Tuning {
     int warps = 0;   // 0 = auto
     int stages = 0;  // 0 = auto
+    unsigned long long* dbg = nullptr;
 };
 Tuning g_tuning;
 
@@ -341,18 +428,25 @@ svt_status launch_ring(GemvParams p, cudaStream_t st) {
     if (mg <= 0) return SVT_OK;
     const int grid = static_cast<int>(mg < sms ? mg : sms);
     int nwa = static_cast<int>((mg + grid - 1) / grid);
-    const int wmax = g_tuning.warps > 0 ? g_tuning.warps : 8;
+    // measured on B200 (tools/sweep_decode.py, cfg2 bf16): the interleaved
+    // stream is consumer-bound up to 6 pairs and best at 6 x 3 stages; the
+    // fused row gather is producer-bound and best at 8 pairs
+    const int wmax = g_tuning.warps > 0 ? g_tuning.warps : (SRC == SRC_INTERLEAVED ? 6 : 8);
     nwa = nwa < 1 ? 1 : (nwa > wmax ? wmax : nwa);
     int S = g_tuning.stages > 0 ? g_tuning.stages : kSmemBudget / (nwa * kSlot);
+    if (g_tuning.stages <= 0 && nwa >= 4 && S > 3) S = 3;
     if (S > 32) S = 32;
     if (S < 2) S = 2;
     while (nwa > 1 && nwa * S * kSlot > kSmemBudget) --nwa;
     p.stages = S;
-    const int bar_bytes = (nwa * S * 8 + 127) & ~127;
+    p.dbg = g_tuning.dbg;
+    // nwa (producer, consumer) warp pairs per CTA, each with S slots and
+    // 2*S mbarriers
+    const int bar_bytes = (nwa * 2 * S * 8 + 127) & ~127;
     const int smem = bar_bytes + nwa * S * kSlot;
     auto kern = gemv_ring_kernel<DT, SRC, MODE>;
     SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, nwa * 32, smem, st>>>(p);
+    kern<<<grid, nwa * 64, smem, st>>>(p);
     SVT_LAUNCH_CHECK("gemv_ring_kernel");
     return SVT_OK;
 }
@@ -395,16 +489,37 @@ svt_status gemv_run(int src, int mode, int dt, GemvParams p, cudaStream_t st) {
                 aligned16(p.W);
     if (src == SRC_ROWS) ring = ring && (p.row_bytes % 16 == 0);
     if (std::getenv("SVT_FORCE_GENERIC")) ring = false;
+    svt_status s;
     if (src == SRC_INTERLEAVED)
-        return mode == MODE_LOGITS ? dispatch<SRC_INTERLEAVED, MODE_LOGITS>(dt, p, ring, st)
-                                   : dispatch<SRC_INTERLEAVED, MODE_ARGMAX>(dt, p, ring, st);
-    return mode == MODE_LOGITS ? dispatch<SRC_ROWS, MODE_LOGITS>(dt, p, ring, st)
-                               : dispatch<SRC_ROWS, MODE_ARGMAX>(dt, p, ring, st);
+        s = mode == MODE_LOGITS ? dispatch<SRC_INTERLEAVED, MODE_LOGITS>(dt, p, ring, st)
+                                : dispatch<SRC_INTERLEAVED, MODE_ARGMAX>(dt, p, ring, st);
+    else
+        s = mode == MODE_LOGITS ? dispatch<SRC_ROWS, MODE_LOGITS>(dt, p, ring, st)
+                                : dispatch<SRC_ROWS, MODE_ARGMAX>(dt, p, ring, st);
+    if (s || mode != MODE_ARGMAX) return s;
+    // per-request reduction of the group keys, as a programmatic dependent
+    // launch (its launch latency overlaps the GEMV's tail)
+    const int nreq = p.group_begin ? p.B : 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((nreq + 7) / 8 < sm_count() * 4 ? (nreq + 7) / 8
+                                                                             : sm_count() * 4));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, argmax_finalize_kernel, p));
+    return SVT_OK;
 }
 
 void gemv_set_tuning(int warps, int stages) {
     g_tuning.warps = warps;
     g_tuning.stages = stages;
 }
+
+void gemv_set_debug(unsigned long long* d) { g_tuning.dbg = d; }
 
 }  // namespace svt

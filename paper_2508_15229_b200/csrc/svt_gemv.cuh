@@ -38,8 +38,7 @@ struct GemvParams {
     int64_t hidden_ld;
     float* logits;
     const int64_t* logits_off;
-    unsigned long long* keys;
-    unsigned int* counters;
+    unsigned long long* gkeys;  // per-group (max << 32 | ~row) keys, reduced by the finalize kernel
     uint32_t* out_ids;
     float* out_max;
     unsigned long long* out_keys;
@@ -47,6 +46,10 @@ struct GemvParams {
     int32_t plan_start;
     int32_t stages;
     int64_t single_rows;
+    // optional instrumentation (svt_set_debug): per (block, pair) cycle
+    // counters {producer total, producer empty-wait, consumer total,
+    // consumer full-wait}
+    unsigned long long* dbg;
 
     __device__ __forceinline__ int64_t total() const {
         return group_begin ? min(group_begin[B], max_groups)
@@ -71,5 +74,6 @@ struct GemvParams {
 
 svt_status gemv_run(int src, int mode, int dt, GemvParams p, cudaStream_t st);
 void gemv_set_tuning(int warps, int stages);
+void gemv_set_debug(unsigned long long* d);
 
 }  // namespace svt

@@ -244,7 +244,7 @@ plan_layout_kernel(const int64_t* __restrict__ n_active, const int64_t* __restri
             m.row0 = (g - g0) * kGroupRows;
             m.nvalid = static_cast<int32_t>(min(n - m.row0, static_cast<int64_t>(kGroupRows)));
             m.ngroups = static_cast<int32_t>(g1 - g0);
-            m.pad = 0;
+            m.pad = 1;  // exact-FMA eligible until the gather finds an unsafe weight
             m.idbase = base + m.row0;
             meta[g] = m;
         }

@@ -43,7 +43,8 @@ struct svt_session {
     float* d_hidden = nullptr;
     uint32_t* d_out_ids = nullptr;
     float* d_out_max = nullptr;
-    void* d_ws = nullptr;
+    uint8_t* d_ws = nullptr;  // one greedy key per row group
+    size_t cap_ws = 0;
     int32_t* d_bad = nullptr;
     // pinned host mirrors
     float* h_hidden = nullptr;
@@ -96,7 +97,7 @@ svt_status ensure_batch(svt_session* s, size_t B) {
     if (B <= s->cap_batch && s->d_meta) return SVT_OK;
     const size_t nb = B + B / 4 + 1;
     void* old[] = {s->d_in_off, s->d_act_off, s->d_meta, s->d_hidden, s->d_out_ids,
-                   s->d_out_max, s->d_ws};
+                   s->d_out_max};
     for (void* p : old)
         if (p) cudaFree(p);
     if (s->h_hidden) cudaFreeHost(s->h_hidden);
@@ -109,9 +110,6 @@ svt_status ensure_batch(svt_session* s, size_t B) {
     SVT_CUDA_TRY(cudaMemset(s->d_hidden, 0, nb * s->ld * sizeof(float)));
     SVT_CUDA_TRY(cudaMalloc(&s->d_out_ids, nb * sizeof(uint32_t)));
     SVT_CUDA_TRY(cudaMalloc(&s->d_out_max, nb * sizeof(float)));
-    const size_t ws = svt_greedy_workspace_bytes(static_cast<int32_t>(nb));
-    SVT_CUDA_TRY(cudaMalloc(&s->d_ws, ws));
-    SVT_CUDA_TRY(cudaMemset(s->d_ws, 0, ws));
     SVT_CUDA_TRY(cudaMallocHost(&s->h_hidden, nb * s->ld * sizeof(float)));
     SVT_CUDA_TRY(cudaMallocHost(&s->h_ids, nb * sizeof(uint32_t)));
     SVT_CUDA_TRY(cudaMallocHost(&s->h_max, nb * sizeof(float)));
@@ -234,6 +232,7 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
             s->cap_groups = cap;
         }
     }
+    if (!st) st = grow(&s->d_ws, &s->cap_ws, svt_greedy_workspace_bytes(batch, groups));
     if (st) return st;
     s->batch = batch;
     s->max_groups = groups;

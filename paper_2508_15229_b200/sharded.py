@@ -52,8 +52,8 @@ class RowShard:
         # identity plan over the slice: no id offsets (row == id index)
         call("svt_plan_layout", n_active.data_ptr(), None, B, self.group_begin.data_ptr(),
              self.group_meta.data_ptr(), self.max_groups, _stream(None))
-        self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_workspace_bytes(B)), dtype=torch.uint8,
-                              device=dev)
+        self.ws = torch.empty(max(1, _lib.lib.svt_greedy_workspace_bytes(B, self.max_groups)),
+                              dtype=torch.uint8, device=dev)
         self.keys = torch.zeros(B, dtype=torch.int64, device=dev)
         self.ids = torch.zeros(B, dtype=torch.int32, device=dev)
         self.max = torch.zeros(B, dtype=torch.float32, device=dev)

@@ -297,13 +297,13 @@ def logits(head: HeadMatrix, hidden) -> np.ndarray:
 _WS_CACHE: dict = {}
 
 
-def _workspace(batch: int) -> torch.Tensor:
+def _workspace(batch: int, groups: int) -> torch.Tensor:
     dev = torch.cuda.current_device()
-    key = (dev, batch)
+    key = (dev, batch, groups)
     ws = _WS_CACHE.get(key)
     if ws is None:
-        ws = torch.zeros(max(1, _lib.lib.svt_greedy_workspace_bytes(batch)), dtype=torch.uint8,
-                         device="cuda")
+        ws = torch.empty(max(1, _lib.lib.svt_greedy_workspace_bytes(batch, groups)),
+                         dtype=torch.uint8, device="cuda")
         _WS_CACHE[key] = ws
     return ws
 
@@ -321,7 +321,7 @@ def greedy_step(subhead: HeadMatrix, hidden, plan: SelectionPlan) -> int:
     mx = torch.empty(2, dtype=torch.float32, device="cuda")
     call("svt_greedy_step", subhead.data.data_ptr(), subhead.storage, subhead.rows(),
          subhead.dim(), h.data_ptr(), ids.data_ptr(), out.data_ptr(), mx.data_ptr(),
-         _workspace(1).data_ptr(), _stream())
+         _workspace(1, (subhead.rows() + 31) // 32).data_ptr(), _stream())
     return int(out[0].item()) & 0xFFFFFFFF
 
 
@@ -411,8 +411,8 @@ class TailoredBatch:
         self.group_meta = torch.zeros((max(1, self.max_groups), 8), dtype=torch.int32, device=dev)
         self.sub: Optional[torch.Tensor] = None
         self.head: Optional[HeadMatrix] = None
-        self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_workspace_bytes(B)), dtype=torch.uint8,
-                              device=dev)
+        self.ws = torch.empty(max(1, _lib.lib.svt_greedy_workspace_bytes(B, self.max_groups)),
+                              dtype=torch.uint8, device=dev)
         self._first_bad_h: Optional[np.ndarray] = None
 
     # ---- (a) select + layout -------------------------------------------

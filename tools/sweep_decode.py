@@ -46,5 +46,32 @@ def main():
     _lib.lib.svt_set_tuning(0, 0)
 
 
+
+
+def debug_counters(which="cfg1"):
+    """Producer/consumer cycle breakdown of one decode launch."""
+    cfg = bench.CFG2 if which == "cfg2" else bench.CFG1
+    B = 64 if which == "cfg2" else 1
+    job = bench.Job(cfg, B, 4, 0, torch, th, synth)
+    dbg = torch.zeros(148 * 8 * 6, dtype=torch.int64, device="cuda")
+    for fused in (False, True):
+        for rep in range(2):
+            _lib.lib.svt_set_debug(dbg.data_ptr())
+            dbg.zero_()
+            job.tb.greedy(job.hidden[0], job.out[0], fused=fused)
+            torch.cuda.synchronize()
+            _lib.lib.svt_set_debug(None)
+        d = dbg.view(-1, 6).cpu().numpy()
+        d = d[d[:, 2] > 0]
+        print(json.dumps({"cfg": which, "fused": fused, "pairs": int(len(d)),
+                          "prod_total": float(d[:, 0].mean()), "prod_wait": float(d[:, 1].mean()),
+                          "cons_total": float(d[:, 2].mean()), "cons_wait": float(d[:, 3].mean()),
+                          "cons_epilogue": float(d[:, 5].mean()),
+                          "cons_total_max": float(d[:, 2].max())}), flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[2] == "debug":
+        debug_counters(sys.argv[1])
+    else:
+        main()
