@@ -3,19 +3,23 @@
 //  * gather_rows_kernel: the reference layout (row-major W_sub[k,:] =
 //    W[S[k],:]); one warp per row, 16-byte vector copies when rows are
 //    16-byte multiples, byte copies otherwise.
-//  * gather_interleaved_kernel: the decode layout. One warp owns a 32-row x
-//    32-chunk tile (16 KB): it reads the 32 selected rows with coalesced
-//    16-byte loads (one row per load instruction, 512 B contiguous), stages
-//    the tile in shared memory with an XOR swizzle (conflict-free both ways),
-//    and writes it back chunk-major so that the decode kernel's bulk copies
-//    and lane reads are contiguous. Both directions are fully coalesced;
-//    HBM traffic = 2 * |S| * d * b (read + write).
+//  * gather_interleaved_kernel: the decode layout. A warp owns a 32-row x
+//    16-chunk tile (8 KB). It copies the 32 selected row slices straight
+//    into shared memory with cp.async (LDGSTS: no register staging, so all
+//    16 x 512 B requests of a tile are in flight at once; each instruction
+//    moves two 256 B row slices, coalesced), swizzled by XOR so both the
+//    row-major fill and the chunk-major read-out are bank-conflict free, and
+//    then writes the tile chunk-major with coalesced 512 B stores. 24 warps
+//    per SM keep ~190 KB of reads in flight. HBM traffic = 2 * |S| * d * b.
+//    While writing, it vets every weight for the decode kernel's exact-FMA
+//    path (GroupMeta.pad bit 0).
 #include "svt_gemv.cuh"
 
 namespace svt {
 namespace {
 
-constexpr int kGatherWarps = 4;
+constexpr int kGatherWarps = 24;
+constexpr int kTileChunks = 16;  // 16-byte chunks per row slice in a tile
 
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ head, int64_t rows,
                                    int64_t row_bytes, const uint32_t* __restrict__ ids,
@@ -57,6 +61,24 @@ __device__ inline uint4 load_chunk_bytes(const uint8_t* row, int64_t row_bytes, 
     return v;
 }
 
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+                 "l"(gmem_src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ bool chunk_fma_safe(const uint4& v, int dt) {
+    if (dt == SVT_BF16)
+        return bf16_fma_safe(v.x) && bf16_fma_safe(v.y) && bf16_fma_safe(v.z) &&
+               bf16_fma_safe(v.w);
+    if (dt == SVT_F16)
+        return f16_fma_safe(v.x) && f16_fma_safe(v.y) && f16_fma_safe(v.z) && f16_fma_safe(v.w);
+    return false;
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(kGatherWarps * 32)
 gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_t row_bytes,
@@ -66,53 +88,54 @@ gather_interleaved_kernel(const uint8_t* __restrict__ head, int64_t rows, int64_
                           uint4* __restrict__ out, int32_t* bad, int dt) {
     extern __shared__ __align__(16) uint4 tiles[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint4* tile = tiles + wid * 32 * 32;
-    const int nblk = (nchunks + 31) >> 5;
+    uint4* tile = tiles + wid * kGroupRows * kTileChunks;
+    const int nblk = (nchunks + kTileChunks - 1) / kTileChunks;
     const int64_t total = min(group_begin[B], max_groups);
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kGatherWarps;
+    const int half = lane >> 4, sub = lane & 15;
     for (int64_t wg = static_cast<int64_t>(blockIdx.x) * kGatherWarps + wid; wg < total * nblk;
          wg += nwarps) {
         const int64_t g = wg / nblk;
         const int cb = static_cast<int>(wg - g * nblk);
         const GroupMeta m = meta[g];
-        bool safe = true;
-        // lane r fetches the plan id of row r; broadcast per row below
+        // lane r owns the plan id of row r; broadcast per row below
         const bool in_plan = lane < m.nvalid;
         const uint32_t my_id = in_plan ? active_ids[m.idbase + lane] : 0xFFFFFFFFu;
         const bool my_ok = in_plan && static_cast<int64_t>(my_id) < rows;
         if (in_plan && !my_ok && bad) *bad = 1;
         const unsigned ok_mask = __ballot_sync(0xFFFFFFFFu, my_ok);
-        const int64_t c = static_cast<int64_t>(cb) * 32 + lane;
-#pragma unroll 8
-        for (int r = 0; r < 32; ++r) {
+        const int64_t c = static_cast<int64_t>(cb) * kTileChunks + sub;
+        // fill: instruction `it` moves row slices 2*it (lanes 0-15) and 2*it+1
+#pragma unroll
+        for (int it = 0; it < kGroupRows / 2; ++it) {
+            const int r = 2 * it + half;
             const uint32_t id = __shfl_sync(0xFFFFFFFFu, my_id, r);
-            uint4 v = make_uint4(0, 0, 0, 0);
+            uint4* dst = tile + r * kTileChunks + (sub ^ (r & 7));
             if (((ok_mask >> r) & 1u) && c < nchunks) {
                 const uint8_t* src = head + static_cast<int64_t>(id) * row_bytes;
                 if constexpr (VEC)
-                    v = ld_stream_u4(reinterpret_cast<const uint4*>(src) + c);
+                    cp_async_16(dst, reinterpret_cast<const uint4*>(src) + c);
                 else
-                    v = load_chunk_bytes(src, row_bytes, c);
+                    *dst = load_chunk_bytes(src, row_bytes, c);
+            } else {
+                *dst = make_uint4(0, 0, 0, 0);
             }
-            tile[r * 32 + (lane ^ (r & 7))] = v;
-            // exact-FMA eligibility of the gathered weights (GroupMeta.pad)
-            if (dt == SVT_BF16)
-                safe = safe && bf16_fma_safe(v.x) && bf16_fma_safe(v.y) && bf16_fma_safe(v.z) &&
-                       bf16_fma_safe(v.w);
-            else if (dt == SVT_F16)
-                safe = safe && f16_fma_safe(v.x) && f16_fma_safe(v.y) && f16_fma_safe(v.z) &&
-                       f16_fma_safe(v.w);
-            else
-                safe = false;
+        }
+        if constexpr (VEC) cp_async_wait_all();
+        __syncwarp();
+        // drain chunk-major: chunk-row cc of the tile = 32 lanes x 16 B
+        bool safe = true;
+        uint4* dst = out + g * static_cast<int64_t>(nchunks) * kGroupRows;
+#pragma unroll
+        for (int cc = 0; cc < kTileChunks; ++cc) {
+            const int64_t ch = static_cast<int64_t>(cb) * kTileChunks + cc;
+            if (ch < nchunks) {
+                const uint4 v = tile[lane * kTileChunks + (cc ^ (lane & 7))];
+                safe = safe && chunk_fma_safe(v, dt);
+                dst[ch * kGroupRows + lane] = v;
+            }
         }
         if (!__all_sync(0xFFFFFFFFu, safe) && lane == 0) atomicAnd(&meta[g].pad, 0);
-        __syncwarp();
-        uint4* dst = out + g * static_cast<int64_t>(nchunks) * kGroupRows;
-#pragma unroll 8
-        for (int cc = 0; cc < 32; ++cc) {
-            const int64_t ch = static_cast<int64_t>(cb) * 32 + cc;
-            if (ch < nchunks) dst[ch * kGroupRows + lane] = tile[lane * 32 + (cc ^ (lane & 7))];
-        }
         __syncwarp();
     }
 }
@@ -161,26 +184,17 @@ extern "C" svt_status svt_gather_interleaved(const void* d_head, svt_dtype dt, s
     const int64_t row_bytes = static_cast<int64_t>(dim) * esize_of(dt);
     const int32_t nchunks = static_cast<int32_t>((row_bytes + 15) / 16);
     const bool vec = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(d_head) & 15u) == 0;
-    const int64_t work = max_groups * ((nchunks + 31) / 32);
+    const int64_t work = max_groups * ((nchunks + kTileChunks - 1) / kTileChunks);
     const int64_t blocks = (work + kGatherWarps - 1) / kGatherWarps;
-    const int grid = static_cast<int>(blocks < sm_count() * 6 ? blocks : sm_count() * 6);
-    const int smem = kGatherWarps * 32 * 32 * 16;
+    const int grid = static_cast<int>(blocks < sm_count() ? blocks : sm_count());
+    const int smem = kGatherWarps * kGroupRows * kTileChunks * 16;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (vec) {
-        SVT_CUDA_TRY(cudaFuncSetAttribute(gather_interleaved_kernel<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        gather_interleaved_kernel<true><<<grid, kGatherWarps * 32, smem, st>>>(
-            static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
-            d_active_ids, d_group_begin, static_cast<GroupMeta*>(const_cast<void*>(d_group_meta)),
-            batch, max_groups, static_cast<uint4*>(d_sub), d_bad, static_cast<int>(dt));
-    } else {
-        SVT_CUDA_TRY(cudaFuncSetAttribute(gather_interleaved_kernel<false>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        gather_interleaved_kernel<false><<<grid, kGatherWarps * 32, smem, st>>>(
-            static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
-            d_active_ids, d_group_begin, static_cast<GroupMeta*>(const_cast<void*>(d_group_meta)),
-            batch, max_groups, static_cast<uint4*>(d_sub), d_bad, static_cast<int>(dt));
-    }
+    auto kern = vec ? gather_interleaved_kernel<true> : gather_interleaved_kernel<false>;
+    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kGatherWarps * 32, smem, st>>>(
+        static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, nchunks,
+        d_active_ids, d_group_begin, static_cast<GroupMeta*>(const_cast<void*>(d_group_meta)),
+        batch, max_groups, static_cast<uint4*>(d_sub), d_bad, static_cast<int>(dt));
     SVT_LAUNCH_CHECK("gather_interleaved_kernel");
     return SVT_OK;
 }
