@@ -58,6 +58,21 @@ const char* svt_last_error(void);
 int svt_device_count(void);
 size_t svt_dtype_size(svt_dtype dt);
 
+/* Device memory and stream plumbing, so an FFI host (cgo, JNI, ctypes, the
+ * C++ drop-in) needs no CUDA runtime of its own. */
+svt_status svt_set_device(int device);
+svt_status svt_device_alloc(void** d_ptr, size_t bytes);
+svt_status svt_device_free(void* d_ptr);
+svt_status svt_host_alloc_pinned(void** h_ptr, size_t bytes);
+svt_status svt_host_free_pinned(void* h_ptr);
+svt_status svt_memcpy_h2d(void* d_dst, const void* h_src, size_t bytes, svt_stream stream);
+svt_status svt_memcpy_d2h(void* h_dst, const void* d_src, size_t bytes, svt_stream stream);
+svt_status svt_memcpy_d2d(void* d_dst, const void* d_src, size_t bytes, svt_stream stream);
+svt_status svt_memset(void* d_ptr, int value, size_t bytes, svt_stream stream);
+svt_status svt_stream_create(svt_stream* out);
+svt_status svt_stream_destroy(svt_stream stream);
+svt_status svt_stream_synchronize(svt_stream stream);
+
 /* ------------------------------------------------------------------------
  * HeadMatrix::random (head.cpp:89-107) regenerated on device.
  * Element i of the row-major rows x dim matrix = splitmix64(seed+(i+1)*γ)

@@ -53,6 +53,18 @@ _SIGS = {
     "svt_last_error": ([], C.c_char_p),
     "svt_device_count": ([], C.c_int),
     "svt_dtype_size": ([C.c_int], _sz),
+    "svt_set_device": ([C.c_int], C.c_int),
+    "svt_device_alloc": ([C.POINTER(_vp), _sz], C.c_int),
+    "svt_device_free": ([_vp], C.c_int),
+    "svt_host_alloc_pinned": ([C.POINTER(_vp), _sz], C.c_int),
+    "svt_host_free_pinned": ([_vp], C.c_int),
+    "svt_memcpy_h2d": ([_vp, _vp, _sz, _vp], C.c_int),
+    "svt_memcpy_d2h": ([_vp, _vp, _sz, _vp], C.c_int),
+    "svt_memcpy_d2d": ([_vp, _vp, _sz, _vp], C.c_int),
+    "svt_memset": ([_vp, C.c_int, _sz, _vp], C.c_int),
+    "svt_stream_create": ([C.POINTER(_vp)], C.c_int),
+    "svt_stream_destroy": ([_vp], C.c_int),
+    "svt_stream_synchronize": ([_vp], C.c_int),
     "svt_set_tuning": ([C.c_int, C.c_int], None),
     "svt_set_debug": ([_vp], None),
     "svt_head_random": ([_vp, C.c_int, C.c_int, _u64, _u64, _u64, _vp], C.c_int),

@@ -65,9 +65,26 @@ def build_dropin(force=False):
     return out
 
 
+def build_dropin_test(force=False):
+    """C++ test of the drop-in API (tests/cpp), run on the GPU by
+    tests/test_dropin_cpp.py."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    out = os.path.join(LIB, "test_dropin")
+    if not os.path.exists(src):
+        return None
+    deps = [src, os.path.join(ROOT, "tests", "cpp", "mini_test.hpp"),
+            os.path.join(LIB, "libsubvocab_b200.so")]
+    if force or _stale(out, deps):
+        cxx = os.environ.get("CXX", "g++")
+        _run([cxx, "-std=c++20", "-O2", "-ffp-contract=off", "-I", INCLUDE, src, "-o", out,
+              "-L", LIB, "-lsubvocab_b200", "-lsvt", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_all(force=False):
     build_svt(force)
     build_dropin(force)
+    build_dropin_test(force)
 
 
 if __name__ == "__main__":

@@ -95,6 +95,68 @@ int svt_device_count(void) {
     return n;
 }
 size_t svt_dtype_size(svt_dtype dt) { return valid_dtype(dt) ? esize_of(dt) : 0; }
+
+svt_status svt_set_device(int device) {
+    if (svt_status s = need_device()) return s;
+    SVT_CUDA_TRY(cudaSetDevice(device));
+    return SVT_OK;
+}
+svt_status svt_device_alloc(void** d_ptr, size_t bytes) {
+    if (svt_status s = need_device()) return s;
+    SVT_CUDA_TRY(cudaMalloc(d_ptr, bytes ? bytes : 16));
+    return SVT_OK;
+}
+svt_status svt_device_free(void* d_ptr) {
+    if (d_ptr) SVT_CUDA_TRY(cudaFree(d_ptr));
+    return SVT_OK;
+}
+svt_status svt_host_alloc_pinned(void** h_ptr, size_t bytes) {
+    if (svt_status s = need_device()) return s;
+    SVT_CUDA_TRY(cudaMallocHost(h_ptr, bytes ? bytes : 16));
+    return SVT_OK;
+}
+svt_status svt_host_free_pinned(void* h_ptr) {
+    if (h_ptr) SVT_CUDA_TRY(cudaFreeHost(h_ptr));
+    return SVT_OK;
+}
+svt_status svt_memcpy_h2d(void* d_dst, const void* h_src, size_t bytes, svt_stream stream) {
+    if (!bytes) return SVT_OK;
+    SVT_CUDA_TRY(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice,
+                                 static_cast<cudaStream_t>(stream)));
+    return SVT_OK;
+}
+svt_status svt_memcpy_d2h(void* h_dst, const void* d_src, size_t bytes, svt_stream stream) {
+    if (!bytes) return SVT_OK;
+    SVT_CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost,
+                                 static_cast<cudaStream_t>(stream)));
+    return SVT_OK;
+}
+svt_status svt_memcpy_d2d(void* d_dst, const void* d_src, size_t bytes, svt_stream stream) {
+    if (!bytes) return SVT_OK;
+    SVT_CUDA_TRY(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDeviceToDevice,
+                                 static_cast<cudaStream_t>(stream)));
+    return SVT_OK;
+}
+svt_status svt_memset(void* d_ptr, int value, size_t bytes, svt_stream stream) {
+    if (!bytes) return SVT_OK;
+    SVT_CUDA_TRY(cudaMemsetAsync(d_ptr, value, bytes, static_cast<cudaStream_t>(stream)));
+    return SVT_OK;
+}
+svt_status svt_stream_create(svt_stream* out) {
+    if (svt_status s = need_device()) return s;
+    cudaStream_t st;
+    SVT_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    *out = st;
+    return SVT_OK;
+}
+svt_status svt_stream_destroy(svt_stream stream) {
+    if (stream) SVT_CUDA_TRY(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+    return SVT_OK;
+}
+svt_status svt_stream_synchronize(svt_stream stream) {
+    SVT_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return SVT_OK;
+}
 void svt_set_tuning(int warps, int stages) { gemv_set_tuning(warps, stages); }
 void svt_set_debug(void* d_counters) {
     gemv_set_debug(static_cast<unsigned long long*>(d_counters));
