@@ -229,8 +229,8 @@ void svt_set_debug(void* d_counters);
  *   winner; NULL returns row_base + winning row.
  * d_hidden: request b's hidden state at d_hidden + b*hidden_ld (f32; hidden_ld
  *   % 4 == 0 and hidden_ld >= dim). Outputs per request: d_out_ids[b] (global
- *   id), d_out_max[b] (the winning logit, optional), d_out_keys[b] (optional
- *   packed (orderable max << 32 | ~global_row) key for cross-shard combines).
+ *   id), d_out_max[b] (the winning logit, optional), d_out_keys (optional,
+ *   16-byte records per request for svt_shard_combine, see below).
  * row_base/plan_start: for vocab-sharded use (a contiguous slice of a larger
  *   plan); pass 0 / 1 for a whole plan.
  * d_workspace: svt_greedy_workspace_bytes(batch, max_groups) bytes of scratch
@@ -257,12 +257,15 @@ svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_
                             int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
                             uint64_t* d_out_keys, void* d_workspace, svt_stream stream);
 
-/* Cross-shard combine for the vocab-sharded head: given the
- * all-gathered keys of G shards ([G][batch], packed as d_out_keys above) and
- * matching ids/max, pick per request the largest key (max value, ties to the
- * lowest global row == lowest id since shards are contiguous and ascending). */
-svt_status svt_shard_combine(const uint64_t* d_keys, const uint32_t* d_ids,
-                             const float* d_max, int32_t shards, int32_t batch,
+/* Cross-shard combine for the vocab-sharded head. Each shard's
+ * greedy call (with d_out_keys) emits one 16-byte record per request:
+ * { u32 key_lo, u32 key_hi, u32 global id, f32 max }, key = orderable(max)
+ * << 32 | ~(row_base + local row). After an all-gather of the records
+ * ([shards][batch], e.g. ncclAllGather), this picks per request the largest
+ * key: the largest value, ties to the lowest global row — the reference's
+ * first-max scan (head.cpp:213-215) over the whole plan, because shards are
+ * contiguous and ascending. */
+svt_status svt_shard_combine(const void* d_records, int32_t shards, int32_t batch,
                              uint32_t* d_out_ids, float* d_out_max, svt_stream stream);
 
 /* ------------------------------------------------------------------------

@@ -310,36 +310,35 @@ svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, siz
 // ---- cross-shard combine ------------------------------------------------------
 namespace svt {
 namespace {
-__global__ void shard_combine_kernel(const unsigned long long* __restrict__ keys,
-                                     const uint32_t* __restrict__ ids,
-                                     const float* __restrict__ mx, int G, int B,
+// records: [G][B] x {u32 key_lo, u32 key_hi, u32 id, f32 max}; the largest
+// key wins, the first shard on equal keys (keys of distinct rows never tie)
+__global__ void shard_combine_kernel(const uint4* __restrict__ rec, int G, int B,
                                      uint32_t* __restrict__ out_ids, float* __restrict__ out_max) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     unsigned long long best = 0;
-    int bg = -1;
+    uint4 win = rec[b];
     for (int g = 0; g < G; ++g) {
-        const unsigned long long k = keys[static_cast<int64_t>(g) * B + b];
-        if (bg < 0 || k > best) {
+        const uint4 r = rec[static_cast<int64_t>(g) * B + b];
+        const unsigned long long k = (static_cast<unsigned long long>(r.y) << 32) | r.x;
+        if (g == 0 || k > best) {
             best = k;
-            bg = g;
+            win = r;
         }
     }
-    out_ids[b] = ids[static_cast<int64_t>(bg) * B + b];
-    if (out_max) out_max[b] = mx ? mx[static_cast<int64_t>(bg) * B + b] : 0.0f;
+    out_ids[b] = win.z;
+    if (out_max) out_max[b] = __uint_as_float(win.w);
 }
 }  // namespace
 }  // namespace svt
 
-extern "C" svt_status svt_shard_combine(const uint64_t* d_keys, const uint32_t* d_ids,
-                                        const float* d_max, int32_t shards, int32_t batch,
+extern "C" svt_status svt_shard_combine(const void* d_records, int32_t shards, int32_t batch,
                                         uint32_t* d_out_ids, float* d_out_max,
                                         svt_stream stream) {
     if (shards <= 0 || batch <= 0) return SVT_OK;
     if (svt_status s = need_device()) return s;
     shard_combine_kernel<<<(batch + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const unsigned long long*>(d_keys), d_ids, d_max, shards, batch,
-        d_out_ids, d_out_max);
+        static_cast<const uint4*>(d_records), shards, batch, d_out_ids, d_out_max);
     SVT_LAUNCH_CHECK("shard_combine_kernel");
     return SVT_OK;
 }

@@ -108,7 +108,10 @@ __global__ void __launch_bounds__(256) argmax_finalize_kernel(const GemvParams p
             }
             p.out_ids[b] = id;
             if (p.out_max) p.out_max[b] = mx;
-            if (p.out_keys) p.out_keys[b] = k;
+            if (p.out_keys)  // 16-byte shard record {key, id, max} for the combine
+                reinterpret_cast<uint4*>(p.out_keys)[b] =
+                    make_uint4(static_cast<uint32_t>(k), static_cast<uint32_t>(k >> 32), id,
+                               __float_as_uint(mx));
         }
     }
 }

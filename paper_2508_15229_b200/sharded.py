@@ -1,14 +1,16 @@
 """Multi-GPU partitioning of the tailored head.
 
 * batch-shard: requests are split across ranks; every rank runs the whole
-  single-GPU path on its own requests; no collective.
-* vocab-shard: the plan (or the full vocabulary for the identity plan) is
-  cut into G contiguous ascending row ranges; rank g streams only its rows,
-  reduces a packed (orderable max << 32 | ~global_row) key per request on
-  the device, and one all-gather of (key, id, max) records over NCCL lets
-  every rank pick the winner with svt_shard_combine. Because shards are
-  contiguous and ascending, "largest key" == the reference scan's first
-  maximum (head.cpp:213-215) over the whole plan.
+  single-GPU path on its own requests; no collective on the data path.
+* vocab-shard: the plan (here: the full vocabulary, the identity plan) is
+  cut into G contiguous ascending row ranges; rank g streams only its rows
+  and reduces one 16-byte record per request on the device
+  {u64 key = orderable(max) << 32 | ~global_row, u32 id, f32 max}; a single
+  all-gather of the records over NCCL (NVLink/NVSwitch) lets every rank pick
+  the winner with svt_shard_combine. Because the shards are contiguous and
+  ascending, "largest key" is exactly the reference's first-maximum scan
+  (head.cpp:213-215) over the whole plan, including its NaN / signed-zero
+  rules (plan row 0 lives on shard 0, which alone sets plan_start).
 """
 from __future__ import annotations
 
@@ -18,6 +20,8 @@ import torch
 from . import _lib
 from ._lib import call
 from .tailored_head import HeadMatrix, _stream
+
+RECORD_WORDS = 4  # int32 words per shard record
 
 
 def shard_ranges(n: int, G: int):
@@ -32,62 +36,82 @@ def shard_ranges(n: int, G: int):
 
 
 class RowShard:
-    """Rows [r0, r1) of a head (a view into the full head, or a rank-local
-    copy) scored for B hidden states per step with the fused greedy kernel.
-    Source rows are contiguous, so no plan ids are read (identity plan)."""
+    """Rows [r0, r1) of a head — a view into a full device head, or a rank's
+    own slice — scored against B hidden states per step by the fused exact
+    GEMV (identity plan: rows are streamed in place, no ids)."""
 
     def __init__(self, head: HeadMatrix, r0: int, r1: int, B: int, plan_start: bool,
-                 local_rows: torch.Tensor = None):
+                 local_rows: torch.Tensor = None, stream=None):
         self.storage = head.storage
         self.dim = head.dim()
         self.r0, self.n, self.B = r0, r1 - r0, B
         self.rows = local_rows if local_rows is not None else head.data[r0:r1]
         self.plan_start = 1 if plan_start else 0
+        self.stream = stream
         g = (self.n + 31) // 32
         self.max_groups = g * B
         dev = "cuda"
         n_active = torch.full((max(B, 1),), self.n, dtype=torch.int64, device=dev)
         self.group_begin = torch.zeros(B + 1, dtype=torch.int64, device=dev)
         self.group_meta = torch.zeros((max(1, self.max_groups), 8), dtype=torch.int32, device=dev)
-        # identity plan over the slice: no id offsets (row == id index)
-        call("svt_plan_layout", n_active.data_ptr(), None, B, self.group_begin.data_ptr(),
-             self.group_meta.data_ptr(), self.max_groups, _stream(None))
+        if B:
+            call("svt_plan_layout", n_active.data_ptr(), None, B, self.group_begin.data_ptr(),
+                 self.group_meta.data_ptr(), self.max_groups, _stream(stream))
         self.ws = torch.empty(max(1, _lib.lib.svt_greedy_workspace_bytes(B, self.max_groups)),
                               dtype=torch.uint8, device=dev)
-        self.keys = torch.zeros(B, dtype=torch.int64, device=dev)
-        self.ids = torch.zeros(B, dtype=torch.int32, device=dev)
-        self.max = torch.zeros(B, dtype=torch.float32, device=dev)
+        self.ids = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
+        self.records = torch.zeros((max(B, 1), RECORD_WORDS), dtype=torch.int32, device=dev)
 
-    def step(self, hidden: torch.Tensor, stream=None):
-        """hidden [B, ld] f32 on the device -> (keys, ids, max) of this shard."""
+    def step(self, hidden: torch.Tensor) -> torch.Tensor:
+        """hidden [B, ld] f32 on the device -> records [B, 4] int32."""
         if self.n == 0:
-            self.keys.zero_()
-            return self.keys, self.ids, self.max
+            self.records.zero_()  # key 0 never wins
+            return self.records
         call("svt_greedy_fused", self.rows.data_ptr(), self.storage, self.n, self.dim,
              self.group_begin.data_ptr(), self.group_meta.data_ptr(), None, self.B,
-             self.max_groups, hidden.data_ptr(), hidden.stride(0), self.r0,
-             self.plan_start, self.ids.data_ptr(), self.max.data_ptr(), self.keys.data_ptr(),
-             self.ws.data_ptr(), _stream(stream))
-        return self.keys, self.ids, self.max
+             self.max_groups, hidden.data_ptr(), hidden.stride(0), self.r0, self.plan_start,
+             self.ids.data_ptr(), None, self.records.data_ptr(), self.ws.data_ptr(),
+             _stream(self.stream))
+        return self.records
 
 
-def combine(keys: torch.Tensor, ids: torch.Tensor, mx: torch.Tensor, out_ids: torch.Tensor,
-            out_max: torch.Tensor = None, stream=None):
-    """keys/ids/max: [G, B] gathered records -> per-request winner (device)."""
-    G, B = keys.shape
-    call("svt_shard_combine", keys.data_ptr(), ids.data_ptr(), mx.data_ptr(), G, B,
-         out_ids.data_ptr(), None if out_max is None else out_max.data_ptr(), _stream(stream))
+def combine(records: torch.Tensor, out_ids: torch.Tensor, out_max: torch.Tensor = None,
+            stream=None) -> torch.Tensor:
+    """records [G, B, 4] int32 (all-gathered) -> per-request winner ids."""
+    G, B = records.shape[0], records.shape[1]
+    call("svt_shard_combine", records.data_ptr(), G, B, out_ids.data_ptr(),
+         None if out_max is None else out_max.data_ptr(), _stream(stream))
     return out_ids
 
 
-def combine_np(keys: np.ndarray, ids: np.ndarray):
-    """Host restatement of svt_shard_combine (largest key, first shard on
-    equal keys) — used by the gloo tests of the collective protocol."""
-    keys = np.asarray(keys, np.uint64)
-    g = np.argmax(keys, axis=0)  # first maximal shard
-    return np.asarray(ids)[g, np.arange(keys.shape[1])]
+class VocabShardedHead:
+    """One rank's part of a vocab-sharded head under torch.distributed (NCCL):
+    rows shard_ranges(V, world)[rank] held locally; step() = local exact GEMV
+    + argmax -> all_gather_into_tensor of the records -> combine."""
+
+    def __init__(self, head: HeadMatrix, B: int, group=None, local_only: bool = False):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        r0, r1 = shard_ranges(head.rows(), self.world)[self.rank]
+        self.shard = RowShard(head, r0, r1, B, plan_start=(self.rank == 0))
+        self.B = B
+        self.gathered = torch.zeros((self.world, max(B, 1), RECORD_WORDS), dtype=torch.int32,
+                                    device="cuda")
+        self.out = torch.zeros(max(B, 1), dtype=torch.int32, device="cuda")
+
+    def step(self, hidden: torch.Tensor) -> torch.Tensor:
+        rec = self.shard.step(hidden)
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(self.gathered, rec, group=self.group)
+            return combine(self.gathered, self.out)
+        return combine(rec.view(1, *rec.shape), self.out)
 
 
+# ---- host restatements (used by the gloo tests of the protocol) -------------
 def pack_key_np(value: float, row: int, plan_row0: bool = False) -> int:
     """Host restatement of the device key (svt_common.cuh make_key)."""
     v = np.float32(value)
@@ -100,9 +124,28 @@ def pack_key_np(value: float, row: int, plan_row0: bool = False) -> int:
     return (o << 32) | (0xFFFFFFFF - row)
 
 
+def shard_record_np(scores: np.ndarray, row_base: int, plan_start: bool, ids=None):
+    """(key, id) of one shard's scores, as the device finalize computes it."""
+    best = 0
+    for k, s in enumerate(np.asarray(scores, np.float32)):
+        key = pack_key_np(s, row_base + k, plan_start and k == 0)
+        best = max(best, key)
+    if best == 0:
+        return 0, 0xFFFFFFFF
+    row = 0xFFFFFFFF - (best & 0xFFFFFFFF)
+    return best, (int(ids[row - row_base]) if ids is not None else row)
+
+
+def combine_np(keys: np.ndarray, ids: np.ndarray):
+    """Host restatement of svt_shard_combine: largest key, first shard on ties."""
+    keys = np.asarray(keys, np.uint64)
+    g = np.argmax(keys, axis=0)
+    return np.asarray(ids)[g, np.arange(keys.shape[1])]
+
+
 def sharded_greedy_local(head: HeadMatrix, hidden: np.ndarray, G: int) -> np.ndarray:
     """Single-process emulation of the vocab-sharded step (every shard on this
-    GPU, the all-gather replaced by a stack): used by tests."""
+    GPU, the all-gather replaced by a stack): used by the parity tests."""
     B, d = hidden.shape
     ld = (d + 3) // 4 * 4
     h = torch.zeros((B, ld), dtype=torch.float32, device="cuda")
@@ -110,11 +153,7 @@ def sharded_greedy_local(head: HeadMatrix, hidden: np.ndarray, G: int) -> np.nda
     recs = []
     for g, (r0, r1) in enumerate(shard_ranges(head.rows(), G)):
         sh = RowShard(head, r0, r1, B, plan_start=(g == 0))
-        k, i, m = sh.step(h)
-        recs.append((k.clone(), i.clone(), m.clone()))
-    keys = torch.stack([r[0] for r in recs])
-    ids = torch.stack([r[1] for r in recs])
-    mx = torch.stack([r[2] for r in recs])
+        recs.append(sh.step(h).clone())
     out = torch.empty(B, dtype=torch.int32, device="cuda")
-    combine(keys, ids, mx, out)
+    combine(torch.stack(recs), out)
     return out.cpu().numpy().view(np.uint32)
