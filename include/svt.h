@@ -257,6 +257,24 @@ svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_
                             int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
                             uint64_t* d_out_keys, void* d_workspace, svt_stream stream);
 
+/* Certified greedy decode (latency-bound small batches, e.g. batch 1): a
+ * split-K FFMA pass over the interleaved sub-heads streams at full HBM
+ * bandwidth and yields f_r with a rigorous bound |f_r - ref_r| <= B_r
+ * (γ-bounds of both summation orders, directed rounding); only rows whose
+ * interval can reach the maximum are recomputed in the exact reference order
+ * (all rows when any value is non-finite). Ids are identical to
+ * svt_greedy_interleaved / the reference; d_out_max is exact when a
+ * recompute ran and the fast estimate when a single row was certified.
+ * d_workspace: svt_certified_workspace_bytes(batch, max_groups) bytes,
+ * zeroed once by the caller (left zeroed by every call); its last 256 bytes
+ * hold two u32 counters {certified without recompute, recomputed}. */
+size_t svt_certified_workspace_bytes(int32_t batch, int64_t max_groups);
+svt_status svt_greedy_certified(const void* d_sub, svt_dtype dt, size_t dim,
+                                const int64_t* d_group_begin, const void* d_group_meta,
+                                const uint32_t* d_active_ids, int32_t batch, int64_t max_groups,
+                                const float* d_hidden, size_t hidden_ld, uint32_t* d_out_ids,
+                                float* d_out_max, void* d_workspace, svt_stream stream);
+
 /* Cross-shard combine for the vocab-sharded head. Each shard's
  * greedy call (with d_out_keys) emits one 16-byte record per request:
  * { u32 key_lo, u32 key_hi, u32 global id, f32 max }, key = orderable(max)

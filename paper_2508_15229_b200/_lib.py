@@ -90,6 +90,9 @@ _SIGS = {
                                 _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_greedy_fused": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,
                           _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_certified_workspace_bytes": ([_i32, _i64], _sz),
+    "svt_greedy_certified": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp,
+                              _vp, _vp], C.c_int),
     "svt_shard_combine": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),

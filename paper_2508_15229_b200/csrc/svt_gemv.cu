@@ -40,16 +40,21 @@
 
 namespace svt {
 
-constexpr int kCR = 16;  // chunk-rows per stage
-
-template <int SRC>
+// chunk-rows per stage (CR): 16 (8 KB) when many warp pairs share an SM,
+// 64 (32 KB) for latency-bound small batches (one pair per SM), where the
+// per-stage wait/release bookkeeping would otherwise dominate a 64-element
+// stage.
+template <int SRC, int CR>
 __host__ __device__ constexpr int stage_w_bytes() {
-    return SRC == SRC_INTERLEAVED ? kCR * kChunkRowBytes : kGroupRows * (kCR + 1) * kChunkBytes;
+    return SRC == SRC_INTERLEAVED ? CR * kChunkRowBytes : kGroupRows * (CR + 1) * kChunkBytes;
 }
-__host__ __device__ constexpr int stage_h_bytes(int E) { return kCR * E * 4; }
-template <int SRC>
+template <int CR>
+__host__ __device__ constexpr int stage_h_bytes(int E) {
+    return CR * E * 4;
+}
+template <int SRC, int CR>
 __host__ __device__ constexpr int slot_bytes(int E) {
-    return stage_w_bytes<SRC>() + stage_h_bytes(E);
+    return stage_w_bytes<SRC, CR>() + stage_h_bytes<CR>(E);
 }
 
 // ---- shared epilogue ------------------------------------------------------
@@ -129,7 +134,7 @@ __device__ __forceinline__ bool lane_valid(const GemvParams& p, const GroupMeta&
     return true;
 }
 
-template <int DT, int SRC>
+template <int DT, int SRC, int CR>
 __device__ __forceinline__ void load_chunk(const uint8_t* wsl, const float* hsl, int cr, int lane,
                                            float (&wv)[Chunk<DT>::E],
                                            float (&hv)[Chunk<DT>::E]) {
@@ -138,7 +143,7 @@ __device__ __forceinline__ void load_chunk(const uint8_t* wsl, const float* hsl,
     if constexpr (SRC == SRC_INTERLEAVED)
         v = reinterpret_cast<const uint4*>(wsl)[cr * kGroupRows + lane];
     else
-        v = reinterpret_cast<const uint4*>(wsl)[lane * (kCR + 1) + cr];
+        v = reinterpret_cast<const uint4*>(wsl)[lane * (CR + 1) + cr];
     Chunk<DT>::widen(v, wv);
 #pragma unroll
     for (int e = 0; e < E; e += 4) {
@@ -156,12 +161,12 @@ __device__ __forceinline__ void load_chunk(const uint8_t* wsl, const float* hsl,
 // (group, stage) sequence issuing bulk copies; the consumer only waits,
 // computes and releases, so the per-stage address/bookkeeping work never sits
 // in front of the serial FADD chain.
-template <int DT, int SRC, int MODE>
+template <int DT, int SRC, int MODE, int kCR>
 __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
     using CK = Chunk<DT>;
     constexpr int E = CK::E;
-    constexpr int kSlot = slot_bytes<SRC>(E);
-    constexpr int kSlotW = stage_w_bytes<SRC>();
+    constexpr int kSlot = slot_bytes<SRC, kCR>(E);
+    constexpr int kSlotW = stage_w_bytes<SRC, kCR>();
 
     // let the (tiny) argmax finalize grid get scheduled now; it waits for
     // this grid's completion in griddepcontrol.wait
@@ -299,13 +304,17 @@ __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
         const uint8_t* wsl = ring + slot * kSlot;
         const float* hsl = reinterpret_cast<const float*>(wsl + kSlotW);
         bool exact_fma = false;
-        if constexpr (DT != SVT_F32 && SRC == SRC_INTERLEAVED && kCR * E == 128) {
+        if constexpr (DT != SVT_F32 && SRC == SRC_INTERLEAVED && (kCR * E) % 128 == 0) {
             // weights of this group vetted by the gather (GroupMeta.pad);
-            // the stage's 128 hidden values: one float4 per lane + a vote
+            // the stage's kCR*E hidden values: float4s per lane + a vote
             if (cm.pad & 1) {
-                const float4 hq = reinterpret_cast<const float4*>(hsl)[lane];
-                const bool ok = hidden_fma_safe<DT>(hq.x) && hidden_fma_safe<DT>(hq.y) &&
-                                hidden_fma_safe<DT>(hq.z) && hidden_fma_safe<DT>(hq.w);
+                bool ok = true;
+#pragma unroll
+                for (int q4 = 0; q4 < kCR * E / 128; ++q4) {
+                    const float4 hq = reinterpret_cast<const float4*>(hsl)[q4 * 32 + lane];
+                    ok = ok && hidden_fma_safe<DT>(hq.x) && hidden_fma_safe<DT>(hq.y) &&
+                         hidden_fma_safe<DT>(hq.z) && hidden_fma_safe<DT>(hq.w);
+                }
                 exact_fma = __all_sync(0xFFFFFFFFu, ok);
             }
         }
@@ -315,7 +324,7 @@ __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
 #pragma unroll
             for (int cr = 0; cr < kCR; ++cr) {
                 float wv[E], hv[E];
-                load_chunk<DT, SRC>(wsl, hsl, cr, lane, wv, hv);
+                load_chunk<DT, SRC, kCR>(wsl, hsl, cr, lane, wv, hv);
 #pragma unroll
                 for (int e = 0; e < E; ++e) acc = __fmaf_rn(wv[e], hv[e], acc);
             }
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
             float pr[E];
             {
                 float wv[E], hv[E];
-                load_chunk<DT, SRC>(wsl, hsl, 0, lane, wv, hv);
+                load_chunk<DT, SRC, kCR>(wsl, hsl, 0, lane, wv, hv);
 #pragma unroll
                 for (int e = 0; e < E; ++e) pr[e] = __fmul_rn(wv[e], hv[e]);
             }
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
                 float pn[E];
                 if (cr + 1 < kCR) {
                     float wv[E], hv[E];
-                    load_chunk<DT, SRC>(wsl, hsl, cr + 1, lane, wv, hv);
+                    load_chunk<DT, SRC, kCR>(wsl, hsl, cr + 1, lane, wv, hv);
 #pragma unroll
                     for (int e = 0; e < E; ++e) pn[e] = __fmul_rn(wv[e], hv[e]);
                 }
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
             const int cc = min(kCR, p.nchunks - c0);
             for (int cr = 0; cr < cc; ++cr) {
                 float wv[E], hv[E];
-                load_chunk<DT, SRC>(wsl, hsl, cr, lane, wv, hv);
+                load_chunk<DT, SRC, kCR>(wsl, hsl, cr, lane, wv, hv);
                 const int ebase = (c0 + cr) * E;
 #pragma unroll
                 for (int e = 0; e < E; ++e)
@@ -422,20 +431,10 @@ Tuning g_tuning;
 
 constexpr int kSmemBudget = 224 * 1024;  // + <= 2 KB of barriers < 227 KB
 
-template <int DT, int SRC, int MODE>
-svt_status launch_ring(GemvParams p, cudaStream_t st) {
+template <int DT, int SRC, int MODE, int CR>
+svt_status launch_ring_cr(GemvParams p, cudaStream_t st, int nwa, int grid) {
     constexpr int E = Chunk<DT>::E;
-    constexpr int kSlot = slot_bytes<SRC>(E);
-    const int sms = sm_count();
-    const int64_t mg = p.max_groups;
-    if (mg <= 0) return SVT_OK;
-    const int grid = static_cast<int>(mg < sms ? mg : sms);
-    int nwa = static_cast<int>((mg + grid - 1) / grid);
-    // measured on B200 (tools/sweep_decode.py, cfg2 bf16): the interleaved
-    // stream is consumer-bound up to 6 pairs and best at 6 x 3 stages; the
-    // fused row gather is producer-bound and best at 8 pairs
-    const int wmax = g_tuning.warps > 0 ? g_tuning.warps : (SRC == SRC_INTERLEAVED ? 6 : 8);
-    nwa = nwa < 1 ? 1 : (nwa > wmax ? wmax : nwa);
+    constexpr int kSlot = slot_bytes<SRC, CR>(E);
     int S = g_tuning.stages > 0 ? g_tuning.stages : kSmemBudget / (nwa * kSlot);
     if (g_tuning.stages <= 0 && nwa >= 4 && S > 3) S = 3;
     if (S > 32) S = 32;
@@ -447,11 +446,28 @@ svt_status launch_ring(GemvParams p, cudaStream_t st) {
     // 2*S mbarriers
     const int bar_bytes = (nwa * 2 * S * 8 + 127) & ~127;
     const int smem = bar_bytes + nwa * S * kSlot;
-    auto kern = gemv_ring_kernel<DT, SRC, MODE>;
+    auto kern = gemv_ring_kernel<DT, SRC, MODE, CR>;
     SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, nwa * 64, smem, st>>>(p);
     SVT_LAUNCH_CHECK("gemv_ring_kernel");
     return SVT_OK;
+}
+
+template <int DT, int SRC, int MODE>
+svt_status launch_ring(GemvParams p, cudaStream_t st) {
+    const int sms = sm_count();
+    const int64_t mg = p.max_groups;
+    if (mg <= 0) return SVT_OK;
+    const int grid = static_cast<int>(mg < sms ? mg : sms);
+    int nwa = static_cast<int>((mg + grid - 1) / grid);
+    // measured on B200 (tools/sweep_decode.py, cfg2 bf16): the interleaved
+    // stream is consumer-bound up to 6 pairs and best at 6 x 3 stages; the
+    // fused row gather is producer-bound and best at 8 pairs
+    const int wmax = g_tuning.warps > 0 ? g_tuning.warps : (SRC == SRC_INTERLEAVED ? 6 : 8);
+    nwa = nwa < 1 ? 1 : (nwa > wmax ? wmax : nwa);
+    // one pair per SM (small batches): deep 32 KB stages
+    if (nwa == 1 && p.nchunks >= 64) return launch_ring_cr<DT, SRC, MODE, 64>(p, st, nwa, grid);
+    return launch_ring_cr<DT, SRC, MODE, 16>(p, st, nwa, grid);
 }
 
 template <int DT, int SRC, int MODE>

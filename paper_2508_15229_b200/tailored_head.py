@@ -525,6 +525,28 @@ class TailoredBatch:
                  self.ws.data_ptr(), _stream(self.stream))
         return out_ids
 
+    def greedy_certified(self, hidden: torch.Tensor, out_ids: torch.Tensor,
+                         out_max: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Same ids as greedy(): split-K fast pass + error bounds + exact
+        recompute of the candidate rows only (svt_greedy_certified)."""
+        if getattr(self, "cws", None) is None:
+            self.cws = torch.zeros(
+                max(1, _lib.lib.svt_certified_workspace_bytes(self.B, self.max_groups)),
+                dtype=torch.uint8, device="cuda")
+        head = self.head
+        call("svt_greedy_certified", self.sub.data_ptr(), head.storage, head.dim(),
+             self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.active.data_ptr(),
+             self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), out_ids.data_ptr(),
+             _ptr(out_max), self.cws.data_ptr(), _stream(self.stream))
+        return out_ids
+
+    def certified_stats(self):
+        """(steps certified without recompute, steps that recomputed)."""
+        if getattr(self, "cws", None) is None:
+            return 0, 0
+        st = self.cws[-256:].view(torch.int32)[:2].cpu().tolist()
+        return st[0], st[1]
+
     def logits(self, hidden: torch.Tensor, fused: bool = False) -> torch.Tensor:
         """Per-request logits, CSR by plan size (offsets = capacity CSR)."""
         head = self.head

@@ -374,3 +374,71 @@ def test_session_host_api_matches_batched_engine(th):
             assert np.array_equal(ids, o.cpu().numpy().view(np.uint32))
         with pytest.raises(th.IntegrityError, match="out of range"):
             s.prepare(words, V, np.array([V + 5], np.uint32), np.array([0, 1], np.int64))
+
+
+def test_certified_greedy_matches_exact_ids(th):
+    """svt_greedy_certified (split-K + bounds + exact recompute of candidates)
+    returns the reference ids: random steps, exact ties (every row equal),
+    zero hidden, NaN hidden, and near-tie rows."""
+    from paper_2508_15229_b200 import synth
+
+    for V, d, st, B, steps in [(128256, 2048, th.SVT_F32, 1, 6), (151936, 896, th.SVT_BF16, 16, 3)]:
+        head, words, prompts, tb, hid = _build_workload(th, V, d, st, B, 512, 2048, steps)
+        W = head.to_host()
+        ld = (d + 3) // 4 * 4
+        for t in range(steps):
+            h = torch.zeros((B, ld), dtype=torch.float32, device="cuda")
+            h[:, :d] = torch.from_numpy(hid[t]).cuda()
+            a = torch.empty(B, dtype=torch.int32, device="cuda")
+            c = torch.empty(B, dtype=torch.int32, device="cuda")
+            tb.greedy(h, a)
+            tb.greedy_certified(h, c)
+            assert np.array_equal(a.cpu().numpy(), c.cpu().numpy()), (V, t)
+        plan = orc.select(prompts[0], words, V, V)
+        want = orc.greedy_step(orc.gather(W, plan.active_ids), hid[0][0], plan.active_ids)[0]
+        h = torch.zeros((B, ld), dtype=torch.float32, device="cuda")
+        h[:, :d] = torch.from_numpy(hid[0]).cuda()
+        c = torch.empty(B, dtype=torch.int32, device="cuda")
+        tb.greedy_certified(h, c)
+        assert int(c[0].item()) == want
+        # zero hidden: every logit is +0.0 -> lowest row of each plan
+        z = torch.zeros((B, ld), dtype=torch.float32, device="cuda")
+        tb.greedy_certified(z, c)
+        for b in range(B):
+            assert int(c[b].item()) & 0xFFFFFFFF == int(tb.plan(b).active_ids[0])
+        # NaN hidden: non-finite -> all rows recomputed -> row 0 (s[0] is NaN)
+        n = z.clone()
+        n[:, 0] = float("nan")
+        tb.greedy_certified(n, c)
+        a = torch.empty(B, dtype=torch.int32, device="cuda")
+        tb.greedy(n, a)
+        assert np.array_equal(a.cpu().numpy(), c.cpu().numpy())
+        fast, slow = tb.certified_stats()
+        assert fast + slow >= steps + 3
+
+
+def test_certified_near_ties_recompute(th):
+    """Rows whose logits differ in the last bits (sum order decides): the
+    certified path must fall back to the exact recompute and still match."""
+    rows, d = 96, 64
+    rng = np.random.default_rng(5)
+    base = rng.uniform(-1, 1, d).astype(np.float32)
+    W = np.tile(base, (rows, 1))
+    # permute columns per row: same multiset of products, different order
+    for r in range(1, rows):
+        W[r] = base[rng.permutation(d)]
+    h = np.ones(d, np.float32)
+    head = th.HeadMatrix.from_host(W)
+    ids = np.arange(rows, dtype=np.uint32)
+    words = words_from_ids(ids[:0], rows)
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), 0, rows,
+                                torch.from_numpy(ids.view(np.int32)).cuda(),
+                                np.array([0, rows], np.int64))
+    tb.gather(head)
+    hd = torch.from_numpy(h).cuda().view(1, d)
+    a = torch.empty(1, dtype=torch.int32, device="cuda")
+    c = torch.empty(1, dtype=torch.int32, device="cuda")
+    tb.greedy(hd, a)
+    tb.greedy_certified(hd, c)
+    want = orc.greedy_step(W, h, ids)[0]
+    assert int(a.item()) == want and int(c.item()) == want
