@@ -275,6 +275,36 @@ svt_status svt_greedy_certified(const void* d_sub, svt_dtype dt, size_t dim,
                                 const float* d_hidden, size_t hidden_ld, uint32_t* d_out_ids,
                                 float* d_out_max, void* d_workspace, svt_stream stream);
 
+/* ------------------------------------------------------------------------
+ * Batched prefill-scoring on the tensor cores (tcgen05/TMEM, BASELINE cfg3):
+ * for `sequences` x `positions` hidden states (bf16, row-major, sequence s's
+ * positions contiguous), and per-sequence sub-heads gathered row-major into
+ * one bf16 buffer (sequence s = rows [d_row_offsets[s], +d_n_rows[s]) of
+ * d_subheads, total_sub_rows rows), return for every position the reference
+ * greedy id (argmax of the sequential f32 dot products, first max, remapped
+ * through d_plan_ids[d_id_offsets[s] + row]). The logits come from
+ * tcgen05.mma (bf16 x bf16 -> f32 in TMEM); ids are certified against the
+ * reference with a rigorous error bound and recomputed in the exact order
+ * where the bound cannot separate candidates (see svt_prefill.cu).
+ * positions % 128 == 0, dim % 64 == 0. d_out_max receives the winning logit
+ * (exact when recomputed, tensor-core value otherwise).
+ * d_workspace: svt_prefill_workspace_bytes(sequences, positions) bytes; it
+ * starts with the per-position top-8 tensor-core logits (f32 [npos][8]) and
+ * rows (u32 [npos][8]). */
+size_t svt_prefill_workspace_bytes(int32_t sequences, int32_t positions);
+/* d_head_row_norms: upward-rounded L2 norms of the full head's rows
+ * (svt_row_norms_bf16 on the head, computed once per head); they bound
+ * Σ|w h| in the certification. */
+svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads, int64_t total_sub_rows,
+                             const int64_t* d_row_offsets, const int64_t* d_n_rows,
+                             const uint32_t* d_plan_ids, const int64_t* d_id_offsets,
+                             const float* d_head_row_norms, int32_t sequences, int32_t positions,
+                             int32_t dim, uint32_t* d_out_ids, float* d_out_max,
+                             void* d_workspace, svt_stream stream);
+/* Upward-rounded L2 norm of each row of a bf16 matrix (dim % 8 == 0). */
+svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int32_t dim, float* d_out,
+                              svt_stream stream);
+
 /* Cross-shard combine for the vocab-sharded head. Each shard's
  * greedy call (with d_out_keys) emits one 16-byte record per request:
  * { u32 key_lo, u32 key_hi, u32 global id, f32 max }, key = orderable(max)

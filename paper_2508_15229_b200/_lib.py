@@ -93,6 +93,10 @@ _SIGS = {
     "svt_certified_workspace_bytes": ([_i32, _i64], _sz),
     "svt_greedy_certified": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp,
                               _vp, _vp], C.c_int),
+    "svt_prefill_workspace_bytes": ([_i32, _i32], _sz),
+    "svt_prefill_score": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
+                           _vp, _vp], C.c_int),
+    "svt_row_norms_bf16": ([_vp, _i64, _i32, _vp, _vp], C.c_int),
     "svt_shard_combine": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),

@@ -1,0 +1,69 @@
+"""Batched prefill-scoring over per-sequence tailored heads (BASELINE cfg3)
+on the tcgen05 tensor cores, with certified reference-exact ids
+(svt_prefill_score)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .tailored_head import HeadMatrix, SVT_BF16, _stream
+
+
+class PrefillScorer:
+    """Plans (one per sequence) + their gathered row-major bf16 sub-heads.
+
+    plans_ids: concatenated plan ids (device u32 / int32 view), id_offsets
+    [S+1] (host int64). positions must be a multiple of 128 and d of 64."""
+
+    def __init__(self, head: HeadMatrix, plan_ids: torch.Tensor, id_offsets: np.ndarray,
+                 positions: int, stream=None):
+        if head.storage != SVT_BF16:
+            raise _lib.ConfigError("prefill scoring runs on bf16 heads")
+        self.head, self.P, self.stream = head, positions, stream
+        self.S = len(id_offsets) - 1
+        self.d = head.dim()
+        n_rows = np.diff(id_offsets).astype(np.int64)
+        self.total = int(n_rows.sum())
+        self.n_rows = torch.from_numpy(n_rows).cuda()
+        self.row_off = torch.from_numpy(np.ascontiguousarray(id_offsets[:-1], np.int64)).cuda()
+        self.id_off = self.row_off
+        self.plan_ids = plan_ids
+        self.sub = torch.empty((max(1, self.total), self.d), dtype=torch.bfloat16, device="cuda")
+        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        call("svt_gather_rows", head.data.data_ptr(), head.storage, head.rows(), self.d,
+             plan_ids.data_ptr(), self.total, self.sub.data_ptr(), bad.data_ptr(),
+             _stream(stream))
+        self.ws = torch.zeros(_lib.lib.svt_prefill_workspace_bytes(self.S, positions),
+                              dtype=torch.uint8, device="cuda")
+        # per-head row norms (once per head) bound Σ|w h| in the certification
+        if getattr(head, "row_norms", None) is None:
+            head.row_norms = torch.empty(head.rows(), dtype=torch.float32, device="cuda")
+            call("svt_row_norms_bf16", head.data.data_ptr(), head.rows(), self.d,
+                 head.row_norms.data_ptr(), _stream(stream))
+
+    def score(self, hidden: torch.Tensor, out_ids: torch.Tensor, out_max=None) -> torch.Tensor:
+        """hidden: bf16 [S*P, d] on the device -> out_ids int32 [S*P]."""
+        call("svt_prefill_score", hidden.data_ptr(), self.sub.data_ptr(), self.total,
+             self.row_off.data_ptr(), self.n_rows.data_ptr(), self.plan_ids.data_ptr(),
+             self.id_off.data_ptr(), self.head.row_norms.data_ptr(), self.S, self.P, self.d,
+             out_ids.data_ptr(),
+             None if out_max is None else out_max.data_ptr(), self.ws.data_ptr(),
+             _stream(self.stream))
+        return out_ids
+
+    def top8(self):
+        """(values f32 [S*P, 8], rows u32 [S*P, 8]) of the last score()."""
+        npos = self.S * self.P
+        v = self.ws[: npos * 32].view(torch.float32).view(npos, 8)
+        r = self.ws[npos * 32: npos * 64].view(torch.int32).view(npos, 8)
+        return v, r
+
+    def stats(self):
+        """Counters of the last score(): (certified without recompute,
+        recomputed, recomputed over all rows, with a non-finite logit)."""
+        npos = self.S * self.P
+        off = (npos * (8 * 8 + 4) + self.S * 4 + npos + 15) // 16 * 16
+        st = self.ws[off: off + 16].view(torch.int32).cpu().tolist()
+        return tuple(st)

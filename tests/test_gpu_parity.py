@@ -442,3 +442,82 @@ def test_certified_near_ties_recompute(th):
     tb.greedy_certified(hd, c)
     want = orc.greedy_step(W, h, ids)[0]
     assert int(a.item()) == want and int(c.item()) == want
+
+
+@pytest.mark.parametrize("S,P,d,V,nT,L", [(3, 128, 256, 6000, 500, 400), (2, 256, 512, 20000, 900, 700)])
+def test_prefill_scoring_tcgen05_ids_exact(th, S, P, d, V, nT, L):
+    """cfg3-style batched prefill scoring on tcgen05: every position's id
+    equals the reference greedy id over its sequence's plan; the tensor-core
+    top-1 logit lies within the certification bound of the exact logit."""
+    from paper_2508_15229_b200 import prefill, synth
+
+    head = th.HeadMatrix.random(V, d, 0x5EED, storage=th.SVT_BF16)
+    W = head.to_host()
+    rng = np.random.default_rng(S * 1000 + d)
+    words = words_from_ids(rng.choice(V, nT, replace=False), V)
+    plans = [orc.select(rng.integers(0, V, L).astype(np.uint32), words, V, V).active_ids
+             for _ in range(S)]
+    off = np.zeros(S + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in plans])
+    ids = torch.from_numpy(np.concatenate(plans).view(np.int32)).cuda()
+    sc = prefill.PrefillScorer(head, ids, off, P)
+    hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
+    hdev = torch.from_numpy(hid).cuda().to(torch.bfloat16)
+    out = torch.empty(S * P, dtype=torch.int32, device="cuda")
+    sc.score(hdev, out)
+    got = out.cpu().numpy().view(np.uint32)
+    tv, tr = sc.top8()
+    tv, tr = tv.cpu().numpy(), tr.cpu().numpy().view(np.uint32)
+    u = 2.0 ** -24
+    gam = lambda n: n * u / (1 - n * u)  # noqa: E731
+    worst = 0.0
+    for s in range(S):
+        sub = orc.gather(W, plans[s])
+        wmax = np.sqrt((sub.astype(np.float64) ** 2).sum(1)).max()
+        for p in range(P):
+            pos = s * P + p
+            want, _ = orc.greedy_step(sub, hid[pos], plans[s])
+            assert got[pos] == want, (s, p)
+            exact = float(orc.logits(sub[tr[pos, 0]: tr[pos, 0] + 1], hid[pos])[0])
+            bound = (gam(2 * d) + gam(d)) * np.sqrt((hid[pos].astype(np.float64) ** 2).sum()) * wmax
+            worst = max(worst, abs(float(tv[pos, 0]) - exact) / bound)
+    assert worst < 1.0, worst
+    print("max |tc - exact| / bound =", worst, "stats", sc.stats())
+
+
+@pytest.mark.parametrize("case", ["duplicate_rows", "nonfinite"])
+def test_prefill_scoring_all_rows_fallback(th, case):
+    """Positions the top-8 cannot certify — more than eight rows tied at the
+    maximum (duplicated head rows) or non-finite logits (overflowing hidden
+    states) — go through the grid-wide all-rows recompute and still match the
+    reference greedy ids (first max, NaN rules of head.cpp:203-217)."""
+    from paper_2508_15229_b200 import prefill, synth
+
+    V, d, S, P = 3000, 128, 2, 128
+    rng = np.random.default_rng(11)
+    base = synth.round_bf16(rng.uniform(-1, 1, (100, d)).astype(np.float32))
+    W = base[np.arange(V) % 100] if case == "duplicate_rows" else \
+        synth.round_bf16(rng.uniform(-1, 1, (V, d)).astype(np.float32))
+    head = th.HeadMatrix.from_host(W, dtype_bytes=2, storage=th.SVT_BF16)
+    W = head.to_host()
+    plans = [np.sort(rng.choice(V, 1500, replace=False)).astype(np.uint32) for _ in range(S)]
+    off = np.zeros(S + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in plans])
+    ids = torch.from_numpy(np.concatenate(plans).view(np.int32)).cuda()
+    sc = prefill.PrefillScorer(head, ids, off, P)
+    hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
+    if case == "nonfinite":
+        hid[::7] *= np.float32(3e38)  # products overflow: ±inf and inf-inf NaN logits
+        hid[3, :] = np.float32(np.inf)
+        hid = synth.round_bf16(hid)
+    hdev = torch.from_numpy(hid).cuda().to(torch.bfloat16)
+    out = torch.empty(S * P, dtype=torch.int32, device="cuda")
+    sc.score(hdev, out)
+    got = out.cpu().numpy().view(np.uint32)
+    for s in range(S):
+        sub = orc.gather(W, plans[s])
+        for p in range(P):
+            want, _ = orc.greedy_step(sub, hid[s * P + p], plans[s])
+            assert got[s * P + p] == want, (case, s, p)
+    st = sc.stats()
+    assert st[2] > 0, st  # the fallback really ran
