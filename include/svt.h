@@ -301,6 +301,19 @@ svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads, int64
                              const float* d_head_row_norms, int32_t sequences, int32_t positions,
                              int32_t dim, uint32_t* d_out_ids, float* d_out_max,
                              void* d_workspace, svt_stream stream);
+/* Tuning (process-wide): pair 0 forces the single-CTA (cta_group::1) GEMM
+ * (default 1: CTA-pair cta_group::2 whenever positions % 256 == 0); nsplit
+ * in [1, 8] = N-range splits per M tile (default 2), one partial top-8
+ * record per (position, split). svt_prefill_offsets gives byte offsets in
+ * the workspace of: [0] top values f32 [S*P][nsplit][8], [1] top rows u32
+ * [S*P][nsplit][8], [2] counters u32 [8] (certified directly, recomputed,
+ * all-rows, non-finite, all-rows list, max |S_s|, candidate pairs,
+ * recomputed positions), [3] profiling cycle counters u64 [8].
+ * out_max of svt_prefill_score: the exact reference logit for recomputed
+ * positions, the tensor-core logit for positions certified directly. */
+svt_status svt_prefill_set_tuning(int32_t pair, int32_t nsplit);
+void svt_prefill_get_tuning(int32_t* pair, int32_t* nsplit);
+void svt_prefill_offsets(int32_t sequences, int32_t positions, int64_t* out4);
 /* Upward-rounded L2 norm of each row of a bf16 matrix (dim % 8 == 0). */
 svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int32_t dim, float* d_out,
                               svt_stream stream);

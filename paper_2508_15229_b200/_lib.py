@@ -97,6 +97,9 @@ _SIGS = {
     "svt_prefill_score": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
                            _vp, _vp], C.c_int),
     "svt_row_norms_bf16": ([_vp, _i64, _i32, _vp, _vp], C.c_int),
+    "svt_prefill_set_tuning": ([_i32, _i32], C.c_int),
+    "svt_prefill_get_tuning": ([_vp, _vp], None),
+    "svt_prefill_offsets": ([_i32, _i32, _vp], None),
     "svt_shard_combine": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),

@@ -35,6 +35,7 @@
 //    the top-8 overflowed or a value was non-finite) in the exact reference
 //    order and applies the reference's tie / NaN rules.
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda.h>
 
@@ -43,43 +44,104 @@
 namespace svt {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, TOPK = 8;
-constexpr int kTileA = BM * BK * 2;  // 16 KB
-constexpr int kTileB = BN * BK * 2;  // 32 KB
-constexpr int kStage = kTileA + kTileB;
+constexpr int BM = 128, BN = 256, BK = 64, TOPK = 8;
+constexpr int kMaxSplit = 8;  // N-range splits per M tile (partial top-8 records per position)
+constexpr int kTileA = BM * BK * 2;  // 16 KB: this CTA's 128 positions x 64 K
 constexpr int kGemmThreads = 192;
 constexpr uint32_t kTmemCols = 512;  // two 128 x 256 f32 accumulators
 
+// Per-CTA-group-size geometry: NCTA = 1 (cta_group::1, M=128) or 2
+// (cta_group::2 CTA pair, M=256; each CTA holds half of the N=256 B tile)
+template <int NCTA>
+struct Geo {
+    static constexpr int kTileB = (BN / NCTA) * BK * 2;  // this CTA's B rows
+    static constexpr int kStage = kTileA + kTileB;
+    static constexpr int kStages = NCTA == 1 ? 4 : 6;
+    static constexpr int kEpiStage = 64 * 128 * 4;  // 64 columns x 128 positions (f32), insertion path
+    static constexpr int kSmem = kStages * kStage + kEpiStage + 1024 /*align*/ + 256 /*barriers*/;
+    // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major
+    static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                       (uint32_t(BN >> 3) << 17) |
+                                       (uint32_t((BM * NCTA) >> 4) << 24);
+};
+
 struct PrefillParams {
-    int P;                 // positions per sequence (multiple of 128)
+    int P;                 // positions per sequence (multiple of 128 * NCTA)
     int S;                 // sequences
     int dim;               // K (multiple of 64)
+    int nsplit;            // N-range splits per M tile
+    int mode;              // profiling only: bit0 no top-8 work, bit1 no TMA, bit2 no MMA,
+                           // bit3 per-role wait/work cycle counters into dbg[0..7]
+    unsigned long long* dbg;
     const int64_t* n_rows;     // [S] |S_s|
     const int64_t* row_off;    // [S] first row of W_s in the concatenated sub-heads
-    float* top_val;            // [S*P][TOPK]
-    uint32_t* top_row;         // [S*P][TOPK]
-    uint8_t* flags;            // [S*P] bit0: non-finite logit seen
+    float* top_val;            // [S*P][nsplit][TOPK] partial top-8 per N range
+    uint32_t* top_row;         // [S*P][nsplit][TOPK]
+    uint8_t* flags;            // [S*P][nsplit] bit0: non-finite logit seen
 };
 
 // ---- PTX wrappers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+template <int NCTA>
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
+                                            uint32_t bar_cluster_addr) {
+    if constexpr (NCTA == 1) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster_addr)
+            : "memory");
+    } else {
+        // the completion lands on the leader CTA's barrier
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster_addr)
+            : "memory");
+    }
 }
+template <int NCTA>
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t cols) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(smem_result)),
-                 "r"(cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (NCTA == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(smem_result)),
+                     "r"(cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(smem_result)),
+                     "r"(cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
 }
+template <int NCTA>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
-                 : "memory");
+    if constexpr (NCTA == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+                     : "memory");
+    else
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+                     : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -87,36 +149,64 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+// arrive on `bar` once all previously issued MMAs complete; for the CTA pair
+// the arrive is multicast to the same barrier in both CTAs
+template <int NCTA>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(bar))
-        : "memory");
+    if constexpr (NCTA == 1)
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(bar))
+            : "memory");
+    else
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+            "[%0], %1;" ::"r"(smem_u32(bar)),
+            "h"(static_cast<uint16_t>(0x3))
+            : "memory");
 }
+template <int NCTA>
 __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (NCTA == 1)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+            : "memory");
 }
-// 32 lanes x 32 columns of 32-bit accumulators: thread t gets its lane's 32
-// consecutive columns
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// 32 lanes x 64 columns of 32-bit accumulators (two .x32 loads, one wait):
+// thread t gets its lane's 64 consecutive columns
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
         "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+        "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
           "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
           "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
           "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]),
+          "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
+          "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+          "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]),
+          "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]),
+          "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr), "r"(taddr + 32u)
+        : "memory");
 }
 
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms of
@@ -131,103 +221,143 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     return d;
 }
 
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=256
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
-                            (uint32_t(BM >> 4) << 24);
-
+// NCTA == 2: a cluster of two CTAs (one TPC) computes a 256-position x 256-row
+// tile per N step with cta_group::2 MMAs issued by the leader (rank 0). Each
+// CTA stages its own 128 positions (A) and half of the 256 plan rows (B), so
+// per-CTA L2->SMEM traffic per K step drops from 48 KB to 32 KB for the same
+// MMA time. TMA completions land on the leader's full barriers; MMA commits
+// are multicast to both CTAs' empty / accumulator-full barriers; both CTAs'
+// epilogue warps release the accumulator on the leader's barrier.
+template <int NCTA>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
                     const __grid_constant__ CUtensorMap tmW, const PrefillParams p) {
+    using G = Geo<NCTA>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-align the ring (TMA 128B swizzle + UMMA descriptors)
+    // 1024-align the ring (TMA 128B swizzle + UMMA descriptors); the offset is
+    // the same in both CTAs of a pair
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * kStage);
-    uint64_t* empty = full + STAGES;
-    uint64_t* acc_full = empty + STAGES;
+    float* epi = reinterpret_cast<float*>(ring + G::kStages * G::kStage);  // [64][128]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + G::kStages * G::kStage + G::kEpiStage);
+    uint64_t* empty = full + G::kStages;
+    uint64_t* acc_full = empty + G::kStages;
     uint64_t* acc_empty = acc_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int mt_per_seq = p.P / BM;
-    const int s = blockIdx.x / mt_per_seq;
-    const int mt = blockIdx.x - s * mt_per_seq;
+    const uint32_t rank = NCTA == 2 ? cluster_rank() : 0u;
+    // tile order: (sequence, M tile, N split) with the split fastest, so the
+    // CTAs resident at once share one or two sequences' H rows and W_s in L2
+    const int mt_per_seq = p.P / (BM * NCTA);
+    const int group = blockIdx.x / NCTA;
+    const int split = group % p.nsplit;
+    const int mtile = group / p.nsplit;
+    const int s = mtile / mt_per_seq;
+    const int m0 = (mtile - s * mt_per_seq) * BM * NCTA + static_cast<int>(rank) * BM;
     const int64_t nrows = p.n_rows[s];
-    const int ntiles = static_cast<int>((nrows + BN - 1) / BN);
+    const int ntiles_all = static_cast<int>((nrows + BN - 1) / BN);
+    const int per_split = (ntiles_all + p.nsplit - 1) / p.nsplit;
+    const int t0 = split * per_split;
+    const int t1 = min(ntiles_all, t0 + per_split);
+    const int ntiles = t1 > t0 ? t1 - t0 : 0;
     const int kiters = p.dim / BK;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < STAGES; ++i) {
+        for (int i = 0; i < G::kStages; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 4);  // one arrive per epilogue warp
+            mbar_init(&acc_empty[i], 4 * NCTA);  // one arrive per epilogue warp of the group
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 1) tmem_alloc<NCTA>(tmem_slot, kTmemCols);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (NCTA == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ---- TMA producer ----
+        // ---- TMA producer (each CTA loads its own A rows and half of B) ----
         if (lane == 0) {
-            const int ya = s * p.P + mt * BM;
-            const int yb0 = static_cast<int>(p.row_off[s]);
+            const int ya = s * p.P + m0;
+            const int yb0 = static_cast<int>(p.row_off[s]) + static_cast<int>(rank) * (BN / NCTA);
             int stage = 0;
             uint32_t phase = 0;
+            long long prod_wait = 0;
             for (int nt = 0; nt < ntiles; ++nt) {
                 for (int kt = 0; kt < kiters; ++kt) {
+                    const long long tw0 = clock64();
                     mbar_wait_parity(&empty[stage], phase ^ 1u);
-                    uint8_t* sa = ring + stage * kStage;
-                    mbar_arrive_expect_tx(&full[stage], kStage);
-                    tma_load_2d(sa, &tmH, kt * BK, ya, &full[stage]);
-                    tma_load_2d(sa + kTileA, &tmW, kt * BK, yb0 + nt * BN, &full[stage]);
-                    if (++stage == STAGES) {
+                    prod_wait += clock64() - tw0;
+                    uint8_t* sa = ring + stage * G::kStage;
+                    if (p.mode & 2) {
+                        if (rank == 0) mbar_arrive(&full[stage]);
+                    } else {
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], G::kStage * NCTA);
+                        const uint32_t bar =
+                            NCTA == 2 ? map_to_rank(&full[stage], 0) : smem_u32(&full[stage]);
+                        tma_load_2d<NCTA>(sa, &tmH, kt * BK, ya, bar);
+                        tma_load_2d<NCTA>(sa + kTileA, &tmW, kt * BK, yb0 + (t0 + nt) * BN, bar);
+                    }
+                    if (++stage == G::kStages) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
             }
+            if (p.mode & 8) atomicAdd(&p.dbg[0], static_cast<unsigned long long>(prod_wait));
         }
     } else if (warp == 1) {
-        // ---- MMA issuer ----
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int nt = 0; nt < ntiles; ++nt) {
-            const int acc = nt & 1;
-            const uint32_t acc_phase = static_cast<uint32_t>((nt >> 1) & 1);
-            mbar_wait_parity(&acc_empty[acc], acc_phase ^ 1u);  // epilogue drained it
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-            for (int kt = 0; kt < kiters; ++kt) {
-                mbar_wait_parity(&full[stage], phase);
+        // ---- MMA issuer (the leader CTA only) ----
+        if (rank == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            long long w_acc = 0, w_full = 0, t_start = clock64();
+            for (int nt = 0; nt < ntiles; ++nt) {
+                const int acc = nt & 1;
+                const uint32_t acc_phase = static_cast<uint32_t>((nt >> 1) & 1);
+                long long tw0 = clock64();
+                mbar_wait_parity(&acc_empty[acc], acc_phase ^ 1u);  // epilogues drained it
+                w_acc += clock64() - tw0;
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a_addr = smem_u32(ring + stage * kStage);
-                    const uint32_t b_addr = a_addr + kTileA;
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int kt = 0; kt < kiters; ++kt) {
+                    tw0 = clock64();
+                    mbar_wait_parity(&full[stage], phase);
+                    w_full += clock64() - tw0;
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a_addr = smem_u32(ring + stage * G::kStage);
+                        const uint32_t b_addr = a_addr + kTileA;
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        // advance 16 bf16 (32 B) inside the 128 B swizzle atom
-                        tc_mma_bf16(d_tmem, umma_desc_sw128(a_addr + k * 32),
-                                    umma_desc_sw128(b_addr + k * 32), kIdesc,
-                                    (kt > 0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < BK / 16; ++k) {
+                            if (p.mode & 4) break;
+                            // advance 16 bf16 (32 B) inside the 128 B swizzle atom
+                            tc_mma_bf16<NCTA>(d_tmem, umma_desc_sw128(a_addr + k * 32),
+                                              umma_desc_sw128(b_addr + k * 32), G::kIdesc,
+                                              (kt > 0 || k > 0) ? 1u : 0u);
+                        }
+                        tc_commit<NCTA>(&empty[stage]);  // slot free once these MMAs complete
                     }
-                    tc_commit(&empty[stage]);  // slot free once these MMAs complete
+                    __syncwarp();
+                    if (++stage == G::kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
                 }
+                if (lane == 0) tc_commit<NCTA>(&acc_full[acc]);
                 __syncwarp();
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
             }
-            if (lane == 0) tc_commit(&acc_full[acc]);
-            __syncwarp();
+            if ((p.mode & 8) && lane == 0) {
+                atomicAdd(&p.dbg[1], static_cast<unsigned long long>(w_acc));
+                atomicAdd(&p.dbg[2], static_cast<unsigned long long>(w_full));
+                atomicAdd(&p.dbg[3], static_cast<unsigned long long>(clock64() - t_start));
+            }
         }
     } else {
         // ---- epilogue: one thread per accumulator row (= position) ----
@@ -240,66 +370,102 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
             tv[i] = -FLT_MAX;
             tr[i] = 0xFFFFFFFFu;
         }
-        bool nonfinite = false;
+        // z stays 0 unless some logit is inf or NaN (fma(inf|nan, 0, z) = NaN)
+        float z = 0.0f;
+        long long e_wait = 0, e_work = 0;
         for (int nt = 0; nt < ntiles; ++nt) {
             const int acc = nt & 1;
+            const long long tw0 = clock64();
             mbar_wait_parity(&acc_full[acc], static_cast<uint32_t>((nt >> 1) & 1));
+            const long long tw1 = clock64();
+            e_wait += tw1 - tw0;
             tc_fence_after();
             const uint32_t taddr =
                 tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(taddr + c0, r);
-                const int64_t col0 = static_cast<int64_t>(nt) * BN + c0;
+            for (int c0 = 0; c0 < BN; c0 += 64) {
+                uint32_t r[64];
+                tmem_ld64(taddr + c0, r);
+                const int64_t col0 = static_cast<int64_t>(t0 + nt) * BN + c0;
+                if (p.mode & 1) continue;
+                if (col0 + 64 > nrows) {
+                    // last tile: columns past |S_s| belong to no plan row
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (col0 + j >= nrows) r[j] = __float_as_uint(-FLT_MAX);
+                }
+                // bitmask of values above the current 8th; z catches inf / NaN
+                const float t8 = tv[TOPK - 1];
+                uint32_t lo = 0, hi = 0;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const float v = __uint_as_float(r[j]);
-                    if (col0 + j < nrows) {
-                        nonfinite |= !isfinite(v);
-                        if (v > tv[TOPK - 1]) {
-                            // insertion into the descending top-8
-                            float cv = v;
-                            uint32_t cr = static_cast<uint32_t>(col0 + j);
+                    const float a = __uint_as_float(r[j]), b = __uint_as_float(r[32 + j]);
+                    lo |= (a > t8 ? 1u : 0u) << j;
+                    hi |= (b > t8 ? 1u : 0u) << j;
+                    z = fmaf(a, 0.0f, z);
+                    z = fmaf(b, 0.0f, z);
+                }
+                if (__any_sync(0xFFFFFFFFu, (lo | hi) != 0u)) {
+                    // rare once the top-8 has filled: stage the chunk column-major
+                    // (conflict-free) and insert only the flagged values
 #pragma unroll
-                            for (int i = 0; i < TOPK; ++i) {
-                                if (cv > tv[i]) {
-                                    const float t = tv[i];
-                                    const uint32_t u = tr[i];
-                                    tv[i] = cv;
-                                    tr[i] = cr;
-                                    cv = t;
-                                    cr = u;
-                                }
-                            }
+                    for (int j = 0; j < 64; ++j) epi[j * 128 + row] = __uint_as_float(r[j]);
+                    __syncwarp();
+                    while (lo | hi) {
+                        int j;
+                        if (lo) {
+                            j = __ffs(lo) - 1;
+                            lo &= lo - 1;
+                        } else {
+                            j = 32 + __ffs(hi) - 1;
+                            hi &= hi - 1;
+                        }
+                        float cv = epi[j * 128 + row];
+                        uint32_t cr = static_cast<uint32_t>(col0 + j);
+#pragma unroll
+                        for (int i = 0; i < TOPK; ++i) {
+                            const bool sw = cv > tv[i];
+                            const float t = tv[i];
+                            const uint32_t u = tr[i];
+                            tv[i] = sw ? cv : t;
+                            tr[i] = sw ? cr : u;
+                            cv = sw ? t : cv;
+                            cr = sw ? u : cr;
                         }
                     }
+                    __syncwarp();
                 }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            e_work += clock64() - tw1;
+            if (lane == 0) {
+                if constexpr (NCTA == 2) mbar_arrive_cluster(map_to_rank(&acc_empty[acc], 0));
+                else mbar_arrive(&acc_empty[acc]);
+            }
         }
-        const int64_t pos = static_cast<int64_t>(s) * p.P + mt * BM + row;
+        if ((p.mode & 8) && lane == 0) {
+            atomicAdd(&p.dbg[4], static_cast<unsigned long long>(e_wait));
+            atomicAdd(&p.dbg[5], static_cast<unsigned long long>(e_work));
+            atomicAdd(&p.dbg[6], static_cast<unsigned long long>(ntiles));
+        }
+        const int64_t rec = (static_cast<int64_t>(s) * p.P + m0 + row) * p.nsplit + split;
 #pragma unroll
         for (int i = 0; i < TOPK; ++i) {
-            p.top_val[pos * TOPK + i] = tv[i];
-            p.top_row[pos * TOPK + i] = tr[i];
+            p.top_val[rec * TOPK + i] = tv[i];
+            p.top_row[rec * TOPK + i] = tr[i];
         }
-        p.flags[pos] = nonfinite ? 1 : 0;
+        p.flags[rec] = z != 0.0f ? 1 : 0;
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (NCTA == 2) cluster_sync_all(); else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kTmemCols);
+        tmem_dealloc<NCTA>(tmem_base, kTmemCols);
     }
 }
 
-// ---- norms: upward-rounded ||h_p||_2 per position, max ||w_r||_2 per sequence
-__device__ __forceinline__ float bf16_at(const uint16_t* p, int64_t i) {
-    return __uint_as_float(static_cast<uint32_t>(p[i]) << 16);
-}
+// ---- norms: upward-rounded ||h_p||_2 per position (and per head row, once)
 
 __global__ void norms_kernel(const uint16_t* __restrict__ X, int64_t nrows, int dim,
                              float* __restrict__ out) {
@@ -369,21 +535,29 @@ __device__ __forceinline__ void write_result(unsigned long long best,
                                                    : float_of_ord(static_cast<uint32_t>(best >> 32));
 }
 
-// 4 positions per warp (8 lanes each = the top-8 candidates); positions that
-// need the all-rows fallback (top-8 overflow, non-finite logits) are rare and
-// appended to a list for all_rows_kernel.
+// Phase A — classify. 4 positions per warp (8 lanes each). The threshold
+// thr = M - 2B (M = largest tensor-core logit over the splits) selects the
+// candidates. One candidate: the id is final here. Several: every
+// (position, row) candidate pair is appended to `pairs` for the exact
+// recompute (phase B) and the position to `rec_list` (phase C). A split whose
+// 8th value reaches thr may hold more candidates than it kept, and non-finite
+// logits void the bound: those positions go to all_rows_kernel.
+// stats: [0] certified directly [1] recomputed [2] all-rows [3] non-finite
+// [4] all-rows list length [5] max |S_s| [6] pair count [7] rec_list length.
 __global__ void __launch_bounds__(256)
-certify_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, int P, int S,
-               int dim, const int64_t* __restrict__ n_rows, const int64_t* __restrict__ row_off,
+certify_kernel(int P, int S, const int64_t* __restrict__ n_rows,
                const uint32_t* __restrict__ plan_ids, const int64_t* __restrict__ id_off,
                const float* __restrict__ top_val, const uint32_t* __restrict__ top_row,
-               const uint8_t* __restrict__ flags, const float* __restrict__ hnorm,
+               const uint8_t* __restrict__ flags, int nsplit, const float* __restrict__ hnorm,
                const unsigned int* __restrict__ wmax_bits, float c_rel,
                uint32_t* __restrict__ out_ids, float* __restrict__ out_max,
                unsigned int* __restrict__ stats, int64_t* __restrict__ all_list,
-               unsigned long long* __restrict__ all_keys) {
+               unsigned long long* __restrict__ all_keys, uint2* __restrict__ pairs,
+               uint32_t* __restrict__ rec_list, unsigned long long* __restrict__ pos_keys) {
     const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
-    const unsigned gmask = 0xFFu << (grp * 8);
+    __shared__ unsigned cnt[4];  // block-local counters, flushed once per block
+    if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+    __syncthreads();
     const int64_t npos = static_cast<int64_t>(S) * P;
     const int64_t nslots = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4;
     for (int64_t base = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4;
@@ -392,55 +566,209 @@ certify_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, i
         const bool live = pos < npos;
         const int s = live ? static_cast<int>(pos / P) : 0;
         const int64_t nrows = live ? n_rows[s] : 0;
-        unsigned long long best = 0;
-        bool recompute = false, all_path = false, flagged = false;
-        if (live && nrows > 0) {
-            const uint16_t* h = H + pos * dim;
-            const uint16_t* Ws = W + row_off[s] * dim;
+        const bool work = live && nrows > 0;
+        float thr = FLT_MAX;
+        bool all = false, flg = false;
+        if (work) {
             const float B = __fmul_ru(__fmul_ru(c_rel, hnorm[pos]), __uint_as_float(wmax_bits[s]));
-            const float top = top_val[pos * TOPK];
-            const float thr = __fsub_rd(top, __fmul_ru(2.0f, B));
-            const float tv = top_val[pos * TOPK + sub];
-            const bool all = flags[pos] != 0 || top_val[pos * TOPK + TOPK - 1] >= thr;
-            const bool cand = tv >= thr;
-            const unsigned m = __ballot_sync(gmask, cand) & gmask;
-            all_path = all;
-            flagged = flags[pos] != 0;
-            if (all) {
-                // handed to all_rows_kernel (every row, grid-wide)
-                recompute = true;
-                if (sub == 0) {
-                    const unsigned e = atomicAdd(&stats[4], 1u);
-                    all_list[e] = pos;
-                    all_keys[e] = 0ull;
-                }
-            } else if (__popc(m) == 1) {
-                if (cand) best = make_key(tv, top_row[pos * TOPK + sub], true, false);
-            } else {
-                recompute = true;
-                if (cand) {
-                    const uint32_t r = top_row[pos * TOPK + sub];
-                    const float v = exact_dot_bf16(Ws + static_cast<int64_t>(r) * dim, h, dim);
-                    best = make_key(v, r, true, r == 0);
-                }
+            float top = -FLT_MAX;
+            for (int j = 0; j < nsplit; ++j) {
+                top = fmaxf(top, top_val[(pos * nsplit + j) * TOPK]);
+                flg |= flags[pos * nsplit + j] != 0;
             }
-        } else {
-            (void)__ballot_sync(gmask, false);
+            thr = __fsub_rd(top, __fmul_ru(2.0f, B));
+            all = flg || !(top > -FLT_MAX);  // nothing beat the sentinel
+            for (int j = 0; j < nsplit; ++j)
+                all |= top_val[(pos * nsplit + j) * TOPK + TOPK - 1] >= thr;
         }
-        // max over the 8 lanes of the group
+        // this lane's candidates (entry `sub` of every split)
+        int mine = 0;
+        float one_v = 0.0f;
+        uint32_t one_r = 0;
+        for (int j = 0; j < nsplit; ++j) {
+            const float tv = work ? top_val[(pos * nsplit + j) * TOPK + sub] : -FLT_MAX;
+            if (work && !all && tv >= thr) {
+                ++mine;
+                one_v = tv;
+                one_r = top_row[(pos * nsplit + j) * TOPK + sub];
+            }
+        }
+        int ncand = mine;
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-            const unsigned long long other = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-            best = other > best ? other : best;
+        for (int o = 4; o > 0; o >>= 1) ncand += __shfl_xor_sync(0xFFFFFFFFu, ncand, o);
+        const bool multi = work && !all && ncand > 1;
+        // append the candidate pairs of multi-candidate positions (one atomic per warp)
+        const int npairs = multi ? mine : 0;
+        int incl = npairs;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
         }
-        if (live && sub == 0 && nrows > 0) {
-            if (!all_path) write_result(best, plan_ids + id_off[s], pos, out_ids, out_max);
-            {
-                atomicAdd(&stats[recompute ? 1 : 0], 1u);
-                if (all_path) atomicAdd(&stats[2], 1u);
-                if (flagged) atomicAdd(&stats[3], 1u);
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        unsigned pbase = 0;
+        if (lane == 31 && total) pbase = atomicAdd(&stats[6], static_cast<unsigned>(total));
+        pbase = __shfl_sync(0xFFFFFFFFu, pbase, 31);
+        if (npairs) {
+            unsigned at = pbase + static_cast<unsigned>(incl - npairs);
+            for (int j = 0; j < nsplit; ++j) {
+                const float tv = top_val[(pos * nsplit + j) * TOPK + sub];
+                if (tv >= thr) pairs[at++] = make_uint2(static_cast<uint32_t>(pos),
+                                                        top_row[(pos * nsplit + j) * TOPK + sub]);
             }
         }
+        if (work && sub == 0) {
+            if (all) {
+                const unsigned e = atomicAdd(&stats[4], 1u);
+                all_list[e] = pos;
+                all_keys[e] = 0ull;
+            } else if (multi) {
+                pos_keys[pos] = 0ull;
+                rec_list[atomicAdd(&stats[7], 1u)] = static_cast<uint32_t>(pos);
+            }
+            atomicAdd(&cnt[(all || multi) ? 1 : 0], 1u);
+            if (all) atomicAdd(&cnt[2], 1u);
+            if (flg) atomicAdd(&cnt[3], 1u);
+        }
+        // the single candidate is the reference argmax (value within 2B of
+        // nothing else); the lane holding it writes the result
+        if (work && !all && ncand == 1 && mine == 1)
+            write_result(make_key(one_v, one_r, true, false), plan_ids + id_off[s], pos, out_ids,
+                         out_max);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && cnt[threadIdx.x]) atomicAdd(&stats[threadIdx.x], cnt[threadIdx.x]);
+}
+
+// Phase B — exact reference-order dot products of the candidate pairs, one
+// pair per lane (32 pairs per warp task). Row segments (kSegElems elements
+// of w and h for each of the warp's 32 pairs) are staged global -> shared by
+// the whole warp with cp.async (LDGSTS, 16 B per lane; two rows' 256-byte
+// segments per instruction = full 128-byte lines) into a kRing-deep ring,
+// streamed back to back across tasks, so each serial f32 chain reads shared
+// memory while later segments are in flight. Keys fold into pos_keys with a
+// 64-bit atomicMax (larger value, then lower row, NaN rules of make_key).
+constexpr int kSegElems = 128;                      // 256 B of bf16 per row per segment
+constexpr int kSegStride = kSegElems * 2 + 16;      // padded rows: conflict-free LDS.128
+constexpr int kRing = 6;
+constexpr int kPairWarps = 2;
+constexpr int kPairSmem = kPairWarps * kRing * 64 * kSegStride;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+        "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(static_cast<int>(pred))
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(kPairWarps * 32, 1)
+recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, int P,
+                       int dim, const int64_t* __restrict__ row_off,
+                       const unsigned int* __restrict__ stats, const uint2* __restrict__ pairs,
+                       unsigned long long* __restrict__ pos_keys) {
+    extern __shared__ __align__(16) uint8_t psmem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // slot layout: rows 0-31 = w of pairs 0-31, rows 32-63 = h of pairs 0-31
+    uint8_t* ring = psmem + warp * kRing * 64 * kSegStride;
+    const int64_t count = stats[6];
+    const int64_t ntasks = (count + 31) / 32;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kPairWarps;
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * kPairWarps + warp;
+    if (first >= ntasks) return;
+    const int64_t mytasks = (ntasks - first + nw - 1) / nw;
+    const int nseg = (dim + kSegElems - 1) / kSegElems;
+    const int64_t units = mytasks * nseg;  // (task, segment) units, streamed back to back
+
+    // issue side: row pointers of the task whose segments are being prefetched
+    int64_t iss_task = -1;
+    const uint16_t* iss_w = W;
+    const uint16_t* iss_h = H;
+    bool iss_act = false;
+    auto issue = [&](int64_t u) {
+        const int64_t k = u / nseg;
+        const int seg = static_cast<int>(u - k * nseg);
+        if (k != iss_task) {
+            iss_task = k;
+            const int64_t i = (first + k * nw) * 32 + lane;
+            iss_act = i < count;
+            const uint2 pr = iss_act ? pairs[i] : make_uint2(0u, 0u);
+            iss_w = W + (row_off[iss_act ? pr.x / P : 0] + pr.y) * static_cast<int64_t>(dim);
+            iss_h = H + static_cast<int64_t>(pr.x) * dim;
+        }
+        uint8_t* slot = ring + static_cast<int>(u % kRing) * 64 * kSegStride;
+        const int e0 = seg * kSegElems;
+        const int nch = min(kSegElems, dim - e0) / 8;  // 16-byte chunks per row
+        const int half = lane >> 4, ch = lane & 15;
+#pragma unroll 4
+        for (int r2 = 0; r2 < 16; ++r2) {
+            const int row = 2 * r2 + half;  // pair index whose row this lane copies
+            const uint16_t* w = reinterpret_cast<const uint16_t*>(
+                __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(iss_w), row));
+            const uint16_t* h = reinterpret_cast<const uint16_t*>(
+                __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(iss_h), row));
+            const bool ok = __shfl_sync(0xFFFFFFFFu, iss_act, row) && ch < nch;
+            cp_async16(slot + row * kSegStride + ch * 16, w + e0 + ch * 8, ok);
+            cp_async16(slot + (32 + row) * kSegStride + ch * 16, h + e0 + ch * 8, ok);
+        }
+    };
+    for (int64_t u = 0; u < kRing; ++u) {
+        if (u < units) issue(u);
+        cp_async_commit();  // one group per unit (empty past the end) keeps the count aligned
+    }
+
+    float acc = 0.0f;
+    for (int64_t u = 0; u < units; ++u) {
+        const int64_t k = u / nseg;
+        const int seg = static_cast<int>(u - k * nseg);
+        cp_async_wait<kRing - 1>();  // this lane's copies of unit u have landed
+        __syncwarp();                // ... and every other lane's
+        const uint8_t* slot = ring + static_cast<int>(u % kRing) * 64 * kSegStride;
+        const uint4* sw = reinterpret_cast<const uint4*>(slot + lane * kSegStride);
+        const uint4* sh = reinterpret_cast<const uint4*>(slot + (32 + lane) * kSegStride);
+        const int nch = min(kSegElems, dim - seg * kSegElems) / 8;
+#pragma unroll 4
+        for (int c = 0; c < nch; ++c) {
+            float wa[8], ha[8];
+            Chunk<SVT_BF16>::widen(sw[c], wa);
+            Chunk<SVT_BF16>::widen(sh[c], ha);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc = ref_mac(acc, wa[e], ha[e]);
+        }
+        __syncwarp();  // every lane is done with this slot before it is refilled
+        if (u + kRing < units) issue(u + kRing);
+        cp_async_commit();
+        if (seg == nseg - 1) {
+            const int64_t i = (first + k * nw) * 32 + lane;
+            if (i < count) {
+                const uint2 pr = pairs[i];
+                atomicMax(&pos_keys[pr.x], make_key(acc, pr.y, true, pr.y == 0));
+            }
+            acc = 0.0f;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// Phase C — ids of the recomputed positions from their folded keys.
+__global__ void rec_finalize_kernel(int P, const int64_t* __restrict__ id_off,
+                                    const uint32_t* __restrict__ plan_ids,
+                                    const unsigned int* __restrict__ stats,
+                                    const uint32_t* __restrict__ rec_list,
+                                    const unsigned long long* __restrict__ pos_keys,
+                                    uint32_t* __restrict__ out_ids, float* __restrict__ out_max) {
+    const int64_t count = stats[7];
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t pos = rec_list[e];
+        write_result(pos_keys[pos], plan_ids + id_off[pos / P], pos, out_ids, out_max);
     }
 }
 
@@ -558,9 +886,94 @@ double gamma_n(double n) {
 }  // namespace
 }  // namespace svt
 
+namespace svt {
+namespace {
+bool g_prefill_pair = true;
+int g_prefill_nsplit = 2;
+}
+}  // namespace svt
+using svt::g_prefill_nsplit;
+using svt::g_prefill_pair;
+
+extern "C" svt_status svt_prefill_set_tuning(int32_t pair, int32_t nsplit) {
+    if (nsplit < 1 || nsplit > svt::kMaxSplit) {
+        svt::set_error("prefill nsplit must be in [1, %d]", svt::kMaxSplit);
+        return SVT_ERR_CONFIG;
+    }
+    g_prefill_pair = pair != 0;
+    g_prefill_nsplit = nsplit;
+    return SVT_OK;
+}
+extern "C" void svt_prefill_get_tuning(int32_t* pair, int32_t* nsplit) {
+    if (pair) *pair = g_prefill_pair ? 1 : 0;
+    if (nsplit) *nsplit = g_prefill_nsplit;
+}
+
+namespace svt {
+namespace {
+// Workspace layout for (S, P, nsplit); every region 256-byte aligned.
+struct PrefillLayout {
+    size_t top_val, top_row, hnorm, wmax, flags, stats, dbg, all_list, all_keys, pos_keys,
+        rec_list, pairs, end;
+    PrefillLayout(int64_t S, int64_t P, int64_t ns) {
+        const int64_t npos = S * P;
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            const size_t at = o;
+            o = (o + bytes + 255) & ~size_t(255);
+            return at;
+        };
+        top_val = take(npos * ns * TOPK * 4);
+        top_row = take(npos * ns * TOPK * 4);
+        hnorm = take(npos * 4);
+        wmax = take(S * 4);
+        flags = take(npos * ns);
+        stats = take(8 * 4);
+        dbg = take(8 * 8);
+        all_list = take(npos * 8);
+        all_keys = take(npos * 8);
+        pos_keys = take(npos * 8);
+        rec_list = take(npos * 4);
+        pairs = take(npos * ns * TOPK * 8);
+        end = o;
+    }
+};
+}  // namespace
+}  // namespace svt
+
+namespace svt {
+namespace {
+// One side stream + fork/join events per device (created on first use).
+struct SideStream {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+    static SideStream per_dev[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    SideStream& s = per_dev[dev];
+    if (!s.stream) {
+        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+    }
+    return &s;
+}
+}  // namespace
+}  // namespace svt
+
 extern "C" size_t svt_prefill_workspace_bytes(int32_t sequences, int32_t positions) {
-    const size_t npos = static_cast<size_t>(sequences) * static_cast<size_t>(positions);
-    return npos * (svt::TOPK * 8 + 1 + 4 + 16) + static_cast<size_t>(sequences) * 4 + 1024;
+    return svt::PrefillLayout(sequences, positions, svt::kMaxSplit).end;
+}
+
+extern "C" void svt_prefill_offsets(int32_t sequences, int32_t positions, int64_t* out) {
+    const svt::PrefillLayout L(sequences, positions, g_prefill_nsplit);
+    out[0] = static_cast<int64_t>(L.top_val);
+    out[1] = static_cast<int64_t>(L.top_row);
+    out[2] = static_cast<int64_t>(L.stats);
+    out[3] = static_cast<int64_t>(L.dbg);
 }
 
 extern "C" svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int32_t dim,
@@ -593,55 +1006,116 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t npos = static_cast<int64_t>(sequences) * positions;
     uint8_t* ws = static_cast<uint8_t*>(d_workspace);
-    float* top_val = reinterpret_cast<float*>(ws);
-    uint32_t* top_row = reinterpret_cast<uint32_t*>(top_val + npos * TOPK);
-    float* hnorm = reinterpret_cast<float*>(top_row + npos * TOPK);
-    unsigned int* wmax = reinterpret_cast<unsigned int*>(hnorm + npos);
-    uint8_t* flags = reinterpret_cast<uint8_t*>(wmax + sequences);
-    unsigned int* stats = reinterpret_cast<unsigned int*>(
-        (reinterpret_cast<uintptr_t>(flags + npos) + 15) & ~uintptr_t(15));
-    int64_t* all_list = reinterpret_cast<int64_t*>(stats + 8);
-    unsigned long long* all_keys = reinterpret_cast<unsigned long long*>(all_list + npos);
+    const int ns = g_prefill_nsplit;
+    const PrefillLayout L(sequences, positions, ns);
+    float* top_val = reinterpret_cast<float*>(ws + L.top_val);
+    uint32_t* top_row = reinterpret_cast<uint32_t*>(ws + L.top_row);
+    float* hnorm = reinterpret_cast<float*>(ws + L.hnorm);
+    unsigned int* wmax = reinterpret_cast<unsigned int*>(ws + L.wmax);
+    uint8_t* flags = ws + L.flags;
+    unsigned int* stats = reinterpret_cast<unsigned int*>(ws + L.stats);
+    int64_t* all_list = reinterpret_cast<int64_t*>(ws + L.all_list);
+    unsigned long long* all_keys = reinterpret_cast<unsigned long long*>(ws + L.all_keys);
+    unsigned long long* pos_keys = reinterpret_cast<unsigned long long*>(ws + L.pos_keys);
+    uint32_t* rec_list = reinterpret_cast<uint32_t*>(ws + L.rec_list);
+    uint2* pairs = reinterpret_cast<uint2*>(ws + L.pairs);
+    if (npos > 0xFFFFFFFFll) {
+        set_error("prefill scoring supports at most 2^32 positions per call");
+        return SVT_ERR_CONFIG;
+    }
 
     CUtensorMap mapH, mapW;
     if (svt_status s = make_map(&mapH, d_hidden, static_cast<uint64_t>(npos), dim, BM)) return s;
-    if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows), dim, BN))
+    // the CTA pair (cta_group::2) needs 256-position M tiles
+    const bool pair = positions % (2 * BM) == 0 && g_prefill_pair;
+    if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows), dim,
+                                pair ? BN / 2 : BN))
         return s;
 
     SVT_CUDA_TRY(cudaMemsetAsync(wmax, 0, sizeof(unsigned int) * sequences, st));
     SVT_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(unsigned int), st));
-    norms_kernel<<<sm_count() * 8, 256, 0, st>>>(static_cast<const uint16_t*>(d_hidden), npos,
-                                                  dim, hnorm);
+    // ||h|| (HBM-bound) and the per-sequence max ||w|| are only needed by the
+    // certification: fork them onto a side stream so they overlap the
+    // tensor-bound GEMM; joined before certify_kernel (graph-capture safe)
+    static const bool serial = getenv("SVT_PREFILL_SERIAL") != nullptr;  // A/B switch
+    SideStream* side = serial ? nullptr : side_stream();
+    SideStream inline_side;
+    if (!side) {
+        inline_side.stream = st;
+        side = &inline_side;
+    }
+    if (side->fork) {
+        SVT_CUDA_TRY(cudaEventRecord(side->fork, st));
+        SVT_CUDA_TRY(cudaStreamWaitEvent(side->stream, side->fork, 0));
+    }
+    norms_kernel<<<sm_count() * 4, 256, 0, side->stream>>>(static_cast<const uint16_t*>(d_hidden),
+                                                            npos, dim, hnorm);
     SVT_LAUNCH_CHECK("norms_kernel");
-    plan_wmax_kernel<<<sequences < 1024 ? sequences : 1024, 256, 0, st>>>(
+    plan_wmax_kernel<<<sequences < 1024 ? sequences : 1024, 256, 0, side->stream>>>(
         d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows, sequences, wmax, stats);
     SVT_LAUNCH_CHECK("plan_wmax_kernel");
+    if (side->join) SVT_CUDA_TRY(cudaEventRecord(side->join, side->stream));
 
     PrefillParams p;
     p.P = positions;
     p.S = sequences;
     p.dim = dim;
+    p.nsplit = ns;
+    {
+        const char* m = getenv("SVT_PREFILL_MODE");
+        p.mode = m ? atoi(m) : 0;
+    }
+    p.dbg = reinterpret_cast<unsigned long long*>(ws + L.dbg);
+    if (p.mode & 8) SVT_CUDA_TRY(cudaMemsetAsync(p.dbg, 0, 8 * sizeof(unsigned long long), st));
     p.n_rows = d_n_rows;
     p.row_off = d_row_offsets;
     p.top_val = top_val;
     p.top_row = top_row;
     p.flags = flags;
-    const int smem = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
-    SVT_CUDA_TRY(cudaFuncSetAttribute(prefill_gemm_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    prefill_gemm_kernel<<<sequences * (positions / BM), kGemmThreads, smem, st>>>(mapH, mapW, p);
+    if (pair) {
+        using G = Geo<2>;
+        SVT_CUDA_TRY(cudaFuncSetAttribute(prefill_gemm_kernel<2>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(sequences * (positions / BM) * ns));
+        cfg.blockDim = dim3(kGemmThreads);
+        cfg.dynamicSmemBytes = G::kSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<2>, mapH, mapW, p));
+    } else {
+        using G = Geo<1>;
+        SVT_CUDA_TRY(cudaFuncSetAttribute(prefill_gemm_kernel<1>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+        prefill_gemm_kernel<1><<<sequences * (positions / BM) * ns, kGemmThreads, G::kSmem, st>>>(
+            mapH, mapW, p);
+    }
     SVT_LAUNCH_CHECK("prefill_gemm_kernel");
 
+    if (side->join) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
     const double c = (gamma_n(2.0 * dim) + gamma_n(dim)) * 1.001;
     const int64_t warps = (npos + 3) / 4;
     const int64_t blocks = (warps + 7) / 8;
     certify_kernel<<<static_cast<int>(blocks < sm_count() * 8 ? blocks : sm_count() * 8), 256, 0,
-                     st>>>(
-        static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads),
-        positions, sequences, dim, d_n_rows, d_row_offsets, d_plan_ids, d_id_offsets, top_val,
-        top_row, flags, hnorm, wmax, static_cast<float>(c) * 1.0001f, d_out_ids, d_out_max, stats,
-        all_list, all_keys);
+                     st>>>(positions, sequences, d_n_rows, d_plan_ids, d_id_offsets, top_val, top_row,
+                           flags, ns, hnorm, wmax, static_cast<float>(c) * 1.0001f, d_out_ids,
+                           d_out_max, stats, all_list, all_keys, pairs, rec_list, pos_keys);
     SVT_LAUNCH_CHECK("certify_kernel");
+    SVT_CUDA_TRY(cudaFuncSetAttribute(recompute_pairs_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+    recompute_pairs_kernel<<<sm_count(), kPairWarps * 32, kPairSmem, st>>>(
+        static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads), positions,
+        dim, d_row_offsets, stats, pairs, pos_keys);
+    SVT_LAUNCH_CHECK("recompute_pairs_kernel");
+    rec_finalize_kernel<<<sm_count(), 256, 0, st>>>(positions, d_id_offsets, d_plan_ids, stats,
+                                                    rec_list, pos_keys, d_out_ids, d_out_max);
+    SVT_LAUNCH_CHECK("rec_finalize_kernel");
     all_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(
         static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads),
         positions, dim, d_n_rows, d_row_offsets, stats, all_list, all_keys);

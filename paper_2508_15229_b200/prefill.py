@@ -3,6 +3,8 @@ on the tcgen05 tensor cores, with certified reference-exact ids
 (svt_prefill_score)."""
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -53,17 +55,40 @@ class PrefillScorer:
              _stream(self.stream))
         return out_ids
 
+    @staticmethod
+    def tuning():
+        """(pair, nsplit) of the prefill GEMM (svt_prefill_get_tuning)."""
+        pr, ns = ctypes.c_int32(), ctypes.c_int32()
+        _lib.lib.svt_prefill_get_tuning(ctypes.byref(pr), ctypes.byref(ns))
+        return pr.value, ns.value
+
+    @staticmethod
+    def set_tuning(pair: bool = True, nsplit: int = 2):
+        call("svt_prefill_set_tuning", int(pair), int(nsplit))
+
+    def _offsets(self):
+        out = (ctypes.c_int64 * 4)()
+        _lib.lib.svt_prefill_offsets(self.S, self.P, out)
+        return list(out)
+
     def top8(self):
-        """(values f32 [S*P, 8], rows u32 [S*P, 8]) of the last score()."""
+        """Partial top-8 records of the last score(): (values f32
+        [S*P, nsplit*8], plan rows u32-as-int32 [S*P, nsplit*8])."""
         npos = self.S * self.P
-        v = self.ws[: npos * 32].view(torch.float32).view(npos, 8)
-        r = self.ws[npos * 32: npos * 64].view(torch.int32).view(npos, 8)
+        ns = self.tuning()[1]
+        o = self._offsets()
+        v = self.ws[o[0]: o[0] + npos * ns * 32].view(torch.float32).view(npos, ns * 8)
+        r = self.ws[o[1]: o[1] + npos * ns * 32].view(torch.int32).view(npos, ns * 8)
         return v, r
 
     def stats(self):
-        """Counters of the last score(): (certified without recompute,
-        recomputed, recomputed over all rows, with a non-finite logit)."""
-        npos = self.S * self.P
-        off = (npos * (8 * 8 + 4) + self.S * 4 + npos + 15) // 16 * 16
-        st = self.ws[off: off + 16].view(torch.int32).cpu().tolist()
-        return tuple(st)
+        """Counters of the last score(): (certified directly, recomputed,
+        recomputed over all rows, with a non-finite logit, candidate pairs)."""
+        o = self._offsets()
+        st = self.ws[o[2]: o[2] + 32].view(torch.int32).cpu().tolist()
+        return st[0], st[1], st[2], st[3], st[6]
+
+    def profile_counters(self):
+        """SVT_PREFILL_MODE bit 3 cycle counters of the last score()."""
+        o = self._offsets()
+        return self.ws[o[3]: o[3] + 64].view(torch.int64).cpu().tolist()
