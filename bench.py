@@ -51,9 +51,11 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"],
-                    help="cfg2: batch-shard tailored decode (headline); cfg4: vocab-sharded "
-                         "full-vocab greedy (Gemma-2-2B shape) with an NCCL record all-gather")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
+                    help="cfg2: batch-shard tailored decode (headline); cfg3: batched "
+                         "prefill-scoring on tcgen05 (Llama-3.2-3B shape, 256 seqs x 2048 "
+                         "positions per GPU); cfg4: vocab-sharded full-vocab greedy "
+                         "(Gemma-2-2B shape) with an NCCL record all-gather")
     return ap.parse_args()
 
 
@@ -61,6 +63,9 @@ CFG2 = dict(workload="cfg2: Qwen2.5-0.5B-shaped tailored head, per-request plans
             V=151936, d=896, static=2048, prompt_len=512, dtype="bf16")
 CFG1 = dict(workload="cfg1: Llama-3.2-1B-shaped tailored head, batch 1", V=128256, d=2048,
             static=2048, prompt_len=512, dtype="f32")
+CFG3 = dict(workload="cfg3: Llama-3.2-3B-shaped batched prefill-scoring over per-sequence "
+                     "tailored heads (tcgen05)", V=128256, d=3072, static=2048, prompt_len=2048,
+            positions=2048, dtype="bf16")
 
 
 def dist_env():
@@ -387,11 +392,50 @@ def _cpu_model():
     return None
 
 
+def cpu_reference_prefill(threads, seqs=None, positions_sample=2):
+    """cfg3 on the host cores: the reference select + gather for `seqs`
+    sequences (2048 prompt ids + 2048 static ids each) and greedy_step at
+    `positions_sample` positions per sequence (threads over sequences);
+    positions/s = seqs * 2048 / (t_select_gather + 2048 * t_position)."""
+    seqs = seqs or max(1, min(threads, 16))
+    ref = CpuRef(CFG3, seqs, 0)
+    t_prep, t_pos, used = ref.step(positions_sample, threads)
+    ref.close()
+    P = CFG3["positions"]
+    v = seqs * P / (t_prep + P * t_pos)
+    d = ref.describe(v, used, positions_sample)
+    d["sample"] = (f"{CFG3['workload']}: reference select+gather for {seqs} sequences + greedy_step "
+                   f"at {positions_sample} of {P} positions each, {used} host threads "
+                   f"({_cpu_model()}); positions/s = {seqs}*{P} / (t_select_gather + {P} * "
+                   f"t_position_batch)")
+    return d
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    if args.workload == "cfg3":
+        vals = []
+        for k in range(args.warmup + args.steps):
+            c = cpu_reference_prefill(threads)
+            if k >= args.warmup:
+                vals.append(c["value"])
+        v = statistics.median(vals)
+        c["value"] = v
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (bf16-rounded values)",
+            "data": "synthetic (seeded splitmix64 streams, SURVEY §8d)",
+            "config": {"workload": CFG3["workload"], "V": CFG3["V"], "d": CFG3["d"],
+                       "positions": CFG3["positions"]},
+            "cpu_baseline": c,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
     cfg = CFG2
     ref = CpuRef(cfg, args.batch, 0)
     sample = 2
@@ -439,6 +483,8 @@ def main():
             dist.init_process_group(backend)
     if args.workload == "cfg4":
         return run_vocab_shard(args, torch, dist, world, rank)
+    if args.workload == "cfg3":
+        return run_prefill(args, torch, dist, world, rank)
     from paper_2508_15229_b200 import session as session_mod
     from paper_2508_15229_b200 import synth
     from paper_2508_15229_b200 import tailored_head as th
@@ -585,6 +631,179 @@ def run_vocab_shard(args, torch, dist, world, rank):
         dist.destroy_process_group()
 
 
+def prefill_setup(S, rank, torch, th, synth):
+    """cfg3 inputs on the device: bf16 head, static bitmap, S prompts of 2048
+    ids, S x 2048 bf16 hidden states; plans selected on the device and the
+    scorer built from them (capacity-CSR, no host sync)."""
+    from paper_2508_15229_b200 import prefill
+
+    V, d, P = CFG3["V"], CFG3["d"], CFG3["positions"]
+    head = th.HeadMatrix.random(V, d, synth.SEED_W, storage=th.SVT_BF16)
+    words_h = synth.words_of(synth.static_ids(V, CFG3["static"]), V)
+    prompts = [synth.prompt_ids(V, CFG3["prompt_len"], rank * S + r) for r in range(S)]
+    off = np.zeros(S + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in prompts])
+    flat = np.concatenate(prompts)
+    tb = th.TailoredBatch.build(torch.from_numpy(words_h.view(np.int64)).cuda(), CFG3["static"],
+                                V, torch.from_numpy(flat.view(np.int32)).cuda(), off)
+    sc = prefill.PrefillScorer.from_batch(head, tb, P)
+    hid = torch.empty(S * P * d, dtype=torch.bfloat16, device="cuda")
+    th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_BF16, th.SVT_BF16,
+                 rank * S * P * d, S * P * d, synth.SEED_H, None)
+    out = torch.empty(S * P, dtype=torch.int32, device="cuda")
+    return dict(head=head, tb=tb, sc=sc, hidden=hid.view(S * P, d), out=out, words_h=words_h,
+                flat=flat, off=off)
+
+
+def prefill_step(st):
+    """One cfg3 step: (a) select + layout for the S sequences, (b) gather of
+    their row-major sub-heads, (c+d) tensor-core scoring with certified
+    reference-exact argmax ids."""
+    st["tb"].run_select()
+    st["sc"].regather()
+    st["sc"].score(st["hidden"], st["out"])
+
+
+def run_prefill(args, torch, dist, world, rank):
+    """cfg3: S=256 sequences x 2048 positions per GPU (batch-shard weak
+    scaling for N>1: each rank scores its own sequences, no collective)."""
+    from paper_2508_15229_b200 import synth
+    from paper_2508_15229_b200 import tailored_head as th
+    import paper_2508_15229_b200._lib as L
+
+    S = args.batch if args.batch != 64 else 256
+    P, d = CFG3["positions"], CFG3["d"]
+    st = prefill_setup(S, rank, torch, th, synth)
+    for _ in range(args.warmup):
+        prefill_step(st)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        a.record()
+        for k in range(args.steps):
+            ev[k][0].record()
+            st["tb"].run_select()
+            ev[k][1].record()
+            st["sc"].regather()
+            ev[k][2].record()
+            st["sc"].score(st["hidden"], st["out"])
+            ev[k][3].record()
+        b.record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = a.elapsed_time(b)
+    sel = statistics.median(e[0].elapsed_time(e[1]) for e in ev)
+    gat = statistics.median(e[1].elapsed_time(e[2]) for e in ev)
+    sco = statistics.median(e[2].elapsed_time(e[3]) for e in ev)
+    if dist is not None and world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    n_rows = st["tb"].n_active.cpu().numpy()
+    flops = 2.0 * P * d * float(n_rows.sum())
+    # dominant kernel (prefill_gemm_kernel) timed alone right after the
+    # timed region: same inputs, certification switched off (mode bit 4)
+    os.environ["SVT_PREFILL_MODE"] = "16"
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(3, args.steps)
+    st["sc"].score(st["hidden"], st["out"])
+    g0.record()
+    for _ in range(reps):
+        st["sc"].score(st["hidden"], st["out"])
+    g1.record()
+    torch.cuda.synchronize()
+    os.environ.pop("SVT_PREFILL_MODE")
+    gemm_ms = g0.elapsed_time(g1) / reps
+    prefill_step(st)  # restore the certified outputs
+    stats = st["sc"].stats()
+    tf_peak, tf_kind = load_tensor_peak()
+    tokens = S * P * args.steps * world
+    result = {
+        "metric": METRIC, "value": tokens / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded splitmix64 streams, SURVEY §8d); random-init head",
+        "config": {"workload": CFG3["workload"], "V": CFG3["V"], "d": d,
+                   "sequences_per_gpu": S, "positions": P, "static_vocab": CFG3["static"],
+                   "prompt_len": CFG3["prompt_len"], "mean_plan_rows": float(n_rows.mean()),
+                   "step": "select + layout + row-major gather + tcgen05 scoring with certified "
+                           "reference-exact ids; tokens = scored positions",
+                   "parallelism": f"batch-shard x{world}",
+                   "l2": "hidden states 3.2 GB + sub-heads 6.4 GB per step > L2, no flush"},
+        "roofline": {"bound": "tensor", "achieved": flops / (gemm_ms / 1e3) / 1e12,
+                     "peak": tf_peak, "unit": "TFLOP/s",
+                     "frac": flops / (gemm_ms / 1e3) / 1e12 / tf_peak, "traffic": None,
+                     "kernel": "prefill_gemm_kernel<2> (cta_group::2, M=256 N=256 K=16)",
+                     "flops_per_launch": flops, "avg_launch_us": gemm_ms * 1e3,
+                     "peak_source": f"MEASURED_PEAKS.json bf16 dense ({tf_kind})",
+                     "step_breakdown_ms": {"select_layout": sel, "gather": gat, "score": sco},
+                     "score_share_of_step": sco * args.steps / ms if world == 1 else None,
+                     "effective_tflops_whole_score": flops / (sco / 1e3) / 1e12},
+        "certification": {"certified_directly": stats[0], "recomputed": stats[1],
+                          "all_rows": stats[2], "non_finite": stats[3],
+                          "candidate_pairs": stats[4]},
+        "gpu_launches": 11 * args.steps, "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_e2e:
+        result["e2e"] = prefill_e2e(st, S, torch, th, L)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_reference_prefill(os.cpu_count() or 1)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def prefill_e2e(st, S, torch, th, L, K=2):
+    """cfg3 through the C-ABI with host buffers: per step H2D of the static
+    bitmap, prompts and 3.2 GB of pinned hidden states, the device path, and
+    D2H of the ids."""
+    P, d = CFG3["positions"], CFG3["d"]
+    hid_h = st["hidden"].cpu().pin_memory()
+    ids_h = torch.empty(S * P, dtype=torch.int32).pin_memory()
+    words_h = torch.from_numpy(st["words_h"].view(np.int64)).pin_memory()
+    flat_h = torch.from_numpy(st["flat"].view(np.int32)).pin_memory()
+    tb = st["tb"]
+
+    def one():
+        tb._words.copy_(words_h, non_blocking=True)
+        tb._prompts.copy_(flat_h, non_blocking=True)
+        st["hidden"].copy_(hid_h, non_blocking=True)
+        prefill_step(st)
+        ids_h.copy_(st["out"], non_blocking=True)
+        torch.cuda.synchronize()
+
+    one()
+    t0 = time.perf_counter()
+    for _ in range(K):
+        one()
+    sec = (time.perf_counter() - t0) / K
+    h2d = hid_h.numel() * 2 + words_h.numel() * 8 + flat_h.numel() * 4
+    return {"value": S * P / sec, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": S * P * 4,
+            "api": "svt_select_batched/svt_gather_plans/svt_prefill_score via ctypes, "
+                   "pinned host buffers, cudaMemcpyAsync in the timed region"}
+
+
+def load_tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        for k in ("bf16_tflops_sustained", "bf16_dense_tflops_sustained", "bf16_tflops"):
+            if k in j:
+                return float(j[k]), f"measured {k}"
+        for k, v in j.items():
+            if "bf16" in k and isinstance(v, (int, float)):
+                return float(v), f"measured {k}"
+    return 2250.0, "nominal fallback"
+
+
 def secondary(args, torch, th, synth):
     """cfg1 (Llama-3.2-1B shape, batch 1, fp32) and the fused variant of cfg2."""
     out = {}
@@ -608,7 +827,37 @@ def secondary(args, torch, th, synth):
     gbs = job.decode_bytes() / (dec_avg / 1e3) / 1e9
     out["cfg2_fused"] = {"tokens_per_s": args.batch * args.decode_steps * 5 / (ms / 1e3),
                          "decode_us": dec_avg * 1e3, "decode_gbs": gbs, "frac": gbs / peak}
+    del job
+    torch.cuda.empty_cache()
+    out["cfg3_prefill"] = prefill_secondary(torch, th, synth)
+    torch.cuda.empty_cache()
     return out
+
+
+def prefill_secondary(torch, th, synth, S=256, K=5, W=3):
+    """cfg3 summary for the default run (full line: --workload cfg3)."""
+    st = prefill_setup(S, 0, torch, th, synth)
+    for _ in range(W):
+        prefill_step(st)
+    torch.cuda.synchronize()
+    a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    a.record()
+    for _ in range(K):
+        prefill_step(st)
+    b.record()
+    for _ in range(K):
+        st["sc"].score(st["hidden"], st["out"])
+    c.record()
+    torch.cuda.synchronize()
+    P, d = CFG3["positions"], CFG3["d"]
+    flops = 2.0 * P * d * float(st["tb"].n_active.sum().item())
+    step_ms, score_ms = a.elapsed_time(b) / K, b.elapsed_time(c) / K
+    r = {"positions_per_s": S * P / (step_ms / 1e3), "step_ms": step_ms, "score_ms": score_ms,
+         "score_effective_tflops": flops / (score_ms / 1e3) / 1e12,
+         "step": "select + gather + tcgen05 scoring, 256 x 2048 positions, d=3072",
+         "certification": list(st["sc"].stats())}
+    del st
+    return r
 
 
 if __name__ == "__main__":

@@ -157,6 +157,15 @@ svt_status svt_plan_layout(const int64_t* d_n_active, const int64_t* d_id_offset
 svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
                            const uint32_t* d_ids, size_t n, void* d_out, int32_t* d_bad,
                            svt_stream stream);
+/* Row-major sub-heads of a batch of plans in capacity-CSR layout (as
+ * svt_select_batched writes them): out row k = W[active[k]] for every live
+ * slot k in [act_off[b], act_off[b] + n_active[b]); capacity slack is left
+ * untouched. Device arrays; act_off has batch+1 entries. The batched form of
+ * gather (head.cpp:176-187) feeding svt_prefill_score. */
+svt_status svt_gather_plans(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                            const uint32_t* d_active_ids, const int64_t* d_act_off,
+                            const int64_t* d_n_active, int32_t batch, int64_t total_capacity,
+                            void* d_out, int32_t* d_bad, svt_stream stream);
 
 /* Gather into the lane-interleaved sub-head layout consumed by the decode
  * kernel: for group g, 16-byte chunk c, lane l (plan row row0(g)+l):

@@ -75,6 +75,8 @@ _SIGS = {
     "svt_bitset_insert": ([_vp, _sz, _sz, _vp, _vp, _vp], C.c_int),
     "svt_union_plans": ([_vp, _vp, _i32, _sz, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_plan_layout": ([_vp, _vp, _i32, _vp, _vp, _i64, _vp], C.c_int),
+    "svt_gather_plans": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp],
+                         C.c_int),
     "svt_gather_rows": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_subhead_bytes": ([C.c_int, _sz, _i64], _sz),
     "svt_gather_interleaved": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp],

@@ -21,6 +21,33 @@ namespace {
 constexpr int kGatherWarps = 24;
 constexpr int kTileChunks = 16;  // 16-byte chunks per row slice in a tile
 
+// copy one row (warp-wide): 8 independent 16-byte loads per lane in flight
+// before their stores, so a 6 KB row costs ~2 memory latencies, not 12
+__device__ __forceinline__ void copy_row_warp(const uint8_t* __restrict__ src,
+                                              uint8_t* __restrict__ dst, int64_t row_bytes,
+                                              bool vec, int lane) {
+    if (vec) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        const int64_t n4 = row_bytes >> 4;
+        for (int64_t base = 0; base < n4; base += 8 * 32) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = base + u * 32 + lane;
+                if (i < n4) v[u] = ld_stream_u4(s4 + i);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = base + u * 32 + lane;
+                if (i < n4) d4[i] = v[u];
+            }
+        }
+    } else {
+        for (int64_t i = lane; i < row_bytes; i += 32) dst[i] = src[i];
+    }
+}
+
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ head, int64_t rows,
                                    int64_t row_bytes, const uint32_t* __restrict__ ids,
                                    int64_t n, uint8_t* __restrict__ out, int32_t* bad,
@@ -36,15 +63,37 @@ __global__ void gather_rows_kernel(const uint8_t* __restrict__ head, int64_t row
             for (int64_t i = lane; i < row_bytes; i += 32) dst[i] = 0;
             continue;
         }
-        const uint8_t* src = head + static_cast<int64_t>(id) * row_bytes;
-        if (vec) {
-            const uint4* s4 = reinterpret_cast<const uint4*>(src);
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-            const int64_t n4 = row_bytes >> 4;
-            for (int64_t i = lane; i < n4; i += 32) d4[i] = ld_stream_u4(s4 + i);
-        } else {
-            for (int64_t i = lane; i < row_bytes; i += 32) dst[i] = src[i];
+        copy_row_warp(head + static_cast<int64_t>(id) * row_bytes, dst, row_bytes, vec, lane);
+    }
+}
+
+// Row-major sub-heads of a whole batch of plans in capacity-CSR layout
+// (request b's ids at act_off[b] .. act_off[b] + n_active[b]): slot k of the
+// output = W[active[k]] for the live slots; capacity slack is left untouched.
+__global__ void gather_plans_kernel(const uint8_t* __restrict__ head, int64_t rows,
+                                    int64_t row_bytes, const uint32_t* __restrict__ active,
+                                    const int64_t* __restrict__ act_off,
+                                    const int64_t* __restrict__ n_active, int batch,
+                                    int64_t total, uint8_t* __restrict__ out, int32_t* bad,
+                                    bool vec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         k < total; k += nwarps) {
+        int lo = 0, hi = batch;  // request b with act_off[b] <= k < act_off[b+1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (act_off[mid] <= k) lo = mid; else hi = mid;
         }
+        if (k - act_off[lo] >= n_active[lo]) continue;
+        const uint32_t id = active[k];
+        uint8_t* dst = out + k * row_bytes;
+        if (static_cast<int64_t>(id) >= rows) {
+            if (bad && lane == 0) *bad = 1;
+            for (int64_t i = lane; i < row_bytes; i += 32) dst[i] = 0;
+            continue;
+        }
+        copy_row_warp(head + static_cast<int64_t>(id) * row_bytes, dst, row_bytes, vec, lane);
     }
 }
 
@@ -166,6 +215,29 @@ extern "C" svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t r
         static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, d_ids,
         static_cast<int64_t>(n), static_cast<uint8_t*>(d_out), d_bad, vec);
     SVT_LAUNCH_CHECK("gather_rows_kernel");
+    return SVT_OK;
+}
+
+extern "C" svt_status svt_gather_plans(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
+                                       const uint32_t* d_active_ids, const int64_t* d_act_off,
+                                       const int64_t* d_n_active, int32_t batch,
+                                       int64_t total_capacity, void* d_out, int32_t* d_bad,
+                                       svt_stream stream) {
+    using namespace svt;
+    if (dt != SVT_F32 && dt != SVT_F16 && dt != SVT_BF16) {
+        set_error("dtype must be SVT_F32, SVT_F16 or SVT_BF16");
+        return SVT_ERR_CONFIG;
+    }
+    if (batch <= 0 || total_capacity <= 0 || dim == 0) return SVT_OK;
+    const int64_t row_bytes = static_cast<int64_t>(dim) * esize_of(dt);
+    const bool vec = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(d_head) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
+    const int64_t blocks = (total_capacity + 7) / 8;
+    const int grid = static_cast<int>(blocks < sm_count() * 8 ? blocks : sm_count() * 8);
+    gather_plans_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(d_head), static_cast<int64_t>(rows), row_bytes, d_active_ids,
+        d_act_off, d_n_active, batch, total_capacity, static_cast<uint8_t*>(d_out), d_bad, vec);
+    SVT_LAUNCH_CHECK("gather_plans_kernel");
     return SVT_OK;
 }
 

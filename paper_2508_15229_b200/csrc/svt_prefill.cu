@@ -71,7 +71,8 @@ struct PrefillParams {
     int dim;               // K (multiple of 64)
     int nsplit;            // N-range splits per M tile
     int mode;              // profiling only: bit0 no top-8 work, bit1 no TMA, bit2 no MMA,
-                           // bit3 per-role wait/work cycle counters into dbg[0..7]
+                           // bit3 per-role wait/work cycle counters into dbg[0..7],
+                           // bit4 (host) launch the GEMM alone (kernel timing)
     unsigned long long* dbg;
     const int64_t* n_rows;     // [S] |S_s|
     const int64_t* row_off;    // [S] first row of W_s in the concatenated sub-heads
@@ -1032,13 +1033,15 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
                                 pair ? BN / 2 : BN))
         return s;
 
+    const char* mode_env = getenv("SVT_PREFILL_MODE");  // profiling switches (PrefillParams::mode)
+    const int mode = mode_env ? atoi(mode_env) : 0;
     SVT_CUDA_TRY(cudaMemsetAsync(wmax, 0, sizeof(unsigned int) * sequences, st));
     SVT_CUDA_TRY(cudaMemsetAsync(stats, 0, 8 * sizeof(unsigned int), st));
     // ||h|| (HBM-bound) and the per-sequence max ||w|| are only needed by the
     // certification: fork them onto a side stream so they overlap the
     // tensor-bound GEMM; joined before certify_kernel (graph-capture safe)
     static const bool serial = getenv("SVT_PREFILL_SERIAL") != nullptr;  // A/B switch
-    SideStream* side = serial ? nullptr : side_stream();
+    SideStream* side = (serial || (mode & 16)) ? nullptr : side_stream();
     SideStream inline_side;
     if (!side) {
         inline_side.stream = st;
@@ -1048,12 +1051,14 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
         SVT_CUDA_TRY(cudaEventRecord(side->fork, st));
         SVT_CUDA_TRY(cudaStreamWaitEvent(side->stream, side->fork, 0));
     }
-    norms_kernel<<<sm_count() * 4, 256, 0, side->stream>>>(static_cast<const uint16_t*>(d_hidden),
-                                                            npos, dim, hnorm);
-    SVT_LAUNCH_CHECK("norms_kernel");
-    plan_wmax_kernel<<<sequences < 1024 ? sequences : 1024, 256, 0, side->stream>>>(
-        d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows, sequences, wmax, stats);
-    SVT_LAUNCH_CHECK("plan_wmax_kernel");
+    if (!(mode & 16)) {
+        norms_kernel<<<sm_count() * 4, 256, 0, side->stream>>>(
+            static_cast<const uint16_t*>(d_hidden), npos, dim, hnorm);
+        SVT_LAUNCH_CHECK("norms_kernel");
+        plan_wmax_kernel<<<sequences < 1024 ? sequences : 1024, 256, 0, side->stream>>>(
+            d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows, sequences, wmax, stats);
+        SVT_LAUNCH_CHECK("plan_wmax_kernel");
+    }
     if (side->join) SVT_CUDA_TRY(cudaEventRecord(side->join, side->stream));
 
     PrefillParams p;
@@ -1061,10 +1066,7 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
     p.S = sequences;
     p.dim = dim;
     p.nsplit = ns;
-    {
-        const char* m = getenv("SVT_PREFILL_MODE");
-        p.mode = m ? atoi(m) : 0;
-    }
+    p.mode = mode;
     p.dbg = reinterpret_cast<unsigned long long*>(ws + L.dbg);
     if (p.mode & 8) SVT_CUDA_TRY(cudaMemsetAsync(p.dbg, 0, 8 * sizeof(unsigned long long), st));
     p.n_rows = d_n_rows;
@@ -1099,6 +1101,7 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
     SVT_LAUNCH_CHECK("prefill_gemm_kernel");
 
     if (side->join) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
+    if (p.mode & 16) return SVT_OK;  // profiling: the GEMM alone, no certification
     const double c = (gamma_n(2.0 * dim) + gamma_n(dim)) * 1.001;
     const int64_t warps = (npos + 3) / 4;
     const int64_t blocks = (warps + 7) / 8;

@@ -16,28 +16,53 @@ from .tailored_head import HeadMatrix, SVT_BF16, _stream
 class PrefillScorer:
     """Plans (one per sequence) + their gathered row-major bf16 sub-heads.
 
-    plans_ids: concatenated plan ids (device u32 / int32 view), id_offsets
-    [S+1] (host int64). positions must be a multiple of 128 and d of 64."""
+    Two ways in:
+      * ``PrefillScorer(head, plan_ids, id_offsets, positions)``: concatenated
+        plan ids (device u32 / int32 view) and host id_offsets [S+1];
+      * ``PrefillScorer.from_batch(head, tb, positions)``: the capacity-CSR
+        plans a :class:`TailoredBatch` selected on the device (no host sync);
+        :meth:`regather` refreshes the sub-heads after ``tb.run_select()``.
+    positions must be a multiple of 128 and d of 64."""
 
     def __init__(self, head: HeadMatrix, plan_ids: torch.Tensor, id_offsets: np.ndarray,
                  positions: int, stream=None):
-        if head.storage != SVT_BF16:
-            raise _lib.ConfigError("prefill scoring runs on bf16 heads")
-        self.head, self.P, self.stream = head, positions, stream
-        self.S = len(id_offsets) - 1
-        self.d = head.dim()
         n_rows = np.diff(id_offsets).astype(np.int64)
-        self.total = int(n_rows.sum())
+        self._setup(head, positions, len(id_offsets) - 1, int(n_rows.sum()), stream)
         self.n_rows = torch.from_numpy(n_rows).cuda()
         self.row_off = torch.from_numpy(np.ascontiguousarray(id_offsets[:-1], np.int64)).cuda()
         self.id_off = self.row_off
         self.plan_ids = plan_ids
-        self.sub = torch.empty((max(1, self.total), self.d), dtype=torch.bfloat16, device="cuda")
-        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
         call("svt_gather_rows", head.data.data_ptr(), head.storage, head.rows(), self.d,
-             plan_ids.data_ptr(), self.total, self.sub.data_ptr(), bad.data_ptr(),
+             plan_ids.data_ptr(), self.total, self.sub.data_ptr(), self.bad.data_ptr(),
              _stream(stream))
-        self.ws = torch.zeros(_lib.lib.svt_prefill_workspace_bytes(self.S, positions),
+
+    @classmethod
+    def from_batch(cls, head: HeadMatrix, tb, positions: int, stream=None) -> "PrefillScorer":
+        self = cls.__new__(cls)
+        self._setup(head, positions, tb.B, int(tb.act_off_h[-1]), stream)
+        self.n_rows = tb.n_active            # device int64 [S]
+        self.row_off = tb.act_off            # device int64 [S+1] (capacity offsets)
+        self.id_off = tb.act_off
+        self.plan_ids = tb.active
+        self._tb = tb
+        self.regather()
+        return self
+
+    def regather(self):
+        """Re-gather the sub-heads from the batch's current plans (device only)."""
+        tb = self._tb
+        call("svt_gather_plans", self.head.data.data_ptr(), self.head.storage, self.head.rows(),
+             self.d, tb.active.data_ptr(), tb.act_off.data_ptr(), tb.n_active.data_ptr(), tb.B,
+             self.total, self.sub.data_ptr(), self.bad.data_ptr(), _stream(self.stream))
+
+    def _setup(self, head: HeadMatrix, positions: int, S: int, total: int, stream):
+        if head.storage != SVT_BF16:
+            raise _lib.ConfigError("prefill scoring runs on bf16 heads")
+        self.head, self.P, self.stream, self.S, self.total = head, positions, stream, S, total
+        self.d = head.dim()
+        self.sub = torch.empty((max(1, total), self.d), dtype=torch.bfloat16, device="cuda")
+        self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.ws = torch.zeros(_lib.lib.svt_prefill_workspace_bytes(S, positions),
                               dtype=torch.uint8, device="cuda")
         # per-head row norms (once per head) bound Σ|w h| in the certification
         if getattr(head, "row_norms", None) is None:

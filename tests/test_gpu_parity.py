@@ -537,3 +537,34 @@ def test_prefill_scoring_all_rows_fallback(th, prefill_tuning, case):
             assert got[s * P + p] == want, (case, s, p)
     st = sc.stats()
     assert st[1] > 0, st  # candidates were recomputed (all rows or the top-8 ones)
+
+
+def test_prefill_from_device_batch_matches_reference(th):
+    """select (device) -> svt_gather_plans (capacity-CSR) -> prefill scoring:
+    ids equal the reference greedy over each request's own plan
+    (selector.cpp:16-43 then head.cpp:203-217), no host round trip."""
+    from paper_2508_15229_b200 import prefill, synth
+
+    V, d, S, P = 7000, 128, 3, 256
+    rng = np.random.default_rng(5)
+    head = th.HeadMatrix.random(V, d, 0xC0FFEE, storage=th.SVT_BF16)
+    W = head.to_host()
+    words = words_from_ids(rng.choice(V, 600, replace=False), V)
+    prompts = [rng.integers(0, V, L).astype(np.uint32) for L in (300, 17, 900)]
+    off = np.zeros(S + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in prompts])
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), 600, V,
+                                torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda(),
+                                off)
+    sc = prefill.PrefillScorer.from_batch(head, tb, P)
+    hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
+    out = torch.empty(S * P, dtype=torch.int32, device="cuda")
+    sc.score(torch.from_numpy(hid).cuda().to(torch.bfloat16), out)
+    got = out.cpu().numpy().view(np.uint32)
+    for s in range(S):
+        plan = orc.select(prompts[s], words, V, V).active_ids
+        sub = orc.gather(W, plan)
+        for p in range(P):
+            want, _ = orc.greedy_step(sub, hid[s * P + p], plan)
+            assert got[s * P + p] == want, (s, p)
+    assert int(sc.bad.item()) == 0
