@@ -9,10 +9,12 @@
 // therefore organised around 32-row "row groups" (one warp each) instead of
 // the usual split-K GEMV:
 //
-//   * data movement: each warp runs its own ring of S shared-memory stages
-//     fed by the bulk-copy (TMA) engine (cp.async.bulk + mbarrier
-//     complete_tx, SASS UBLKCP). A stage covers kCR 16-byte chunk-columns of
-//     the group's 32 rows (8 KB) plus the matching slice of the hidden state.
+//   * data movement: warps come in (producer, consumer) pairs sharing a ring
+//     of S shared-memory stages with full/empty mbarriers; the producer feeds
+//     it with the bulk-copy (TMA) engine (cp.async.bulk + mbarrier
+//     complete_tx, SASS UBLKCP). A stage covers CR 16-byte chunk-columns of
+//     the group's 32 rows (CR=16: 8 KB, CR=64: 32 KB) plus the matching slice
+//     of the hidden state.
 //       - INTERLEAVED source (sub-heads from svt_gather_interleaved): a stage
 //         is ONE contiguous 8 KB bulk copy;
 //       - ROWS source (fused gather from the full row-major head through the
@@ -27,12 +29,13 @@
 //     take a branch-free, fully unrolled path with products formed a chunk
 //     ahead of the serial FADD chain; only a row's tail stage is guarded.
 //   * epilogue: either the logits are stored, or a (value, row) key is
-//     max-reduced across the warp and across the request's groups with a u64
-//     red.max; the last group of a request (acq_rel completion counter)
-//     decodes the winner, remaps it through the plan ids (remap_out,
-//     selector.cpp:50-56) and resets the workspace.
-// The grid is persistent: gridDim.x <= #SMs CTAs of `nwa` warps; warp w takes
-// groups w, w + TW, ... with w = warp * gridDim.x + block so that small
+//     max-reduced across the warp and stored, one u64 per group (plain
+//     store, no atomics); argmax_finalize_kernel, launched as a programmatic
+//     dependent (PDL) of the GEMV grid, reduces each request's group keys,
+//     remaps the winner through the plan ids (remap_out, selector.cpp:50-56)
+//     and writes the id / max / combine record.
+// The grid is persistent: gridDim.x <= #SMs CTAs of `nwa` warp pairs; pair w
+// takes groups w, w + TW, ... with w = pair * gridDim.x + block so that small
 // batches spread across SMs first.
 #include <cstdlib>
 
