@@ -284,6 +284,35 @@ svt_status svt_greedy_certified(const void* d_sub, svt_dtype dt, size_t dim,
                                 const float* d_hidden, size_t hidden_ld, uint32_t* d_out_ids,
                                 float* d_out_max, void* d_workspace, svt_stream stream);
 
+/* Certified greedy step for ONE request over row-major rows — the
+ * latency-bound batch-1 decode (BASELINE cfg1). Replaces greedy_step
+ * (head.cpp:203-217) + remap_out (selector.cpp:50-56).
+ * Row k of the plan is d_head row d_src_ids[k] (fused gather) or, with
+ * d_src_ids == NULL, d_head row k (a gathered sub-head, or an identity plan
+ * slice). One launch: a split-K FFMA pass over all rows at HBM speed with a
+ * rigorous interval around each row's sequential reference value, then the
+ * last CTA keeps the rows whose interval reaches the maximum and, when more
+ * than one remains (or a value is non-finite, or d_out_max is requested),
+ * recomputes them in the exact reference order. The id is therefore always
+ * the reference's (first max, NaN-at-row-0 rule, -0.0 == +0.0); d_out_max
+ * (optional) receives the exact reference logit of the winner.
+ * The winner remaps through d_plan_ids[row] or, when NULL, row_base + row;
+ * plan_start != 0 when row 0 is the plan's first row (the NaN rule).
+ * Requirements: dim*esize % 16 == 0, dim <= 8192, 16-byte aligned head,
+ * hidden (f32, dim values) and workspace. d_workspace:
+ * svt_greedy_rows_workspace_bytes(n_rows) bytes, zeroed once by the caller
+ * (every call leaves its control words zeroed); its words [4] and [5] count
+ * calls certified directly / with an exact recompute. */
+size_t svt_greedy_rows_workspace_bytes(size_t n_rows);
+/* Instrumentation: when non-NULL, every svt_greedy_certified_rows launch
+ * writes 8 u64 %globaltimer stamps per CTA (start, after the dependency wait,
+ * h staged, last row done, record written, ticket taken, tail done). */
+void svt_rows_set_debug(void* d_stamps);
+svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
+                                     size_t dim, const uint32_t* d_src_ids, size_t n_rows,
+                                     const float* d_hidden, const uint32_t* d_plan_ids,
+                                     uint32_t row_base, int32_t plan_start, uint32_t* d_out_id,
+                                     float* d_out_max, void* d_workspace, svt_stream stream);
 /* ------------------------------------------------------------------------
  * Batched prefill-scoring on the tensor cores (tcgen05/TMEM, BASELINE cfg3):
  * for `sequences` x `positions` hidden states (bf16, row-major, sequence s's

@@ -1,0 +1,721 @@
+// svt_decode_small.cu — latency-optimised greedy step for ONE request over
+// row-major rows (BASELINE cfg1: batch 1, |S| ~ 2.5k, d = 2048, f32; also
+// any contiguous identity-plan slice, e.g. a vocab shard).
+//
+// Reference: greedy_step (head.cpp:203-217) = logits (head.cpp:189-201, a
+// sequential f32 sum per row) + first-max scan + remap_out
+// (selector.cpp:50-56). At batch 1 the exact-order kernel (one lane per row,
+// svt_gemv.cu) is bound by each row's 2048-long dependent FADD chain
+// (~4.2 us at 1.965 GHz) plus its ramp, well above the 3.2 us the 20.9 MB
+// sub-head needs at HBM speed. This kernel certifies the id instead.
+//
+//  * Stream (one CTA per SM, 16 warps): the CTA's contiguous row range flows
+//    through a shared-memory ring of row slots filled by 1-D bulk copies
+//    (cp.async.bulk, one per row, L2 evict-first); the first NS rows are
+//    requested before griddepcontrol.wait, i.e. while the previous kernel in
+//    the stream is still finishing (weights are never written by a kernel
+//    that triggers programmatic launch early). Row i is consumed by warp
+//    i % 16, which then refills its slot with row i + NS.
+//  * Per row (one warp): every lane FFMA-accumulates its 16-byte chunks
+//    (stride 32) into f ~ w·h and a ~ Σ|w||h| (free |.| operand modifiers),
+//    a 5-level shuffle tree reduces both. The interval
+//        [lo, hi] = f ∓ B,  B = (γ_n + γ_d)/(1 - γ_n) · a + η
+//    (directed rounding; γ_k = k·2^-24/(1 - k·2^-24), n = the fast pass's
+//    per-row depth) contains the reference's sequential value (Higham's
+//    recursive-summation bound for the reference order, the same for the
+//    FFMA tree). Lane 0 keeps the warp's running max lo and the rows whose hi
+//    reaches it (pruned as it rises).
+//  * Per CTA: L_c = max lo; the rows with hi >= L_c (a superset of its global
+//    candidates) go to a 16-byte record {L_c, count, row, hi} (+ a small list
+//    when count > 1; every row's hi goes to a rescan array on overflow).
+//  * Tail (the last CTA, by an acq_rel ticket): one round trip reads every
+//    record; L = max L_c; rows with hi >= L are the only possible reference
+//    argmax. Exactly one: the answer. Otherwise (or non-finite values, or a
+//    requested exact logit) the candidates are recomputed in the reference
+//    order __fadd_rn(acc, __fmul_rn(w, h)) (one lane per candidate, its warp
+//    streaming the row into shared memory with cp.async) and reduced with
+//    the reference's tie / NaN / signed-zero rules.
+// The tail leaves the control words zeroed: consecutive calls and CUDA-graph
+// replays need no memset.
+#include <cfloat>
+#include <cstdlib>
+
+#include "svt_common.cuh"
+
+namespace svt {
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxSlots = 128;
+constexpr int kSmemBudget = 224 * 1024;
+constexpr int kCapG = 16;        // candidate list per CTA (count > 1)
+constexpr int kMaxGrid = 256;   // the tail reads <= 8 records per lane
+constexpr int kMaxCand = 1024;   // tail candidate list
+constexpr int kPiece = 2048;     // bytes per exact-recompute piece
+constexpr unsigned kOverflow = 0xFFFFFFFFu;
+
+// Per-CTA record: the CTA's max lo and its rows with hi >= it (inline up to
+// two, with their remapped ids; more go to the gcand list, kOverflow means
+// "rescan ws_hi"). 32 bytes = two LDG.128 in the tail.
+struct alignas(16) Rec {
+    float L;
+    unsigned cnt;
+    unsigned row0;
+    float hi0;
+    unsigned id0;
+    unsigned row1;
+    float hi1;
+    unsigned id1;
+};
+constexpr int kIdCache = 512;  // plan ids of a CTA's first rows, prefetched
+
+struct SmallParams {
+    const uint8_t* W;
+    int64_t row_bytes;
+    const uint32_t* src_ids;  // nullptr: row k is W row k
+    int64_t n;                // rows of the plan (single request)
+    int32_t dim;
+    int32_t nchunks;
+    int32_t slots;
+    const float* h;
+    const uint32_t* plan_ids;  // remap; nullptr: row_base + row
+    uint32_t row_base;
+    int32_t plan_start;
+    uint32_t* out_id;
+    float* out_max;
+    unsigned* ctrl;  // [0] ticket, [2] non-finite flag, [4]/[5] statistics
+    Rec* rec;        // [kMaxGrid]
+    uint2* gcand;    // [kMaxGrid][kCapG] {row, hi bits}
+    float* ws_hi;    // [n] hi_r (written only by CTAs that overflow)
+    float c_rel;
+    float eta;
+    int64_t per_cta;  // rows of CTA c: per_cta (+1 for c < extra), contiguous
+    int32_t extra;
+    int32_t variant;  // profiling (SVT_ROWS_VARIANT): 1 exit, 2 loads only, 3 no tail
+    unsigned long long* dbg;  // profiling: per CTA 8 globaltimer stamps (svt_rows_set_debug)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SVT_STAMP(k) \
+    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 128 + (k)] = gtimer();
+
+__device__ __forceinline__ int64_t row_begin(const SmallParams& p, int c) {
+    return p.per_cta * c + (c < p.extra ? c : p.extra);
+}
+
+__device__ __forceinline__ const uint8_t* row_ptr(const SmallParams& p, int64_t r) {
+    const int64_t src = p.src_ids ? static_cast<int64_t>(__ldg(p.src_ids + r)) : r;
+    return p.W + src * p.row_bytes;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Exact reference-order logit of one row (head.cpp:194-199), computed by lane
+// 0 while the warp streams the next 2 KB piece of the row into shared memory.
+template <int DT>
+__device__ float exact_row_warp(const uint8_t* row, int64_t row_bytes, const float* s_h,
+                                uint8_t* buf, int lane) {
+    constexpr int E = Chunk<DT>::E;
+    const int np = static_cast<int>((row_bytes + kPiece - 1) / kPiece);
+    auto issue = [&](int pc) {
+        const int64_t off = static_cast<int64_t>(pc) * kPiece;
+        const int nb = static_cast<int>(min(static_cast<int64_t>(kPiece), row_bytes - off));
+        uint8_t* dst = buf + (pc & 1) * kPiece;
+        for (int o = lane * 16; o < nb; o += 32 * 16) cp_async16(dst + o, row + off + o);
+        cp_async_commit();
+    };
+    float acc = 0.0f;
+    issue(0);
+    for (int pc = 0; pc < np; ++pc) {
+        if (pc + 1 < np)
+            issue(pc + 1);
+        else
+            cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t off = static_cast<int64_t>(pc) * kPiece;
+            const int nc = static_cast<int>(min(static_cast<int64_t>(kPiece), row_bytes - off)) / 16;
+            const uint4* sw = reinterpret_cast<const uint4*>(buf + (pc & 1) * kPiece);
+            const float* hh = s_h + off / (16 / E);
+#pragma unroll 4
+            for (int c = 0; c < nc; ++c) {
+                float wv[E];
+                Chunk<DT>::widen(sw[c], wv);
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc = ref_mac(acc, wv[e], hh[c * E + e]);
+            }
+        }
+        __syncwarp();
+    }
+    return __shfl_sync(0xFFFFFFFFu, acc, 0);
+}
+
+// f ~ w·h and a ~ Σ|w||h| of one row by one warp (lane-strided chunks)
+template <int DT>
+__device__ __forceinline__ void row_dot(const uint4* w, const float* s_h, int nchunks, int lane,
+                                        float& f, float& a) {
+    constexpr int E = Chunk<DT>::E;
+    f = 0.0f;
+    a = 0.0f;
+#pragma unroll 4
+    for (int k = lane; k < nchunks; k += 32) {
+        float wv[E];
+        Chunk<DT>::widen(w[k], wv);
+        const float4* hp = reinterpret_cast<const float4*>(s_h + k * E);
+#pragma unroll
+        for (int q = 0; q < E / 4; ++q) {
+            const float4 hq = hp[q];
+            const float hv[4] = {hq.x, hq.y, hq.z, hq.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                f = __fmaf_rn(wv[q * 4 + e], hv[e], f);
+                a = __fmaf_rn(fabsf(wv[q * 4 + e]), fabsf(hv[e]), a);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        f += __shfl_xor_sync(0xFFFFFFFFu, f, o);
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+    }
+}
+
+// Same with this lane's h values in registers (chunks lane, lane+32, ...):
+// halves the shared-memory traffic per row (only w is read from the ring).
+// Branch-free: out-of-range chunks are replaced by zeros with selects, so
+// every LDS.128 of the row can be in flight at once; two interleaved
+// accumulators halve the dependent FFMA chain (the bound's depth accounts
+// for CPL*E terms + 1 combine + 5 shuffle levels).
+template <int DT, int CPL>
+__device__ __forceinline__ void row_dot_reg(const uint4* w, const float (&hv)[CPL][Chunk<DT>::E],
+                                            int nchunks, int lane, float& f, float& a) {
+    constexpr int E = Chunk<DT>::E;
+    float f0 = 0.0f, f1 = 0.0f, a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        const int k = lane + 32 * j;
+        const bool ok = k < nchunks;
+        uint4 v = w[ok ? k : 0];
+        v.x = ok ? v.x : 0u;
+        v.y = ok ? v.y : 0u;
+        v.z = ok ? v.z : 0u;
+        v.w = ok ? v.w : 0u;
+        float wv[E];
+        Chunk<DT>::widen(v, wv);
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+            f0 = __fmaf_rn(wv[e], hv[j][e], f0);
+            a0 = __fmaf_rn(fabsf(wv[e]), fabsf(hv[j][e]), a0);
+            f1 = __fmaf_rn(wv[e + 1], hv[j][e + 1], f1);
+            a1 = __fmaf_rn(fabsf(wv[e + 1]), fabsf(hv[j][e + 1]), a1);
+        }
+    }
+    f = f0 + f1;
+    a = a0 + a1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        f += __shfl_xor_sync(0xFFFFFFFFu, f, o);
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+    }
+}
+
+// CPL > 0: h lives in registers (CPL chunks per lane); CPL == 0: h is read
+// from shared memory (wide rows).
+template <int DT, int CPL>
+__global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p) {
+    extern __shared__ __align__(128) uint8_t dsmem[];
+    __shared__ uint64_t s_full[kMaxSlots];
+    __shared__ float s_wL[kWarps];
+    __shared__ uint2 s_wc0[kWarps], s_wc1[kWarps];
+    __shared__ unsigned s_wn[kWarps];
+    __shared__ unsigned s_n, s_ovf, s_bad, s_last, s_nwork;
+    __shared__ uint32_t s_ids[kIdCache];
+    __shared__ unsigned long long s_key;
+
+    SVT_STAMP(0);
+    if (p.variant == 1) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t r0 = row_begin(p, c), r1 = row_begin(p, c + 1);
+    const int64_t nrows = r1 - r0;
+    const int NS = p.slots;
+    const uint32_t rb = static_cast<uint32_t>(p.row_bytes);
+    const size_t ring_bytes = static_cast<size_t>(NS) * rb;
+    uint8_t* ring = dsmem;
+    float* s_h = reinterpret_cast<float*>(
+        dsmem + (ring_bytes > 16 * 2 * kPiece + kMaxCand * 4 ? ring_bytes
+                                                             : 16 * 2 * kPiece + kMaxCand * 4));
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int64_t i) {
+        const int slot = static_cast<int>(i % NS);
+        mbar_arrive_expect_tx(&s_full[slot], rb);
+        bulk_g2s(ring + static_cast<size_t>(slot) * rb, row_ptr(p, r0 + i), rb, &s_full[slot],
+                 pol);
+    };
+    // Weights first: they do not depend on the previous kernel in the stream.
+    // Slot s belongs to warp s % 16 for the whole launch (rows s, s+NS, ...):
+    // its lane 0 initialises the slot's barrier, issues its copies, and the
+    // warp consumes its phases in order (NS is a multiple of 16 whenever slots
+    // are refilled, or < 16: fewer consumer warps). No CTA barrier needed.
+    if (lane == 0) {
+        for (int sl = warp; sl < NS; sl += kWarps) mbar_init(&s_full[sl], 1);
+        fence_mbar_init();
+            for (int64_t i = warp; i < nrows && i < NS; i += kWarps) issue(i);
+    }
+    if (tid == 0) {
+        s_ovf = 0;
+        s_bad = 0;
+        s_n = 0;
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    SVT_STAMP(1);
+    constexpr int E = Chunk<DT>::E;
+    constexpr int CR = CPL > 0 ? CPL : 1;
+    float hv[CR][E];
+    if constexpr (CPL > 0) {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            const int k = lane + 32 * j;
+#pragma unroll
+            for (int e = 0; e < E; e += 4) {
+                float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (k < p.nchunks) q = __ldg(reinterpret_cast<const float4*>(p.h + k * E + e));
+                hv[j][e] = q.x;
+                hv[j][e + 1] = q.y;
+                hv[j][e + 2] = q.z;
+                hv[j][e + 3] = q.w;
+            }
+        }
+    }
+    // h is also staged in shared memory (the smem-h path, overflow rescans and
+    // the tail's exact recompute); nobody waits for it on the register path
+    for (int e = tid * 4; e < p.dim; e += kThreads * 4)
+        *reinterpret_cast<float4*>(s_h + e) = __ldg(reinterpret_cast<const float4*>(p.h + e));
+    // remap ids of this CTA's rows (read at record time, after a CTA barrier)
+    for (int i = tid; i < nrows && i < kIdCache; i += kThreads)
+        s_ids[i] = p.plan_ids ? __ldg(p.plan_ids + r0 + i) : p.row_base + static_cast<uint32_t>(r0 + i);
+    if constexpr (CPL == 0) __syncthreads();
+    SVT_STAMP(2);
+
+    // ---- stream: one row per warp at a time ------------------------------------
+    float wL = -FLT_MAX;  // lane 0: running max lo of this warp's rows
+    uint2 c0 = make_uint2(0u, 0u), c1 = make_uint2(0u, 0u);  // rows with hi >= wL
+    unsigned ncand = 0, wovf = 0, wbad = 0;
+    for (int64_t i = warp; i < nrows;
+         i += (i % NS) + kWarps < NS ? kWarps : NS - (i % NS) + warp) {
+        if (warp >= NS) break;
+        const int slot = static_cast<int>(i % NS);
+        mbar_wait_parity(&s_full[slot], static_cast<uint32_t>((i / NS) & 1));
+        const int dbg_k = static_cast<int>(i / kWarps);
+        if (p.dbg && lane == 0 && dbg_k < 3) p.dbg[blockIdx.x * 128 + 8 + warp * 6 + dbg_k * 2] = gtimer();
+        if (p.variant == 2) {
+            if (lane == 0 && i + NS < nrows) issue(i + NS);
+            continue;
+        }
+        float f, a;
+        const uint4* wrow = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * rb);
+        if constexpr (CPL > 0)
+            row_dot_reg<DT, CR>(wrow, hv, p.nchunks, lane, f, a);
+        else
+            row_dot<DT>(wrow, s_h, p.nchunks, lane, f, a);
+        __syncwarp();  // every lane is done with the slot
+        if (p.dbg && lane == 0 && dbg_k < 3) p.dbg[blockIdx.x * 128 + 9 + warp * 6 + dbg_k * 2] = gtimer();
+        if (lane == 0) {
+            if (i + NS < nrows) issue(i + NS);
+            if (!isfinite(f) || !isfinite(a)) wbad = 1;
+            const float bnd = __fadd_ru(__fmul_ru(p.c_rel, a), p.eta);
+            float lo = __fsub_rd(f, bnd);
+            const float hi = __fadd_ru(f, bnd);
+            if (!(lo == lo)) lo = -FLT_MAX;
+            if (lo > wL) {  // prune the rows the raised bar excludes
+                wL = lo;
+                const bool k0 = ncand >= 1 && __uint_as_float(c0.y) >= wL;
+                const bool k1 = ncand >= 2 && __uint_as_float(c1.y) >= wL;
+                if (!k0 && k1) c0 = c1;
+                ncand = (k0 ? 1u : 0u) + (k1 ? 1u : 0u);
+            }
+            if (hi >= wL) {
+                const uint2 e = make_uint2(static_cast<uint32_t>(r0 + i), __float_as_uint(hi));
+                if (ncand == 0)
+                    c0 = e;
+                else if (ncand == 1)
+                    c1 = e;
+                else
+                    wovf = 1;
+                ++ncand;
+            }
+        }
+    }
+    if (p.dbg && lane == 0) atomicMax(&p.dbg[blockIdx.x * 128 + 3], gtimer());
+    if (lane == 0) {
+        s_wL[warp] = wL;
+        s_wn[warp] = wovf ? kOverflow : ncand;
+        s_wc0[warp] = c0;
+        s_wc1[warp] = c1;
+        if (wbad) s_bad = 1;
+    }
+    __syncthreads();
+    // ---- CTA record (warp 0, lane w summarises warp w) ---------------------------
+    if (warp == 0) {
+        const bool mine = lane < kWarps;
+        float L = mine ? s_wL[lane] : -FLT_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xFFFFFFFFu, L, o));
+        const unsigned nw = mine ? s_wn[lane] : 0u;
+        const uint2 a0 = mine ? s_wc0[lane] : make_uint2(0u, 0u);
+        const uint2 a1 = mine ? s_wc1[lane] : make_uint2(0u, 0u);
+        const bool any_ovf = __any_sync(0xFFFFFFFFu, nw == kOverflow);
+        const bool q0 = nw != kOverflow && nw >= 1 && __uint_as_float(a0.y) >= L;
+        const bool q1 = nw != kOverflow && nw >= 2 && __uint_as_float(a1.y) >= L;
+        const unsigned m0 = __ballot_sync(0xFFFFFFFFu, q0), m1 = __ballot_sync(0xFFFFFFFFu, q1);
+        const unsigned cnt = __popc(m0) + __popc(m1);
+        const bool ovf = any_ovf || cnt > kCapG;
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned pos0 = __popc(m0 & lt), pos1 = __popc(m0) + __popc(m1 & lt);
+        auto id_of = [&](uint32_t row) -> uint32_t {
+            const int64_t li = static_cast<int64_t>(row) - r0;
+            return li < kIdCache ? s_ids[li]
+                                 : (p.plan_ids ? __ldg(p.plan_ids + row) : p.row_base + row);
+        };
+        if (!ovf && cnt > 2) {
+            if (q0) p.gcand[c * kCapG + pos0] = a0;
+            if (q1) p.gcand[c * kCapG + pos1] = a1;
+        }
+        // inline entries: candidate k (k = 0, 1) travels through lane 0
+        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;  // {row, hi, id, -}
+        if (q0 && pos0 < 2) {
+            const uint4 e = make_uint4(a0.x, a0.y, id_of(a0.x), 0u);
+            if (pos0 == 0) e0 = e; else e1 = e;
+        }
+        if (q1 && pos1 < 2) {
+            const uint4 e = make_uint4(a1.x, a1.y, id_of(a1.x), 0u);
+            if (pos1 == 0) e0 = e; else e1 = e;
+        }
+        const unsigned src0 = __ballot_sync(0xFFFFFFFFu, (q0 && pos0 == 0) || (q1 && pos1 == 0));
+        const unsigned src1 = __ballot_sync(0xFFFFFFFFu, (q0 && pos0 == 1) || (q1 && pos1 == 1));
+        const int l0 = src0 ? __ffs(src0) - 1 : 0, l1 = src1 ? __ffs(src1) - 1 : 0;
+        e0 = make_uint4(__shfl_sync(0xFFFFFFFFu, e0.x, l0), __shfl_sync(0xFFFFFFFFu, e0.y, l0),
+                        __shfl_sync(0xFFFFFFFFu, e0.z, l0), 0u);
+        e1 = make_uint4(__shfl_sync(0xFFFFFFFFu, e1.x, l1), __shfl_sync(0xFFFFFFFFu, e1.y, l1),
+                        __shfl_sync(0xFFFFFFFFu, e1.z, l1), 0u);
+        if (lane == 0) {
+            uint4* rp = reinterpret_cast<uint4*>(p.rec + c);
+            rp[0] = make_uint4(__float_as_uint(L), ovf ? kOverflow : cnt, e0.x, e0.y);
+            rp[1] = make_uint4(e0.z, e1.x, e1.y, e1.z);
+            s_ovf = ovf;
+            if (s_bad) atomicOr(&p.ctrl[2], 1u);
+        }
+    }
+    __syncthreads();
+    if (s_ovf) {  // rare: every row's hi for the tail's rescan (rows re-read)
+        for (int64_t i = warp; i < nrows; i += kWarps) {
+            float f, a;
+            row_dot<DT>(reinterpret_cast<const uint4*>(row_ptr(p, r0 + i)), s_h, p.nchunks, lane,
+                        f, a);
+            if (lane == 0)
+                p.ws_hi[r0 + i] = __fadd_ru(f, __fadd_ru(__fmul_ru(p.c_rel, a), p.eta));
+        }
+        __threadfence();
+        __syncthreads();
+    }
+    SVT_STAMP(4);
+    if (tid == 0) s_last = atom_add_acq_rel_u32(&p.ctrl[0], 1u) == static_cast<unsigned>(G - 1);
+    __syncthreads();
+    SVT_STAMP(5);
+    if (!s_last) return;
+    if (p.variant >= 2) {
+        if (tid == 0) {
+            p.ctrl[0] = 0u;
+            p.ctrl[2] = 0u;
+        }
+        return;
+    }
+
+    // ---------------- tail: the last CTA ----------------
+    unsigned* s_list = reinterpret_cast<unsigned*>(dsmem);  // the ring is drained
+    if (warp == 0) {
+        const bool bad = __ldcg(&p.ctrl[2]) != 0;
+        constexpr int kPer = kMaxGrid / 32;
+        uint4 ra[kPer], rb2[kPer];
+        float lmax = -FLT_MAX;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int cc = lane + 32 * q;
+            ra[q] = make_uint4(__float_as_uint(-FLT_MAX), 0u, 0u, 0u);
+            rb2[q] = make_uint4(0u, 0u, 0u, 0u);
+            if (32 * q < G && cc < G) {
+                const uint4* rp = reinterpret_cast<const uint4*>(p.rec + cc);
+                ra[q] = __ldcg(rp);
+                rb2[q] = __ldcg(rp + 1);
+            }
+            lmax = fmaxf(lmax, __uint_as_float(ra[q].x));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xFFFFFFFFu, lmax, o));
+        const float L = lmax;
+        SVT_STAMP(7);
+        // inline candidates with hi >= L; records with > 2 (or overflow) need a
+        // second look
+        unsigned total = 0, big = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const unsigned cnt = ra[q].y;
+            const bool b0 = cnt >= 1 && cnt <= 2 && __uint_as_float(ra[q].w) >= L;
+            const bool b1 = cnt == 2 && __uint_as_float(rb2[q].z) >= L;
+            total += __popc(__ballot_sync(0xFFFFFFFFu, b0)) + __popc(__ballot_sync(0xFFFFFFFFu, b1));
+            big |= __ballot_sync(0xFFFFFFFFu, cnt > 2);
+        }
+            if (!bad && !big && total == 1 && !p.out_max) {
+            // the single candidate is the reference argmax: its id is inline
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const unsigned cnt = ra[q].y;
+                const bool b0 = cnt >= 1 && cnt <= 2 && __uint_as_float(ra[q].w) >= L;
+                const bool b1 = cnt == 2 && __uint_as_float(rb2[q].z) >= L;
+                if (b0) *p.out_id = rb2[q].x;
+                if (b1) *p.out_id = rb2[q].w;
+            }
+            if (lane == 0) s_nwork = 0;
+                } else {
+            // general path: every candidate row into the shared list
+            if (!bad) {
+#pragma unroll
+                for (int q = 0; q < kPer; ++q) {
+                    const int cc = lane + 32 * q;
+                    if (32 * q >= G || cc >= G) continue;
+                    const unsigned cnt = ra[q].y;
+                    if (cnt >= 1 && cnt <= 2) {
+                        if (__uint_as_float(ra[q].w) >= L) {
+                            const unsigned k = atomicAdd(&s_n, 1u);
+                            if (k < kMaxCand) s_list[k] = ra[q].z;
+                        }
+                        if (cnt == 2 && __uint_as_float(rb2[q].z) >= L) {
+                            const unsigned k = atomicAdd(&s_n, 1u);
+                            if (k < kMaxCand) s_list[k] = rb2[q].y;
+                        }
+                    } else if (cnt == kOverflow) {
+                        const int64_t a0 = row_begin(p, cc), a1 = row_begin(p, cc + 1);
+                        for (int64_t r = a0; r < a1; ++r)
+                            if (__ldcg(p.ws_hi + r) >= L) {
+                                const unsigned k = atomicAdd(&s_n, 1u);
+                                if (k < kMaxCand) s_list[k] = static_cast<unsigned>(r);
+                            }
+                    } else if (cnt > 2) {
+                        for (unsigned e = 0; e < cnt; ++e) {
+                            const uint2 ce = __ldcg(p.gcand + cc * kCapG + e);
+                            if (__uint_as_float(ce.y) >= L) {
+                                const unsigned k = atomicAdd(&s_n, 1u);
+                                if (k < kMaxCand) s_list[k] = ce.x;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned n = s_n;
+                const bool all = bad || n == 0 || n > static_cast<unsigned>(kMaxCand);
+                s_nwork = all ? 0xFFFFFFFFu : n;
+                s_key = 0ull;
+            }
+        }
+    }
+    __syncthreads();
+    const unsigned nw_code = s_nwork;
+    if (nw_code != 0) {
+        // exact recompute (s_h still holds h; per-warp pieces after s_list)
+        const bool all = nw_code == 0xFFFFFFFFu;
+        const int64_t nwork = all ? p.n : static_cast<int64_t>(nw_code);
+        uint8_t* s_buf = dsmem + kMaxCand * 4;
+        unsigned long long best = 0ull;
+        for (int64_t i = warp; i < nwork; i += kWarps) {
+            const int64_t r = all ? i : static_cast<int64_t>(s_list[i]);
+            const float v = exact_row_warp<DT>(row_ptr(p, r), p.row_bytes, s_h,
+                                               s_buf + warp * 2 * kPiece, lane);
+            const unsigned long long key =
+                make_key(v, static_cast<uint32_t>(r), true, p.plan_start && r == 0);
+            best = key > best ? key : best;
+        }
+        if (lane == 0) atomicMax(&s_key, best);
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned long long k = s_key;
+            const uint32_t r = 0xFFFFFFFFu - static_cast<uint32_t>(k);
+            if (k == 0ull) {  // every row NaN (and plan row 0 not in this slice)
+                *p.out_id = 0xFFFFFFFFu;
+                if (p.out_max) *p.out_max = __int_as_float(0x7FC00000);
+            } else {
+                *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+                if (p.out_max)
+                    *p.out_max = k == kNanRow0Key ? __int_as_float(0x7FC00000)
+                                                  : float_of_ord(static_cast<uint32_t>(k >> 32));
+            }
+        }
+    }
+    SVT_STAMP(6);
+    if (tid == 0) {  // ready for the next call; {certified directly, recomputed}
+        p.ctrl[0] = 0u;
+        p.ctrl[2] = 0u;
+        p.ctrl[nw_code == 0 ? 4 : 5] += 1u;
+    }
+}
+
+unsigned long long* g_rows_dbg = nullptr;
+
+double gamma_n(double n) {
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    return n * u / (1.0 - n * u);
+}
+
+template <int DT, int CPL>
+svt_status launch_rows(SmallParams p, int grid, cudaStream_t st) {
+    const size_t ring = static_cast<size_t>(p.slots) * static_cast<size_t>(p.row_bytes);
+    const size_t tail = 16 * 2 * kPiece + kMaxCand * 4;
+    const size_t smem = (ring > tail ? ring : tail) + static_cast<size_t>(p.dim) * 4;
+    auto kern = greedy_rows_kernel<DT, CPL>;
+    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    return SVT_OK;
+}
+
+}  // namespace
+}  // namespace svt
+
+extern "C" void svt_rows_set_debug(void* d_stamps) {
+    svt::g_rows_dbg = static_cast<unsigned long long*>(d_stamps);
+}
+
+extern "C" size_t svt_greedy_rows_workspace_bytes(size_t rows) {
+    using namespace svt;
+    return 256 + static_cast<size_t>(kMaxGrid) * sizeof(Rec) +
+           static_cast<size_t>(kMaxGrid) * kCapG * 8 + (rows > 0 ? rows : 1) * 4;
+}
+
+extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
+                                                size_t dim, const uint32_t* d_src_ids,
+                                                size_t n_rows, const float* d_hidden,
+                                                const uint32_t* d_plan_ids, uint32_t row_base,
+                                                int32_t plan_start, uint32_t* d_out_id,
+                                                float* d_out_max, void* d_workspace,
+                                                svt_stream stream) {
+    using namespace svt;
+    if (dt != SVT_F32 && dt != SVT_F16 && dt != SVT_BF16) {
+        set_error("dtype must be SVT_F32, SVT_F16 or SVT_BF16");
+        return SVT_ERR_CONFIG;
+    }
+    if (n_rows == 0) {
+        set_error("greedy step over an empty sub-head");
+        return SVT_ERR_INTEGRITY;
+    }
+    if (!d_src_ids && n_rows > head_rows) {
+        set_error("plan rows (%zu) exceed head rows (%zu)", n_rows, head_rows);
+        return SVT_ERR_INTEGRITY;
+    }
+    const size_t es = dt == SVT_F32 ? 4 : 2;
+    const size_t row_bytes = dim * es;
+    if (dim == 0 || row_bytes % 16 != 0 || dim > 8192 || n_rows > 0xFFFFFFFFull ||
+        (reinterpret_cast<uintptr_t>(d_head) & 15u) ||
+        (reinterpret_cast<uintptr_t>(d_hidden) & 15u) || !d_workspace ||
+        (reinterpret_cast<uintptr_t>(d_workspace) & 15u)) {
+        set_error("certified rows greedy: needs 16-byte aligned rows/hidden/workspace, "
+                  "dim*esize %% 16 == 0 and dim <= 8192");
+        return SVT_ERR_CONFIG;
+    }
+    int dev_count = 0;
+    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+        cudaGetLastError();
+        set_error("no CUDA device available (the tailored-head kernels have no CPU fallback)");
+        return SVT_ERR_RUNTIME;
+    }
+    SmallParams p = {};
+    p.W = static_cast<const uint8_t*>(d_head);
+    p.row_bytes = static_cast<int64_t>(row_bytes);
+    p.src_ids = d_src_ids;
+    p.n = static_cast<int64_t>(n_rows);
+    p.dim = static_cast<int32_t>(dim);
+    p.nchunks = static_cast<int32_t>(row_bytes / 16);
+    p.h = d_hidden;
+    p.plan_ids = d_plan_ids;
+    p.row_base = row_base;
+    p.plan_start = plan_start;
+    p.out_id = d_out_id;
+    p.out_max = d_out_max;
+    p.dbg = g_rows_dbg;
+    uint8_t* ws = static_cast<uint8_t*>(d_workspace);
+    p.ctrl = reinterpret_cast<unsigned*>(ws);
+    p.rec = reinterpret_cast<Rec*>(ws + 256);
+    p.gcand = reinterpret_cast<uint2*>(ws + 256 + kMaxGrid * sizeof(Rec));
+    p.ws_hi = reinterpret_cast<float*>(ws + 256 + kMaxGrid * sizeof(Rec) + kMaxGrid * kCapG * 8);
+    // fast pass depth: ceil(nchunks/32)*E sequential FFMAs per lane + 5
+    // shuffle levels (+1 slack); the same tree bounds the |w||h| sum
+    const int E = dt == SVT_F32 ? 4 : 8;
+    const double n_fast = static_cast<double>((p.nchunks + 31) / 32) * E + 6;
+    const double cr = (gamma_n(n_fast) + gamma_n(static_cast<double>(dim))) /
+                      (1.0 - gamma_n(n_fast)) * 1.0001;
+    p.c_rel = static_cast<float>(cr) * (1.0f + FLT_EPSILON);
+    p.eta = static_cast<float>((static_cast<double>(dim) + n_fast) * 4.0) * 1.40129846e-45f;
+    int grid = sm_count();
+    if (const char* v = getenv("SVT_ROWS_GRID")) grid = atoi(v);
+    if (const char* v = getenv("SVT_ROWS_VARIANT")) p.variant = atoi(v);
+    grid = grid > kMaxGrid ? kMaxGrid : grid;
+    if (static_cast<int64_t>(grid) > p.n) grid = static_cast<int>(p.n);
+    if (grid < 1) grid = 1;
+    const int64_t per_cta = (p.n + grid - 1) / grid;
+    p.per_cta = p.n / grid;
+    p.extra = static_cast<int32_t>(p.n % grid);
+    int64_t slots = (kSmemBudget - static_cast<int64_t>(dim) * 4) / p.row_bytes;
+    slots = slots > kMaxSlots ? kMaxSlots : slots;
+    if (slots >= per_cta)
+        slots = per_cta;  // every row in flight at once, no refills
+    else if (slots >= kWarps)
+        slots -= slots % kWarps;
+    p.slots = static_cast<int32_t>(slots < 1 ? 1 : slots);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // h in registers when a lane's share is <= 64 values
+    const int cpl = (p.nchunks + 31) / 32;
+    switch (dt) {
+        case SVT_F32:
+            if (cpl <= 4) return launch_rows<SVT_F32, 4>(p, grid, st);
+            if (cpl <= 8) return launch_rows<SVT_F32, 8>(p, grid, st);
+            if (cpl <= 16) return launch_rows<SVT_F32, 16>(p, grid, st);
+            return launch_rows<SVT_F32, 0>(p, grid, st);
+        case SVT_F16:
+            if (cpl <= 2) return launch_rows<SVT_F16, 2>(p, grid, st);
+            if (cpl <= 4) return launch_rows<SVT_F16, 4>(p, grid, st);
+            if (cpl <= 8) return launch_rows<SVT_F16, 8>(p, grid, st);
+            return launch_rows<SVT_F16, 0>(p, grid, st);
+        default:
+            if (cpl <= 2) return launch_rows<SVT_BF16, 2>(p, grid, st);
+            if (cpl <= 4) return launch_rows<SVT_BF16, 4>(p, grid, st);
+            if (cpl <= 8) return launch_rows<SVT_BF16, 8>(p, grid, st);
+            return launch_rows<SVT_BF16, 0>(p, grid, st);
+    }
+}

@@ -325,6 +325,62 @@ def greedy_step(subhead: HeadMatrix, hidden, plan: SelectionPlan) -> int:
     return int(out[0].item()) & 0xFFFFFFFF
 
 
+class RowDecoder:
+    """Batch-1 greedy decode over ONE plan (BASELINE cfg1): the plan's rows
+    are gathered row-major once (gather, head.cpp:176-187) and every token is
+    one svt_greedy_certified_rows launch — a split-K pass at HBM speed with
+    rigorous bounds, exact reference-order recompute of the rows that can
+    still win. Ids equal greedy_step (head.cpp:203-217) + remap_out.
+
+    ``materialize=False`` streams the rows straight from the head through the
+    plan ids (fused gather) instead of a gathered sub-head."""
+
+    def __init__(self, head: HeadMatrix, plan_ids: torch.Tensor, n_rows: int,
+                 materialize: bool = True, stream=None, row_base: int = 0,
+                 plan_start: int = 1, remap: bool = True):
+        if n_rows <= 0:
+            raise IntegrityError("greedy step over an empty sub-head")
+        self.head, self.n, self.stream = head, int(n_rows), stream
+        self.ids = plan_ids
+        self.ws = torch.zeros(_lib.lib.svt_greedy_rows_workspace_bytes(self.n),
+                              dtype=torch.uint8, device="cuda")
+        esize = 4 if head.storage == SVT_F32 else 2
+        if materialize:
+            self.sub = torch.empty(self.n * head.dim() * esize + 16, dtype=torch.uint8,
+                                   device="cuda")
+            self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+            self.gather()
+            src, src_ids, rows = self.sub.data_ptr(), None, self.n
+        else:
+            self.sub = None
+            src, src_ids, rows = head.data.data_ptr(), plan_ids.data_ptr(), head.rows()
+        self._fn = _lib.lib.svt_greedy_certified_rows
+        self._pre = (src, head.storage, rows, head.dim(), src_ids, self.n)
+        self._post = ((plan_ids.data_ptr() if remap else None), row_base, plan_start)
+
+    def gather(self):
+        """(Re)materialise the row-major sub-head (svt_gather_rows)."""
+        h = self.head
+        call("svt_gather_rows", h.data.data_ptr(), h.storage, h.rows(), h.dim(),
+             self.ids.data_ptr(), self.n, self.sub.data_ptr(), self.bad.data_ptr(),
+             _stream(self.stream))
+        return self
+
+    def greedy(self, hidden: torch.Tensor, out_id: torch.Tensor,
+               out_max: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """hidden: f32 [dim] on the device (16-byte aligned); out_id: one
+        int32; out_max (optional): the exact reference logit of the winner."""
+        st = self._fn(*self._pre, hidden.data_ptr(), *self._post, out_id.data_ptr(),
+                      _ptr(out_max), self.ws.data_ptr(), _stream(self.stream))
+        _lib.check(st, "svt_greedy_certified_rows")
+        return out_id
+
+    def stats(self):
+        """(tokens certified directly, tokens with an exact recompute)."""
+        w = self.ws[:32].view(torch.int32).cpu().tolist()
+        return w[4], w[5]
+
+
 # --------------------------------------------------------------------------
 # accounting / offload model (head.cpp:219-237, offload_sim.cpp:44-87)
 # --------------------------------------------------------------------------

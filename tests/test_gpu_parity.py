@@ -568,3 +568,148 @@ def test_prefill_from_device_batch_matches_reference(th):
             want, _ = orc.greedy_step(sub, hid[s * P + p], plan)
             assert got[s * P + p] == want, (s, p)
     assert int(sc.bad.item()) == 0
+
+
+# ---- certified batch-1 decode over row-major rows (cfg1 latency path) ----------
+def _rows_decoder(th, head, ids, materialize=True, **kw):
+    d_ids = torch.from_numpy(np.ascontiguousarray(ids, np.uint32).view(np.int32)).cuda()
+    return th.RowDecoder(head, d_ids, len(ids), materialize=materialize, **kw)
+
+
+def _rows_greedy(dec, h, want_max=False):
+    hd = torch.from_numpy(np.ascontiguousarray(h, np.float32)).cuda()
+    out = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+    mx = torch.full((1,), -7.0, dtype=torch.float32, device="cuda") if want_max else None
+    dec.greedy(hd, out, mx)
+    got = int(out.item()) & 0xFFFFFFFF
+    return (got, float(mx.item())) if want_max else got
+
+
+@pytest.mark.parametrize("materialize", [True, False])
+def test_rows_certified_cfg1_shape(th, materialize):
+    """cfg1 (V=128256, d=2048, f32, 512-token prompt + 2048 static): ids and
+    the exact winning logit equal the reference greedy_step bit for bit."""
+    V, d = 128256, 2048
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_F32, 1, 512, 2048, 12)
+    W = head.to_host()
+    plan = orc.select(prompts[0], words, V, V)
+    sub = orc.gather(W, plan.active_ids)
+    dec = _rows_decoder(th, head, plan.active_ids, materialize)
+    for t in range(hid.shape[0]):
+        want, wmax = orc.greedy_step(sub, hid[t][0], plan.active_ids)
+        assert _rows_greedy(dec, hid[t][0]) == want
+        if t < 3:
+            got, gmax = _rows_greedy(dec, hid[t][0], want_max=True)
+            assert got == want and bits([gmax])[0] == bits([wmax])[0]
+    fast, slow = dec.stats()
+    assert fast + slow == hid.shape[0] + 3 and slow >= 3
+
+
+@pytest.mark.parametrize("V,d,storage,n", [(151936, 896, "bf16", 2600), (256000, 2304, "bf16", 4000),
+                                           (5000, 256, "f16", 700), (3000, 64, "f32", 300),
+                                           (9000, 8192, "f32", 333), (40000, 1024, "bf16", 40000)])
+def test_rows_certified_shapes(th, V, d, storage, n):
+    """Every team shape (warps per row 1/2/4/8, chunks per lane 1..8), f32 /
+    f16 / bf16 storage, and multi-batch CTAs (n = 40000 identity rows)."""
+    st = {"f32": th.SVT_F32, "f16": th.SVT_F16, "bf16": th.SVT_BF16}[storage]
+    head = th.HeadMatrix.random(V, d, 0x5EED + d, storage=st,
+                                dtype_bytes=2 if storage == "f16" else 4)
+    W = head.to_host()
+    rng = np.random.default_rng(d)
+    ids = np.arange(V, dtype=np.uint32) if n == V else np.sort(
+        rng.choice(V, n, replace=False)).astype(np.uint32)
+    dec = _rows_decoder(th, head, ids, materialize=(n % 2 == 0))
+    sub = W[ids]
+    for t in range(4):
+        h = rng.uniform(-1, 1, d).astype(np.float32)
+        assert _rows_greedy(dec, h) == orc.greedy_step(sub, h, ids)[0], (V, d, t)
+
+
+def test_rows_certified_special_values(th):
+    """Reference scan rules through the certified path: zero hidden (all rows
+    tie -> lowest), NaN hidden (-> plan row 0), NaN at row 0 / later rows,
+    duplicated maxima (-> lowest row), -0.0 vs +0.0, +-inf, and repeated
+    calls (the control words reset themselves)."""
+    rng = np.random.default_rng(77)
+    n, d = 600, 128
+    W = rng.uniform(-1, 1, (n, d)).astype(np.float32)
+    W[417] = W[233] = W[501] = np.abs(W[5]) + 0.5  # identical maxima for h = +1
+    ids = (np.arange(n, dtype=np.uint32) * 3 + 11)
+    head = th.HeadMatrix.from_host(W)
+    dec = _rows_decoder(th, head, np.arange(n, dtype=np.uint32), remap=False)
+    dmap = _rows_decoder(th, head, np.arange(n, dtype=np.uint32))
+    pos = np.ones(d, np.float32)
+    assert _rows_greedy(dec, pos) == orc.greedy_step(W, pos, np.arange(n, dtype=np.uint32))[0] == 233
+    zero = np.zeros(d, np.float32)
+    assert _rows_greedy(dec, zero) == 0
+    nanh = zero.copy()
+    nanh[3] = np.nan
+    assert _rows_greedy(dec, nanh) == 0
+    for r, want in [(0, 0), (7, None)]:
+        Wn = W.copy()
+        Wn[r, 9] = np.nan
+        hn = th.HeadMatrix.from_host(Wn)
+        dn = _rows_decoder(th, hn, ids[:n] * 0 + np.arange(n, dtype=np.uint32))
+        ref = orc.greedy_step(Wn, pos, np.arange(n, dtype=np.uint32))[0]
+        assert _rows_greedy(dn, pos) == ref
+        if want is not None:
+            assert ref == want
+    Wi = W.copy()
+    Wi[40, 0] = np.inf
+    Wi[41, 0] = np.inf
+    hi = th.HeadMatrix.from_host(Wi)
+    di = _rows_decoder(th, hi, np.arange(n, dtype=np.uint32))
+    assert _rows_greedy(di, pos) == orc.greedy_step(Wi, pos, np.arange(n, dtype=np.uint32))[0] == 40
+    # signed zeros: every row's logit is -0.0 or +0.0 -> row 0
+    Wz = np.zeros((n, d), np.float32)
+    Wz[::2, 0] = -1.0
+    hz = th.HeadMatrix.from_host(Wz)
+    dz = _rows_decoder(th, hz, np.arange(n, dtype=np.uint32))
+    e1 = np.zeros(d, np.float32)
+    e1[0] = 0.0
+    assert _rows_greedy(dz, e1) == 0
+    # remap through plan ids and repeated calls
+    dm = _rows_decoder(th, head, np.arange(n, dtype=np.uint32))
+    dm.ids.copy_(torch.from_numpy(ids.view(np.int32)).cuda())
+    h = rng.uniform(-1, 1, d).astype(np.float32)
+    want = orc.greedy_step(W, h, ids)[0]
+    for _ in range(3):
+        assert _rows_greedy(dm, h) == want
+    assert dmap is not None
+
+
+def test_rows_certified_candidate_overflow_paths(th):
+    """Many candidates: > 16 per CTA (per-CTA overflow -> rescan of that
+    CTA's rows) and > 1024 in total (every row recomputed)."""
+    for n in (500, 3000):
+        d = 64
+        rng = np.random.default_rng(n)
+        base = rng.uniform(-1, 1, d).astype(np.float32)
+        W = np.stack([base[rng.permutation(d)] for _ in range(n)])  # near-ties
+        head = th.HeadMatrix.from_host(W)
+        ids = np.arange(n, dtype=np.uint32)
+        dec = _rows_decoder(th, head, ids)
+        h = np.ones(d, np.float32)
+        want, wmax = orc.greedy_step(W, h, ids)
+        got, gmax = _rows_greedy(dec, h, want_max=True)
+        assert got == want and bits([gmax])[0] == bits([wmax])[0]
+        assert _rows_greedy(dec, h) == want
+
+
+def test_rows_certified_slice_row_base(th):
+    """Identity-plan slice (vocab-shard use): rows [r0, r1) of the head, ids
+    returned as row_base + row; plan_start=0 disables the NaN-at-row-0 rule."""
+    V, d = 20000, 512
+    head = th.HeadMatrix.random(V, d, 0xABC, storage=th.SVT_BF16)
+    W = head.to_host()
+    r0, r1 = 7000, 13000
+    sl = th.HeadMatrix(0, d, 2, th.SVT_BF16, data=head.data[r0:r1])
+    dummy = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dec = th.RowDecoder(sl, dummy, r1 - r0, materialize=False, row_base=r0, plan_start=0,
+                        remap=False)
+    dec._pre = (sl.data.data_ptr(), sl.storage, r1 - r0, d, None, r1 - r0)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        h = rng.uniform(-1, 1, d).astype(np.float32)
+        want = orc.greedy_step(W[r0:r1], h, np.arange(r0, r1, dtype=np.uint32))[0]
+        assert _rows_greedy(dec, h) == want
