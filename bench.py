@@ -51,11 +51,15 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
+    ap.add_argument("--sweep-sizes", default="1024,4096,16384,65536,128256")
+    ap.add_argument("--sweep-batches", default="1,32,256")
+    ap.add_argument("--sweep-dtypes", default="bf16,f32")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg2: batch-shard tailored decode (headline); cfg3: batched "
                          "prefill-scoring on tcgen05 (Llama-3.2-3B shape, 256 seqs x 2048 "
                          "positions per GPU); cfg4: vocab-sharded full-vocab greedy "
-                         "(Gemma-2-2B shape) with an NCCL record all-gather")
+                         "(Gemma-2-2B shape) with an NCCL record all-gather; cfg5: subset-size "
+                         "sweep |S| 1k..128k x batch 1/32/256, tailored vs full-vocab")
     return ap.parse_args()
 
 
@@ -506,6 +510,8 @@ def main():
         return run_vocab_shard(args, torch, dist, world, rank)
     if args.workload == "cfg3":
         return run_prefill(args, torch, dist, world, rank)
+    if args.workload == "cfg5":
+        return run_sweep(args, torch, rank)
     from paper_2508_15229_b200 import session as session_mod
     from paper_2508_15229_b200 import synth
     from paper_2508_15229_b200 import tailored_head as th
@@ -931,6 +937,173 @@ def prefill_secondary(torch, th, synth, S=256, K=5, W=3):
          "certification": list(st["sc"].stats())}
     del st
     return r
+
+
+CFG5 = dict(workload="cfg5: subset-size sweep, Llama-3.2-1B-shaped head (V=128256, d=2048)",
+            V=128256, d=2048)
+
+
+def _graph_ms(torch, fn, reps, flush, sink, K=3):
+    """Per-step device time of fn(): CUDA graphs of reps x (256 MB read-flush
+    + fn) and reps x flush, replayed K times; difference / reps."""
+    s = torch.cuda.Stream()
+    out = []
+    for with_fn in (False, True):
+        with torch.cuda.stream(s):
+            torch.sum(flush, dim=0, out=sink)
+            if with_fn:
+                fn(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                torch.sum(flush, dim=0, out=sink)
+                if with_fn:
+                    fn(s)
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(K):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b) / K)
+        del g
+    return (out[1] - out[0]) / reps
+
+
+def run_sweep(args, torch, rank):
+    """cfg5 (BASELINE configs[4]): tailored vs full-vocab head over |S| in
+    {1k, 4k, 16k, 64k, 128k = V} at batch 1/32/256, bf16 and f32 weights,
+    shared-subset and per-request plans (seeded uniform subsets). One step =
+    one greedy token for the whole batch; the L2 is flushed (256 MB read)
+    before every step and the flush time subtracted (graph differences).
+    Paths: batch 1 -> svt_greedy_certified_rows; per-request -> the
+    exact-order GEMV (interleaved sub-heads when they fit 24 GB, else fused
+    gather); shared bf16 -> tcgen05 GEMM with certified ids (svt_prefill_score,
+    positions padded to 128); shared f32 -> the exact-order GEMV with the
+    same plan for every request."""
+    from paper_2508_15229_b200 import prefill, synth
+    from paper_2508_15229_b200 import tailored_head as th
+
+    V, d = CFG5["V"], CFG5["d"]
+    sizes = [int(x) for x in args.sweep_sizes.split(",")]
+    batches = [int(x) for x in args.sweep_batches.split(",")]
+    dtypes = args.sweep_dtypes.split(",")
+    peak, peak_kind = load_peaks()
+    tpeak, _ = load_tensor_peak()
+    flush = torch.ones(256 << 18, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
+    rows = []
+    rng = np.random.default_rng(0xCF65)
+    for dt in dtypes:
+        st = th.SVT_BF16 if dt == "bf16" else th.SVT_F32
+        wb = 2 if dt == "bf16" else 4
+        head = th.HeadMatrix.random(V, d, synth.SEED_W, storage=st)
+        for B in batches:
+            hid = torch.empty(B * d, dtype=torch.float32, device="cuda")
+            th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_F32,
+                         th.SVT_BF16 if dt == "bf16" else th.SVT_F32, 0, B * d, synth.SEED_H,
+                         None)
+            hid = hid.view(B, d)
+            out = torch.empty((B + 127) // 128 * 128, dtype=torch.int32, device="cuda")
+            for k in sizes:
+                k = min(k, V)
+                shared_ids = (np.arange(V, dtype=np.uint32) if k == V else
+                              np.sort(rng.choice(V, k, replace=False)).astype(np.uint32))
+                modes = ["shared"] if B == 1 else ["shared", "per_request"]
+                for mode in modes:
+                    rec = {"dtype": dt, "batch": B, "subset": k, "mode": mode,
+                           "full_vocab": k == V}
+                    keep = []
+                    if B == 1:
+                        ids_d = torch.from_numpy(shared_ids.view(np.int32)).cuda()
+                        dec = th.RowDecoder(head, ids_d, k)
+                        keep.append(dec)
+                        h0 = hid[0]
+
+                        def fn(s, dec=dec, h0=h0):
+                            dec.stream = s
+                            dec.greedy(h0, out)
+                        rec["path"] = "svt_greedy_certified_rows"
+                        nbytes = k * d * wb + d * 4 + 8
+                        flops = None
+                    elif mode == "shared" and dt == "bf16":
+                        P = (B + 127) // 128 * 128
+                        ids_d = torch.from_numpy(shared_ids.view(np.int32)).cuda()
+                        sc = prefill.PrefillScorer(head, ids_d, np.array([0, k], np.int64), P)
+                        # pad to whole 128-position tiles with copies of the last hidden
+                        # state (zeros would make every row tie -> all-rows recompute)
+                        hb = torch.empty((P, d), dtype=torch.bfloat16, device="cuda")
+                        hb[:B] = hid.to(torch.bfloat16)
+                        hb[B:] = hb[B - 1]
+                        keep += [sc, hb]
+
+                        def fn(s, sc=sc, hb=hb):
+                            sc.stream = s
+                            sc.score(hb, out)
+                        rec["path"] = "svt_prefill_score (tcgen05, %d positions)" % P
+                        nbytes = k * d * wb + P * d * 2 + B * 8
+                        flops = 2.0 * P * k * d
+                    else:
+                        plans = ([shared_ids] * B if mode == "shared" else
+                                 [np.sort(rng.choice(V, k, replace=False)).astype(np.uint32)
+                                  if k < V else shared_ids for _ in range(B)])
+                        tb = th.TailoredBatch.from_plans(V, plans)
+                        sub_bytes = th._lib.lib.svt_subhead_bytes(st, d, tb.max_groups)
+                        fused = sub_bytes > (24 << 30)
+                        if fused:
+                            tb.attach(head)
+                        else:
+                            tb.gather(head)
+                        hl = torch.zeros((B, (d + 3) // 4 * 4), dtype=torch.float32,
+                                         device="cuda")
+                        hl[:, :d] = hid
+                        keep += [tb, hl]
+
+                        def fn(s, tb=tb, hl=hl, fused=fused):
+                            tb.stream = s
+                            tb.greedy(hl, out, fused=fused)
+                        rec["path"] = "gemv_ring_kernel<%s,%s,argmax>" % (
+                            dt, "ROWS (fused gather)" if fused else "INTERLEAVED")
+                        nbytes = B * (k * d * wb + d * 4 + 8) + (B * k * 4 if fused else 0)
+                        flops = None
+                    reps = 4 if nbytes < (4 << 30) else 2
+                    ms = _graph_ms(torch, fn, reps, flush, sink)
+                    rec["us_per_step"] = ms * 1e3
+                    rec["tokens_per_s"] = B / (ms / 1e3)
+                    rec["algorithmic_bytes"] = nbytes
+                    rec["gbs"] = nbytes / (ms / 1e3) / 1e9
+                    rec["hbm_frac"] = rec["gbs"] / peak
+                    if flops is not None:
+                        rec["tflops"] = flops / (ms / 1e3) / 1e12
+                        rec["tensor_frac"] = rec["tflops"] / tpeak
+                    rows.append(rec)
+                    print(json.dumps(rec), file=sys.stderr, flush=True)
+                    del keep
+                    torch.cuda.empty_cache()
+        del head
+        torch.cuda.empty_cache()
+    # tailored vs full-vocab speed-up per (dtype, batch, mode)
+    full = {(r["dtype"], r["batch"], r["mode"]): r["us_per_step"] for r in rows if r["full_vocab"]}
+    for r in rows:
+        f = full.get((r["dtype"], r["batch"], r["mode"]))
+        if f:
+            r["speedup_vs_full_vocab"] = f / r["us_per_step"]
+    main_row = next((r for r in rows if r["batch"] == 1 and r["dtype"] == dtypes[0]
+                     and r["subset"] == min(sizes)), rows[0])
+    result = {"metric": METRIC, "value": main_row["tokens_per_s"], "unit": UNIT, "n_gpus": 1,
+              "steps": 1, "warmup": 1, "ms_per_step": main_row["us_per_step"] / 1e3,
+              "higher_is_better": True, "scaling": "none", "vs_baseline": None,
+              "dtype": dtypes[0], "data": "synthetic (seeded uniform subsets); random-init head",
+              "config": {"workload": CFG5["workload"], "V": V, "d": d, "sizes": sizes,
+                         "batches": batches, "dtypes": dtypes,
+                         "l2": "256 MB read-flush before every step (subtracted)"},
+              "peaks": {"hbm_gbs": peak, "hbm_source": peak_kind, "bf16_tflops": tpeak},
+              "sweep": rows}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
 
 
 if __name__ == "__main__":

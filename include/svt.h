@@ -341,7 +341,7 @@ svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads, int64
                              void* d_workspace, svt_stream stream);
 /* Tuning (process-wide): pair 0 forces the single-CTA (cta_group::1) GEMM
  * (default 1: CTA-pair cta_group::2 whenever positions % 256 == 0); nsplit
- * in [1, 8] = N-range splits per M tile (default 2), one partial top-8
+ * in [1, 128] = N-range splits per M tile (default 0 = automatic), one partial top-8
  * record per (position, split). svt_prefill_offsets gives byte offsets in
  * the workspace of: [0] top values f32 [S*P][nsplit][8], [1] top rows u32
  * [S*P][nsplit][8], [2] counters u32 [8] (certified directly, recomputed,
@@ -350,6 +350,11 @@ svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads, int64
  * out_max of svt_prefill_score: the exact reference logit for recomputed
  * positions, the tensor-core logit for positions certified directly. */
 svt_status svt_prefill_set_tuning(int32_t pair, int32_t nsplit);
+/* Split count a svt_prefill_score call over (sequences, positions) uses with
+ * the current tuning. nsplit 0 (the default) is automatic: 2, raised (up to
+ * 128) until the GEMM grid covers every SM — e.g. a shared-subset decode
+ * batch scored as ONE sequence of `batch` positions. */
+int32_t svt_prefill_effective_nsplit(int32_t sequences, int32_t positions);
 void svt_prefill_get_tuning(int32_t* pair, int32_t* nsplit);
 void svt_prefill_offsets(int32_t sequences, int32_t positions, int64_t* out4);
 /* Upward-rounded L2 norm of each row of a bf16 matrix (dim % 8 == 0). */

@@ -105,6 +105,7 @@ _SIGS = {
     "svt_row_norms_bf16": ([_vp, _i64, _i32, _vp, _vp], C.c_int),
     "svt_prefill_set_tuning": ([_i32, _i32], C.c_int),
     "svt_prefill_get_tuning": ([_vp, _vp], None),
+    "svt_prefill_effective_nsplit": ([_i32, _i32], _i32),
     "svt_prefill_offsets": ([_i32, _i32, _vp], None),
     "svt_shard_combine": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),

@@ -49,7 +49,8 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSlots = 128;
 constexpr int kSmemBudget = 224 * 1024;
-constexpr int kCapG = 16;        // candidate list per CTA (count > 1)
+constexpr int kWarpCand = 4;     // rows per warp kept within reach of its running max
+constexpr int kCapG = 64;        // candidate list per CTA (16 warps x 4; count > 2)
 constexpr int kMaxGrid = 256;   // the tail reads <= 8 records per lane
 constexpr int kMaxCand = 1024;   // tail candidate list
 constexpr int kPiece = 2048;     // bytes per exact-recompute piece
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
     extern __shared__ __align__(128) uint8_t dsmem[];
     __shared__ uint64_t s_full[kMaxSlots];
     __shared__ float s_wL[kWarps];
-    __shared__ uint2 s_wc0[kWarps], s_wc1[kWarps];
+    __shared__ uint2 s_wc[kWarpCand][kWarps];
     __shared__ unsigned s_wn[kWarps];
     __shared__ unsigned s_n, s_ovf, s_bad, s_last, s_nwork;
     __shared__ uint32_t s_ids[kIdCache];
@@ -316,7 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
 
     // ---- stream: one row per warp at a time ------------------------------------
     float wL = -FLT_MAX;  // lane 0: running max lo of this warp's rows
-    uint2 c0 = make_uint2(0u, 0u), c1 = make_uint2(0u, 0u);  // rows with hi >= wL
+    uint2 cw[kWarpCand];  // lane 0: rows with hi >= wL (pruned as wL rises)
+#pragma unroll
+    for (int j = 0; j < kWarpCand; ++j) cw[j] = make_uint2(0u, 0u);
     unsigned ncand = 0, wovf = 0, wbad = 0;
     for (int64_t i = warp; i < nrows;
          i += (i % NS) + kWarps < NS ? kWarps : NS - (i % NS) + warp) {
@@ -344,21 +347,26 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
             float lo = __fsub_rd(f, bnd);
             const float hi = __fadd_ru(f, bnd);
             if (!(lo == lo)) lo = -FLT_MAX;
-            if (lo > wL) {  // prune the rows the raised bar excludes
+            p.ws_hi[r0 + i] = hi;  // for a rescan should this warp overflow
+            if (lo > wL) {  // prune the rows the raised bar excludes (keep order)
                 wL = lo;
-                const bool k0 = ncand >= 1 && __uint_as_float(c0.y) >= wL;
-                const bool k1 = ncand >= 2 && __uint_as_float(c1.y) >= wL;
-                if (!k0 && k1) c0 = c1;
-                ncand = (k0 ? 1u : 0u) + (k1 ? 1u : 0u);
+                unsigned k = 0;
+#pragma unroll
+                for (int j = 0; j < kWarpCand; ++j) {
+                    const bool keep = j < static_cast<int>(ncand) && __uint_as_float(cw[j].y) >= wL;
+#pragma unroll
+                    for (int t = 0; t < kWarpCand; ++t)
+                        if (keep && t == static_cast<int>(k)) cw[t] = cw[j];
+                    k += keep ? 1u : 0u;
+                }
+                ncand = k;
             }
             if (hi >= wL) {
                 const uint2 e = make_uint2(static_cast<uint32_t>(r0 + i), __float_as_uint(hi));
-                if (ncand == 0)
-                    c0 = e;
-                else if (ncand == 1)
-                    c1 = e;
-                else
-                    wovf = 1;
+#pragma unroll
+                for (int t = 0; t < kWarpCand; ++t)
+                    if (t == static_cast<int>(ncand)) cw[t] = e;
+                if (ncand >= kWarpCand) wovf = 1;
                 ++ncand;
             }
         }
@@ -367,8 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
     if (lane == 0) {
         s_wL[warp] = wL;
         s_wn[warp] = wovf ? kOverflow : ncand;
-        s_wc0[warp] = c0;
-        s_wc1[warp] = c1;
+#pragma unroll
+        for (int j = 0; j < kWarpCand; ++j) s_wc[j][warp] = cw[j];
         if (wbad) s_bad = 1;
     }
     __syncthreads();
@@ -379,38 +387,40 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xFFFFFFFFu, L, o));
         const unsigned nw = mine ? s_wn[lane] : 0u;
-        const uint2 a0 = mine ? s_wc0[lane] : make_uint2(0u, 0u);
-        const uint2 a1 = mine ? s_wc1[lane] : make_uint2(0u, 0u);
-        const bool any_ovf = __any_sync(0xFFFFFFFFu, nw == kOverflow);
-        const bool q0 = nw != kOverflow && nw >= 1 && __uint_as_float(a0.y) >= L;
-        const bool q1 = nw != kOverflow && nw >= 2 && __uint_as_float(a1.y) >= L;
-        const unsigned m0 = __ballot_sync(0xFFFFFFFFu, q0), m1 = __ballot_sync(0xFFFFFFFFu, q1);
-        const unsigned cnt = __popc(m0) + __popc(m1);
-        const bool ovf = any_ovf || cnt > kCapG;
+        const bool ovf = __any_sync(0xFFFFFFFFu, nw == kOverflow);
         const unsigned lt = (1u << lane) - 1u;
-        const unsigned pos0 = __popc(m0 & lt), pos1 = __popc(m0) + __popc(m1 & lt);
         auto id_of = [&](uint32_t row) -> uint32_t {
             const int64_t li = static_cast<int64_t>(row) - r0;
             return li < kIdCache ? s_ids[li]
                                  : (p.plan_ids ? __ldg(p.plan_ids + row) : p.row_base + row);
         };
-        if (!ovf && cnt > 2) {
-            if (q0) p.gcand[c * kCapG + pos0] = a0;
-            if (q1) p.gcand[c * kCapG + pos1] = a1;
+        // entries (warp w, slot j) with hi >= L, numbered slot-major
+        unsigned cnt = 0;
+        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;  // {row, hi, id, -} of #0 and #1
+        bool has0 = false, has1 = false;
+#pragma unroll
+        for (int j = 0; j < kWarpCand; ++j) {
+            const uint2 a = mine ? s_wc[j][lane] : make_uint2(0u, 0u);
+            const bool q = nw != kOverflow && j < static_cast<int>(nw) &&
+                           __uint_as_float(a.y) >= L;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, q);
+            const unsigned pos = cnt + __popc(m & lt);
+            if (q && pos < static_cast<unsigned>(kCapG)) p.gcand[c * kCapG + pos] = a;
+            if (q && pos < 2) {
+                const uint4 e = make_uint4(a.x, a.y, id_of(a.x), 0u);
+                if (pos == 0) {
+                    e0 = e;
+                    has0 = true;
+                } else {
+                    e1 = e;
+                    has1 = true;
+                }
+            }
+            cnt += __popc(m);
         }
-        // inline entries: candidate k (k = 0, 1) travels through lane 0
-        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;  // {row, hi, id, -}
-        if (q0 && pos0 < 2) {
-            const uint4 e = make_uint4(a0.x, a0.y, id_of(a0.x), 0u);
-            if (pos0 == 0) e0 = e; else e1 = e;
-        }
-        if (q1 && pos1 < 2) {
-            const uint4 e = make_uint4(a1.x, a1.y, id_of(a1.x), 0u);
-            if (pos1 == 0) e0 = e; else e1 = e;
-        }
-        const unsigned src0 = __ballot_sync(0xFFFFFFFFu, (q0 && pos0 == 0) || (q1 && pos1 == 0));
-        const unsigned src1 = __ballot_sync(0xFFFFFFFFu, (q0 && pos0 == 1) || (q1 && pos1 == 1));
-        const int l0 = src0 ? __ffs(src0) - 1 : 0, l1 = src1 ? __ffs(src1) - 1 : 0;
+        const unsigned s0 = __ballot_sync(0xFFFFFFFFu, has0);
+        const unsigned s1 = __ballot_sync(0xFFFFFFFFu, has1);
+        const int l0 = s0 ? __ffs(s0) - 1 : 0, l1 = s1 ? __ffs(s1) - 1 : 0;
         e0 = make_uint4(__shfl_sync(0xFFFFFFFFu, e0.x, l0), __shfl_sync(0xFFFFFFFFu, e0.y, l0),
                         __shfl_sync(0xFFFFFFFFu, e0.z, l0), 0u);
         e1 = make_uint4(__shfl_sync(0xFFFFFFFFu, e1.x, l1), __shfl_sync(0xFFFFFFFFu, e1.y, l1),
@@ -424,14 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
         }
     }
     __syncthreads();
-    if (s_ovf) {  // rare: every row's hi for the tail's rescan (rows re-read)
-        for (int64_t i = warp; i < nrows; i += kWarps) {
-            float f, a;
-            row_dot<DT>(reinterpret_cast<const uint4*>(row_ptr(p, r0 + i)), s_h, p.nchunks, lane,
-                        f, a);
-            if (lane == 0)
-                p.ws_hi[r0 + i] = __fadd_ru(f, __fadd_ru(__fmul_ru(p.c_rel, a), p.eta));
-        }
+    if (s_ovf) {  // rare: make every row's hi (written by lane 0s) visible for the rescan
         __threadfence();
         __syncthreads();
     }
@@ -532,7 +535,13 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
             if (lane == 0) {
                 const unsigned n = s_n;
                 const bool all = bad || n == 0 || n > static_cast<unsigned>(kMaxCand);
-                s_nwork = all ? 0xFFFFFFFFu : n;
+                if (!all && n == 1 && !p.out_max) {  // one row left after the global bar
+                    const uint32_t r = s_list[0];
+                    *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+                    s_nwork = 0;
+                } else {
+                    s_nwork = all ? 0xFFFFFFFFu : n;
+                }
                 s_key = 0ull;
             }
         }

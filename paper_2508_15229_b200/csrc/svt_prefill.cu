@@ -821,17 +821,28 @@ __global__ void all_finalize_kernel(int P, const int64_t* __restrict__ id_off,
 
 // per-sequence max row norm from a per-head row-norm table (computed once
 // per head) through the plan ids
+// Work item = (sequence, 2048-row chunk of its plan): large plans (a shared
+// subset of up to |V| rows scored as one sequence) spread over the grid
+// instead of one block walking 128k dependent norm lookups.
+constexpr int kWmaxChunk = 2048;
 __global__ void plan_wmax_kernel(const float* __restrict__ head_norm,
                                  const uint32_t* __restrict__ plan_ids,
                                  const int64_t* __restrict__ id_off,
-                                 const int64_t* __restrict__ n_rows, int S,
+                                 const int64_t* __restrict__ n_rows, int S, int chunks_per_seq,
                                  unsigned int* __restrict__ wmax_bits,
                                  unsigned int* __restrict__ stats) {
-    for (int s = blockIdx.x; s < S; s += gridDim.x) {
-        if (threadIdx.x == 0) atomicMax(&stats[5], static_cast<unsigned int>(n_rows[s]));
+    const int64_t items = static_cast<int64_t>(S) * chunks_per_seq;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int s = static_cast<int>(it / chunks_per_seq);
+        const int64_t c0 = (it - static_cast<int64_t>(s) * chunks_per_seq) * kWmaxChunk;
+        const int64_t n = n_rows[s];
+        if (c0 == 0 && threadIdx.x == 0) atomicMax(&stats[5], static_cast<unsigned int>(n));
+        if (c0 >= n) continue;
+        const int64_t c1 = min(n, c0 + kWmaxChunk);
+        const uint32_t* ids = plan_ids + id_off[s];
         float m = 0.0f;
-        for (int64_t r = threadIdx.x; r < n_rows[s]; r += blockDim.x)
-            m = fmaxf(m, head_norm[plan_ids[id_off[s] + r]]);
+#pragma unroll 4
+        for (int64_t r = c0 + threadIdx.x; r < c1; r += blockDim.x) m = fmaxf(m, head_norm[ids[r]]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
         if ((threadIdx.x & 31) == 0) atomicMax(&wmax_bits[s], __float_as_uint(m));
@@ -890,15 +901,31 @@ double gamma_n(double n) {
 namespace svt {
 namespace {
 bool g_prefill_pair = true;
-int g_prefill_nsplit = 2;
+int g_prefill_nsplit = 0;  // 0: automatic (effective_nsplit)
+constexpr int kMaxSplitAuto = 128;
+
+// N-range splits per M tile for a launch: the tuned value, or (automatic)
+// 2 raised until the grid fills every SM — few sequences x positions (e.g. a
+// shared-subset decode batch scored as one sequence) would otherwise run on
+// a handful of CTAs.
+int effective_nsplit(int64_t S, int64_t P, bool pair) {
+    if (g_prefill_nsplit > 0) return g_prefill_nsplit;
+    const int ncta = pair ? 2 : 1;
+    const int64_t groups = S * (P / (BM * ncta));
+    const int64_t want = sm_count() / ncta;
+    int64_t ns = 2;
+    if (groups > 0 && groups * ns < want) ns = (want + groups - 1) / groups;
+    return static_cast<int>(ns > kMaxSplitAuto ? kMaxSplitAuto : ns);
+}
+bool use_pair(int64_t P) { return P % (2 * BM) == 0 && g_prefill_pair; }
 }
 }  // namespace svt
 using svt::g_prefill_nsplit;
 using svt::g_prefill_pair;
 
 extern "C" svt_status svt_prefill_set_tuning(int32_t pair, int32_t nsplit) {
-    if (nsplit < 1 || nsplit > svt::kMaxSplit) {
-        svt::set_error("prefill nsplit must be in [1, %d]", svt::kMaxSplit);
+    if (nsplit < 0 || nsplit > svt::kMaxSplitAuto) {
+        svt::set_error("prefill nsplit must be 0 (automatic) or in [1, %d]", svt::kMaxSplitAuto);
         return SVT_ERR_CONFIG;
     }
     g_prefill_pair = pair != 0;
@@ -966,11 +993,24 @@ SideStream* side_stream() {
 }  // namespace svt
 
 extern "C" size_t svt_prefill_workspace_bytes(int32_t sequences, int32_t positions) {
-    return svt::PrefillLayout(sequences, positions, svt::kMaxSplit).end;
+    using namespace svt;
+    // room for every split count a call with the current tuning can use
+    int ns = kMaxSplit;
+    for (bool pr : {false, true}) {
+        const int e = effective_nsplit(sequences, positions, pr);
+        ns = e > ns ? e : ns;
+    }
+    return PrefillLayout(sequences, positions, ns).end;
+}
+
+extern "C" int32_t svt_prefill_effective_nsplit(int32_t sequences, int32_t positions) {
+    return svt::effective_nsplit(sequences, positions, svt::use_pair(positions));
 }
 
 extern "C" void svt_prefill_offsets(int32_t sequences, int32_t positions, int64_t* out) {
-    const svt::PrefillLayout L(sequences, positions, g_prefill_nsplit);
+    const svt::PrefillLayout L(sequences, positions,
+                               svt::effective_nsplit(sequences, positions,
+                                                     svt::use_pair(positions)));
     out[0] = static_cast<int64_t>(L.top_val);
     out[1] = static_cast<int64_t>(L.top_row);
     out[2] = static_cast<int64_t>(L.stats);
@@ -1007,7 +1047,9 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t npos = static_cast<int64_t>(sequences) * positions;
     uint8_t* ws = static_cast<uint8_t*>(d_workspace);
-    const int ns = g_prefill_nsplit;
+    // the CTA pair (cta_group::2) needs 256-position M tiles
+    const bool pair = use_pair(positions);
+    const int ns = effective_nsplit(sequences, positions, pair);
     const PrefillLayout L(sequences, positions, ns);
     float* top_val = reinterpret_cast<float*>(ws + L.top_val);
     uint32_t* top_row = reinterpret_cast<uint32_t*>(ws + L.top_row);
@@ -1027,8 +1069,6 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
 
     CUtensorMap mapH, mapW;
     if (svt_status s = make_map(&mapH, d_hidden, static_cast<uint64_t>(npos), dim, BM)) return s;
-    // the CTA pair (cta_group::2) needs 256-position M tiles
-    const bool pair = positions % (2 * BM) == 0 && g_prefill_pair;
     if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows), dim,
                                 pair ? BN / 2 : BN))
         return s;
@@ -1055,8 +1095,13 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
         norms_kernel<<<sm_count() * 4, 256, 0, side->stream>>>(
             static_cast<const uint16_t*>(d_hidden), npos, dim, hnorm);
         SVT_LAUNCH_CHECK("norms_kernel");
-        plan_wmax_kernel<<<sequences < 1024 ? sequences : 1024, 256, 0, side->stream>>>(
-            d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows, sequences, wmax, stats);
+        // chunks per sequence: enough for any plan the sub-head rows can hold
+        // (chunks past a plan's end are skipped)
+        const int cps = static_cast<int>((total_sub_rows + kWmaxChunk - 1) / kWmaxChunk) + 1;
+        const int64_t items = static_cast<int64_t>(sequences) * cps;
+        plan_wmax_kernel<<<static_cast<int>(items < sm_count() * 8 ? items : sm_count() * 8), 256, 0,
+                           side->stream>>>(d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows,
+                                           sequences, cps, wmax, stats);
         SVT_LAUNCH_CHECK("plan_wmax_kernel");
     }
     if (side->join) SVT_CUDA_TRY(cudaEventRecord(side->join, side->stream));

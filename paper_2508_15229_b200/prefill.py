@@ -88,7 +88,7 @@ class PrefillScorer:
         return pr.value, ns.value
 
     @staticmethod
-    def set_tuning(pair: bool = True, nsplit: int = 2):
+    def set_tuning(pair: bool = True, nsplit: int = 0):
         call("svt_prefill_set_tuning", int(pair), int(nsplit))
 
     def _offsets(self):
@@ -100,7 +100,7 @@ class PrefillScorer:
         """Partial top-8 records of the last score(): (values f32
         [S*P, nsplit*8], plan rows u32-as-int32 [S*P, nsplit*8])."""
         npos = self.S * self.P
-        ns = self.tuning()[1]
+        ns = _lib.lib.svt_prefill_effective_nsplit(self.S, self.P)
         o = self._offsets()
         v = self.ws[o[0]: o[0] + npos * ns * 32].view(torch.float32).view(npos, ns * 8)
         r = self.ws[o[1]: o[1] + npos * ns * 32].view(torch.int32).view(npos, ns * 8)

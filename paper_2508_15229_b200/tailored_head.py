@@ -484,6 +484,37 @@ class TailoredBatch:
         tb.run_select()
         return tb
 
+    @classmethod
+    def from_plans(cls, V: int, plans, stream=None) -> "TailoredBatch":
+        """A batch over explicit plans (strictly increasing id arrays, e.g.
+        produced elsewhere or loaded from plan files) — no select; the plan
+        counters report every row as dynamic."""
+        B = len(plans)
+        caps = np.array([len(q) for q in plans], np.int64)
+        tb = cls(V, B, caps, stream)
+        if B and int(caps.sum()):
+            flat = np.concatenate([np.asarray(q, np.uint32) for q in plans])
+            if int(flat.max()) >= V:
+                raise IntegrityError(f"plan id {int(flat.max())} out of range for vocabulary "
+                                     f"size {V}")
+            tb.active[: flat.size].copy_(torch.from_numpy(flat.view(np.int32)))
+        if B:
+            n = torch.from_numpy(caps).cuda()
+            tb.n_active.copy_(n)
+            tb.n_dynamic.copy_(n)
+            tb.n_static.zero_()
+            tb.first_bad_d.fill_(-1)
+        call("svt_plan_layout", tb.n_active.data_ptr(), tb.act_off.data_ptr(), B,
+             tb.group_begin.data_ptr(), tb.group_meta.data_ptr(), tb.max_groups,
+             _stream(stream))
+        return tb
+
+    def attach(self, head: HeadMatrix):
+        """Use ``head`` for the fused (no sub-head) decode without gathering."""
+        self.head = head
+        self._fast = None
+        return self
+
     def run_select(self):
         call("svt_select_batched", self._words.data_ptr(), self.V, self.V,
              self._prompts.data_ptr(), self._prompt_off.data_ptr(), self.B,
@@ -547,7 +578,8 @@ class TailoredBatch:
                       self.active.data_ptr(), self.B, self.max_groups)
             self._fast = {
                 False: (_lib.lib.svt_greedy_interleaved,
-                        (self.sub.data_ptr(), h.storage, h.dim()) + common),
+                        ((self.sub.data_ptr() if self.sub is not None else None), h.storage,
+                         h.dim()) + common),
                 True: (_lib.lib.svt_greedy_fused,
                        (h.data.data_ptr(), h.storage, h.rows(), h.dim()) + common),
             }

@@ -713,3 +713,37 @@ def test_rows_certified_slice_row_base(th):
         h = rng.uniform(-1, 1, d).astype(np.float32)
         want = orc.greedy_step(W[r0:r1], h, np.arange(r0, r1, dtype=np.uint32))[0]
         assert _rows_greedy(dec, h) == want
+
+
+@pytest.mark.parametrize("storage", ["bf16", "f32"])
+def test_explicit_plans_large_subsets(th, storage):
+    """TailoredBatch.from_plans (cfg5's explicit subsets, up to 16k rows per
+    request, one shared plan among them) through the interleaved and the
+    fused-gather decode: ids equal the reference greedy_step."""
+    V, d = 40000, 256
+    st = th.SVT_BF16 if storage == "bf16" else th.SVT_F32
+    head = th.HeadMatrix.random(V, d, 0x5EED, storage=st)
+    W = head.to_host()
+    rng = np.random.default_rng(9)
+    shared = np.sort(rng.choice(V, 16384, replace=False)).astype(np.uint32)
+    plans = [shared, np.sort(rng.choice(V, 1000, replace=False)).astype(np.uint32),
+             np.arange(V, dtype=np.uint32)[:12345], shared]
+    B = len(plans)
+    hid = rng.uniform(-1, 1, (B, d)).astype(np.float32)
+    if storage == "bf16":
+        hid = bf16_np(hid)
+    hd = torch.from_numpy(hid).cuda()
+    for fused in (False, True):
+        tb = th.TailoredBatch.from_plans(V, plans)
+        if fused:
+            tb.attach(head)
+        else:
+            tb.gather(head)
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        tb.greedy(hd, out, fused=fused)
+        got = out.cpu().numpy().view(np.uint32)
+        for b in range(B):
+            want = orc.greedy_step(W[plans[b]], hid[b], plans[b])[0]
+            assert got[b] == want, (fused, b)
+    with pytest.raises(th.IntegrityError):
+        th.TailoredBatch.from_plans(V, [np.array([V], np.uint32)])
