@@ -642,12 +642,15 @@ def run_vocab_shard(args, torch, dist, world, rank):
         "data": "synthetic (seeded splitmix64); random-init head",
         "config": {"workload": CFG4["workload"], "V": V, "d": d, "batch": B,
                    "decode_steps": steps, "parallelism": f"vocab-shard x{world}",
-                   "step": f"{steps} decode tokens; each = per-rank exact GEMV + argmax record + "
-                           "NCCL all-gather + combine",
+                   "step": f"{steps} decode tokens; each = per-rank greedy over its row slice "
+                           "(certified split-K at batch 1, exact-order GEMV otherwise) -> exact "
+                           "(max, id) record -> NCCL all-gather -> combine",
                    "l2": "per-rank slice > L2 at G<=8 (1.18 GB / G), no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "gemv_ring_kernel<bf16,ROWS,argmax> + finalize + all-gather",
+                     "kernel": ("svt_greedy_certified_rows (exact shard record)" if vs.shard.certified
+                                else "gemv_ring_kernel<bf16,ROWS,argmax> + finalize") +
+                               " + all-gather + combine",
                      "bytes_per_launch": per_rank_bytes, "avg_launch_us": step_avg * 1e3,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
         "gpu_launches": 3 * steps * args.steps, "clocks": clk.summary(),

@@ -298,6 +298,9 @@ svt_status svt_greedy_certified(const void* d_sub, svt_dtype dt, size_t dim,
  * (optional) receives the exact reference logit of the winner.
  * The winner remaps through d_plan_ids[row] or, when NULL, row_base + row;
  * plan_start != 0 when row 0 is the plan's first row (the NaN rule).
+ * d_out_record (optional, 16 bytes): the vocab-shard record {u64 key =
+ * orderable(exact max) << 32 | ~(row_base + row), u32 id, f32 max} consumed
+ * by svt_shard_combine; like d_out_max it forces the exact winner value.
  * Requirements: dim*esize % 16 == 0, dim <= 8192, 16-byte aligned head,
  * hidden (f32, dim values) and workspace. d_workspace:
  * svt_greedy_rows_workspace_bytes(n_rows) bytes, zeroed once by the caller
@@ -312,7 +315,8 @@ svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t he
                                      size_t dim, const uint32_t* d_src_ids, size_t n_rows,
                                      const float* d_hidden, const uint32_t* d_plan_ids,
                                      uint32_t row_base, int32_t plan_start, uint32_t* d_out_id,
-                                     float* d_out_max, void* d_workspace, svt_stream stream);
+                                     float* d_out_max, void* d_out_record, void* d_workspace,
+                                     svt_stream stream);
 /* ------------------------------------------------------------------------
  * Batched prefill-scoring on the tensor cores (tcgen05/TMEM, BASELINE cfg3):
  * for `sequences` x `positions` hidden states (bf16, row-major, sequence s's

@@ -85,6 +85,7 @@ struct SmallParams {
     int32_t plan_start;
     uint32_t* out_id;
     float* out_max;
+    uint4* out_key;  // optional shard record {key lo, key hi, id, max} (exact winner value)
     unsigned* ctrl;  // [0] ticket, [2] non-finite flag, [4]/[5] statistics
     Rec* rec;        // [kMaxGrid]
     uint2* gcand;    // [kMaxGrid][kCapG] {row, hi bits}
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
             total += __popc(__ballot_sync(0xFFFFFFFFu, b0)) + __popc(__ballot_sync(0xFFFFFFFFu, b1));
             big |= __ballot_sync(0xFFFFFFFFu, cnt > 2);
         }
-            if (!bad && !big && total == 1 && !p.out_max) {
+            if (!bad && !big && total == 1 && !p.out_max && !p.out_key) {
             // the single candidate is the reference argmax: its id is inline
 #pragma unroll
             for (int q = 0; q < kPer; ++q) {
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
             if (lane == 0) {
                 const unsigned n = s_n;
                 const bool all = bad || n == 0 || n > static_cast<unsigned>(kMaxCand);
-                if (!all && n == 1 && !p.out_max) {  // one row left after the global bar
+                if (!all && n == 1 && !p.out_max && !p.out_key) {  // one row left after the bar
                     const uint32_t r = s_list[0];
                     *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
                     s_nwork = 0;
@@ -567,15 +568,21 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
         if (tid == 0) {
             const unsigned long long k = s_key;
             const uint32_t r = 0xFFFFFFFFu - static_cast<uint32_t>(k);
-            if (k == 0ull) {  // every row NaN (and plan row 0 not in this slice)
-                *p.out_id = 0xFFFFFFFFu;
-                if (p.out_max) *p.out_max = __int_as_float(0x7FC00000);
-            } else {
-                *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
-                if (p.out_max)
-                    *p.out_max = k == kNanRow0Key ? __int_as_float(0x7FC00000)
-                                                  : float_of_ord(static_cast<uint32_t>(k >> 32));
+            uint32_t id = 0xFFFFFFFFu;
+            float mx = __int_as_float(0x7FC00000);
+            unsigned long long gk = 0ull;  // key over the global row order (shard combine)
+            if (k != 0ull) {  // (k == 0: every row NaN and plan row 0 not in this slice)
+                id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+                if (k != kNanRow0Key) mx = float_of_ord(static_cast<uint32_t>(k >> 32));
+                gk = k == kNanRow0Key
+                         ? k
+                         : (k & 0xFFFFFFFF00000000ull) | (0xFFFFFFFFu - (p.row_base + r));
             }
+            *p.out_id = id;
+            if (p.out_max) *p.out_max = mx;
+            if (p.out_key)
+                *p.out_key = make_uint4(static_cast<uint32_t>(gk), static_cast<uint32_t>(gk >> 32),
+                                        id, __float_as_uint(mx));
         }
     }
     SVT_STAMP(6);
@@ -633,7 +640,8 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
                                                 size_t n_rows, const float* d_hidden,
                                                 const uint32_t* d_plan_ids, uint32_t row_base,
                                                 int32_t plan_start, uint32_t* d_out_id,
-                                                float* d_out_max, void* d_workspace,
+                                                float* d_out_max, void* d_out_record,
+                                                void* d_workspace,
                                                 svt_stream stream) {
     using namespace svt;
     if (dt != SVT_F32 && dt != SVT_F16 && dt != SVT_BF16) {
@@ -677,6 +685,7 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
     p.plan_start = plan_start;
     p.out_id = d_out_id;
     p.out_max = d_out_max;
+    p.out_key = static_cast<uint4*>(d_out_record);
     p.dbg = g_rows_dbg;
     uint8_t* ws = static_cast<uint8_t*>(d_workspace);
     p.ctrl = reinterpret_cast<unsigned*>(ws);
@@ -720,11 +729,13 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
             if (cpl <= 2) return launch_rows<SVT_F16, 2>(p, grid, st);
             if (cpl <= 4) return launch_rows<SVT_F16, 4>(p, grid, st);
             if (cpl <= 8) return launch_rows<SVT_F16, 8>(p, grid, st);
+            if (cpl <= 9) return launch_rows<SVT_F16, 9>(p, grid, st);
             return launch_rows<SVT_F16, 0>(p, grid, st);
         default:
             if (cpl <= 2) return launch_rows<SVT_BF16, 2>(p, grid, st);
             if (cpl <= 4) return launch_rows<SVT_BF16, 4>(p, grid, st);
             if (cpl <= 8) return launch_rows<SVT_BF16, 8>(p, grid, st);
+            if (cpl <= 9) return launch_rows<SVT_BF16, 9>(p, grid, st);  // d = 2304 (cfg4)
             return launch_rows<SVT_BF16, 0>(p, grid, st);
     }
 }

@@ -14,6 +14,8 @@
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -61,11 +63,26 @@ class RowShard:
                               dtype=torch.uint8, device=dev)
         self.ids = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
         self.records = torch.zeros((max(B, 1), RECORD_WORDS), dtype=torch.int32, device=dev)
+        # batch 1: the certified single-request kernel (split-K at HBM speed,
+        # exact winner value for the record); otherwise the exact-order GEMV
+        esize = 4 if self.storage == 0 else 2
+        self.certified = (B == 1 and self.n > 0 and (self.dim * esize) % 16 == 0
+                          and self.dim <= 8192 and self.rows.data_ptr() % 16 == 0
+                          and not os.environ.get("SVT_SHARD_EXACT"))
+        if self.certified:
+            self.cws = torch.zeros(_lib.lib.svt_greedy_rows_workspace_bytes(self.n),
+                                   dtype=torch.uint8, device=dev)
 
     def step(self, hidden: torch.Tensor) -> torch.Tensor:
         """hidden [B, ld] f32 on the device -> records [B, 4] int32."""
         if self.n == 0:
             self.records.zero_()  # key 0 never wins
+            return self.records
+        if self.certified:
+            call("svt_greedy_certified_rows", self.rows.data_ptr(), self.storage, self.n,
+                 self.dim, None, self.n, hidden.data_ptr(), None, self.r0, self.plan_start,
+                 self.ids.data_ptr(), None, self.records.data_ptr(), self.cws.data_ptr(),
+                 _stream(self.stream))
             return self.records
         call("svt_greedy_fused", self.rows.data_ptr(), self.storage, self.n, self.dim,
              self.group_begin.data_ptr(), self.group_meta.data_ptr(), None, self.B,

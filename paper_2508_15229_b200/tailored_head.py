@@ -367,11 +367,14 @@ class RowDecoder:
         return self
 
     def greedy(self, hidden: torch.Tensor, out_id: torch.Tensor,
-               out_max: Optional[torch.Tensor] = None) -> torch.Tensor:
+               out_max: Optional[torch.Tensor] = None,
+               out_record: Optional[torch.Tensor] = None) -> torch.Tensor:
         """hidden: f32 [dim] on the device (16-byte aligned); out_id: one
-        int32; out_max (optional): the exact reference logit of the winner."""
+        int32; out_max (optional): the exact reference logit of the winner;
+        out_record (optional, 4 int32): the vocab-shard record for
+        svt_shard_combine."""
         st = self._fn(*self._pre, hidden.data_ptr(), *self._post, out_id.data_ptr(),
-                      _ptr(out_max), self.ws.data_ptr(), _stream(self.stream))
+                      _ptr(out_max), _ptr(out_record), self.ws.data_ptr(), _stream(self.stream))
         _lib.check(st, "svt_greedy_certified_rows")
         return out_id
 

@@ -747,3 +747,32 @@ def test_explicit_plans_large_subsets(th, storage):
             assert got[b] == want, (fused, b)
     with pytest.raises(th.IntegrityError):
         th.TailoredBatch.from_plans(V, [np.array([V], np.uint32)])
+
+
+def test_vocab_sharded_certified_batch1(th):
+    """Batch 1 vocab shards run the certified rows kernel with exact shard
+    records: random steps, an exact tie straddling shard boundaries (lowest
+    global id wins), NaN at global row 0 (shard 0 wins outright) and an
+    all-zero hidden state (every row ties -> row 0)."""
+    from paper_2508_15229_b200 import sharded
+
+    V, d = 24000, 512
+    rng = np.random.default_rng(21)
+    W = bf16_np(rng.uniform(-1, 1, (V, d)).astype(np.float32))
+    h = bf16_np(rng.uniform(-1, 1, d).astype(np.float32))
+    top = np.abs(W).max() * 0 + 1.0
+    Wt = W.copy()
+    for r in (11999, 12000, 17999):  # straddles the G=2 and G=4 boundaries
+        Wt[r] = np.sign(h) * top
+    Wn = W.copy()
+    Wn[0, 5] = np.nan
+    full = np.arange(V, dtype=np.uint32)
+    cases = [(W, rng.uniform(-1, 1, d).astype(np.float32)), (W, h), (Wt, h), (Wn, h),
+             (W, np.zeros(d, np.float32))]
+    for Wc, hc in cases:
+        hc = bf16_np(hc)
+        head = th.HeadMatrix.from_host(Wc, storage=th.SVT_BF16)
+        want = orc.greedy_step(Wc, hc, full)[0]
+        for G in (1, 2, 3, 4):
+            got = sharded.sharded_greedy_local(head, hc[None, :], G)
+            assert int(got[0]) == int(want), (G, want, got)
