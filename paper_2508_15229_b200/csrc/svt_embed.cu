@@ -10,6 +10,7 @@
 //  * staged: the host copies the L rows into a pinned staging buffer and a
 //    single cudaMemcpyAsync moves them on the caller's (side) stream, so the
 //    transfer overlaps whatever runs on the compute stream.
+#include <cstdlib>
 #include <cstring>
 
 #include "svt_common.cuh"
@@ -78,8 +79,15 @@ extern "C" svt_status svt_embed_lookup_zero_copy(const void* h_table, svt_dtype 
     const int64_t row_bytes = static_cast<int64_t>(dim) * esize_of(dt);
     const bool vec = row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(dev_table) & 15u) == 0 &&
                      (reinterpret_cast<uintptr_t>(d_out) & 15u) == 0;
+    // The host link (~50 GB/s, ~2 us) needs only ~100 KB in flight: a few
+    // CTAs (each warp keeps 2 KB of 16-byte reads outstanding) saturate it
+    // and leave the other SMs to the decode stream this lookup overlaps.
+    static const int cap = [] {
+        const char* v = getenv("SVT_EMBED_GRID");
+        return v ? atoi(v) : 32;
+    }();
     const int64_t blocks = (static_cast<int64_t>(n) + 7) / 8;
-    const int grid = static_cast<int>(blocks < sm_count() * 4 ? blocks : sm_count() * 4);
+    const int grid = static_cast<int>(blocks < cap ? blocks : cap);
     embed_zero_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint8_t*>(dev_table), static_cast<int64_t>(rows), row_bytes, d_ids,
         static_cast<int64_t>(n), static_cast<uint8_t*>(d_out), d_bad, vec);
