@@ -425,6 +425,33 @@ svt_status svt_breakeven_rows(double link_bandwidth, double device_flops,
                               size_t prompt_len, double model_flops_per_token, size_t* out_rows);
 
 /* ------------------------------------------------------------------------
+ * (f1) Plan wire format — host only, no device needed.
+ * Replaces: artifacts::to_json(const SelectionPlan&) (artifacts.cpp:169-174)
+ * as the CLI writes it (one compact object per line, subvocab.cpp:413) or
+ * save_json writes it (dump(2), artifacts.cpp:249-254), and
+ * artifacts::plan_from_json (artifacts.cpp:175-192).
+ * Text is byte-identical to nlohmann::json's: keys sorted, indent < 0 =
+ * compact, indent >= 0 = pretty. Query-then-call: with out == NULL only
+ * *needed (bytes including the terminating NUL) is set.
+ * ---------------------------------------------------------------------- */
+svt_status svt_plan_to_json(const uint32_t* h_ids, size_t n, size_t n_static, size_t n_dynamic,
+                            size_t full_vocab_size, int32_t indent, char* out, size_t cap,
+                            size_t* needed);
+/* A batch of plans in capacity-CSR (host copies of svt_select_batched's
+ * output): one compact line per plan. */
+svt_status svt_plans_to_jsonl(const uint32_t* h_ids, const int64_t* h_offsets,
+                              const int64_t* h_n_active, const int64_t* h_n_static,
+                              const int64_t* h_n_dynamic, int32_t batch, size_t full_vocab_size,
+                              char* out, size_t cap, size_t* needed);
+/* Parse one plan object. SVT_ERR_PARSE for malformed JSON, a missing field
+ * ("<origin>: missing field \"n_static\"", require() order) or a wrong type;
+ * SVT_ERR_INTEGRITY for ids that are not strictly increasing or >=
+ * full_vocab_size. h_ids == NULL: sizes only (*n_ids). */
+svt_status svt_plan_from_json(const char* text, size_t len, const char* origin, uint32_t* h_ids,
+                              size_t cap, size_t* n_ids, size_t* n_static, size_t* n_dynamic,
+                              size_t* full_vocab_size);
+
+/* ------------------------------------------------------------------------
  * Session: device-resident tailored head for a micro-batch, driven with HOST
  * buffers (the reference-facing call an external runtime makes; used by the
  * C++ drop-in and by bench.py's e2e measurement). A session owns device

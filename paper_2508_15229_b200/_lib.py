@@ -117,6 +117,9 @@ _SIGS = {
     "svt_session_greedy_host": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
     "svt_session_greedy_device": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
     "svt_session_stream": ([_vp], _vp),
+    "svt_plan_to_json": ([_vp, _sz, _sz, _sz, _sz, _i32, _vp, _sz, _vp], C.c_int),
+    "svt_plans_to_jsonl": ([_vp, _vp, _vp, _vp, _vp, _i32, _sz, _vp, _sz, _vp], C.c_int),
+    "svt_plan_from_json": ([C.c_char_p, _sz, C.c_char_p, _vp, _sz, _vp, _vp, _vp, _vp], C.c_int),
     "svt_memory_report": ([_sz, _sz, C.c_int, _sz, _vp], C.c_int),
     "svt_simulate": ([C.c_double, C.c_double, C.c_double, _sz, _sz, C.c_int, _sz, C.c_double,
                       _vp], C.c_int),

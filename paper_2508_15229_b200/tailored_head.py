@@ -325,6 +325,35 @@ def greedy_step(subhead: HeadMatrix, hidden, plan: SelectionPlan) -> int:
     return int(out[0].item()) & 0xFFFFFFFF
 
 
+
+# --------------------------------------------------------------------------
+# (f1) plan wire format (artifacts.cpp:169-192)
+# --------------------------------------------------------------------------
+def plan_to_json(plan: SelectionPlan, indent: Optional[int] = None) -> str:
+    """artifacts::to_json(plan).dump(indent): nlohmann's text, byte for byte
+    (indent None = compact, the CLI's plans file line)."""
+    ids = np.ascontiguousarray(plan.active_ids, np.uint32)
+    need = C.c_size_t()
+    args = (ids.ctypes.data if ids.size else None, ids.size, plan.n_static, plan.n_dynamic,
+            plan.full_vocab_size, -1 if indent is None else int(indent))
+    call("svt_plan_to_json", *args, None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value)
+    call("svt_plan_to_json", *args, buf, need.value, None)
+    return buf.value.decode()
+
+
+def plan_from_json(text: str, origin: str = "<mem>") -> SelectionPlan:
+    """artifacts::plan_from_json: ParseError on malformed JSON / a missing
+    field, IntegrityError on unsorted or out-of-range ids."""
+    raw = text.encode()
+    n, ns, nd, full = C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+    call("svt_plan_from_json", raw, len(raw), origin.encode(), None, 0, C.byref(n), None, None,
+         None)
+    ids = np.zeros(max(1, n.value), np.uint32)
+    call("svt_plan_from_json", raw, len(raw), origin.encode(), ids.ctypes.data, ids.size,
+         C.byref(n), C.byref(ns), C.byref(nd), C.byref(full))
+    return SelectionPlan(ids[: n.value].copy(), ns.value, nd.value, full.value)
+
 class RowDecoder:
     """Batch-1 greedy decode over ONE plan (BASELINE cfg1): the plan's rows
     are gathered row-major once (gather, head.cpp:176-187) and every token is
@@ -555,6 +584,21 @@ class TailoredBatch:
 
     def plans(self):
         return [self.plan(b) for b in range(self.B)]
+
+    def plans_jsonl(self) -> str:
+        """The batch's device-selected plans as the CLI's plans file: one
+        compact JSON object per line (subvocab.cpp:413), one D2H copy."""
+        meta = self.meta.cpu().numpy()
+        ids = self.active.cpu().numpy().view(np.uint32)
+        off = np.ascontiguousarray(self.act_off_h[:-1] if self.B else np.zeros(1, np.int64))
+        na, ns, nd = (np.ascontiguousarray(meta[i]) for i in range(3))
+        need = C.c_size_t()
+        args = (ids.ctypes.data, off.ctypes.data, na.ctypes.data, ns.ctypes.data,
+                nd.ctypes.data, self.B, self.V)
+        call("svt_plans_to_jsonl", *args, None, 0, C.byref(need))
+        buf = C.create_string_buffer(need.value)
+        call("svt_plans_to_jsonl", *args, buf, need.value, None)
+        return buf.value.decode()
 
     # ---- (b) interleaved gather ------------------------------------------
     def gather(self, head: HeadMatrix):

@@ -13,6 +13,7 @@
 #include "subvocab/error.hpp"
 #include "subvocab/head.hpp"
 #include "subvocab/offload_sim.hpp"
+#include "subvocab/plan_json.hpp"
 #include "subvocab/selector.hpp"
 #include "subvocab/tailored_decoder.hpp"
 #include "subvocab/token_set.hpp"
@@ -117,6 +118,32 @@ TEST_CASE("selector: remap_out / global_to_local invert the gather") {
     CHECK_THROWS_AS(remap_out(plan, 4), IntegrityError);
     for (std::size_t k = 0; k < plan.size(); ++k) CHECK(plan.global_to_local(plan.active_ids[k]) == k);
     CHECK(!plan.global_to_local(1).has_value());
+}
+
+TEST_CASE("artifacts: plan JSON round-trips and validates (test_artifacts.cpp:44-62)") {
+    SelectionPlan plan = plan_of({0, 2, 3, 4}, 8);
+    plan.n_static = 2;
+    plan.n_dynamic = 2;
+    const std::string compact = artifacts::plan_to_json_text(plan);
+    CHECK(compact == "{\"active_ids\":[0,2,3,4],\"full_vocab_size\":8,\"n_dynamic\":2,\"n_static\":2}");
+    const SelectionPlan back = artifacts::plan_from_json_text(artifacts::plan_to_json_text(plan, 2), "<mem>");
+    CHECK(back.active_ids == plan.active_ids);
+    CHECK(back.n_static == 2 && back.n_dynamic == 2 && back.full_vocab_size == 8);
+    CHECK_THROWS_AS(artifacts::plan_from_json_text(
+                        "{\"active_ids\":[2,2],\"full_vocab_size\":8,\"n_dynamic\":2,\"n_static\":2}", "<mem>"),
+                    IntegrityError);
+    CHECK_THROWS_AS(artifacts::plan_from_json_text(
+                        "{\"active_ids\":[2,9],\"full_vocab_size\":8,\"n_dynamic\":2,\"n_static\":2}", "<mem>"),
+                    IntegrityError);
+    bool named = false;
+    try {
+        artifacts::plan_from_json_text("{\"active_ids\":[0],\"full_vocab_size\":8,\"n_dynamic\":2}",
+                                       "plan.json");
+    } catch (const ParseError& e) {
+        named = std::string(e.what()).find("plan.json") != std::string::npos;
+    }
+    CHECK(named);
+    CHECK(artifacts::plans_to_jsonl({plan, plan}) == compact + "\n" + compact + "\n");
 }
 
 TEST_CASE("selector: reporting convention strings") {

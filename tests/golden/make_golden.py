@@ -5,7 +5,8 @@ from /root/reference/proj/src by oracle/Makefile). Run here, where
     make -C oracle ref && python tests/golden/make_golden.py
 
 Each case records seeded inputs and the reference's outputs:
-select() plans, logits() bit patterns and greedy_step() ids.
+select() plans, logits() bit patterns and greedy_step() ids. The reference's
+golden plan file is copied verbatim as the wire-format fixture.
 """
 from __future__ import annotations
 
@@ -93,5 +94,15 @@ def main():
         print("wrote", name)
 
 
+def copy_plan_fixture():
+    """The reference's own golden plan file (fixtures/golden/plan_aca.json,
+    the output of its save_json: nlohmann dump(2) + newline) pins the plan
+    wire format (tests/test_plan_json.py)."""
+    src = "/root/reference/proj/tests/fixtures/golden/plan_aca.json"
+    with open(src, "rb") as f, open(os.path.join(OUT, "plan_aca.json"), "wb") as g:
+        g.write(f.read())
+
+
 if __name__ == "__main__":
     main()
+    copy_plan_fixture()
