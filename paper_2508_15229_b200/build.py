@@ -41,13 +41,28 @@ def _stale(target, sources):
 
 
 def build_svt(force=False):
+    """One object per translation unit, compiled in parallel (only the stale
+    ones), then one shared-library link."""
+    from concurrent.futures import ThreadPoolExecutor
+
     os.makedirs(LIB, exist_ok=True)
+    obj_dir = os.path.join(LIB, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
     out = os.path.join(LIB, "libsvt.so")
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "svt.h")]
-    if force or _stale(out, deps):
-        _run([NVCC, *NVFLAGS, *ARCH, "-shared", "-I", INCLUDE, "-I", CSRC, *srcs, "-o", out,
-              "-lcudart"])
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "svt.h")]
+    objs = [os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, [s] + headers)]
+
+    def compile_one(so):
+        src, obj = so
+        _run([NVCC, *NVFLAGS, *ARCH, "-c", "-I", INCLUDE, "-I", CSRC, src, "-o", obj])
+
+    if todo:
+        with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
+            list(ex.map(compile_one, todo))
+    if force or todo or _stale(out, objs):
+        _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-lcudart"])
     return out
 
 

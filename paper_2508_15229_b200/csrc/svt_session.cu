@@ -11,6 +11,7 @@
 // launch.
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "svt_gemv.cuh"
@@ -50,6 +51,13 @@ struct svt_session {
     float* h_hidden = nullptr;
     uint32_t* h_ids = nullptr;
     float* h_max = nullptr;
+    // per-step CUDA graph of the host-buffer call (H2D -> GEMV -> finalize ->
+    // D2H): one launch per step instead of four API calls; the memcpy nodes'
+    // host pointers are patched per call. Rebuilt after every prepare.
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaGraphNode_t node_h2d = nullptr, node_d2h = nullptr;
+    std::unordered_map<const void*, bool> pinned_cache;
 
     int64_t* n_active_d() { return d_meta; }
     int64_t* n_static_d() { return d_meta + cap_batch; }
@@ -92,6 +100,27 @@ bool is_pinned(const void* p) {
     }
     return a.type == cudaMemoryTypeHost;
 }
+
+// is_pinned with a per-session memo (callers reuse their staging buffers; a
+// pointer query per step costs more than the D2H of the ids)
+bool pinned_cached(svt_session* s, const void* p) {
+    auto it = s->pinned_cache.find(p);
+    if (it != s->pinned_cache.end()) return it->second;
+    if (s->pinned_cache.size() > 4096) s->pinned_cache.clear();
+    const bool v = is_pinned(p);
+    s->pinned_cache.emplace(p, v);
+    return v;
+}
+
+void drop_graph(svt_session* s) {
+    if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
+    if (s->graph) cudaGraphDestroy(s->graph);
+    s->graph_exec = nullptr;
+    s->graph = nullptr;
+    s->node_h2d = s->node_d2h = nullptr;
+    s->pinned_cache.clear();  // host buffers may have been freed and reused
+}
+
 
 svt_status ensure_batch(svt_session* s, size_t B) {
     if (B <= s->cap_batch && s->d_meta) return SVT_OK;
@@ -180,6 +209,7 @@ svt_status svt_session_create(svt_session** out, const void* d_head, svt_dtype d
 svt_status svt_session_destroy(svt_session* s) {
     if (!s) return SVT_OK;
     cudaStreamSynchronize(s->stream);
+    drop_graph(s);
     free_all(s);
     if (s->own_stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -200,6 +230,7 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
                   static_universe, s->rows);
         return SVT_ERR_INTEGRITY;
     }
+    drop_graph(s);  // plans, layouts and buffers may change
     if (batch < 0) {
         set_error("negative batch");
         return SVT_ERR_CONFIG;
@@ -342,6 +373,66 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
     const size_t B = static_cast<size_t>(s->batch);
     if (B == 0) return SVT_OK;
     cudaStream_t q = s->stream;
+    // (graph memcpy nodes can only be re-pointed when 1-D: contiguous rows)
+    if (!h_out_max && host_ld == s->dim && s->ld == s->dim && pinned_cached(s, h_hidden) &&
+        pinned_cached(s, h_out_ids)) {
+        // graph path: one launch + one synchronisation per step
+        for (int32_t b = 0; b < s->batch; ++b)
+            if (s->n_active[b] == 0) {
+                set_error("greedy step over an empty sub-head");
+                return SVT_ERR_INTEGRITY;
+            }
+        if (!s->graph_exec) {
+            SVT_CUDA_TRY(cudaStreamBeginCapture(q, cudaStreamCaptureModeThreadLocal));
+            const size_t hb = B * s->dim * sizeof(float);
+            cudaError_t e = cudaMemcpyAsync(s->d_hidden, h_hidden, hb, cudaMemcpyHostToDevice, q);
+            svt_status st = e == cudaSuccess ? svt_session_greedy_device(s, s->d_hidden, s->ld,
+                                                                        s->d_out_ids, nullptr)
+                                             : SVT_OK;
+            if (e == cudaSuccess && st == SVT_OK)
+                e = cudaMemcpyAsync(h_out_ids, s->d_out_ids, B * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, q);
+            cudaGraph_t g = nullptr;
+            const cudaError_t e2 = cudaStreamEndCapture(q, &g);
+            if (e != cudaSuccess || st != SVT_OK || e2 != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                if (st) return st;
+                return svt::cuda_status(e != cudaSuccess ? e : e2, "session step graph capture");
+            }
+            s->graph = g;
+            size_t n = 0;
+            SVT_CUDA_TRY(cudaGraphGetNodes(g, nullptr, &n));
+            std::vector<cudaGraphNode_t> nodes(n);
+            SVT_CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &n));
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType t;
+                SVT_CUDA_TRY(cudaGraphNodeGetType(nd, &t));
+                if (t != cudaGraphNodeTypeMemcpy) continue;
+                cudaMemcpy3DParms mp = {};
+                SVT_CUDA_TRY(cudaGraphMemcpyNodeGetParams(nd, &mp));
+                (mp.kind == cudaMemcpyDeviceToHost ? s->node_d2h : s->node_h2d) = nd;
+            }
+            if (!s->node_h2d || !s->node_d2h) {
+                drop_graph(s);
+                set_error("session step graph: memcpy nodes not found");
+                return SVT_ERR_RUNTIME;
+            }
+            SVT_CUDA_TRY(cudaGraphInstantiate(&s->graph_exec, g, 0));
+        } else {
+            SVT_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(s->graph_exec, s->node_h2d,
+                                                            s->d_hidden, h_hidden,
+                                                            B * s->dim * sizeof(float),
+                                                            cudaMemcpyHostToDevice));
+            SVT_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(s->graph_exec, s->node_d2h,
+                                                            h_out_ids, s->d_out_ids,
+                                                            B * sizeof(uint32_t),
+                                                            cudaMemcpyDeviceToHost));
+        }
+        SVT_CUDA_TRY(cudaGraphLaunch(s->graph_exec, q));
+        SVT_CUDA_TRY(cudaStreamSynchronize(q));
+        return SVT_OK;
+    }
     if (is_pinned(h_hidden)) {
         SVT_CUDA_TRY(cudaMemcpy2DAsync(s->d_hidden, s->ld * sizeof(float), h_hidden,
                                        host_ld * sizeof(float), s->dim * sizeof(float), B,

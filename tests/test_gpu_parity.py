@@ -776,3 +776,29 @@ def test_vocab_sharded_certified_batch1(th):
         for G in (1, 2, 3, 4):
             got = sharded.sharded_greedy_local(head, hc[None, :], G)
             assert int(got[0]) == int(want), (G, want, got)
+
+
+def test_session_step_graph_pinned_buffers(th):
+    """Pinned contiguous host buffers take the per-session step graph (H2D ->
+    GEMV -> finalize -> D2H, memcpy nodes re-pointed per call): ids equal the
+    batched engine across steps with different buffers, a pageable call in
+    between, and a re-prepare with another batch (the graph is rebuilt)."""
+    from paper_2508_15229_b200 import session
+
+    V, d = 151936, 896
+    for B, steps in ((8, 3), (5, 2)):
+        head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_BF16, B, 512, 2048,
+                                                        steps, seed_off=B)
+        hid_pinned = torch.from_numpy(hid).pin_memory()
+        outs = torch.empty((steps, B), dtype=torch.int32).pin_memory()
+        with session.Session(head, max_batch=8) as s:
+            off = np.zeros(B + 1, np.int64)
+            off[1:] = np.cumsum([len(p) for p in prompts])
+            for rep in range(2):  # prepare twice: graph dropped and rebuilt
+                s.prepare(words, V, np.concatenate(prompts), off)
+                for t in range(steps):
+                    s.greedy(hid_pinned[t], outs[t])
+                    o = torch.empty(B, dtype=torch.int32, device="cuda")
+                    tb.greedy(torch.from_numpy(hid[t]).cuda(), o)
+                    assert torch.equal(outs[t], o.cpu()), (B, rep, t)
+                    assert np.array_equal(s.greedy(hid[t]), o.cpu().numpy().view(np.uint32))
