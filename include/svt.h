@@ -452,6 +452,43 @@ svt_status svt_plan_from_json(const char* text, size_t len, const char* origin, 
                               size_t* full_vocab_size);
 
 /* ------------------------------------------------------------------------
+ * (f4) Tolerance filter of the static builder (static_builder.cpp:79-121),
+ * on the GPU: the non-protected candidates ordered by (df, id) lose the
+ * longest prefix whose df total stays within tau * doc_count. One CTA finds
+ * the cut by value (binary search on the df threshold, no sort) and writes
+ * kept = candidates \ pruned (ceil(universe/64) words) and the pruned ids
+ * ascending (capacity |candidates|); *d_n_pruned and *d_pruned_df_sum are
+ * device scalars. d_always_keep_words may be NULL; df beyond n_df counts 0.
+ * doc_count < 1 -> SVT_ERR_CONFIG (the reference's ConfigError).
+ * ---------------------------------------------------------------------- */
+svt_status svt_tolerance_filter(const uint64_t* d_candidate_words,
+                                const uint64_t* d_always_keep_words, size_t universe,
+                                const uint32_t* d_df, size_t n_df, int64_t doc_count, double tau,
+                                uint64_t* d_kept_words, uint32_t* d_pruned, int64_t* d_n_pruned,
+                                uint64_t* d_pruned_df_sum, svt_stream stream);
+/* (f3) Profiler::add (profiler.cpp:56-97) over a CSR batch of documents, one
+ * CTA per document with its distinct-input / distinct-output sets as shared-
+ * memory bitmaps. Accumulates into d_df (u32 [V]) and the two union bitmaps
+ * (ceil(V/64) words, OR); writes per document (submission order)
+ * distinct_input, overlap_occurrence, overlap_distinct (exact integer
+ * quotients, equal to the reference's doubles) and d_err_kind: 0 ok, 1 an
+ * input id >= V, 2 an output id >= V, 3 an empty output (d_err_id = the first
+ * offending id). Documents with an error contribute nothing. V <= ~880k (the
+ * two bitmaps must fit shared memory). */
+svt_status svt_profile_batch(size_t vocab_size, const uint32_t* d_input_ids,
+                             const int64_t* d_input_offsets, const uint32_t* d_output_ids,
+                             const int64_t* d_output_offsets, int64_t n_docs, uint32_t* d_df,
+                             uint64_t* d_input_union, uint64_t* d_output_union,
+                             uint32_t* d_distinct_input, double* d_overlap_occurrence,
+                             double* d_overlap_distinct, int32_t* d_err_kind, uint32_t* d_err_id,
+                             svt_stream stream);
+/* Profiler::merge (profiler.cpp:106-127), device part: df += df_b, unions |= b. */
+svt_status svt_profile_merge(size_t vocab_size, uint32_t* d_df, const uint32_t* d_df_b,
+                             uint64_t* d_input_union, const uint64_t* d_input_union_b,
+                             uint64_t* d_output_union, const uint64_t* d_output_union_b,
+                             svt_stream stream);
+
+/* ------------------------------------------------------------------------
  * Session: device-resident tailored head for a micro-batch, driven with HOST
  * buffers (the reference-facing call an external runtime makes; used by the
  * C++ drop-in and by bench.py's e2e measurement). A session owns device

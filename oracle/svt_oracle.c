@@ -387,3 +387,113 @@ void orc_prompt_ids(uint64_t seed, size_t V, size_t L, uint32_t* out) {
     uint64_t state = seed;
     for (size_t i = 0; i < L; ++i) out[i] = (uint32_t)(orc_splitmix_next(&state) % V);
 }
+
+/* ---- (f4) tolerance_filter, static_builder.cpp:79-121 ---------------------- */
+static int u32_cmp(const void* a, const void* b) {
+    const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return x < y ? -1 : (x > y);
+}
+static const uint32_t* g_tol_df;
+static size_t g_tol_ndf;
+static uint64_t tol_df_of(uint32_t id) { return id < g_tol_ndf ? g_tol_df[id] : 0; }
+static int tol_cmp(const void* a, const void* b) {
+    const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    const uint64_t dx = tol_df_of(x), dy = tol_df_of(y);
+    if (dx != dy) return dx < dy ? -1 : 1;
+    return x < y ? -1 : (x > y);
+}
+
+int orc_tolerance_filter(const uint64_t* cand_words, const uint64_t* keep_words, size_t universe,
+                         const uint32_t* df, size_t n_df, int64_t doc_count, double tau,
+                         uint64_t* kept_words, uint32_t* pruned, size_t* n_pruned,
+                         uint64_t* df_sum) {
+    if (doc_count < 1) return ORC_CONFIG;
+    const size_t nw = n_words(universe);
+    size_t np_ = 0;
+    uint32_t* prunable = (uint32_t*)malloc((universe ? universe : 1) * sizeof(uint32_t));
+    for (size_t w = 0; w < nw; ++w) {
+        kept_words[w] = 0;
+        for (int b = 0; b < 64; ++b) {
+            if (!((cand_words[w] >> b) & 1)) continue;
+            const uint32_t id = (uint32_t)(w * 64 + (size_t)b);
+            if (keep_words && ((keep_words[w] >> b) & 1))
+                kept_words[w] |= 1ULL << b; /* protected, never pruned */
+            else
+                prunable[np_++] = id;
+        }
+    }
+    g_tol_df = df;
+    g_tol_ndf = n_df;
+    qsort(prunable, np_, sizeof(uint32_t), tol_cmp);
+    const double budget = tau * (double)doc_count;
+    uint64_t cumulative = 0;
+    size_t cut = 0;
+    while (cut < np_) {
+        const uint64_t next = cumulative + tol_df_of(prunable[cut]);
+        if ((double)next > budget) break;
+        cumulative = next;
+        ++cut;
+    }
+    for (size_t i = cut; i < np_; ++i) kept_words[prunable[i] / 64] |= 1ULL << (prunable[i] % 64);
+    /* the pruned prefix, ascending by id */
+    size_t k = 0;
+    for (size_t i = 0; i < cut; ++i) pruned[k++] = prunable[i];
+    qsort(pruned, k, sizeof(uint32_t), u32_cmp);
+    *n_pruned = k;
+    *df_sum = cumulative;
+    free(prunable);
+    return ORC_OK;
+}
+
+/* ---- (f3) Profiler::add, profiler.cpp:56-97 -------------------------------- */
+int orc_profile_doc(size_t V, const uint32_t* in, size_t n_in, const uint32_t* out, size_t n_out,
+                    uint32_t* df, uint64_t* in_union, uint64_t* out_union,
+                    uint32_t* distinct_input, double* overlap_occ, double* overlap_dist,
+                    uint32_t* bad_id, int* bad_side) {
+    for (size_t i = 0; i < n_in; ++i)
+        if (in[i] >= V) {
+            *bad_id = in[i];
+            *bad_side = 0;
+            return ORC_INTEGRITY;
+        }
+    for (size_t i = 0; i < n_out; ++i)
+        if (out[i] >= V) {
+            *bad_id = out[i];
+            *bad_side = 1;
+            return ORC_INTEGRITY;
+        }
+    if (n_out == 0) return ORC_PARSE;
+    const size_t nw = n_words(V);
+    uint64_t* inset = (uint64_t*)calloc(nw ? nw : 1, sizeof(uint64_t));
+    uint64_t* outset = (uint64_t*)calloc(nw ? nw : 1, sizeof(uint64_t));
+    uint32_t distinct = 0;
+    for (size_t i = 0; i < n_in; ++i) {
+        const uint32_t id = in[i];
+        const uint64_t bit = 1ULL << (id % 64);
+        if (!(inset[id / 64] & bit)) {
+            inset[id / 64] |= bit;
+            in_union[id / 64] |= bit;
+            ++distinct;
+        }
+    }
+    uint64_t copied = 0, seen = 0, distinct_copied = 0;
+    for (size_t i = 0; i < n_out; ++i) {
+        const uint32_t id = out[i];
+        const uint64_t bit = 1ULL << (id % 64);
+        const int in_input = (inset[id / 64] & bit) != 0;
+        if (in_input) ++copied;
+        if (!(outset[id / 64] & bit)) {
+            outset[id / 64] |= bit;
+            ++seen;
+            ++df[id];
+            out_union[id / 64] |= bit;
+            if (in_input) ++distinct_copied;
+        }
+    }
+    *distinct_input = distinct;
+    *overlap_occ = (double)copied / (double)n_out;
+    *overlap_dist = (double)distinct_copied / (double)seen;
+    free(inset);
+    free(outset);
+    return ORC_OK;
+}

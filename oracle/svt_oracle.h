@@ -105,6 +105,24 @@ int orc_breakeven_rows(double link_bw, double device_flops, double lookup_latenc
                        size_t* rows);
 
 /* ---- synthetic workload streams ------------------------------ */
+/* ---- (f4) tolerance_filter (static_builder.cpp:79-121) ---------------------
+ * prunable = candidates \ always_keep (keep may be NULL), sorted by (df, id);
+ * prune the prefix while double(cumulative + df) <= tau * doc_count.
+ * kept_words: ceil(universe/64) words; pruned: ascending ids. */
+int orc_tolerance_filter(const uint64_t* cand_words, const uint64_t* keep_words, size_t universe,
+                         const uint32_t* df, size_t n_df, int64_t doc_count, double tau,
+                         uint64_t* kept_words, uint32_t* pruned, size_t* n_pruned,
+                         uint64_t* df_sum);
+
+/* ---- (f3) Profiler::add for one document (profiler.cpp:56-97) --------------
+ * Accumulates df / input_union / output_union; returns 0 (stats written),
+ * 4 IntegrityError (*bad_id = first input id >= V, *bad_side = 0; or the
+ * first output id, *bad_side = 1) or 3 ParseError (empty output). */
+int orc_profile_doc(size_t V, const uint32_t* in, size_t n_in, const uint32_t* out, size_t n_out,
+                    uint32_t* df, uint64_t* in_union, uint64_t* out_union,
+                    uint32_t* distinct_input, double* overlap_occ, double* overlap_dist,
+                    uint32_t* bad_id, int* bad_side);
+
 uint64_t orc_splitmix_next(uint64_t* state);
 /* n distinct ids drawn from splitmix64(seed) mod V, in draw order. */
 void orc_static_ids(uint64_t seed, size_t V, size_t n, uint32_t* out);

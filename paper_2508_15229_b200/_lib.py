@@ -120,6 +120,11 @@ _SIGS = {
     "svt_plan_to_json": ([_vp, _sz, _sz, _sz, _sz, _i32, _vp, _sz, _vp], C.c_int),
     "svt_plans_to_jsonl": ([_vp, _vp, _vp, _vp, _vp, _i32, _sz, _vp, _sz, _vp], C.c_int),
     "svt_plan_from_json": ([C.c_char_p, _sz, C.c_char_p, _vp, _sz, _vp, _vp, _vp, _vp], C.c_int),
+    "svt_tolerance_filter": ([_vp, _vp, _sz, _vp, _sz, _i64, C.c_double, _vp, _vp, _vp, _vp,
+                              _vp], C.c_int),
+    "svt_profile_batch": ([_sz, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                           _vp], C.c_int),
+    "svt_profile_merge": ([_sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_memory_report": ([_sz, _sz, C.c_int, _sz, _vp], C.c_int),
     "svt_simulate": ([C.c_double, C.c_double, C.c_double, _sz, _sz, C.c_int, _sz, C.c_double,
                       _vp], C.c_int),
