@@ -55,14 +55,15 @@ def parse():
     ap.add_argument("--sweep-batches", default="1,32,256")
     ap.add_argument("--sweep-dtypes", default="bf16,f32")
     ap.add_argument("--workload", default="cfg2",
-                    choices=["cfg2", "cfg3", "cfg4", "cfg5", "embed"],
+                    choices=["cfg2", "cfg3", "cfg4", "cfg5", "embed", "corpus"],
                     help="cfg2: batch-shard tailored decode (headline); cfg3: batched "
                          "prefill-scoring on tcgen05 (Llama-3.2-3B shape, 256 seqs x 2048 "
                          "positions per GPU); cfg4: vocab-sharded full-vocab greedy "
                          "(Gemma-2-2B shape) with an NCCL record all-gather; cfg5: subset-size "
                          "sweep |S| 1k..128k x batch 1/32/256, tailored vs full-vocab; embed: "
                          "offloaded embedding lookup from pinned host memory (zero-copy vs "
-                         "staged) with overlap against the decode stream")
+                         "staged) with overlap against the decode stream; corpus: the static "
+                         "builder's profiler + tolerance filter (SURVEY 8f f3/f4)")
     return ap.parse_args()
 
 
@@ -517,6 +518,8 @@ def main():
         return run_sweep(args, torch, rank)
     if args.workload == "embed":
         return run_embed(args, torch, rank)
+    if args.workload == "corpus":
+        return run_corpus(args, torch, rank)
     from paper_2508_15229_b200 import session as session_mod
     from paper_2508_15229_b200 import synth
     from paper_2508_15229_b200 import tailored_head as th
@@ -1258,6 +1261,138 @@ def run_embed(args, torch, rank):
                            "peak_source": "pinned H2D cudaMemcpy of 256 MB, measured in this run",
                            "kernel": "embed_zero_copy_kernel"},
               "results": res}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def run_corpus(args, torch, rank):
+    """f3/f4: profile a synthetic task corpus on the GPU
+    (Qwen2.5 vocabulary V=151936; 65,536 documents of 512 input + 128 output
+    tokens, Zipf-distributed ids so documents share tokens), then the
+    tolerance filter over the corpus's output union. Timed with CUDA events
+    on device-resident document CSR arrays; the reference's profile() and
+    tolerance_filter() (oracle/_ref, 1 host thread, the reference has no
+    threading) are timed on a bounded sample beside it."""
+    import ctypes as C
+    from paper_2508_15229_b200 import corpus
+    from paper_2508_15229_b200 import tailored_head as th
+
+    V, n_docs, Li, Lo = 151936, 65536, 512, 128
+    rng = np.random.default_rng(0xC0)
+    zipf = lambda n: (rng.zipf(1.2, n) - 1) % V  # noqa: E731
+    ins = zipf(n_docs * Li).astype(np.uint32)
+    outs = zipf(n_docs * Lo).astype(np.uint32)
+    ioff = np.arange(n_docs + 1, dtype=np.int64) * Li
+    ooff = np.arange(n_docs + 1, dtype=np.int64) * Lo
+    d_in = torch.from_numpy(ins.view(np.int32)).cuda()
+    d_out = torch.from_numpy(outs.view(np.int32)).cuda()
+    d_io, d_oo = torch.from_numpy(ioff).cuda(), torch.from_numpy(ooff).cuda()
+    nw = (V + 63) // 64
+    df = torch.zeros(V, dtype=torch.int32, device="cuda")
+    iu = torch.zeros(nw, dtype=torch.int64, device="cuda")
+    ou = torch.zeros(nw, dtype=torch.int64, device="cuda")
+    di = torch.empty(n_docs, dtype=torch.int32, device="cuda")
+    oc = torch.empty(n_docs, dtype=torch.float64, device="cuda")
+    od = torch.empty(n_docs, dtype=torch.float64, device="cuda")
+    ek = torch.empty(n_docs, dtype=torch.int32, device="cuda")
+    ei = torch.empty(n_docs, dtype=torch.int32, device="cuda")
+
+    def prof():
+        df.zero_()
+        iu.zero_()
+        ou.zero_()
+        th._lib.call("svt_profile_batch", V, d_in.data_ptr(), d_io.data_ptr(), d_out.data_ptr(),
+                     d_oo.data_ptr(), n_docs, df.data_ptr(), iu.data_ptr(), ou.data_ptr(),
+                     di.data_ptr(), oc.data_ptr(), od.data_ptr(), ek.data_ptr(), ei.data_ptr(),
+                     None)
+    for _ in range(3):
+        prof()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = max(3, args.steps // 4)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        a.record()
+        for _ in range(K):
+            prof()
+        b.record()
+        torch.cuda.synchronize()
+    prof_ms = a.elapsed_time(b) / K
+    tokens = n_docs * (Li + Lo)
+    # tolerance filter over the output union with the corpus df
+    cand = th.TokenSet(V)
+    cand.words[:] = ou.cpu().numpy().view(np.uint64)
+    dfh = df.cpu().numpy().view(np.uint32).copy()
+    d_cand = torch.from_numpy(cand.words.view(np.int64)).cuda()
+    d_df = torch.from_numpy(dfh.view(np.int32)).cuda()
+    kept = torch.empty(nw, dtype=torch.int64, device="cuda")
+    pruned = torch.empty(V, dtype=torch.int32, device="cuda")
+    scal = torch.zeros(2, dtype=torch.int64, device="cuda")
+
+    def tolf():
+        th._lib.call("svt_tolerance_filter", d_cand.data_ptr(), None, V, d_df.data_ptr(), V,
+                     n_docs, 0.01, kept.data_ptr(), pruned.data_ptr(), scal.data_ptr(),
+                     scal.data_ptr() + 8, None)
+    for _ in range(3):
+        tolf()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(K):
+        tolf()
+    b.record()
+    torch.cuda.synchronize()
+    tol_ms = a.elapsed_time(b) / K
+    # the reference on a bounded sample (1 thread)
+    ref = {}
+    rp = os.path.join(ROOT, "oracle", "_ref", "libsubvocab_ref_static.so")
+    if os.path.exists(rp):
+        R = C.CDLL(rp)
+        R.refs_profile.argtypes = [C.c_size_t] + [C.c_void_p] * 5 + [C.c_size_t] + [
+            C.c_void_p] * 3 + [C.POINTER(C.c_int64)] + [C.c_void_p] * 4
+        R.refs_tolerance_filter.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                            C.c_size_t, C.c_int64, C.c_double, C.c_void_p,
+                                            C.c_void_p, C.POINTER(C.c_size_t),
+                                            C.POINTER(C.c_uint64)]
+        ns = 4096
+        idx = np.arange(ns, dtype=np.int64)
+        sdf = np.zeros(V, np.uint32)
+        z1, z2 = np.zeros(nw, np.uint64), np.zeros(nw, np.uint64)
+        keep = [np.zeros(ns, np.int64), np.zeros(ns, np.uint32), np.zeros(ns), np.zeros(ns)]
+        cnt = C.c_int64()
+        t0 = time.perf_counter()
+        R.refs_profile(V, ins.ctypes.data, ioff.ctypes.data, outs.ctypes.data, ooff.ctypes.data,
+                       idx.ctypes.data, ns, sdf.ctypes.data, z1.ctypes.data, z2.ctypes.data,
+                       C.byref(cnt), *(k.ctypes.data for k in keep))
+        ref_prof_s = time.perf_counter() - t0
+        kw = np.zeros(nw, np.uint64)
+        pr = np.zeros(V, np.uint32)
+        n, sm = C.c_size_t(), C.c_uint64()
+        t0 = time.perf_counter()
+        R.refs_tolerance_filter(cand.words.ctypes.data, None, V, dfh.ctypes.data, V, n_docs,
+                                0.01, kw.ctypes.data, pr.ctypes.data, C.byref(n), C.byref(sm))
+        ref_tol_s = time.perf_counter() - t0
+        same = (n.value == int(scal[0].item()) and sm.value == int(scal[1].item())
+                and np.array_equal(pr[: n.value], pruned[: n.value].cpu().numpy().view(np.uint32)))
+        ref = {"profile_tokens_per_s": ns * (Li + Lo) / ref_prof_s,
+               "profile_sample": f"{ns} documents", "tolerance_ms": ref_tol_s * 1e3,
+               "tolerance_result_identical": bool(same), "cores": 1, "kind": "reference"}
+    peak, peak_kind = load_peaks()
+    id_bytes = tokens * 4
+    result = {"metric": "corpus profiler tokens/s (SURVEY 8f f3) + tolerance filter latency (f4)",
+              "value": tokens / (prof_ms / 1e3), "unit": "tokens/s", "n_gpus": 1, "steps": K,
+              "warmup": 3, "ms_per_step": prof_ms, "higher_is_better": True, "scaling": "none",
+              "vs_baseline": None, "dtype": "u32",
+              "data": "synthetic Zipf(1.2) token ids (seeded)",
+              "config": {"workload": "f3/f4: profile 65,536 documents x (512 in + 128 out) over "
+                                     "V=151936, then tolerance_filter(tau=0.01) of the output "
+                                     "union", "V": V, "documents": n_docs},
+              "roofline": {"bound": "latency (shared-memory atomics per token)",
+                           "achieved": id_bytes / (prof_ms / 1e3) / 1e9, "peak": peak,
+                           "unit": "GB/s", "frac": id_bytes / (prof_ms / 1e3) / 1e9 / peak,
+                           "note": "id bytes streamed / time; the per-document bitmap clear "
+                                   "(38 KB of shared memory) and atomics dominate"},
+              "tolerance_filter_ms": tol_ms,
+              "pruned": int(scal[0].item()), "pruned_df_sum": int(scal[1].item()),
+              "clocks": clk.summary(), "cpu_baseline": ref}
     if rank == 0:
         print(json.dumps(result), flush=True)
 

@@ -154,10 +154,12 @@ def test_oracle_profiler_matches_reference():
             mut(docs[2])
         st, info = orc_profile(50, docs)
         ii, io, oi, oo, idx = csr(docs)
-        z = np.zeros(64, np.uint64)
-        rst = REF.refs_profile(50, _p(ii), _p(io), _p(oi), _p(oo), _p(idx), 4, _p(np.zeros(50, np.uint32)),
-                               _p(z), _p(z.copy()), C.byref(C.c_int64()), _p(np.zeros(4, np.int64)),
-                               _p(np.zeros(4, np.uint32)), _p(np.zeros(4)), _p(np.zeros(4)))
+        bufs = [np.zeros(50, np.uint32), np.zeros(64, np.uint64), np.zeros(64, np.uint64),
+                np.zeros(4, np.int64), np.zeros(4, np.uint32), np.zeros(4), np.zeros(4)]
+        cnt = C.c_int64()
+        rst = REF.refs_profile(50, _p(ii), _p(io), _p(oi), _p(oo), _p(idx), 4, _p(bufs[0]),
+                               _p(bufs[1]), _p(bufs[2]), C.byref(cnt), _p(bufs[3]), _p(bufs[4]),
+                               _p(bufs[5]), _p(bufs[6]))
         assert st == rst == code
         msg = REF.refs_last_error().decode()
         assert f"document {docs[2][2]}" in msg and word in msg
