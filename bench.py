@@ -669,6 +669,15 @@ def run_vocab_shard(args, torch, dist, world, rank):
         dist.destroy_process_group()
 
 
+def prefill_fused():
+    """cfg3 scorer flavour: sub-heads gathered beforehand (default: the tiled
+    TMA loads run the GEMM at the tensor peak) or, with SVT_PREFILL_FUSED=1,
+    plan rows gathered inside the GEMM by TMA tile::gather4 (no 6.4 GB
+    sub-head buffer, but 32 four-row copies per 16 KB stage limit the GEMM to
+    ~28% of peak)."""
+    return os.environ.get("SVT_PREFILL_FUSED", "0") != "0"
+
+
 def prefill_setup(S, rank, torch, th, synth):
     """cfg3 inputs on the device: bf16 head, static bitmap, S prompts of 2048
     ids, S x 2048 bf16 hidden states; plans selected on the device and the
@@ -684,7 +693,7 @@ def prefill_setup(S, rank, torch, th, synth):
     flat = np.concatenate(prompts)
     tb = th.TailoredBatch.build(torch.from_numpy(words_h.view(np.int64)).cuda(), CFG3["static"],
                                 V, torch.from_numpy(flat.view(np.int32)).cuda(), off)
-    sc = prefill.PrefillScorer.from_batch(head, tb, P)
+    sc = prefill.PrefillScorer.from_batch(head, tb, P, fused=prefill_fused())
     hid = torch.empty(S * P * d, dtype=torch.bfloat16, device="cuda")
     th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_BF16, th.SVT_BF16,
                  rank * S * P * d, S * P * d, synth.SEED_H, None)
@@ -769,14 +778,18 @@ def run_prefill(args, torch, dist, world, rank):
         "config": {"workload": CFG3["workload"], "V": CFG3["V"], "d": d,
                    "sequences_per_gpu": S, "positions": P, "static_vocab": CFG3["static"],
                    "prompt_len": CFG3["prompt_len"], "mean_plan_rows": float(n_rows.mean()),
-                   "step": "select + layout + row-major gather + tcgen05 scoring with certified "
-                           "reference-exact ids; tokens = scored positions",
+                   "step": ("select + layout + tcgen05 scoring with the plan rows gathered "
+                            "by TMA tile::gather4 inside the GEMM" if prefill_fused() else
+                            "select + layout + row-major gather + tcgen05 scoring") +
+                           " with certified reference-exact ids; tokens = scored positions",
                    "parallelism": f"batch-shard x{world}",
-                   "l2": "hidden states 3.2 GB + sub-heads 6.4 GB per step > L2, no flush"},
+                   "l2": "hidden states 3.2 GB (+ 6.4 GB sub-heads when not fused) per step "
+                         "> L2, no flush"},
         "roofline": {"bound": "tensor", "achieved": flops / (gemm_ms / 1e3) / 1e12,
                      "peak": tf_peak, "unit": "TFLOP/s",
                      "frac": flops / (gemm_ms / 1e3) / 1e12 / tf_peak, "traffic": None,
-                     "kernel": "prefill_gemm_kernel<2> (cta_group::2, M=256 N=256 K=16)",
+                     "kernel": "prefill_gemm_kernel<2> (cta_group::2, M=256 N=256 K=16%s)" % (
+                         ", B via tile::gather4" if prefill_fused() else ""),
                      "flops_per_launch": flops, "avg_launch_us": gemm_ms * 1e3,
                      "peak_source": f"MEASURED_PEAKS.json bf16 dense ({tf_kind})",
                      "step_breakdown_ms": {"select_layout": sel, "gather": gat, "score": sco},
@@ -785,7 +798,7 @@ def run_prefill(args, torch, dist, world, rank):
         "certification": {"certified_directly": stats[0], "recomputed": stats[1],
                           "all_rows": stats[2], "non_finite": stats[3],
                           "candidate_pairs": stats[4]},
-        "gpu_launches": 11 * args.steps, "clocks": clk.summary(),
+        "gpu_launches": (10 if prefill_fused() else 11) * args.steps, "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_e2e:
         result["e2e"] = prefill_e2e(st, S, torch, th, L)

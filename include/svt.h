@@ -160,13 +160,13 @@ svt_status svt_gather_rows(const void* d_head, svt_dtype dt, size_t rows, size_t
 /* Row-major sub-heads of a batch of plans in capacity-CSR layout (as
  * svt_select_batched writes them): out row k = W[active[k]] for every live
  * slot k in [act_off[b], act_off[b] + n_active[b]); capacity slack is left
- * untouched. Device arrays; act_off has batch+1 entries. The batched form of
+ * untouched. act_off / n_active may point into a larger batch (a window of
+ * `batch` requests): slots [act_off[0], act_off[0] + total_capacity). Device arrays; act_off has batch+1 entries. The batched form of
  * gather (head.cpp:176-187) feeding svt_prefill_score. */
 svt_status svt_gather_plans(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
                             const uint32_t* d_active_ids, const int64_t* d_act_off,
                             const int64_t* d_n_active, int32_t batch, int64_t total_capacity,
                             void* d_out, int32_t* d_bad, svt_stream stream);
-
 /* Gather into the lane-interleaved sub-head layout consumed by the decode
  * kernel: for group g, 16-byte chunk c, lane l (plan row row0(g)+l):
  *   d_sub + ((g * nchunks + c) * 32 + l) * 16,  nchunks = ceil(dim*esize/16),
@@ -343,6 +343,17 @@ svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads, int64
                              const float* d_head_row_norms, int32_t sequences, int32_t positions,
                              int32_t dim, uint32_t* d_out_ids, float* d_out_max,
                              void* d_workspace, svt_stream stream);
+/* The same with the gather fused into the GEMM: B tiles are loaded straight
+ * from the full row-major bf16 head (head_rows x dim) through the plan ids
+ * with TMA tile::gather4 (4 head rows per copy), so no sub-head is
+ * materialised; sequence s's plan is d_plan_ids[d_id_offsets[s] ..
+ * + d_n_rows[s]). Same results and workspace as svt_prefill_score. */
+svt_status svt_prefill_score_fused(const void* d_hidden, const void* d_head, int64_t head_rows,
+                                   const int64_t* d_n_rows, const uint32_t* d_plan_ids,
+                                   const int64_t* d_id_offsets, const float* d_head_row_norms,
+                                   int32_t sequences, int32_t positions, int32_t dim,
+                                   uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
+                                   svt_stream stream);
 /* Tuning (process-wide): pair 0 forces the single-CTA (cta_group::1) GEMM
  * (default 1: CTA-pair cta_group::2 whenever positions % 256 == 0); nsplit
  * in [1, 128] = N-range splits per M tile (default 0 = automatic), one partial top-8

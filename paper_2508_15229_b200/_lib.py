@@ -102,6 +102,8 @@ _SIGS = {
     "svt_prefill_workspace_bytes": ([_i32, _i32], _sz),
     "svt_prefill_score": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
                            _vp, _vp], C.c_int),
+    "svt_prefill_score_fused": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
+                                 _vp, _vp], C.c_int),
     "svt_row_norms_bf16": ([_vp, _i64, _i32, _vp, _vp], C.c_int),
     "svt_prefill_set_tuning": ([_i32, _i32], C.c_int),
     "svt_prefill_get_tuning": ([_vp, _vp], None),

@@ -78,8 +78,10 @@ __global__ void gather_plans_kernel(const uint8_t* __restrict__ head, int64_t ro
                                     bool vec) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (int64_t k = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-         k < total; k += nwarps) {
+    // act_off may be a window of a larger batch: slots [act_off[0], act_off[0] + total)
+    const int64_t base = act_off[0];
+    for (int64_t k = base + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         k < base + total; k += nwarps) {
         int lo = 0, hi = batch;  // request b with act_off[b] <= k < act_off[b+1]
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;

@@ -76,6 +76,9 @@ struct PrefillParams {
     unsigned long long* dbg;
     const int64_t* n_rows;     // [S] |S_s|
     const int64_t* row_off;    // [S] first row of W_s in the concatenated sub-heads
+                               // (fused: first plan id of sequence s in plan_ids)
+    const uint32_t* plan_ids;  // fused gather: B rows are head rows plan_ids[row_off[s] + r]
+                               // loaded by TMA tile::gather4 (nullptr: gathered sub-heads)
     float* top_val;            // [S*P][nsplit][TOPK] partial top-8 per N range
     uint32_t* top_row;         // [S*P][nsplit][TOPK]
     uint8_t* flags;            // [S*P][nsplit] bit0: non-finite logit seen
@@ -119,6 +122,23 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
             : "memory");
     }
 }
+// four head rows (columns [x, x+64)) into 512 contiguous bytes of shared
+// memory; the 128-byte swizzle follows the destination address, so 2 x 4
+// rows fill one 8-row atom exactly as a tiled 8-row box would
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, int x,
+                                            uint4 rows, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(rows.x), "r"(rows.y), "r"(rows.z),
+        "r"(rows.w), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+
 template <int NCTA>
 __device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t cols) {
     if constexpr (NCTA == 1) {
@@ -265,9 +285,17 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
     const int ntiles = t1 > t0 ? t1 - t0 : 0;
     const int kiters = p.dim / BK;
 
+    const bool fused = p.plan_ids != nullptr;
+    // fused pair: the leader's full barrier also waits for the peer's
+    // forwarder (the peer's gathered B rows complete on the peer's barrier)
+    const uint32_t full_count = (fused && NCTA == 2 && rank == 0) ? 2u : 1u;
+    // plan ids of this CTA's B rows (fused): double-buffered for the pair;
+    // the single-CTA ring leaves room for one buffer only
+    constexpr int kIdBufs = NCTA == 2 ? 2 : 1;
+    __shared__ __align__(16) uint32_t s_ids[kIdBufs][BN / NCTA];
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < G::kStages; ++i) {
-            mbar_init(&full[i], 1);
+            mbar_init(&full[i], full_count);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -282,7 +310,76 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == 0 && fused) {
+        // ---- TMA producer, fused gather: B rows come straight from the head
+        // through the plan ids (tile::gather4); the whole warp prefetches the
+        // next N tile's ids with cp.async while lane 0 issues this tile's copies
+        constexpr int kRows = BN / NCTA;
+        const int64_t base = p.row_off[s];
+        auto fetch_ids = [&](int nt, int buf) {
+            const int64_t r0 = static_cast<int64_t>(t0 + nt) * BN + static_cast<int64_t>(rank) * kRows;
+            for (int i = lane; i < kRows; i += 32) {
+                int64_t r = r0 + i;
+                r = r < nrows ? r : nrows - 1;  // past the plan: any valid row (masked later)
+                cp_async4(&s_ids[buf][i], p.plan_ids + base + r);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (ntiles > 0) fetch_ids(0, 0);
+        const int ya = s * p.P + m0;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int nt = 0; nt < ntiles; ++nt) {
+            if (kIdBufs == 1 && nt > 0) fetch_ids(nt, 0);  // previous tile fully issued
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            if (kIdBufs == 2 && nt + 1 < ntiles) fetch_ids(nt + 1, (nt + 1) & 1);
+            const uint4* ids4 = reinterpret_cast<const uint4*>(s_ids[nt % kIdBufs]);
+            if (lane == 0) {
+                for (int kt = 0; kt < kiters; ++kt) {
+                    mbar_wait_parity(&empty[stage], phase ^ 1u);
+                    uint8_t* sa = ring + stage * G::kStage;
+                    uint8_t* sb = sa + kTileA;
+                    if constexpr (NCTA == 2) {
+                        // A: both CTAs' 128-position halves complete on the leader's
+                        // barrier; B: each CTA's gathered rows on its own barrier
+                        if (rank == 0)
+                            mbar_arrive_expect_tx(&full[stage], 2 * kTileA + G::kTileB);
+                        else
+                            mbar_arrive_expect_tx(&full[stage], G::kTileB);
+                        tma_load_2d<2>(sa, &tmH, kt * BK, ya, map_to_rank(&full[stage], 0));
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], G::kStage);
+                        tma_load_2d<1>(sa, &tmH, kt * BK, ya, smem_u32(&full[stage]));
+                    }
+                    const uint32_t bar = smem_u32(&full[stage]);
+#pragma unroll 8
+                    for (int g = 0; g < kRows / 4; ++g)
+                        tma_gather4(sb + g * 512, &tmW, kt * BK, ids4[g], bar);
+                    if (++stage == G::kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1 && fused && NCTA == 2 && rank == 1) {
+        // ---- peer forwarder: its gathered B rows have landed -> arrive on the
+        // leader's full barrier (the leader's MMA reads both CTAs' B halves)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int it = 0; it < ntiles * kiters; ++it) {
+                mbar_wait_parity(&full[stage], phase);
+                mbar_arrive_cluster(map_to_rank(&full[stage], 0));
+                if (++stage == G::kStages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 0) {
         // ---- TMA producer (each CTA loads its own A rows and half of B) ----
         if (lane == 0) {
             const int ya = s * p.P + m0;
@@ -673,6 +770,7 @@ __device__ __forceinline__ void cp_async_wait() {
 __global__ void __launch_bounds__(kPairWarps * 32, 1)
 recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, int P,
                        int dim, const int64_t* __restrict__ row_off,
+                       const uint32_t* __restrict__ row_ids,
                        const unsigned int* __restrict__ stats, const uint2* __restrict__ pairs,
                        unsigned long long* __restrict__ pos_keys) {
     extern __shared__ __align__(16) uint8_t psmem[];
@@ -701,7 +799,9 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restric
             const int64_t i = (first + k * nw) * 32 + lane;
             iss_act = i < count;
             const uint2 pr = iss_act ? pairs[i] : make_uint2(0u, 0u);
-            iss_w = W + (row_off[iss_act ? pr.x / P : 0] + pr.y) * static_cast<int64_t>(dim);
+            const int64_t rr = row_off[iss_act ? pr.x / P : 0] + pr.y;
+            iss_w = W + (row_ids ? static_cast<int64_t>(row_ids[iss_act ? rr : 0]) : rr) *
+                            static_cast<int64_t>(dim);
             iss_h = H + static_cast<int64_t>(pr.x) * dim;
         }
         uint8_t* slot = ring + static_cast<int>(u % kRing) * 64 * kSegStride;
@@ -779,6 +879,7 @@ __global__ void rec_finalize_kernel(int P, const int64_t* __restrict__ id_off,
 __global__ void __launch_bounds__(256)
 all_rows_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, int P, int dim,
                 const int64_t* __restrict__ n_rows, const int64_t* __restrict__ row_off,
+                const uint32_t* __restrict__ row_ids,
                 const unsigned int* __restrict__ stats, const int64_t* __restrict__ all_list,
                 unsigned long long* __restrict__ all_keys) {
     const int lane = threadIdx.x & 31;
@@ -793,7 +894,9 @@ all_rows_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, 
         const int s = static_cast<int>(pos / P);
         unsigned long long best = 0;
         if (r < n_rows[s]) {
-            const float v = exact_dot_bf16(W + (row_off[s] + r) * dim, H + pos * dim, dim);
+            const int64_t rr = row_off[s] + r;
+            const float v = exact_dot_bf16(W + (row_ids ? static_cast<int64_t>(row_ids[rr]) : rr) * dim,
+                                           H + pos * dim, dim);
             best = make_key(v, static_cast<uint32_t>(r), true, r == 0);
         }
 #pragma unroll
@@ -1031,13 +1134,19 @@ extern "C" svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int3
     return SVT_OK;
 }
 
-extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads,
-                                        int64_t total_sub_rows, const int64_t* d_row_offsets,
-                                        const int64_t* d_n_rows, const uint32_t* d_plan_ids,
-                                        const int64_t* d_id_offsets, const float* d_head_row_norms,
-                                        int32_t sequences, int32_t positions, int32_t dim,
-                                        uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
-                                        svt_stream stream) {
+namespace svt {
+namespace {
+// W: the gathered sub-heads (row_ids == nullptr; rows row_off[s] + r) or the
+// full head (row_ids = plan ids; rows row_ids[row_off[s] + r], TMA gather4)
+svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_rows,
+                              const int64_t* d_row_offsets, const int64_t* d_n_rows,
+                              const uint32_t* row_ids, const uint32_t* d_plan_ids,
+                              const int64_t* d_id_offsets, const float* d_head_row_norms,
+                              int32_t sequences, int32_t positions, int32_t dim,
+                              uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
+                              svt_stream stream) {
+    const void* d_subheads = W;
+    const int64_t total_sub_rows = w_rows;
     using namespace svt;
     if (sequences <= 0 || positions <= 0) return SVT_OK;
     if (positions % BM != 0 || dim % BK != 0 || dim <= 0) {
@@ -1070,7 +1179,7 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
     CUtensorMap mapH, mapW;
     if (svt_status s = make_map(&mapH, d_hidden, static_cast<uint64_t>(npos), dim, BM)) return s;
     if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows), dim,
-                                pair ? BN / 2 : BN))
+                                row_ids ? 1u : (pair ? BN / 2 : BN)))
         return s;
 
     const char* mode_env = getenv("SVT_PREFILL_MODE");  // profiling switches (PrefillParams::mode)
@@ -1116,6 +1225,7 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
     if (p.mode & 8) SVT_CUDA_TRY(cudaMemsetAsync(p.dbg, 0, 8 * sizeof(unsigned long long), st));
     p.n_rows = d_n_rows;
     p.row_off = d_row_offsets;
+    p.plan_ids = row_ids;
     p.top_val = top_val;
     p.top_row = top_row;
     p.flags = flags;
@@ -1159,17 +1269,48 @@ extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subh
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
     recompute_pairs_kernel<<<sm_count(), kPairWarps * 32, kPairSmem, st>>>(
         static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads), positions,
-        dim, d_row_offsets, stats, pairs, pos_keys);
+        dim, d_row_offsets, row_ids, stats, pairs, pos_keys);
     SVT_LAUNCH_CHECK("recompute_pairs_kernel");
     rec_finalize_kernel<<<sm_count(), 256, 0, st>>>(positions, d_id_offsets, d_plan_ids, stats,
                                                     rec_list, pos_keys, d_out_ids, d_out_max);
     SVT_LAUNCH_CHECK("rec_finalize_kernel");
     all_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(
         static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads),
-        positions, dim, d_n_rows, d_row_offsets, stats, all_list, all_keys);
+        positions, dim, d_n_rows, d_row_offsets, row_ids, stats, all_list, all_keys);
     SVT_LAUNCH_CHECK("all_rows_kernel");
     all_finalize_kernel<<<64, 256, 0, st>>>(positions, d_id_offsets, d_plan_ids, stats, all_list,
                                             all_keys, d_out_ids, d_out_max);
     SVT_LAUNCH_CHECK("all_finalize_kernel");
     return SVT_OK;
+}
+}  // namespace
+}  // namespace svt
+
+extern "C" svt_status svt_prefill_score(const void* d_hidden, const void* d_subheads,
+                                        int64_t total_sub_rows, const int64_t* d_row_offsets,
+                                        const int64_t* d_n_rows, const uint32_t* d_plan_ids,
+                                        const int64_t* d_id_offsets, const float* d_head_row_norms,
+                                        int32_t sequences, int32_t positions, int32_t dim,
+                                        uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
+                                        svt_stream stream) {
+    return svt::prefill_score_impl(d_hidden, d_subheads, total_sub_rows, d_row_offsets, d_n_rows,
+                                   nullptr, d_plan_ids, d_id_offsets, d_head_row_norms, sequences,
+                                   positions, dim, d_out_ids, d_out_max, d_workspace, stream);
+}
+
+extern "C" svt_status svt_prefill_score_fused(const void* d_hidden, const void* d_head,
+                                              int64_t head_rows, const int64_t* d_n_rows,
+                                              const uint32_t* d_plan_ids,
+                                              const int64_t* d_id_offsets,
+                                              const float* d_head_row_norms, int32_t sequences,
+                                              int32_t positions, int32_t dim, uint32_t* d_out_ids,
+                                              float* d_out_max, void* d_workspace,
+                                              svt_stream stream) {
+    if (head_rows <= 0 || head_rows > 0x7FFFFFFF) {
+        svt::set_error("fused prefill scoring needs 1 <= head rows < 2^31");
+        return SVT_ERR_CONFIG;
+    }
+    return svt::prefill_score_impl(d_hidden, d_head, head_rows, d_id_offsets, d_n_rows, d_plan_ids,
+                                   d_plan_ids, d_id_offsets, d_head_row_norms, sequences, positions,
+                                   dim, d_out_ids, d_out_max, d_workspace, stream);
 }

@@ -25,21 +25,29 @@ class PrefillScorer:
     positions must be a multiple of 128 and d of 64."""
 
     def __init__(self, head: HeadMatrix, plan_ids: torch.Tensor, id_offsets: np.ndarray,
-                 positions: int, stream=None):
+                 positions: int, stream=None, fused: bool = False):
         n_rows = np.diff(id_offsets).astype(np.int64)
-        self._setup(head, positions, len(id_offsets) - 1, int(n_rows.sum()), stream)
+        self.fused = fused
+        self._setup(head, positions, len(id_offsets) - 1, 0 if fused else int(n_rows.sum()),
+                    stream)
         self.n_rows = torch.from_numpy(n_rows).cuda()
         self.row_off = torch.from_numpy(np.ascontiguousarray(id_offsets[:-1], np.int64)).cuda()
         self.id_off = self.row_off
         self.plan_ids = plan_ids
+        if fused:
+            return
         call("svt_gather_rows", head.data.data_ptr(), head.storage, head.rows(), self.d,
              plan_ids.data_ptr(), self.total, self.sub.data_ptr(), self.bad.data_ptr(),
              _stream(stream))
 
     @classmethod
-    def from_batch(cls, head: HeadMatrix, tb, positions: int, stream=None) -> "PrefillScorer":
+    def from_batch(cls, head: HeadMatrix, tb, positions: int, stream=None,
+                   fused: bool = False) -> "PrefillScorer":
+        """fused=True: no sub-heads; the GEMM gathers the plan rows from the
+        head itself (svt_prefill_score_fused, TMA tile::gather4)."""
         self = cls.__new__(cls)
-        self._setup(head, positions, tb.B, int(tb.act_off_h[-1]), stream)
+        self.fused = fused
+        self._setup(head, positions, tb.B, 0 if fused else int(tb.act_off_h[-1]), stream)
         self.n_rows = tb.n_active            # device int64 [S]
         self.row_off = tb.act_off            # device int64 [S+1] (capacity offsets)
         self.id_off = tb.act_off
@@ -49,7 +57,10 @@ class PrefillScorer:
         return self
 
     def regather(self):
-        """Re-gather the sub-heads from the batch's current plans (device only)."""
+        """Re-gather the sub-heads from the batch's current plans (device
+        only; nothing to do for the fused scorer)."""
+        if self.fused:
+            return
         tb = self._tb
         call("svt_gather_plans", self.head.data.data_ptr(), self.head.storage, self.head.rows(),
              self.d, tb.active.data_ptr(), tb.act_off.data_ptr(), tb.n_active.data_ptr(), tb.B,
@@ -72,6 +83,13 @@ class PrefillScorer:
 
     def score(self, hidden: torch.Tensor, out_ids: torch.Tensor, out_max=None) -> torch.Tensor:
         """hidden: bf16 [S*P, d] on the device -> out_ids int32 [S*P]."""
+        if self.fused:
+            call("svt_prefill_score_fused", hidden.data_ptr(), self.head.data.data_ptr(),
+                 self.head.rows(), self.n_rows.data_ptr(), self.plan_ids.data_ptr(),
+                 self.id_off.data_ptr(), self.head.row_norms.data_ptr(), self.S, self.P, self.d,
+                 out_ids.data_ptr(), None if out_max is None else out_max.data_ptr(),
+                 self.ws.data_ptr(), _stream(self.stream))
+            return out_ids
         call("svt_prefill_score", hidden.data_ptr(), self.sub.data_ptr(), self.total,
              self.row_off.data_ptr(), self.n_rows.data_ptr(), self.plan_ids.data_ptr(),
              self.id_off.data_ptr(), self.head.row_norms.data_ptr(), self.S, self.P, self.d,

@@ -456,7 +456,8 @@ def prefill_tuning(request):
 
 @pytest.mark.parametrize("S,P,d,V,nT,L", [(3, 128, 256, 6000, 500, 400), (2, 256, 512, 20000, 900, 700),
                                           (2, 512, 192, 9000, 2500, 1200)])
-def test_prefill_scoring_tcgen05_ids_exact(th, prefill_tuning, S, P, d, V, nT, L):
+@pytest.mark.parametrize("fused", [False, True], ids=["gathered", "gather4"])
+def test_prefill_scoring_tcgen05_ids_exact(th, prefill_tuning, S, P, d, V, nT, L, fused):
     """cfg3-style batched prefill scoring on tcgen05: every position's id
     equals the reference greedy id over its sequence's plan; the tensor-core
     top-1 logit lies within the certification bound of the exact logit.
@@ -473,7 +474,7 @@ def test_prefill_scoring_tcgen05_ids_exact(th, prefill_tuning, S, P, d, V, nT, L
     off = np.zeros(S + 1, np.int64)
     off[1:] = np.cumsum([len(p) for p in plans])
     ids = torch.from_numpy(np.concatenate(plans).view(np.int32)).cuda()
-    sc = prefill.PrefillScorer(head, ids, off, P)
+    sc = prefill.PrefillScorer(head, ids, off, P, fused=fused)
     hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
     hdev = torch.from_numpy(hid).cuda().to(torch.bfloat16)
     out = torch.empty(S * P, dtype=torch.int32, device="cuda")
@@ -501,8 +502,9 @@ def test_prefill_scoring_tcgen05_ids_exact(th, prefill_tuning, S, P, d, V, nT, L
     print("max |tc - exact| / bound =", worst, "stats", sc.stats())
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["gathered", "gather4"])
 @pytest.mark.parametrize("case", ["duplicate_rows", "nonfinite"])
-def test_prefill_scoring_all_rows_fallback(th, prefill_tuning, case):
+def test_prefill_scoring_all_rows_fallback(th, prefill_tuning, case, fused):
     """Positions the top-8 cannot certify — more than eight rows tied at the
     maximum (duplicated head rows) or non-finite logits (overflowing hidden
     states) — go through the grid-wide all-rows recompute and still match the
@@ -520,7 +522,7 @@ def test_prefill_scoring_all_rows_fallback(th, prefill_tuning, case):
     off = np.zeros(S + 1, np.int64)
     off[1:] = np.cumsum([len(p) for p in plans])
     ids = torch.from_numpy(np.concatenate(plans).view(np.int32)).cuda()
-    sc = prefill.PrefillScorer(head, ids, off, P)
+    sc = prefill.PrefillScorer(head, ids, off, P, fused=fused)
     hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
     if case == "nonfinite":
         hid[::7] *= np.float32(3e38)  # products overflow: ±inf and inf-inf NaN logits
@@ -539,7 +541,8 @@ def test_prefill_scoring_all_rows_fallback(th, prefill_tuning, case):
     assert st[1] > 0, st  # candidates were recomputed (all rows or the top-8 ones)
 
 
-def test_prefill_from_device_batch_matches_reference(th):
+@pytest.mark.parametrize("fused", [False, True], ids=["gathered", "gather4"])
+def test_prefill_from_device_batch_matches_reference(th, fused):
     """select (device) -> svt_gather_plans (capacity-CSR) -> prefill scoring:
     ids equal the reference greedy over each request's own plan
     (selector.cpp:16-43 then head.cpp:203-217), no host round trip."""
@@ -556,7 +559,7 @@ def test_prefill_from_device_batch_matches_reference(th):
     tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), 600, V,
                                 torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda(),
                                 off)
-    sc = prefill.PrefillScorer.from_batch(head, tb, P)
+    sc = prefill.PrefillScorer.from_batch(head, tb, P, fused=fused)
     hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
     out = torch.empty(S * P, dtype=torch.int32, device="cuda")
     sc.score(torch.from_numpy(hid).cuda().to(torch.bfloat16), out)
