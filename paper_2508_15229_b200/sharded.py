@@ -116,7 +116,9 @@ class VocabShardedHead:
         r0, r1 = shard_ranges(head.rows(), self.world)[self.rank]
         self.shard = RowShard(head, r0, r1, B, plan_start=(self.rank == 0))
         self.B = B
-        self.gathered = torch.zeros((self.world, max(B, 1), RECORD_WORDS), dtype=torch.int32,
+        # flat [world * B, 4] so every backend accepts it (gloo insists on
+        # concatenation along dim 0); viewed as [world, B, 4] for the combine
+        self.gathered = torch.zeros((self.world * max(B, 1), RECORD_WORDS), dtype=torch.int32,
                                     device="cuda")
         self.out = torch.zeros(max(B, 1), dtype=torch.int32, device="cuda")
 
@@ -124,7 +126,7 @@ class VocabShardedHead:
         rec = self.shard.step(hidden)
         if self.world > 1:
             self.dist.all_gather_into_tensor(self.gathered, rec, group=self.group)
-            return combine(self.gathered, self.out)
+            return combine(self.gathered.view(self.world, -1, RECORD_WORDS), self.out)
         return combine(rec.view(1, *rec.shape), self.out)
 
 
