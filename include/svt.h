@@ -298,6 +298,10 @@ svt_status svt_greedy_certified(const void* d_sub, svt_dtype dt, size_t dim,
  * (optional) receives the exact reference logit of the winner.
  * The winner remaps through d_plan_ids[row] or, when NULL, row_base + row;
  * plan_start != 0 when row 0 is the plan's first row (the NaN rule).
+ * flags: SVT_ROWS_WEIGHTS_STABLE when the rows (and ids) were not written by
+ * the kernel immediately before this launch in the stream: the first wave
+ * of row copies is then issued before the programmatic-dependency wait and
+ * overlaps the previous kernel's tail (repeated decode steps).
  * d_out_record (optional, 16 bytes): the vocab-shard record {u64 key =
  * orderable(exact max) << 32 | ~(row_base + row), u32 id, f32 max} consumed
  * by svt_shard_combine; like d_out_max it forces the exact winner value.
@@ -311,10 +315,12 @@ size_t svt_greedy_rows_workspace_bytes(size_t n_rows);
  * writes 8 u64 %globaltimer stamps per CTA (start, after the dependency wait,
  * h staged, last row done, record written, ticket taken, tail done). */
 void svt_rows_set_debug(void* d_stamps);
+#define SVT_ROWS_WEIGHTS_STABLE 1 /* rows/ids not written by the preceding kernel */
 svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
                                      size_t dim, const uint32_t* d_src_ids, size_t n_rows,
                                      const float* d_hidden, const uint32_t* d_plan_ids,
-                                     uint32_t row_base, int32_t plan_start, uint32_t* d_out_id,
+                                     uint32_t row_base, int32_t plan_start, int32_t flags,
+                                     uint32_t* d_out_id,
                                      float* d_out_max, void* d_out_record, void* d_workspace,
                                      svt_stream stream);
 /* ------------------------------------------------------------------------

@@ -97,8 +97,8 @@ _SIGS = {
                               _vp, _vp], C.c_int),
     "svt_greedy_rows_workspace_bytes": ([_sz], _sz),
     "svt_rows_set_debug": ([_vp], None),
-    "svt_greedy_certified_rows": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _u32, _i32, _vp,
-                                   _vp, _vp, _vp, _vp], C.c_int),
+    "svt_greedy_certified_rows": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _u32, _i32, _i32,
+                                   _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_prefill_workspace_bytes": ([_i32, _i32], _sz),
     "svt_prefill_score": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
                            _vp, _vp], C.c_int),

@@ -11,11 +11,12 @@
 //
 //  * Stream (one CTA per SM, 16 warps): the CTA's contiguous row range flows
 //    through a shared-memory ring of row slots filled by 1-D bulk copies
-//    (cp.async.bulk, one per row, L2 evict-first); the first NS rows are
-//    requested before griddepcontrol.wait, i.e. while the previous kernel in
-//    the stream is still finishing (weights are never written by a kernel
-//    that triggers programmatic launch early). Row i is consumed by warp
-//    i % 16, which then refills its slot with row i + NS.
+//    (cp.async.bulk, one per row, L2 evict-first); when the caller marks the
+//    rows stable (SVT_ROWS_WEIGHTS_STABLE: not written by the kernel this
+//    launch depends on), the first NS rows are requested before
+//    griddepcontrol.wait, i.e. while the previous kernel in the stream is
+//    still finishing. Row i is consumed by warp i % 16, which then refills
+//    its slot with row i + NS.
 //  * Per row (one warp): every lane FFMA-accumulates its 16-byte chunks
 //    (stride 32) into f ~ w·h and a ~ Σ|w||h| (free |.| operand modifiers),
 //    a 5-level shuffle tree reduces both. The interval
@@ -83,6 +84,7 @@ struct SmallParams {
     const uint32_t* plan_ids;  // remap; nullptr: row_base + row
     uint32_t row_base;
     int32_t plan_start;
+    int32_t flags;  // SVT_ROWS_* bits
     uint32_t* out_id;
     float* out_max;
     uint4* out_key;  // optional shard record {key lo, key hi, id, max} (exact winner value)
@@ -270,14 +272,19 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
         bulk_g2s(ring + static_cast<size_t>(slot) * rb, row_ptr(p, r0 + i), rb, &s_full[slot],
                  pol);
     };
-    // Weights first: they do not depend on the previous kernel in the stream.
     // Slot s belongs to warp s % 16 for the whole launch (rows s, s+NS, ...):
     // its lane 0 initialises the slot's barrier, issues its copies, and the
     // warp consumes its phases in order (NS is a multiple of 16 whenever slots
     // are refilled, or < 16: fewer consumer warps). No CTA barrier needed.
+    // With SVT_ROWS_WEIGHTS_STABLE the caller guarantees the rows were not
+    // written by the kernel this launch depends on (programmatically), so the
+    // first wave of copies goes out before griddepcontrol.wait and overlaps
+    // the previous kernel's tail; otherwise it waits like every other read.
+    const bool early = (p.flags & SVT_ROWS_WEIGHTS_STABLE) != 0;
     if (lane == 0) {
         for (int sl = warp; sl < NS; sl += kWarps) mbar_init(&s_full[sl], 1);
         fence_mbar_init();
+        if (early)
             for (int64_t i = warp; i < nrows && i < NS; i += kWarps) issue(i);
     }
     if (tid == 0) {
@@ -287,6 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
+    if (!early && lane == 0)
+        for (int64_t i = warp; i < nrows && i < NS; i += kWarps) issue(i);
     SVT_STAMP(1);
     constexpr int E = Chunk<DT>::E;
     constexpr int CR = CPL > 0 ? CPL : 1;
@@ -639,7 +648,8 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
                                                 size_t dim, const uint32_t* d_src_ids,
                                                 size_t n_rows, const float* d_hidden,
                                                 const uint32_t* d_plan_ids, uint32_t row_base,
-                                                int32_t plan_start, uint32_t* d_out_id,
+                                                int32_t plan_start, int32_t flags,
+                                                uint32_t* d_out_id,
                                                 float* d_out_max, void* d_out_record,
                                                 void* d_workspace,
                                                 svt_stream stream) {
@@ -683,6 +693,7 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
     p.plan_ids = d_plan_ids;
     p.row_base = row_base;
     p.plan_start = plan_start;
+    p.flags = flags;
     p.out_id = d_out_id;
     p.out_max = d_out_max;
     p.out_key = static_cast<uint4*>(d_out_record);

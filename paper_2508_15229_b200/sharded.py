@@ -69,6 +69,7 @@ class RowShard:
         self.certified = (B == 1 and self.n > 0 and (self.dim * esize) % 16 == 0
                           and self.dim <= 8192 and self.rows.data_ptr() % 16 == 0
                           and not os.environ.get("SVT_SHARD_EXACT"))
+        self._stable = 0
         if self.certified:
             self.cws = torch.zeros(_lib.lib.svt_greedy_rows_workspace_bytes(self.n),
                                    dtype=torch.uint8, device=dev)
@@ -79,10 +80,12 @@ class RowShard:
             self.records.zero_()  # key 0 never wins
             return self.records
         if self.certified:
+            # the shard's rows are written once, long before any step
             call("svt_greedy_certified_rows", self.rows.data_ptr(), self.storage, self.n,
                  self.dim, None, self.n, hidden.data_ptr(), None, self.r0, self.plan_start,
-                 self.ids.data_ptr(), None, self.records.data_ptr(), self.cws.data_ptr(),
-                 _stream(self.stream))
+                 self._stable, self.ids.data_ptr(), None, self.records.data_ptr(),
+                 self.cws.data_ptr(), _stream(self.stream))
+            self._stable = 1
             return self.records
         call("svt_greedy_fused", self.rows.data_ptr(), self.storage, self.n, self.dim,
              self.group_begin.data_ptr(), self.group_meta.data_ptr(), None, self.B,

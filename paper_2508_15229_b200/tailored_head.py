@@ -386,9 +386,13 @@ class RowDecoder:
         self._fn = _lib.lib.svt_greedy_certified_rows
         self._pre = (src, head.storage, rows, head.dim(), src_ids, self.n)
         self._post = ((plan_ids.data_ptr() if remap else None), row_base, plan_start)
+        # the first step after a (re)gather must not prefetch rows before the
+        # dependency wait; later steps may (SVT_ROWS_WEIGHTS_STABLE)
+        self._stable = 0
 
     def gather(self):
         """(Re)materialise the row-major sub-head (svt_gather_rows)."""
+        self._stable = 0
         h = self.head
         call("svt_gather_rows", h.data.data_ptr(), h.storage, h.rows(), h.dim(),
              self.ids.data_ptr(), self.n, self.sub.data_ptr(), self.bad.data_ptr(),
@@ -402,9 +406,11 @@ class RowDecoder:
         int32; out_max (optional): the exact reference logit of the winner;
         out_record (optional, 4 int32): the vocab-shard record for
         svt_shard_combine."""
-        st = self._fn(*self._pre, hidden.data_ptr(), *self._post, out_id.data_ptr(),
-                      _ptr(out_max), _ptr(out_record), self.ws.data_ptr(), _stream(self.stream))
+        st = self._fn(*self._pre, hidden.data_ptr(), *self._post, self._stable,
+                      out_id.data_ptr(), _ptr(out_max), _ptr(out_record), self.ws.data_ptr(),
+                      _stream(self.stream))
         _lib.check(st, "svt_greedy_certified_rows")
+        self._stable = 1
         return out_id
 
     def stats(self):
