@@ -252,19 +252,26 @@ void svt_set_debug(void* d_counters);
  *   head.cpp:205-206; the host-buffer APIs raise it).
  * ---------------------------------------------------------------------- */
 size_t svt_greedy_workspace_bytes(int32_t batch, int64_t max_groups);
+/* flags: SVT_WEIGHTS_STABLE when the sub-heads / head rows (and plan
+ * records) were not written by the kernel immediately before this launch in
+ * the stream (repeated decode steps after one gather): the first ring stages'
+ * weight copies are then issued before the programmatic-dependency wait and
+ * overlap the previous step's tail; hidden states are always read after it. */
+#define SVT_WEIGHTS_STABLE 1
 svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
                                   const int64_t* d_group_begin, const void* d_group_meta,
                                   const uint32_t* d_active_ids, int32_t batch,
                                   int64_t max_groups, const float* d_hidden, size_t hidden_ld,
-                                  uint32_t row_base, int32_t plan_start, uint32_t* d_out_ids,
-                                  float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
-                                  svt_stream stream);
+                                  uint32_t row_base, int32_t plan_start, int32_t flags,
+                                  uint32_t* d_out_ids, float* d_out_max, uint64_t* d_out_keys,
+                                  void* d_workspace, svt_stream stream);
 svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
                             const int64_t* d_group_begin, const void* d_group_meta,
                             const uint32_t* d_active_ids, int32_t batch, int64_t max_groups,
                             const float* d_hidden, size_t hidden_ld, uint32_t row_base,
-                            int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
-                            uint64_t* d_out_keys, void* d_workspace, svt_stream stream);
+                            int32_t plan_start, int32_t flags, uint32_t* d_out_ids,
+                            float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
+                            svt_stream stream);
 
 /* Certified greedy decode (latency-bound small batches, e.g. batch 1): a
  * split-K FFMA pass over the interleaved sub-heads streams at full HBM
@@ -315,7 +322,7 @@ size_t svt_greedy_rows_workspace_bytes(size_t n_rows);
  * writes 8 u64 %globaltimer stamps per CTA (start, after the dependency wait,
  * h staged, last row done, record written, ticket taken, tail done). */
 void svt_rows_set_debug(void* d_stamps);
-#define SVT_ROWS_WEIGHTS_STABLE 1 /* rows/ids not written by the preceding kernel */
+#define SVT_ROWS_WEIGHTS_STABLE 1 /* = SVT_WEIGHTS_STABLE (rows/ids not written by the preceding kernel) */
 svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
                                      size_t dim, const uint32_t* d_src_ids, size_t n_rows,
                                      const float* d_hidden, const uint32_t* d_plan_ids,

@@ -15,6 +15,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libsvt.so")
 
 SVT_F32, SVT_F16, SVT_BF16 = 0, 1, 2
+SVT_WEIGHTS_STABLE = 1  # svt.h: rows not written by the kernel a launch depends on
 GROUP_ROWS = 32
 GROUP_META_BYTES = 32
 
@@ -89,9 +90,9 @@ _SIGS = {
     "svt_greedy_step": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_greedy_workspace_bytes": ([_i32, _i64], _sz),
     "svt_greedy_interleaved": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,
-                                _vp, _vp, _vp, _vp, _vp], C.c_int),
+                                _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_greedy_fused": ([_vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _u32, _i32,
-                          _vp, _vp, _vp, _vp, _vp], C.c_int),
+                          _i32, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_certified_workspace_bytes": ([_i32, _i64], _sz),
     "svt_greedy_certified": ([_vp, C.c_int, _sz, _vp, _vp, _vp, _i32, _i64, _vp, _sz, _vp, _vp,
                               _vp, _vp], C.c_int),

@@ -228,7 +228,7 @@ svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
 static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t rows, size_t dim,
                                 const int64_t* gb, const void* meta, const uint32_t* ids,
                                 int32_t batch, int64_t max_groups, const float* hidden,
-                                size_t ld, uint32_t row_base, int32_t plan_start,
+                                size_t ld, uint32_t row_base, int32_t plan_start, int32_t flags,
                                 uint32_t* out_ids, float* out_max, uint64_t* out_keys, void* ws,
                                 svt_stream stream) {
     if (svt_status s = check_dtype(dt)) return s;
@@ -253,6 +253,7 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
     p.out_keys = reinterpret_cast<unsigned long long*>(out_keys);
     p.row_base = row_base;
     p.plan_start = plan_start;
+    p.weights_stable = (flags & SVT_WEIGHTS_STABLE) ? 1 : 0;
     return gemv_run(src, MODE_ARGMAX, dt, p, static_cast<cudaStream_t>(stream));
 }
 
@@ -260,23 +261,26 @@ svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
                                   const int64_t* d_group_begin, const void* d_group_meta,
                                   const uint32_t* d_active_ids, int32_t batch,
                                   int64_t max_groups, const float* d_hidden, size_t hidden_ld,
-                                  uint32_t row_base, int32_t plan_start, uint32_t* d_out_ids,
-                                  float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
-                                  svt_stream stream) {
+                                  uint32_t row_base, int32_t plan_start, int32_t flags,
+                                  uint32_t* d_out_ids, float* d_out_max, uint64_t* d_out_keys,
+                                  void* d_workspace, svt_stream stream) {
     return greedy_common(SRC_INTERLEAVED, d_sub, dt, 0, dim, d_group_begin, d_group_meta,
                          d_active_ids, batch, max_groups, d_hidden, hidden_ld, row_base,
-                         plan_start, d_out_ids, d_out_max, d_out_keys, d_workspace, stream);
+                         plan_start, flags, d_out_ids, d_out_max, d_out_keys, d_workspace,
+                         stream);
 }
 
 svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_t dim,
                             const int64_t* d_group_begin, const void* d_group_meta,
                             const uint32_t* d_active_ids, int32_t batch, int64_t max_groups,
                             const float* d_hidden, size_t hidden_ld, uint32_t row_base,
-                            int32_t plan_start, uint32_t* d_out_ids, float* d_out_max,
-                            uint64_t* d_out_keys, void* d_workspace, svt_stream stream) {
+                            int32_t plan_start, int32_t flags, uint32_t* d_out_ids,
+                            float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
+                            svt_stream stream) {
     return greedy_common(SRC_ROWS, d_head, dt, rows, dim, d_group_begin, d_group_meta,
                          d_active_ids, batch, max_groups, d_hidden, hidden_ld, row_base,
-                         plan_start, d_out_ids, d_out_max, d_out_keys, d_workspace, stream);
+                         plan_start, flags, d_out_ids, d_out_max, d_out_keys, d_workspace,
+                         stream);
 }
 
 svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, size_t dim,

@@ -81,6 +81,9 @@ __device__ __forceinline__ void group_epilogue(const GemvParams& p, const GroupM
 // one warp per request: max over the request's group keys, decode, remap
 // through the plan ids (remap_out, selector.cpp:50-56)
 __global__ void __launch_bounds__(256) argmax_finalize_kernel(const GemvParams p) {
+    // the next decode step's GEMV may be scheduled now (it waits for this
+    // grid in griddepcontrol.wait before reading anything upstream)
+    asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lane = threadIdx.x & 31;
     const int nreq = p.group_begin ? p.B : 1;
@@ -217,70 +220,97 @@ __global__ void __launch_bounds__(512, 1) gemv_ring_kernel(const GemvParams p) {
     if (producer) {
         const uint64_t pol_w = policy_evict_first();
         const int dim4 = (p.dim + 3) & ~3;
-        int64_t ig = w;
-        int is = 0, islot = 0;
-        uint32_t ephase = 0;
-        GroupMeta im = p.group(w);
-        GroupMeta im_next = (w + TW < total_groups) ? p.group(w + TW) : dummy;
-        const uint8_t* isrc = nullptr;  // ROWS: this lane's source row
-        unsigned imask = 0;
-        for (int64_t q = 0; q < nq; ++q) {
-            // use k = q / S of this slot needs the consumer's release of use
-            // k-1, i.e. completion of empty-phase k-1 (parity = ephase ^ 1)
-            if (q >= S) {
+        // walk state over this pair's (group, stage) sequence
+        struct Walk {
+            int64_t ig;
+            int is, islot;
+            uint32_t ephase;
+            GroupMeta im, im_next;
+            const uint8_t* isrc;  // ROWS: this lane's source row
+            unsigned imask;
+        };
+        Walk w0;
+        w0.ig = w;
+        w0.is = 0;
+        w0.islot = 0;
+        w0.ephase = 0;
+        w0.im = p.group(w);
+        w0.im_next = (w + TW < total_groups) ? p.group(w + TW) : dummy;
+        w0.isrc = nullptr;
+        w0.imask = 0;
+        // part bit 0: arm the slot + weight copies; bit 1: hidden copies
+        auto issue = [&](Walk& k, int64_t q, int part) {
+            if ((part & 1) && q >= S) {
+                // use u = q / S of this slot needs the consumer's release of
+                // use u-1, i.e. completion of empty-phase u-1 (parity ephase^1)
                 const long long tw = p.dbg ? clock64() : 0;
-                mbar_wait_parity(&empty[islot], ephase ^ 1u);
+                mbar_wait_parity(&empty[k.islot], k.ephase ^ 1u);
                 if (p.dbg) dbg_wait += clock64() - tw;
             }
-            if (is == 0 && SRC == SRC_ROWS) {
+            if (k.is == 0 && SRC == SRC_ROWS) {
                 int64_t srow = 0;
-                const bool ok = lane_valid<SRC>(p, im, lane, &srow);
-                isrc = p.W + (ok ? srow : 0) * p.row_bytes;
-                imask = __ballot_sync(0xFFFFFFFFu, ok);
+                const bool ok = lane_valid<SRC>(p, k.im, lane, &srow);
+                k.isrc = p.W + (ok ? srow : 0) * p.row_bytes;
+                k.imask = __ballot_sync(0xFFFFFFFFu, ok);
             }
-            uint8_t* wdst = ring + islot * kSlot;
+            uint8_t* wdst = ring + k.islot * kSlot;
             uint8_t* hdst = wdst + kSlotW;
-            const int c0 = is * kCR;
+            const int c0 = k.is * kCR;
             const int cc = min(kCR, p.nchunks - c0);
             const int e0 = c0 * E;
             const int hb = min(cc * E, dim4 - e0) * 4;
-            const float* hsrc = p.hidden + static_cast<int64_t>(im.b) * p.hidden_ld + e0;
+            const float* hsrc = p.hidden + static_cast<int64_t>(k.im.b) * p.hidden_ld + e0;
             if constexpr (SRC == SRC_INTERLEAVED) {
                 if (lane == 0) {
                     const uint32_t wb = static_cast<uint32_t>(cc) * kChunkRowBytes;
-                    mbar_arrive_expect_tx(&full[islot], wb + hb);
-                    bulk_g2s(wdst,
-                             p.W + (ig * p.nchunks + c0) * static_cast<int64_t>(kChunkRowBytes),
-                             wb, &full[islot], pol_w);
-                    bulk_g2s(hdst, hsrc, hb, &full[islot], pol_w);
+                    if (part & 1) {
+                        mbar_arrive_expect_tx(&full[k.islot], wb + hb);
+                        bulk_g2s(wdst,
+                                 p.W + (k.ig * p.nchunks + c0) * static_cast<int64_t>(kChunkRowBytes),
+                                 wb, &full[k.islot], pol_w);
+                    }
+                    if (part & 2) bulk_g2s(hdst, hsrc, hb, &full[k.islot], pol_w);
                 }
             } else {
                 const uint32_t slice = static_cast<uint32_t>(cc) * kChunkBytes;
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[islot], __popc(imask) * slice + hb);
-                    bulk_g2s(hdst, hsrc, hb, &full[islot], pol_w);
+                    if (part & 1)
+                        mbar_arrive_expect_tx(&full[k.islot], __popc(k.imask) * slice + hb);
+                    if (part & 2) bulk_g2s(hdst, hsrc, hb, &full[k.islot], pol_w);
                 }
                 __syncwarp();
-                if ((imask >> lane) & 1u)
-                    bulk_g2s(wdst + lane * (kCR + 1) * kChunkBytes, isrc + c0 * kChunkBytes,
-                             slice, &full[islot], pol_w);
+                if ((part & 1) && ((k.imask >> lane) & 1u))
+                    bulk_g2s(wdst + lane * (kCR + 1) * kChunkBytes, k.isrc + c0 * kChunkBytes,
+                             slice, &full[k.islot], pol_w);
             }
-            if (++is == ns) {
-                is = 0;
-                ig += TW;
-                im = im_next;
-                if (ig + TW < total_groups) im_next = p.group(ig + TW);
+            if (++k.is == ns) {
+                k.is = 0;
+                k.ig += TW;
+                k.im = k.im_next;
+                if (k.ig + TW < total_groups) k.im_next = p.group(k.ig + TW);
             }
-            if (++islot == S) {
-                islot = 0;
-                ephase ^= 1u;
+            if (++k.islot == S) {
+                k.islot = 0;
+                k.ephase ^= 1u;
             }
-        }
+        };
+        // Weights stable (not written by the kernel this launch depends on):
+        // the first S stages' weight copies go out before the dependency
+        // wait and overlap the previous kernel's tail; the hidden states
+        // (written upstream) only after it.
+        const int64_t npre = p.weights_stable ? (nq < S ? nq : S) : 0;
+        Walk k = w0;
+        for (int64_t q = 0; q < npre; ++q) issue(k, q, 1);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        k = w0;
+        for (int64_t q = 0; q < npre; ++q) issue(k, q, 2);
+        for (int64_t q = npre; q < nq; ++q) issue(k, q, 3);
         dbg_flush(0);
         return;
     }
 
     // ---- consumer ----
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int full_stages = p.dim / (kCR * E);  // stages with no element past dim
     int64_t g = w;
     int s = 0, slot = 0;
@@ -451,8 +481,19 @@ svt_status launch_ring_cr(GemvParams p, cudaStream_t st, int nwa, int grid) {
     const int smem = bar_bytes + nwa * S * kSlot;
     auto kern = gemv_ring_kernel<DT, SRC, MODE, CR>;
     SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, nwa * 64, smem, st>>>(p);
-    SVT_LAUNCH_CHECK("gemv_ring_kernel");
+    // programmatic dependent launch: CTAs may be scheduled while the previous
+    // kernel finishes; everything upstream is read after griddepcontrol.wait
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(nwa * 64));
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
     return SVT_OK;
 }
 
@@ -511,6 +552,8 @@ svt_status gemv_run(int src, int mode, int dt, GemvParams p, cudaStream_t st) {
                 aligned16(p.W);
     if (src == SRC_ROWS) ring = ring && (p.row_bytes % 16 == 0);
     if (std::getenv("SVT_FORCE_GENERIC")) ring = false;
+    if (const char* e = std::getenv("SVT_GEMV_EARLY"))  // A/B switch: 0 disables the early stream
+        if (atoi(e) == 0) p.weights_stable = 0;
     svt_status s;
     if (src == SRC_INTERLEAVED)
         s = mode == MODE_LOGITS ? dispatch<SRC_INTERLEAVED, MODE_LOGITS>(dt, p, ring, st)

@@ -45,6 +45,7 @@ struct GemvParams {
     uint32_t row_base;
     int32_t plan_start;
     int32_t stages;
+    int32_t weights_stable;  // sub-head / rows not written by the kernel this launch depends on
     int64_t single_rows;
     // optional instrumentation (svt_set_debug): per (block, pair) cycle
     // counters {producer total, producer empty-wait, consumer total,

@@ -58,6 +58,7 @@ struct svt_session {
     cudaGraphExec_t graph_exec = nullptr;
     cudaGraphNode_t node_h2d = nullptr, node_d2h = nullptr;
     std::unordered_map<const void*, bool> pinned_cache;
+    bool weights_stable = false;  // set after the first decode step following a prepare
 
     int64_t* n_active_d() { return d_meta; }
     int64_t* n_static_d() { return d_meta + cap_batch; }
@@ -231,6 +232,7 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
         return SVT_ERR_INTEGRITY;
     }
     drop_graph(s);  // plans, layouts and buffers may change
+    s->weights_stable = false;
     if (batch < 0) {
         set_error("negative batch");
         return SVT_ERR_CONFIG;
@@ -358,10 +360,13 @@ svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size
             set_error("greedy step over an empty sub-head");
             return SVT_ERR_INTEGRITY;
         }
+    // the sub-heads were gathered by prepare(): only the first step after it
+    // must not prefetch them ahead of the dependency wait
+    const int32_t flags = s->weights_stable ? SVT_WEIGHTS_STABLE : 0;
+    s->weights_stable = true;
     return svt_greedy_interleaved(s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req,
-                                  s->d_active, s->batch,
-                                  s->max_groups, d_hidden, hidden_ld, 0, 1, d_out_ids, d_out_max,
-                                  nullptr, s->d_ws, s->stream);
+                                  s->d_active, s->batch, s->max_groups, d_hidden, hidden_ld, 0, 1,
+                                  flags, d_out_ids, d_out_max, nullptr, s->d_ws, s->stream);
 }
 
 svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t host_ld,

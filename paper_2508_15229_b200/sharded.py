@@ -90,8 +90,9 @@ class RowShard:
         call("svt_greedy_fused", self.rows.data_ptr(), self.storage, self.n, self.dim,
              self.group_begin.data_ptr(), self.group_meta.data_ptr(), None, self.B,
              self.max_groups, hidden.data_ptr(), hidden.stride(0), self.r0, self.plan_start,
-             self.ids.data_ptr(), None, self.records.data_ptr(), self.ws.data_ptr(),
-             _stream(self.stream))
+             self._stable, self.ids.data_ptr(), None, self.records.data_ptr(),
+             self.ws.data_ptr(), _stream(self.stream))
+        self._stable = 1
         return self.records
 
 

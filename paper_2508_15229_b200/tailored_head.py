@@ -24,8 +24,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (SVT_BF16, SVT_F16, SVT_F32, ConfigError, Error, IntegrityError, ParseError,
-                   call)
+from ._lib import (SVT_BF16, SVT_F16, SVT_F32, SVT_WEIGHTS_STABLE, ConfigError, Error,
+                   IntegrityError, ParseError, call)
 
 __all__ = [
     "Error", "ConfigError", "ParseError", "IntegrityError", "TokenSet", "SelectionPlan",
@@ -545,15 +545,18 @@ class TailoredBatch:
         call("svt_plan_layout", tb.n_active.data_ptr(), tb.act_off.data_ptr(), B,
              tb.group_begin.data_ptr(), tb.group_meta.data_ptr(), tb.max_groups,
              _stream(stream))
+        tb._stable = False
         return tb
 
     def attach(self, head: HeadMatrix):
         """Use ``head`` for the fused (no sub-head) decode without gathering."""
         self.head = head
         self._fast = None
+        self._stable = False
         return self
 
     def run_select(self):
+        self._stable = False
         call("svt_select_batched", self._words.data_ptr(), self.V, self.V,
              self._prompts.data_ptr(), self._prompt_off.data_ptr(), self.B,
              self.active.data_ptr(), self.act_off.data_ptr(), self.n_active.data_ptr(),
@@ -616,6 +619,7 @@ class TailoredBatch:
             # sticky error flag: set by the kernel when a plan id is >= rows
             self.gather_bad = torch.zeros(1, dtype=torch.int32, device="cuda")
             self._fast = None
+        self._stable = False
         call("svt_gather_interleaved", head.data.data_ptr(), head.storage, head.rows(),
              head.dim(), self.active.data_ptr(), self.group_begin.data_ptr(),
              self.group_meta.data_ptr(), self.B, self.max_groups, self.sub.data_ptr(),
@@ -644,11 +648,16 @@ class TailoredBatch:
                out_keys: Optional[torch.Tensor] = None, row_base: int = 0,
                plan_start: int = 1) -> torch.Tensor:
         """hidden: [B, ld] float32 on the device (ld % 4 == 0, ld >= dim)."""
+        # SVT_WEIGHTS_STABLE from the second step after a select / gather on:
+        # the sub-heads and group records are then not written by the kernel
+        # the step depends on, so its first weight stages stream early
+        flags = SVT_WEIGHTS_STABLE if getattr(self, "_stable", False) else 0
+        self._stable = True
         if out_max is None and out_keys is None and row_base == 0 and plan_start == 1 and (
                 fused or self.sub is not None):
             fn, pre = self._fast_args()[bool(fused)]
-            st = fn(*pre, hidden.data_ptr(), hidden.stride(0), 0, 1, out_ids.data_ptr(), None,
-                    None, self.ws.data_ptr(), _stream(self.stream))
+            st = fn(*pre, hidden.data_ptr(), hidden.stride(0), 0, 1, flags, out_ids.data_ptr(),
+                    None, None, self.ws.data_ptr(), _stream(self.stream))
             _lib.check(st, "greedy")
             return out_ids
         head = self.head
@@ -656,13 +665,13 @@ class TailoredBatch:
             call("svt_greedy_fused", head.data.data_ptr(), head.storage, head.rows(), head.dim(),
                  self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.active.data_ptr(),
                  self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), row_base,
-                 plan_start, out_ids.data_ptr(), _ptr(out_max), _ptr(out_keys),
+                 plan_start, flags, out_ids.data_ptr(), _ptr(out_max), _ptr(out_keys),
                  self.ws.data_ptr(), _stream(self.stream))
         else:
             call("svt_greedy_interleaved", self.sub.data_ptr(), head.storage, head.dim(),
                  self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.active.data_ptr(),
                  self.B, self.max_groups, hidden.data_ptr(), hidden.stride(0), row_base,
-                 plan_start, out_ids.data_ptr(), _ptr(out_max), _ptr(out_keys),
+                 plan_start, flags, out_ids.data_ptr(), _ptr(out_max), _ptr(out_keys),
                  self.ws.data_ptr(), _stream(self.stream))
         return out_ids
 

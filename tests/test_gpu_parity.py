@@ -805,3 +805,40 @@ def test_session_step_graph_pinned_buffers(th):
                     tb.greedy(torch.from_numpy(hid[t]).cuda(), o)
                     assert torch.equal(outs[t], o.cpu()), (B, rep, t)
                     assert np.array_equal(s.greedy(hid[t]), o.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_decode_steps_across_reselect(th, fused):
+    """Decode steps stream their weights ahead of the programmatic-dependency
+    wait only while the sub-heads are unchanged: after run_select() on new
+    prompts (+ gather) the next step must see the new plans and rows."""
+    V, d, B = 20000, 256, 6
+    head = th.HeadMatrix.random(V, d, 0x77, storage=th.SVT_BF16)
+    W = head.to_host()
+    rng = np.random.default_rng(31)
+    words = words_from_ids(rng.choice(V, 300, replace=False), V)
+    prompts = [rng.integers(0, V, 200).astype(np.uint32) for _ in range(B)]
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in prompts])
+    d_prompts = torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda()
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), 300, V, d_prompts,
+                                off)
+    if fused:
+        tb.attach(head)
+    else:
+        tb.gather(head)
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    for rnd in range(3):
+        for t in range(3):
+            h = bf16_np(rng.uniform(-1, 1, (B, d)).astype(np.float32))
+            tb.greedy(torch.from_numpy(h).cuda(), out, fused=fused)
+            got = out.cpu().numpy().view(np.uint32)
+            for b in range(B):
+                plan = orc.select(prompts[b], words, V, V).active_ids
+                assert got[b] == orc.greedy_step(W[plan], h[b], plan)[0], (rnd, t, b)
+        # new prompts in place, re-select (+ re-gather)
+        prompts = [rng.integers(0, V, 200).astype(np.uint32) for _ in range(B)]
+        d_prompts.copy_(torch.from_numpy(np.concatenate(prompts).view(np.int32)))
+        tb.run_select()
+        if not fused:
+            tb.gather(head)
