@@ -9,13 +9,13 @@
 // (~4.2 us at 1.965 GHz) plus its ramp, well above the 3.2 us the 20.9 MB
 // sub-head needs at HBM speed. This kernel certifies the id instead.
 //
-//  * Stream (one CTA per SM, 16 warps): the CTA's contiguous row range flows
+//  * Stream (one CTA per SM, 15 warps): the CTA's contiguous row range flows
 //    through a shared-memory ring of row slots filled by 1-D bulk copies
 //    (cp.async.bulk, one per row, L2 evict-first); when the caller marks the
 //    rows stable (SVT_ROWS_WEIGHTS_STABLE: not written by the kernel this
 //    launch depends on), the first NS rows are requested before
 //    griddepcontrol.wait, i.e. while the previous kernel in the stream is
-//    still finishing. Row i is consumed by warp i % 16, which then refills
+//    still finishing. Row i is consumed by warp i % 15, which then refills
 //    its slot with row i + NS.
 //  * Per row (one warp): every lane FFMA-accumulates its 16-byte chunks
 //    (stride 32) into f ~ w·h and a ~ Σ|w||h| (free |.| operand modifiers),
@@ -27,17 +27,21 @@
 //    FFMA tree). Lane 0 keeps the warp's running max lo and the rows whose hi
 //    reaches it (pruned as it rises).
 //  * Per CTA: L_c = max lo; the rows with hi >= L_c (a superset of its global
-//    candidates) go to a 16-byte record {L_c, count, row, hi} (+ a small list
-//    when count > 1; every row's hi goes to a rescan array on overflow).
-//  * Tail (the last CTA, by an acq_rel ticket): one round trip reads every
-//    record; L = max L_c; rows with hi >= L are the only possible reference
-//    argmax. Exactly one: the answer. Otherwise (or non-finite values, or a
-//    requested exact logit) the candidates are recomputed in the reference
-//    order __fadd_rn(acc, __fmul_rn(w, h)) (one lane per candidate, its warp
-//    streaming the row into shared memory with cp.async) and reduced with
-//    the reference's tie / NaN / signed-zero rules.
-// The tail leaves the control words zeroed: consecutive calls and CUDA-graph
-// replays need no memset.
+//    candidates) go to a 32-byte record {L_c, count, two inline candidates
+//    with their remapped ids} (+ a list when count > 2; every row's hi goes
+//    to a rescan array). The CTA then exits: no fence, no ticket.
+//  * Finalize (a separate one-warp grid, a programmatic dependent of the rows
+//    grid): grid completion makes every record visible; one round trip reads
+//    them; L = max L_c; rows with hi >= L are the only possible reference
+//    argmax. Exactly one: the answer, its id already in the record.
+//    Otherwise (or non-finite values, or a requested exact logit / shard
+//    record) the candidates are recomputed in the reference order
+//    __fadd_rn(acc, __fmul_rn(w, h)) (lane 0 chains while the warp streams
+//    the row into shared memory with cp.async) and reduced with the
+//    reference's tie / NaN / signed-zero rules. The finalize triggers its own
+//    dependents on entry, so the next step's rows grid is scheduled (and,
+//    with stable weights, streams its first rows) while it runs; the rows
+//    kernel has 15 warps so the finalize warp fits beside a rows CTA.
 #include <cfloat>
 #include <cstdlib>
 
@@ -46,16 +50,20 @@
 namespace svt {
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 480;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxSlots = 128;
-constexpr int kSmemBudget = 224 * 1024;
+// a CTA whose rows all fit stays within 184 KB, leaving room on its SM for
+// the one-warp finalize grid; streaming (ring) CTAs use up to 220 KB
+constexpr int kSmemBudget = 184 * 1024;
+constexpr int kSmemBudgetRing = 220 * 1024;
 constexpr int kWarpCand = 4;     // rows per warp kept within reach of its running max
 constexpr int kCapG = 64;        // candidate list per CTA (16 warps x 4; count > 2)
 constexpr int kMaxGrid = 256;   // the tail reads <= 8 records per lane
 constexpr int kMaxCand = 1024;   // tail candidate list
 constexpr int kPiece = 2048;     // bytes per exact-recompute piece
 constexpr unsigned kOverflow = 0xFFFFFFFFu;
+constexpr unsigned kBad = 0xFFFFFFFEu;  // record count: a non-finite value in the CTA
 
 // Per-CTA record: the CTA's max lo and its rows with hi >= it (inline up to
 // two, with their remapped ids; more go to the gcand list, kOverflow means
@@ -94,9 +102,11 @@ struct SmallParams {
     float* ws_hi;    // [n] hi_r (written only by CTAs that overflow)
     float c_rel;
     float eta;
+    int32_t grid;     // CTAs of the rows grid (records to reduce)
     int64_t per_cta;  // rows of CTA c: per_cta (+1 for c < extra), contiguous
     int32_t extra;
     int32_t variant;  // profiling (SVT_ROWS_VARIANT): 1 exit, 2 loads only, 3 no tail
+    int32_t l2_keep;  // weight stream L2 policy: 0 evict-first, 1 evict-last (SVT_ROWS_L2)
     unsigned long long* dbg;  // profiling: per CTA 8 globaltimer stamps (svt_rows_set_debug)
 };
 
@@ -105,8 +115,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define SVT_STAMP(k) \
-    if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 128 + (k)] = gtimer();
+// slot 0: %globaltimer at CTA start (cross-CTA / cross-launch ordering);
+// slot 127: clock64 at CTA start; other slots: clock64 - that (SM cycles,
+// precise within a CTA)
+#define SVT_STAMP(k)                                                              \
+    if (p.dbg && threadIdx.x == 0) {                                              \
+        if ((k) == 0) {                                                           \
+            p.dbg[blockIdx.x * 128] = gtimer();                                   \
+            p.dbg[blockIdx.x * 128 + 127] = clock64();                            \
+        } else {                                                                  \
+            p.dbg[blockIdx.x * 128 + (k)] = clock64() - p.dbg[blockIdx.x * 128 + 127]; \
+        }                                                                         \
+    }
+#define SVT_WSTAMP(slot) \
+    (p.dbg[blockIdx.x * 128 + (slot)] = clock64() - p.dbg[blockIdx.x * 128 + 127])
 
 __device__ __forceinline__ int64_t row_begin(const SmallParams& p, int c) {
     return p.per_cta * c + (c < p.extra ? c : p.extra);
@@ -123,6 +145,10 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async4_ids(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
 }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -241,6 +267,8 @@ __device__ __forceinline__ void row_dot_reg(const uint4* w, const float (&hv)[CP
 
 // CPL > 0: h lives in registers (CPL chunks per lane); CPL == 0: h is read
 // from shared memory (wide rows).
+// (15 warps: one SM sub-partition keeps room for the finalize warp, so it can
+// be resident next to a rows CTA without capping the rows kernel's registers)
 template <int DT, int CPL>
 __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p) {
     extern __shared__ __align__(128) uint8_t dsmem[];
@@ -248,39 +276,52 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
     __shared__ float s_wL[kWarps];
     __shared__ uint2 s_wc[kWarpCand][kWarps];
     __shared__ unsigned s_wn[kWarps];
-    __shared__ unsigned s_n, s_ovf, s_bad, s_last, s_nwork;
+    __shared__ unsigned s_n, s_ovf, s_bad;
     __shared__ uint32_t s_ids[kIdCache];
-    __shared__ unsigned long long s_key;
 
     SVT_STAMP(0);
     if (p.variant == 1) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = gridDim.x, c = blockIdx.x;
+    const int c = blockIdx.x;
     const int64_t r0 = row_begin(p, c), r1 = row_begin(p, c + 1);
     const int64_t nrows = r1 - r0;
     const int NS = p.slots;
     const uint32_t rb = static_cast<uint32_t>(p.row_bytes);
     const size_t ring_bytes = static_cast<size_t>(NS) * rb;
     uint8_t* ring = dsmem;
-    float* s_h = reinterpret_cast<float*>(
-        dsmem + (ring_bytes > 16 * 2 * kPiece + kMaxCand * 4 ? ring_bytes
-                                                             : 16 * 2 * kPiece + kMaxCand * 4));
-    const uint64_t pol = policy_evict_first();
+    float* s_h = reinterpret_cast<float*>(dsmem + ring_bytes);
+    // L2 policy of the weight stream: evict-first by default (the rows are
+    // streamed once per step); SVT_ROWS_L2=normal keeps them for the next step
+    const uint64_t pol = p.l2_keep ? policy_evict_last() : policy_evict_first();
     auto issue = [&](int64_t i) {
         const int slot = static_cast<int>(i % NS);
         mbar_arrive_expect_tx(&s_full[slot], rb);
         bulk_g2s(ring + static_cast<size_t>(slot) * rb, row_ptr(p, r0 + i), rb, &s_full[slot],
                  pol);
     };
-    // Slot s belongs to warp s % 16 for the whole launch (rows s, s+NS, ...):
+    // Slot s belongs to warp s % kWarps for the whole launch (rows s, s+NS, ...):
     // its lane 0 initialises the slot's barrier, issues its copies, and the
-    // warp consumes its phases in order (NS is a multiple of 16 whenever slots
-    // are refilled, or < 16: fewer consumer warps). No CTA barrier needed.
+    // warp consumes its phases in order (NS is a multiple of kWarps whenever
+    // slots are refilled, or < kWarps: fewer consumer warps). No CTA barrier.
     // With SVT_ROWS_WEIGHTS_STABLE the caller guarantees the rows were not
     // written by the kernel this launch depends on (programmatically), so the
     // first wave of copies goes out before griddepcontrol.wait and overlaps
     // the previous kernel's tail; otherwise it waits like every other read.
     const bool early = (p.flags & SVT_ROWS_WEIGHTS_STABLE) != 0;
+    // remap ids of this CTA's rows (read at record time, after a CTA barrier):
+    // asynchronous copies, so no thread stalls on them; stable ids go out
+    // before the dependency wait as well
+    auto fetch_ids = [&]() {
+        if (p.plan_ids) {
+            for (int i = tid; i < nrows && i < kIdCache; i += kThreads)
+                cp_async4_ids(&s_ids[i], p.plan_ids + r0 + i);
+            cp_async_commit();
+        } else {
+            for (int i = tid; i < nrows && i < kIdCache; i += kThreads)
+                s_ids[i] = p.row_base + static_cast<uint32_t>(r0 + i);
+        }
+    };
+    if (early) fetch_ids();
     if (lane == 0) {
         for (int sl = warp; sl < NS; sl += kWarps) mbar_init(&s_full[sl], 1);
         fence_mbar_init();
@@ -294,8 +335,11 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
-    if (!early && lane == 0)
-        for (int64_t i = warp; i < nrows && i < NS; i += kWarps) issue(i);
+    if (!early) {
+        if (lane == 0)
+            for (int64_t i = warp; i < nrows && i < NS; i += kWarps) issue(i);
+        fetch_ids();
+    }
     SVT_STAMP(1);
     constexpr int E = Chunk<DT>::E;
     constexpr int CR = CPL > 0 ? CPL : 1;
@@ -315,14 +359,11 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
             }
         }
     }
-    // h is also staged in shared memory (the smem-h path, overflow rescans and
-    // the tail's exact recompute); nobody waits for it on the register path
-    for (int e = tid * 4; e < p.dim; e += kThreads * 4)
-        *reinterpret_cast<float4*>(s_h + e) = __ldg(reinterpret_cast<const float4*>(p.h + e));
-    // remap ids of this CTA's rows (read at record time, after a CTA barrier)
-    for (int i = tid; i < nrows && i < kIdCache; i += kThreads)
-        s_ids[i] = p.plan_ids ? __ldg(p.plan_ids + r0 + i) : p.row_base + static_cast<uint32_t>(r0 + i);
-    if constexpr (CPL == 0) __syncthreads();
+    if constexpr (CPL == 0) {  // wide rows: h from shared memory
+        for (int e = tid * 4; e < p.dim; e += kThreads * 4)
+            *reinterpret_cast<float4*>(s_h + e) = __ldg(reinterpret_cast<const float4*>(p.h + e));
+        __syncthreads();
+    }
     SVT_STAMP(2);
 
     // ---- stream: one row per warp at a time ------------------------------------
@@ -337,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
         const int slot = static_cast<int>(i % NS);
         mbar_wait_parity(&s_full[slot], static_cast<uint32_t>((i / NS) & 1));
         const int dbg_k = static_cast<int>(i / kWarps);
-        if (p.dbg && lane == 0 && dbg_k < 3) p.dbg[blockIdx.x * 128 + 8 + warp * 6 + dbg_k * 2] = gtimer();
+        if (p.dbg && lane == 0 && dbg_k < 3) SVT_WSTAMP(8 + warp * 6 + dbg_k * 2);
         if (p.variant == 2) {
             if (lane == 0 && i + NS < nrows) issue(i + NS);
             continue;
@@ -349,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
         else
             row_dot<DT>(wrow, s_h, p.nchunks, lane, f, a);
         __syncwarp();  // every lane is done with the slot
-        if (p.dbg && lane == 0 && dbg_k < 3) p.dbg[blockIdx.x * 128 + 9 + warp * 6 + dbg_k * 2] = gtimer();
+        if (p.dbg && lane == 0 && dbg_k < 3) SVT_WSTAMP(9 + warp * 6 + dbg_k * 2);
         if (lane == 0) {
             if (i + NS < nrows) issue(i + NS);
             if (!isfinite(f) || !isfinite(a)) wbad = 1;
@@ -381,7 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
             }
         }
     }
-    if (p.dbg && lane == 0) atomicMax(&p.dbg[blockIdx.x * 128 + 3], gtimer());
+    if (p.dbg && lane == 0)
+        atomicMax(&p.dbg[blockIdx.x * 128 + 3], clock64() - p.dbg[blockIdx.x * 128 + 127]);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // this thread's id copies landed
     if (lane == 0) {
         s_wL[warp] = wL;
         s_wn[warp] = wovf ? kOverflow : ncand;
@@ -437,169 +480,166 @@ __global__ void __launch_bounds__(kThreads, 1) greedy_rows_kernel(SmallParams p)
                         __shfl_sync(0xFFFFFFFFu, e1.z, l1), 0u);
         if (lane == 0) {
             uint4* rp = reinterpret_cast<uint4*>(p.rec + c);
-            rp[0] = make_uint4(__float_as_uint(L), ovf ? kOverflow : cnt, e0.x, e0.y);
+            rp[0] = make_uint4(__float_as_uint(L), s_bad ? kBad : (ovf ? kOverflow : cnt), e0.x,
+                               e0.y);
             rp[1] = make_uint4(e0.z, e1.x, e1.y, e1.z);
-            s_ovf = ovf;
-            if (s_bad) atomicOr(&p.ctrl[2], 1u);
         }
     }
-    __syncthreads();
-    if (s_ovf) {  // rare: make every row's hi (written by lane 0s) visible for the rescan
-        __threadfence();
-        __syncthreads();
-    }
+    // Records, candidate lists and the rescan array become visible to the
+    // finalize grid through grid completion (its griddepcontrol.wait): no
+    // fence and no ticket here.
     SVT_STAMP(4);
-    if (tid == 0) s_last = atom_add_acq_rel_u32(&p.ctrl[0], 1u) == static_cast<unsigned>(G - 1);
-    __syncthreads();
-    SVT_STAMP(5);
-    if (!s_last) return;
-    if (p.variant >= 2) {
-        if (tid == 0) {
-            p.ctrl[0] = 0u;
-            p.ctrl[2] = 0u;
-        }
-        return;
-    }
+}
 
-    // ---------------- tail: the last CTA ----------------
-    unsigned* s_list = reinterpret_cast<unsigned*>(dsmem);  // the ring is drained
-    if (warp == 0) {
-        const bool bad = __ldcg(&p.ctrl[2]) != 0;
-        constexpr int kPer = kMaxGrid / 32;
-        uint4 ra[kPer], rb2[kPer];
-        float lmax = -FLT_MAX;
+// ---- finalize: one warp, launched as a programmatic dependent of the rows
+// kernel. It triggers its own dependents first (the next decode step's rows
+// kernel may be scheduled and stream its weights while this runs), waits for
+// the rows grid, then reduces the CTA records: L = max L_c; the rows with
+// hi >= L are the only possible reference argmax. One row: its remapped id is
+// already in the record. Otherwise (non-finite values, several candidates,
+// or an exact logit / shard record requested) the candidates are recomputed
+// in the reference order and reduced with the reference's rules.
+template <int DT>
+__global__ void __launch_bounds__(32, 16) greedy_rows_finalize_kernel(SmallParams p) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    extern __shared__ __align__(128) uint8_t fsmem[];
+    __shared__ unsigned s_n;
+    const int lane = threadIdx.x;
+    const int G = p.grid;
+    unsigned* s_list = reinterpret_cast<unsigned*>(fsmem);                  // [kMaxCand]
+    uint8_t* s_buf = fsmem + kMaxCand * 4;                                  // 2 pieces
+    float* s_h = reinterpret_cast<float*>(fsmem + kMaxCand * 4 + 2 * kPiece);  // [dim]
+    if (lane == 0) s_n = 0;
+    __syncwarp();
+    constexpr int kPer = kMaxGrid / 32;
+    uint4 ra[kPer], rb2[kPer];
+    float lmax = -FLT_MAX;
+    bool bad = false;
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int cc = lane + 32 * q;
-            ra[q] = make_uint4(__float_as_uint(-FLT_MAX), 0u, 0u, 0u);
-            rb2[q] = make_uint4(0u, 0u, 0u, 0u);
-            if (32 * q < G && cc < G) {
-                const uint4* rp = reinterpret_cast<const uint4*>(p.rec + cc);
-                ra[q] = __ldcg(rp);
-                rb2[q] = __ldcg(rp + 1);
-            }
-            lmax = fmaxf(lmax, __uint_as_float(ra[q].x));
+    for (int q = 0; q < kPer; ++q) {
+        const int cc = lane + 32 * q;
+        ra[q] = make_uint4(__float_as_uint(-FLT_MAX), 0u, 0u, 0u);
+        rb2[q] = make_uint4(0u, 0u, 0u, 0u);
+        if (32 * q < G && cc < G) {
+            const uint4* rp = reinterpret_cast<const uint4*>(p.rec + cc);
+            ra[q] = rp[0];
+            rb2[q] = rp[1];
         }
+        lmax = fmaxf(lmax, __uint_as_float(ra[q].x));
+        bad = bad || ra[q].y == kBad;
+    }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xFFFFFFFFu, lmax, o));
-        const float L = lmax;
-        SVT_STAMP(7);
-        // inline candidates with hi >= L; records with > 2 (or overflow) need a
-        // second look
-        unsigned total = 0, big = 0;
+    for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xFFFFFFFFu, lmax, o));
+    bad = __any_sync(0xFFFFFFFFu, bad);
+    const float L = lmax;
+    if (p.dbg && lane == 0) p.dbg[125] = gtimer();  // finalize: records reduced
+    // inline candidates with hi >= L; records with > 2 (or overflow) need a
+    // second look
+    unsigned total = 0, big = 0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        const unsigned cnt = ra[q].y;
+        const bool b0 = cnt >= 1 && cnt <= 2 && __uint_as_float(ra[q].w) >= L;
+        const bool b1 = cnt == 2 && __uint_as_float(rb2[q].z) >= L;
+        total += __popc(__ballot_sync(0xFFFFFFFFu, b0)) + __popc(__ballot_sync(0xFFFFFFFFu, b1));
+        big |= __ballot_sync(0xFFFFFFFFu, cnt > 2);
+    }
+    const bool want_exact = p.out_max || p.out_key;
+    unsigned nw_code = 0;
+    if (!bad && !big && total == 1 && !want_exact) {
+        // the single candidate is the reference argmax: its id is inline
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const unsigned cnt = ra[q].y;
             const bool b0 = cnt >= 1 && cnt <= 2 && __uint_as_float(ra[q].w) >= L;
             const bool b1 = cnt == 2 && __uint_as_float(rb2[q].z) >= L;
-            total += __popc(__ballot_sync(0xFFFFFFFFu, b0)) + __popc(__ballot_sync(0xFFFFFFFFu, b1));
-            big |= __ballot_sync(0xFFFFFFFFu, cnt > 2);
+            if (b0) *p.out_id = rb2[q].x;
+            if (b1) *p.out_id = rb2[q].w;
         }
-            if (!bad && !big && total == 1 && !p.out_max && !p.out_key) {
-            // the single candidate is the reference argmax: its id is inline
+    } else {
+        // general path: every candidate row into the shared list
+        if (!bad) {
 #pragma unroll
             for (int q = 0; q < kPer; ++q) {
+                const int cc = lane + 32 * q;
+                if (32 * q >= G || cc >= G) continue;
                 const unsigned cnt = ra[q].y;
-                const bool b0 = cnt >= 1 && cnt <= 2 && __uint_as_float(ra[q].w) >= L;
-                const bool b1 = cnt == 2 && __uint_as_float(rb2[q].z) >= L;
-                if (b0) *p.out_id = rb2[q].x;
-                if (b1) *p.out_id = rb2[q].w;
-            }
-            if (lane == 0) s_nwork = 0;
-                } else {
-            // general path: every candidate row into the shared list
-            if (!bad) {
-#pragma unroll
-                for (int q = 0; q < kPer; ++q) {
-                    const int cc = lane + 32 * q;
-                    if (32 * q >= G || cc >= G) continue;
-                    const unsigned cnt = ra[q].y;
-                    if (cnt >= 1 && cnt <= 2) {
-                        if (__uint_as_float(ra[q].w) >= L) {
+                if (cnt >= 1 && cnt <= 2) {
+                    if (__uint_as_float(ra[q].w) >= L) {
+                        const unsigned k = atomicAdd(&s_n, 1u);
+                        if (k < kMaxCand) s_list[k] = ra[q].z;
+                    }
+                    if (cnt == 2 && __uint_as_float(rb2[q].z) >= L) {
+                        const unsigned k = atomicAdd(&s_n, 1u);
+                        if (k < kMaxCand) s_list[k] = rb2[q].y;
+                    }
+                } else if (cnt == kOverflow) {
+                    const int64_t a0 = row_begin(p, cc), a1 = row_begin(p, cc + 1);
+                    for (int64_t r = a0; r < a1; ++r)
+                        if (p.ws_hi[r] >= L) {
                             const unsigned k = atomicAdd(&s_n, 1u);
-                            if (k < kMaxCand) s_list[k] = ra[q].z;
+                            if (k < kMaxCand) s_list[k] = static_cast<unsigned>(r);
                         }
-                        if (cnt == 2 && __uint_as_float(rb2[q].z) >= L) {
+                } else if (cnt > 2) {
+                    for (unsigned e = 0; e < cnt; ++e) {
+                        const uint2 ce = p.gcand[cc * kCapG + e];
+                        if (__uint_as_float(ce.y) >= L) {
                             const unsigned k = atomicAdd(&s_n, 1u);
-                            if (k < kMaxCand) s_list[k] = rb2[q].y;
-                        }
-                    } else if (cnt == kOverflow) {
-                        const int64_t a0 = row_begin(p, cc), a1 = row_begin(p, cc + 1);
-                        for (int64_t r = a0; r < a1; ++r)
-                            if (__ldcg(p.ws_hi + r) >= L) {
-                                const unsigned k = atomicAdd(&s_n, 1u);
-                                if (k < kMaxCand) s_list[k] = static_cast<unsigned>(r);
-                            }
-                    } else if (cnt > 2) {
-                        for (unsigned e = 0; e < cnt; ++e) {
-                            const uint2 ce = __ldcg(p.gcand + cc * kCapG + e);
-                            if (__uint_as_float(ce.y) >= L) {
-                                const unsigned k = atomicAdd(&s_n, 1u);
-                                if (k < kMaxCand) s_list[k] = ce.x;
-                            }
+                            if (k < kMaxCand) s_list[k] = ce.x;
                         }
                     }
                 }
             }
-            __syncwarp();
+        }
+        __syncwarp();
+        const unsigned n = s_n;
+        const bool all = bad || n == 0 || n > static_cast<unsigned>(kMaxCand);
+        if (!all && n == 1 && !want_exact) {  // one row left after the global bar
             if (lane == 0) {
-                const unsigned n = s_n;
-                const bool all = bad || n == 0 || n > static_cast<unsigned>(kMaxCand);
-                if (!all && n == 1 && !p.out_max && !p.out_key) {  // one row left after the bar
-                    const uint32_t r = s_list[0];
-                    *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
-                    s_nwork = 0;
-                } else {
-                    s_nwork = all ? 0xFFFFFFFFu : n;
+                const uint32_t r = s_list[0];
+                *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+            }
+        } else {
+            nw_code = all ? 0xFFFFFFFFu : n;
+            // exact recompute of the candidates (every row when `all`)
+            for (int e = lane * 4; e < p.dim; e += 32 * 4)
+                *reinterpret_cast<float4*>(s_h + e) =
+                    __ldg(reinterpret_cast<const float4*>(p.h + e));
+            __syncwarp();
+            const int64_t nwork = all ? p.n : static_cast<int64_t>(n);
+            unsigned long long best = 0ull;
+            for (int64_t i = 0; i < nwork; ++i) {
+                const int64_t r = all ? i : static_cast<int64_t>(s_list[i]);
+                const float v = exact_row_warp<DT>(row_ptr(p, r), p.row_bytes, s_h, s_buf, lane);
+                const unsigned long long key =
+                    make_key(v, static_cast<uint32_t>(r), true, p.plan_start && r == 0);
+                best = key > best ? key : best;
+            }
+            if (lane == 0) {
+                const unsigned long long k = best;
+                const uint32_t r = 0xFFFFFFFFu - static_cast<uint32_t>(k);
+                uint32_t id = 0xFFFFFFFFu;
+                float mx = __int_as_float(0x7FC00000);
+                unsigned long long gk = 0ull;  // key over the global row order (shard combine)
+                if (k != 0ull) {  // (k == 0: every row NaN and plan row 0 not in this slice)
+                    id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+                    if (k != kNanRow0Key) mx = float_of_ord(static_cast<uint32_t>(k >> 32));
+                    gk = k == kNanRow0Key
+                             ? k
+                             : (k & 0xFFFFFFFF00000000ull) | (0xFFFFFFFFu - (p.row_base + r));
                 }
-                s_key = 0ull;
+                *p.out_id = id;
+                if (p.out_max) *p.out_max = mx;
+                if (p.out_key)
+                    *p.out_key = make_uint4(static_cast<uint32_t>(gk),
+                                            static_cast<uint32_t>(gk >> 32), id,
+                                            __float_as_uint(mx));
             }
         }
     }
-    __syncthreads();
-    const unsigned nw_code = s_nwork;
-    if (nw_code != 0) {
-        // exact recompute (s_h still holds h; per-warp pieces after s_list)
-        const bool all = nw_code == 0xFFFFFFFFu;
-        const int64_t nwork = all ? p.n : static_cast<int64_t>(nw_code);
-        uint8_t* s_buf = dsmem + kMaxCand * 4;
-        unsigned long long best = 0ull;
-        for (int64_t i = warp; i < nwork; i += kWarps) {
-            const int64_t r = all ? i : static_cast<int64_t>(s_list[i]);
-            const float v = exact_row_warp<DT>(row_ptr(p, r), p.row_bytes, s_h,
-                                               s_buf + warp * 2 * kPiece, lane);
-            const unsigned long long key =
-                make_key(v, static_cast<uint32_t>(r), true, p.plan_start && r == 0);
-            best = key > best ? key : best;
-        }
-        if (lane == 0) atomicMax(&s_key, best);
-        __syncthreads();
-        if (tid == 0) {
-            const unsigned long long k = s_key;
-            const uint32_t r = 0xFFFFFFFFu - static_cast<uint32_t>(k);
-            uint32_t id = 0xFFFFFFFFu;
-            float mx = __int_as_float(0x7FC00000);
-            unsigned long long gk = 0ull;  // key over the global row order (shard combine)
-            if (k != 0ull) {  // (k == 0: every row NaN and plan row 0 not in this slice)
-                id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
-                if (k != kNanRow0Key) mx = float_of_ord(static_cast<uint32_t>(k >> 32));
-                gk = k == kNanRow0Key
-                         ? k
-                         : (k & 0xFFFFFFFF00000000ull) | (0xFFFFFFFFu - (p.row_base + r));
-            }
-            *p.out_id = id;
-            if (p.out_max) *p.out_max = mx;
-            if (p.out_key)
-                *p.out_key = make_uint4(static_cast<uint32_t>(gk), static_cast<uint32_t>(gk >> 32),
-                                        id, __float_as_uint(mx));
-        }
-    }
-    SVT_STAMP(6);
-    if (tid == 0) {  // ready for the next call; {certified directly, recomputed}
-        p.ctrl[0] = 0u;
-        p.ctrl[2] = 0u;
-        p.ctrl[nw_code == 0 ? 4 : 5] += 1u;
-    }
+    if (p.dbg && lane == 0) p.dbg[126] = gtimer();  // finalize: done
+    if (lane == 0) p.ctrl[nw_code == 0 ? 4 : 5] += 1u;  // {certified directly, recomputed}
 }
 
 unsigned long long* g_rows_dbg = nullptr;
@@ -611,23 +651,36 @@ double gamma_n(double n) {
 
 template <int DT, int CPL>
 svt_status launch_rows(SmallParams p, int grid, cudaStream_t st) {
-    const size_t ring = static_cast<size_t>(p.slots) * static_cast<size_t>(p.row_bytes);
-    const size_t tail = 16 * 2 * kPiece + kMaxCand * 4;
-    const size_t smem = (ring > tail ? ring : tail) + static_cast<size_t>(p.dim) * 4;
+    const size_t smem = static_cast<size_t>(p.slots) * static_cast<size_t>(p.row_bytes) +
+                        static_cast<size_t>(p.dim) * 4;
     auto kern = greedy_rows_kernel<DT, CPL>;
     SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
+    p.grid = grid;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    // the one-warp finalize, a programmatic dependent of the rows grid
+    const size_t fsmem = kMaxCand * 4 + 2 * kPiece + static_cast<size_t>(p.dim) * 4;
+    auto fin = greedy_rows_finalize_kernel<DT>;
+    SVT_CUDA_TRY(cudaFuncSetAttribute(fin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(fsmem)));
+    cudaLaunchConfig_t fc = {};
+    fc.gridDim = dim3(1);
+    fc.blockDim = dim3(32);
+    fc.dynamicSmemBytes = fsmem;
+    fc.stream = st;
+    fc.attrs = attr;
+    fc.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&fc, fin, p));
     return SVT_OK;
 }
 
@@ -714,6 +767,7 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
     int grid = sm_count();
     if (const char* v = getenv("SVT_ROWS_GRID")) grid = atoi(v);
     if (const char* v = getenv("SVT_ROWS_VARIANT")) p.variant = atoi(v);
+    if (const char* v = getenv("SVT_ROWS_L2")) p.l2_keep = v[0] == 'k' || v[0] == 'l';
     grid = grid > kMaxGrid ? kMaxGrid : grid;
     if (static_cast<int64_t>(grid) > p.n) grid = static_cast<int>(p.n);
     if (grid < 1) grid = 1;
@@ -722,10 +776,16 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
     p.extra = static_cast<int32_t>(p.n % grid);
     int64_t slots = (kSmemBudget - static_cast<int64_t>(dim) * 4) / p.row_bytes;
     slots = slots > kMaxSlots ? kMaxSlots : slots;
-    if (slots >= per_cta)
+    if (slots >= per_cta) {
         slots = per_cta;  // every row in flight at once, no refills
-    else if (slots >= kWarps)
-        slots -= slots % kWarps;
+    } else {
+        slots = (kSmemBudgetRing - static_cast<int64_t>(dim) * 4) / p.row_bytes;
+        slots = slots > kMaxSlots ? kMaxSlots : slots;
+        if (slots >= per_cta)
+            slots = per_cta;
+        else if (slots >= kWarps)
+            slots -= slots % kWarps;
+    }
     p.slots = static_cast<int32_t>(slots < 1 ? 1 : slots);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // h in registers when a lane's share is <= 64 values
