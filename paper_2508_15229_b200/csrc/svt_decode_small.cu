@@ -523,8 +523,8 @@ __global__ void __launch_bounds__(32, 16) greedy_rows_finalize_kernel(SmallParam
         rb2[q] = make_uint4(0u, 0u, 0u, 0u);
         if (32 * q < G && cc < G) {
             const uint4* rp = reinterpret_cast<const uint4*>(p.rec + cc);
-            ra[q] = rp[0];
-            rb2[q] = rp[1];
+            ra[q] = __ldcg(rp);  // written by the rows grid: read at L2
+            rb2[q] = __ldcg(rp + 1);
         }
         lmax = fmaxf(lmax, __uint_as_float(ra[q].x));
         bad = bad || ra[q].y == kBad;
@@ -577,13 +577,13 @@ __global__ void __launch_bounds__(32, 16) greedy_rows_finalize_kernel(SmallParam
                 } else if (cnt == kOverflow) {
                     const int64_t a0 = row_begin(p, cc), a1 = row_begin(p, cc + 1);
                     for (int64_t r = a0; r < a1; ++r)
-                        if (p.ws_hi[r] >= L) {
+                        if (__ldcg(p.ws_hi + r) >= L) {
                             const unsigned k = atomicAdd(&s_n, 1u);
                             if (k < kMaxCand) s_list[k] = static_cast<unsigned>(r);
                         }
                 } else if (cnt > 2) {
                     for (unsigned e = 0; e < cnt; ++e) {
-                        const uint2 ce = p.gcand[cc * kCapG + e];
+                        const uint2 ce = __ldcg(p.gcand + cc * kCapG + e);
                         if (__uint_as_float(ce.y) >= L) {
                             const unsigned k = atomicAdd(&s_n, 1u);
                             if (k < kMaxCand) s_list[k] = ce.x;
@@ -639,7 +639,10 @@ __global__ void __launch_bounds__(32, 16) greedy_rows_finalize_kernel(SmallParam
         }
     }
     if (p.dbg && lane == 0) p.dbg[126] = gtimer();  // finalize: done
-    if (lane == 0) p.ctrl[nw_code == 0 ? 4 : 5] += 1u;  // {certified directly, recomputed}
+    // {certified directly, recomputed}: a fire-and-forget reduction, so the
+    // grid's completion (which the next step waits for) is not held by a
+    // load round trip
+    if (lane == 0) atomicAdd(&p.ctrl[nw_code == 0 ? 4 : 5], 1u);
 }
 
 unsigned long long* g_rows_dbg = nullptr;
