@@ -8,12 +8,16 @@
 //
 // Instead of sorting, one CTA finds the prefix by value:
 //   S(v) = sum of df over prunable ids with df < v is non-decreasing in v,
-//   so v* = max{v : S(v) <= B} (B = floor(budget)) is found by binary search
-//   over v (each probe a block-wide reduction over the candidate bitmap).
+//   so v* = max{v : S(v) <= B} (B = floor(budget)) is the smallest df value
+//   x with S(x) + x * count(x) > B. It is found by a 4-level radix select on
+//   the 32-bit df (8 bits per level, per-warp shared-memory histograms of df
+//   sums). Every level is one coalesced pass over the id range (df[id] and
+//   the candidate / protected words, prunable ids selected by bit tests).
 //   Every prunable id with df < v* is pruned; of the c* ids with df == v*,
 //   the first j = (B - S(v*)) / v* in id order are pruned too (j < c*, else
-//   v* was not maximal). The pruned list comes out ascending by id and
-//   kept = candidates \ pruned, in a second pass with a block-wide scan.
+//   v* was not maximal). A last pass over id chunks (8 consecutive ids per
+//   thread, block scans) writes the pruned ids ascending and
+//   kept = candidates \ pruned word by word.
 // Edge cases follow the reference's comparison: budget < 0 prunes nothing,
 // NaN / +inf budget prunes every prunable id; df beyond the df array is 0.
 #include <cmath>
@@ -24,6 +28,11 @@ namespace svt {
 namespace {
 
 constexpr int kTolThreads = 1024;
+constexpr int kTolWarps = kTolThreads / 32;
+constexpr int kItems = 8;  // consecutive ids per thread per output chunk
+constexpr int kChunk = kTolThreads * kItems;
+constexpr int kBuckets = 256;
+constexpr size_t kTolSmem = sizeof(unsigned long long) * kTolWarps * kBuckets;  // 64 KB
 
 struct TolParams {
     const uint64_t* cand;
@@ -40,23 +49,10 @@ struct TolParams {
 };
 
 __device__ __forceinline__ uint64_t df_of(const TolParams& p, int64_t id) {
-    return id < p.n_df ? static_cast<uint64_t>(p.df[id]) : 0ull;
+    return id < p.n_df ? static_cast<uint64_t>(__ldg(p.df + id)) : 0ull;
 }
 __device__ __forceinline__ uint64_t prunable_word(const TolParams& p, int64_t w) {
-    return p.cand[w] & ~(p.keep ? p.keep[w] : 0ull);
-}
-
-// block-wide sum of a u64 (every thread gets the total)
-__device__ uint64_t block_sum(uint64_t v, uint64_t* red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    uint64_t t = 0;
-    for (int i = 0; i < kTolThreads / 32; ++i) t += red[i];
-    return t;
+    return __ldg(p.cand + w) & ~(p.keep ? __ldg(p.keep + w) : 0ull);
 }
 
 // block-wide exclusive scan of a u64 per thread (thread order); returns the
@@ -73,7 +69,7 @@ __device__ uint64_t block_excl_scan(uint64_t v, uint64_t* red, uint64_t* total) 
     if (lane == 31) red[warp] = incl;
     __syncthreads();
     uint64_t before = 0, all = 0;
-    for (int i = 0; i < kTolThreads / 32; ++i) {
+    for (int i = 0; i < kTolWarps; ++i) {
         if (i < warp) before += red[i];
         all += red[i];
     }
@@ -81,114 +77,157 @@ __device__ uint64_t block_excl_scan(uint64_t v, uint64_t* red, uint64_t* total) 
     return before + incl - v;
 }
 
-__global__ void __launch_bounds__(kTolThreads, 1) tolerance_kernel(TolParams p) {
-    __shared__ uint64_t red[kTolThreads / 32];
-    const int t = threadIdx.x;
-    // contiguous word range per thread (ascending id order across threads)
-    const int64_t per = (p.nwords + kTolThreads - 1) / kTolThreads;
-    const int64_t w0 = min(p.nwords, per * t), w1 = min(p.nwords, w0 + per);
+// add d to this warp's bucket; when the whole warp agrees on the bucket (the
+// common case for skewed df) one lane adds the warp's sum, otherwise each
+// lane adds its own (64-bit shared atomics are CAS loops: avoid same-address
+// contention)
+__device__ __forceinline__ void hist_add(unsigned long long* mine, bool in, uint32_t bkt,
+                                         uint64_t d) {
+    const uint32_t inmask = __ballot_sync(0xFFFFFFFFu, in);
+    if (inmask == 0u) return;
+    const int lead = __ffs(inmask) - 1;
+    const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, bkt, lead);
+    if (__all_sync(0xFFFFFFFFu, !in || bkt == b0)) {
+        uint64_t v = in ? d : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if ((threadIdx.x & 31) == lead) atomicAdd(&mine[b0], static_cast<unsigned long long>(v));
+    } else if (in) {
+        atomicAdd(&mine[bkt], static_cast<unsigned long long>(d));
+    }
+}
 
-    // ---- v* by binary search on S(v) <= B ----------------------------------
-    uint64_t vstar;
+__global__ void __launch_bounds__(kTolThreads, 1) tolerance_kernel(TolParams p) {
+    extern __shared__ unsigned long long hist[];  // [warp][bucket] df sums
+    __shared__ uint64_t red[kTolWarps];
+    __shared__ uint64_t s_below;
+    __shared__ uint32_t s_prefix;
+    __shared__ int s_all;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t n_ids = p.nwords * 64;
+
+    // ---- v* by radix select over the df values --------------------------------
+    uint64_t vstar, S = 0;
     if (p.mode == 1) {
         vstar = 0;  // nothing fits (budget < 0)
     } else if (p.mode == 2) {
         vstar = 1ull << 33;  // everything fits (NaN / +inf budget)
     } else {
-        // S(v) is monotone; S(0) = 0 <= B. Search the largest v in [0, 2^32]
-        // (df values are u32; 2^32 means "every prunable id").
-        uint64_t lo = 0, hi = 1ull << 32;
-        while (lo < hi) {
-            const uint64_t mid = lo + (hi - lo + 1) / 2;
-            uint64_t s = 0;
-            for (int64_t w = w0; w < w1; ++w) {
-                uint64_t bits = prunable_word(p, w);
-                while (bits) {
-                    const int b = __ffsll(static_cast<long long>(bits)) - 1;
-                    bits &= bits - 1;
-                    const uint64_t d = df_of(p, w * 64 + b);
-                    if (d < mid) s += d;
+        if (t == 0) {
+            s_below = 0;
+            s_prefix = 0;
+            s_all = 0;
+        }
+        unsigned long long* mine = hist + warp * kBuckets;
+        for (int level = 0; level < 4; ++level) {
+            const int shift = 24 - 8 * level;
+            const uint64_t hi_mask =
+                level == 0 ? 0ull : (0xFFFFFFFFull << (shift + 8)) & 0xFFFFFFFFull;
+            for (int i = t; i < kTolWarps * kBuckets; i += kTolThreads) hist[i] = 0ull;
+            __syncthreads();
+            const uint64_t prefix = s_prefix;
+            // a warp covers 32 consecutive ids: one df line, one bitmap word
+            for (int64_t base = 0; base < n_ids; base += 4 * kTolThreads) {
+                uint64_t d[4];
+                bool in[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t id = base + k * kTolThreads + t;
+                    in[k] = id < n_ids && ((prunable_word(p, id >> 6) >> (id & 63)) & 1ull);
+                    d[k] = in[k] ? df_of(p, id) : 0ull;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool m = in[k] && (d[k] & hi_mask) == prefix;
+                    hist_add(mine, m, static_cast<uint32_t>((d[k] >> shift) & 0xFF), d[k]);
                 }
             }
-            s = block_sum(s, red);
-            if (s <= p.B)
-                lo = mid;
-            else
-                hi = mid - 1;
+            __syncthreads();
+            // fold the per-warp histograms; the first bucket whose sum crosses
+            // the remaining budget holds v*
+            if (t < kBuckets) {
+                unsigned long long sum = 0;
+                for (int w = 0; w < kTolWarps; ++w) sum += hist[w * kBuckets + t];
+                hist[t] = sum;  // (warp 0's row; only thread t touches column t)
+            }
+            __syncthreads();
+            if (t == 0) {
+                uint64_t below = s_below;
+                int pick = -1;
+                for (int b = 0; b < kBuckets; ++b) {
+                    if (below + hist[b] > p.B) {
+                        pick = b;
+                        break;
+                    }
+                    below += hist[b];
+                }
+                if (pick < 0)
+                    s_all = 1;  // (only at level 0) every prunable id fits
+                else
+                    s_prefix =
+                        static_cast<uint32_t>(prefix | (static_cast<uint64_t>(pick) << shift));
+                s_below = below;
+            }
+            __syncthreads();
+            if (s_all) break;
         }
-        vstar = lo;
+        vstar = s_all ? (1ull << 32) : static_cast<uint64_t>(s_prefix);
+        S = s_below;
     }
-    // S(v*) and c* = |{df == v*}|
-    uint64_t s_lt = 0, c_eq = 0;
-    for (int64_t w = w0; w < w1; ++w) {
-        uint64_t bits = prunable_word(p, w);
-        while (bits) {
-            const int b = __ffsll(static_cast<long long>(bits)) - 1;
-            bits &= bits - 1;
-            const uint64_t d = df_of(p, w * 64 + b);
-            s_lt += d < vstar ? d : 0;
-            c_eq += d == vstar ? 1 : 0;
-        }
-    }
-    const uint64_t S = block_sum(s_lt, red);
+    // j ids with df == v* are pruned too (v* > 0 whenever it bounds the cut:
+    // a crossing bucket has a positive sum)
     uint64_t j = 0;
-    if (p.mode == 0 && vstar <= 0xFFFFFFFFull && vstar > 0) {
-        const uint64_t room = (p.B - S) / vstar;
-        j = room;  // < c* by maximality of v*
-    }
-    // ---- outputs: ids with df < v*, plus the first j with df == v* ----------
-    uint64_t total_eq = 0;
-    const uint64_t eq_before = block_excl_scan(c_eq, red, &total_eq);
-    if (j > total_eq) j = total_eq;
-    // pruned count of this thread's range
-    uint64_t mine = 0;
-    {
-        uint64_t eq_seen = eq_before;
-        for (int64_t w = w0; w < w1; ++w) {
-            uint64_t bits = prunable_word(p, w);
-            while (bits) {
-                const int b = __ffsll(static_cast<long long>(bits)) - 1;
-                bits &= bits - 1;
-                const uint64_t d = df_of(p, w * 64 + b);
-                if (d < vstar) {
-                    ++mine;
-                } else if (d == vstar) {
-                    mine += eq_seen < j ? 1 : 0;
-                    ++eq_seen;
-                }
+    if (p.mode == 0 && vstar <= 0xFFFFFFFFull && vstar > 0) j = (p.B - S) / vstar;
+
+    // ---- outputs: pruned ids (ascending) and kept words -------------------------
+    uint64_t out_at = 0, eq_seen = 0, dsum = 0;
+    for (int64_t base = 0; base < n_ids; base += kChunk) {
+        const int64_t id0 = base + static_cast<int64_t>(t) * kItems;  // 8 ids in one word
+        const uint64_t cw = id0 < n_ids ? __ldg(p.cand + (id0 >> 6)) : 0ull;
+        const uint64_t pw = id0 < n_ids ? prunable_word(p, id0 >> 6) : 0ull;
+        const uint32_t pbits = static_cast<uint32_t>((pw >> (id0 & 63)) & 0xFFu);
+        uint64_t d[kItems];
+        uint32_t n_eq = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            d[k] = (pbits >> k) & 1u ? df_of(p, id0 + k) : 0ull;
+            n_eq += ((pbits >> k) & 1u) && d[k] == vstar ? 1u : 0u;
+        }
+        uint64_t eq_tot = 0;
+        uint64_t eq_rank = eq_seen + block_excl_scan(n_eq, red, &eq_tot);
+        uint32_t cut = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            if (!((pbits >> k) & 1u)) continue;
+            if (d[k] < vstar) {
+                cut |= 1u << k;
+            } else if (d[k] == vstar) {
+                if (eq_rank < j) cut |= 1u << k;
+                ++eq_rank;
             }
         }
-    }
-    uint64_t total_pruned = 0;
-    uint64_t at = block_excl_scan(mine, red, &total_pruned);
-    {
-        uint64_t eq_seen = eq_before;
-        for (int64_t w = w0; w < w1; ++w) {
-            const uint64_t cand = p.cand[w];
-            uint64_t bits = prunable_word(p, w);
-            uint64_t pr = 0;
-            while (bits) {
-                const int b = __ffsll(static_cast<long long>(bits)) - 1;
-                bits &= bits - 1;
-                const uint64_t d = df_of(p, w * 64 + b);
-                bool cut = false;
-                if (d < vstar) {
-                    cut = true;
-                } else if (d == vstar) {
-                    cut = eq_seen < j;
-                    ++eq_seen;
-                }
-                if (cut) {
-                    pr |= 1ull << b;
-                    p.pruned[at++] = static_cast<uint32_t>(w * 64 + b);
-                }
+        uint64_t cut_tot = 0;
+        uint64_t pos = out_at + block_excl_scan(__popc(cut), red, &cut_tot);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+            if ((cut >> k) & 1u) {
+                p.pruned[pos++] = static_cast<uint32_t>(id0 + k);
+                dsum += d[k];
             }
-            p.kept[w] = cand & ~pr;
-        }
+        // the word's pruned mask from its 8 threads (lanes 8q .. 8q+7)
+        uint64_t pm = static_cast<uint64_t>(cut) << (id0 & 63);
+        pm |= __shfl_xor_sync(0xFFFFFFFFu, pm, 1);
+        pm |= __shfl_xor_sync(0xFFFFFFFFu, pm, 2);
+        pm |= __shfl_xor_sync(0xFFFFFFFFu, pm, 4);
+        if ((lane & 7) == 0 && id0 < n_ids) p.kept[id0 >> 6] = cw & ~pm;
+        out_at += cut_tot;
+        eq_seen += eq_tot;
     }
+    uint64_t dsum_tot = 0;
+    block_excl_scan(dsum, red, &dsum_tot);
     if (t == 0) {
-        *p.n_pruned = static_cast<int64_t>(total_pruned);
-        *p.df_sum = S + j * (vstar <= 0xFFFFFFFFull ? vstar : 0ull);
+        *p.n_pruned = static_cast<int64_t>(out_at);
+        *p.df_sum = dsum_tot;
     }
 }
 
@@ -232,7 +271,9 @@ extern "C" svt_status svt_tolerance_filter(const uint64_t* d_candidate_words,
         p.mode = 0;
         p.B = static_cast<uint64_t>(std::floor(budget));
     }
-    tolerance_kernel<<<1, kTolThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+    SVT_CUDA_TRY(cudaFuncSetAttribute(tolerance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kTolSmem)));
+    tolerance_kernel<<<1, kTolThreads, kTolSmem, static_cast<cudaStream_t>(stream)>>>(p);
     SVT_LAUNCH_CHECK("tolerance_kernel");
     return SVT_OK;
 }

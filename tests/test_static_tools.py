@@ -82,10 +82,12 @@ def test_oracle_tolerance_matches_reference():
     assert st == tol(ORC, "orc_", words_of([1], 8), None, 8, np.ones(8, np.uint32), 0, 0.5)[0] == 2
 
 
-def profile_docs(rng, V, n, bad=None):
+def profile_docs(rng, V, n, bad=None, long_every=0):
     docs = []
     for d in range(n):
         li, lo = int(rng.integers(0, 300)), int(rng.integers(1, 200))
+        if long_every and d % long_every == 0:  # past the register-staged size
+            li, lo = int(rng.integers(1000, 3000)), int(rng.integers(500, 1500))
         pool = rng.integers(0, V, 64)  # shared ids make copies likely
         inp = np.where(rng.random(li) < 0.5, rng.choice(pool, li), rng.integers(0, V, li))
         out = np.where(rng.random(lo) < 0.5, rng.choice(pool, lo), rng.integers(0, V, lo))
@@ -193,6 +195,19 @@ def test_gpu_tolerance_filter_matches_oracle():
         c.words[:] = words_of(cand, U)
         r = corpus.tolerance_filter(c, df, 200000, tau)
         assert np.array_equal(r.pruned, pruned) and r.pruned_df_sum == s
+    # df values across the whole u32 range (every radix level picks a
+    # non-zero digit) with a large budget; sums stay below 2^53
+    U = 70000
+    cand = np.unique(rng.integers(0, U, 40000))
+    df = rng.integers(0, 2**32, U, dtype=np.uint64).astype(np.uint32)
+    df[::7] = rng.integers(0, 300, df[::7].size).astype(np.uint32)
+    for M, tau in ((10**9, 1e-3), (10**9, 7.0), (10**12, 0.5), (10**15, 1.0)):
+        st, kept, pruned, s = tol(ORC, "orc_", words_of(cand, U), None, U, df, M, tau)
+        c = TokenSet(U)
+        c.words[:] = words_of(cand, U)
+        r = corpus.tolerance_filter(c, df, M, tau)
+        assert np.array_equal(r.pruned, pruned) and r.pruned_df_sum == s, (M, tau)
+        assert np.array_equal(r.kept.words, kept[: r.kept.words.size])
     with pytest.raises(corpus.ConfigError):
         corpus.tolerance_filter(TokenSet(8), np.zeros(8, np.uint32), 0, 0.5)
 
@@ -211,6 +226,15 @@ def test_gpu_profiler_matches_oracle():
         got = [(s.doc_index, s.distinct_input, s.overlap_occurrence, s.overlap_distinct)
                for s in p.per_doc]
         assert got == stats  # doubles compared exactly
+    # long documents (the global-memory path) interleaved with short ones
+    for V in (3000, 151936):
+        docs = profile_docs(rng, V, 90, long_every=4)
+        st, (df, iu, ou, stats) = orc_profile(V, docs)
+        p = corpus.profile([corpus.Document(a, b, i) for a, b, i in docs], V)
+        assert np.array_equal(p.df, df)
+        assert np.array_equal(p.input_union.words, iu) and np.array_equal(p.output_union.words, ou)
+        assert [(s.doc_index, s.distinct_input, s.overlap_occurrence, s.overlap_distinct)
+                for s in p.per_doc] == stats
     # shard merge == one profile of all documents; duplicates rejected
     docs = profile_docs(np.random.default_rng(8), 5000, 40)
     a = corpus.profile([corpus.Document(*d) for d in docs[:15]], 5000)
@@ -230,3 +254,13 @@ def test_gpu_profiler_matches_oracle():
     with pytest.raises(corpus.IntegrityError,
                        match=f"document {docs[4][2]}: input token id 6000 out of range"):
         corpus.profile(bad[4:], 5000)
+    # errors inside long documents: the first offending position wins
+    li = np.arange(2500, dtype=np.uint32) % 5000
+    lo = np.arange(1200, dtype=np.uint32) % 5000
+    li2, lo2 = li.copy(), lo.copy()
+    lo2[900], lo2[1100] = 7001, 7002
+    with pytest.raises(corpus.IntegrityError, match="output token id 7001 out of range"):
+        corpus.profile([corpus.Document(li, lo, 0), corpus.Document(li2, lo2, 1)], 5000)
+    li2[2100], li2[2300] = 8001, 8002
+    with pytest.raises(corpus.IntegrityError, match="input token id 8001 out of range"):
+        corpus.profile([corpus.Document(li, lo, 0), corpus.Document(li2, lo2, 1)], 5000)
