@@ -678,6 +678,13 @@ def prefill_fused():
     return os.environ.get("SVT_PREFILL_FUSED", "0") != "0"
 
 
+def prefill_split():
+    """cfg3 gathered scorer: the static rows shared by every sequence are
+    gathered once and only each plan's dynamic rows per sequence (default;
+    SVT_PREFILL_SPLIT=0 gathers every plan row per sequence)."""
+    return not prefill_fused() and os.environ.get("SVT_PREFILL_SPLIT", "1") != "0"
+
+
 def prefill_setup(S, rank, torch, th, synth):
     """cfg3 inputs on the device: bf16 head, static bitmap, S prompts of 2048
     ids, S x 2048 bf16 hidden states; plans selected on the device and the
@@ -693,7 +700,8 @@ def prefill_setup(S, rank, torch, th, synth):
     flat = np.concatenate(prompts)
     tb = th.TailoredBatch.build(torch.from_numpy(words_h.view(np.int64)).cuda(), CFG3["static"],
                                 V, torch.from_numpy(flat.view(np.int32)).cuda(), off)
-    sc = prefill.PrefillScorer.from_batch(head, tb, P, fused=prefill_fused())
+    sc = prefill.PrefillScorer.from_batch(head, tb, P, fused=prefill_fused(),
+                                          split=prefill_split())
     hid = torch.empty(S * P * d, dtype=torch.bfloat16, device="cuda")
     th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_BF16, th.SVT_BF16,
                  rank * S * P * d, S * P * d, synth.SEED_H, None)
@@ -780,6 +788,9 @@ def run_prefill(args, torch, dist, world, rank):
                    "prompt_len": CFG3["prompt_len"], "mean_plan_rows": float(n_rows.mean()),
                    "step": ("select + layout + tcgen05 scoring with the plan rows gathered "
                             "by TMA tile::gather4 inside the GEMM" if prefill_fused() else
+                            "select + static/dynamic split + gather of the static rows once "
+                            "and of each plan's dynamic rows + tcgen05 scoring"
+                            if prefill_split() else
                             "select + layout + row-major gather + tcgen05 scoring") +
                            " with certified reference-exact ids; tokens = scored positions",
                    "parallelism": f"batch-shard x{world}",

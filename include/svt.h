@@ -367,6 +367,41 @@ svt_status svt_prefill_score_fused(const void* d_hidden, const void* d_head, int
                                    int32_t sequences, int32_t positions, int32_t dim,
                                    uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
                                    svt_stream stream);
+/* Static/dynamic split of hybrid plans (plan = T ∪ D_s, selector.cpp:16-43).
+ * svt_prefill_split_plans turns the capacity-CSR plans of
+ * svt_select_batched (d_active_ids at d_act_off[s], d_n_active[s] ids) and
+ * the static set (bitmap d_static_words over `universe` ids, its ascending ids
+ * d_static_ids[n_static]) into:
+ *   d_dyn_ids   the plan ids not in T, in plan order, at d_act_off[s]
+ *               (capacity layout of the plans; count d_n_dyn[s]);
+ *   d_vids      the virtual plan [T, padding to nTp = svt_prefill_static_pad
+ *               (n_static), D_s \ T] at d_vid_offsets[s] = d_act_off[s] +
+ *               s * nTp (capacity d_act_off[S] + S * nTp);
+ *   d_vrows     nTp + |D_s \ T| (0 for an empty plan);
+ *   d_static_valid  n_static, or 0 when a plan does not contain all of T (its
+ *               rows are then all dynamic and the static block is masked).
+ * svt_prefill_score_split scores with the static rows d_static_rows
+ * [n_static, dim] shared by every sequence (gathered once, e.g. with
+ * svt_gather_rows) and the dynamic rows gathered per sequence
+ * (svt_gather_plans over d_dyn_ids / d_n_dyn -> rows d_dyn_offsets[s] + j):
+ * only D_s \ T is gathered per sequence. Ids, maxima and workspace are those
+ * of svt_prefill_score on the full plans (ties resolve by id). */
+int64_t svt_prefill_static_pad(int64_t n_static);
+svt_status svt_prefill_split_plans(const uint32_t* d_active_ids, const int64_t* d_act_off,
+                                   const int64_t* d_n_active, int32_t sequences,
+                                   const uint64_t* d_static_words, size_t universe,
+                                   const uint32_t* d_static_ids, int64_t n_static,
+                                   uint32_t* d_dyn_ids, int64_t* d_n_dyn, uint32_t* d_vids,
+                                   int64_t* d_vid_offsets, int64_t* d_vrows,
+                                   int64_t* d_static_valid, svt_stream stream);
+svt_status svt_prefill_score_split(const void* d_hidden, const void* d_static_rows,
+                                   int64_t n_static, const int64_t* d_static_valid,
+                                   const void* d_dyn_rows, int64_t total_dyn_rows,
+                                   const int64_t* d_dyn_offsets, const int64_t* d_vrows,
+                                   const uint32_t* d_vids, const int64_t* d_vid_offsets,
+                                   const float* d_head_row_norms, int32_t sequences,
+                                   int32_t positions, int32_t dim, uint32_t* d_out_ids,
+                                   float* d_out_max, void* d_workspace, svt_stream stream);
 /* Tuning (process-wide): pair 0 forces the single-CTA (cta_group::1) GEMM
  * (default 1: CTA-pair cta_group::2 whenever positions % 256 == 0); nsplit
  * in [1, 128] = N-range splits per M tile (default 0 = automatic), one partial top-8

@@ -105,6 +105,11 @@ _SIGS = {
                            _vp, _vp], C.c_int),
     "svt_prefill_score_fused": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp,
                                  _vp, _vp], C.c_int),
+    "svt_prefill_static_pad": ([_i64], _i64),
+    "svt_prefill_split_plans": ([_vp, _vp, _vp, _i32, _vp, C.c_size_t, _vp, _i64, _vp, _vp, _vp,
+                                 _vp, _vp, _vp, _vp], C.c_int),
+    "svt_prefill_score_split": ([_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i32,
+                                 _i32, _i32, _vp, _vp, _vp, _vp], C.c_int),
     "svt_row_norms_bf16": ([_vp, _i64, _i32, _vp, _vp], C.c_int),
     "svt_prefill_set_tuning": ([_i32, _i32], C.c_int),
     "svt_prefill_get_tuning": ([_vp, _vp], None),

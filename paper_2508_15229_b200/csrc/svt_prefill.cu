@@ -79,6 +79,11 @@ struct PrefillParams {
                                // (fused: first plan id of sequence s in plan_ids)
     const uint32_t* plan_ids;  // fused gather: B rows are head rows plan_ids[row_off[s] + r]
                                // loaded by TMA tile::gather4 (nullptr: gathered sub-heads)
+    // static/dynamic split (nTp > 0): plan rows [0, nTp) of every sequence
+    // are the shared static rows (tensor map tmS, rows [st_valid[s], nTp)
+    // masked), rows nTp + j the sequence's dynamic rows row_off[s] + j
+    int64_t nTp;
+    const int64_t* st_valid;   // [S] static rows present (n_static or 0)
     float* top_val;            // [S*P][nsplit][TOPK] partial top-8 per N range
     uint32_t* top_row;         // [S*P][nsplit][TOPK]
     uint8_t* flags;            // [S*P][nsplit] bit0: non-finite logit seen
@@ -252,7 +257,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
 template <int NCTA>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
-                    const __grid_constant__ CUtensorMap tmW, const PrefillParams p) {
+                    const __grid_constant__ CUtensorMap tmW,
+                    const __grid_constant__ CUtensorMap tmS, const PrefillParams p) {
     using G = Geo<NCTA>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-align the ring (TMA 128B swizzle + UMMA descriptors); the offset is
@@ -278,6 +284,8 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
     const int s = mtile / mt_per_seq;
     const int m0 = (mtile - s * mt_per_seq) * BM * NCTA + static_cast<int>(rank) * BM;
     const int64_t nrows = p.n_rows[s];
+    // masked static rows (split): [hole0, nTp)
+    const int64_t hole0 = p.nTp > 0 ? p.st_valid[s] : 0;
     const int ntiles_all = static_cast<int>((nrows + BN - 1) / BN);
     const int per_split = (ntiles_all + p.nsplit - 1) / p.nsplit;
     const int t0 = split * per_split;
@@ -400,7 +408,14 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
                         const uint32_t bar =
                             NCTA == 2 ? map_to_rank(&full[stage], 0) : smem_u32(&full[stage]);
                         tma_load_2d<NCTA>(sa, &tmH, kt * BK, ya, bar);
-                        tma_load_2d<NCTA>(sa + kTileA, &tmW, kt * BK, yb0 + (t0 + nt) * BN, bar);
+                        const int64_t v0 = static_cast<int64_t>(t0 + nt) * BN;
+                        if (v0 < p.nTp)  // a static tile, shared by every sequence
+                            tma_load_2d<NCTA>(sa + kTileA, &tmS, kt * BK,
+                                              static_cast<int>(v0) + static_cast<int>(rank) * (BN / NCTA),
+                                              bar);
+                        else
+                            tma_load_2d<NCTA>(sa + kTileA, &tmW, kt * BK,
+                                              yb0 + static_cast<int>(v0 - p.nTp), bar);
                     }
                     if (++stage == G::kStages) {
                         stage = 0;
@@ -486,11 +501,12 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
                 tmem_ld64(taddr + c0, r);
                 const int64_t col0 = static_cast<int64_t>(t0 + nt) * BN + c0;
                 if (p.mode & 1) continue;
-                if (col0 + 64 > nrows) {
-                    // last tile: columns past |S_s| belong to no plan row
+                if (col0 + 64 > nrows || (col0 < p.nTp && col0 + 64 > hole0)) {
+                    // columns past |S_s|, or static padding, belong to no plan row
 #pragma unroll
                     for (int j = 0; j < 64; ++j)
-                        if (col0 + j >= nrows) r[j] = __float_as_uint(-FLT_MAX);
+                        if (col0 + j >= nrows || (col0 + j >= hole0 && col0 + j < p.nTp))
+                            r[j] = __float_as_uint(-FLT_MAX);
                 }
                 // bitmask of values above the current 8th; z catches inf / NaN
                 const float t8 = tv[TOPK - 1];
@@ -622,12 +638,46 @@ __device__ float exact_dot_bf16(const uint16_t* __restrict__ w, const uint16_t* 
     return acc;
 }
 
-__device__ __forceinline__ void write_result(unsigned long long best,
-                                             const uint32_t* __restrict__ ids, int64_t pos,
-                                             uint32_t* __restrict__ out_ids,
+// Plan row v of sequence s: its head id and its bf16 row in memory. Rows are
+// the gathered sub-heads (row_off[s] + v), the head itself through the plan
+// ids (fused), or — split — the shared static rows for v < nTp and the
+// sequence's gathered dynamic rows after. Keys carry head ids (the plan is
+// ascending, so "lower id" is the reference's "earlier plan row" even when
+// the split orders rows static-first); a NaN at the plan's first row is the
+// plan's smallest id.
+struct RowMap {
+    const uint16_t* W;         // gathered rows (split: dynamic rows) or the head (fused)
+    const uint16_t* Wst;       // split: static rows
+    const int64_t* row_off;    // [S]
+    const uint32_t* row_ids;   // fused: head row of plan row v = row_ids[row_off[s] + v]
+    int64_t nTp;               // split: static rows padded to the N tile (0: no split)
+    const int64_t* st_valid;   // split: [S] static rows present
+    const uint32_t* ids;       // plan ids (split: per-sequence static ids, padding, dynamic ids)
+    const int64_t* id_off;     // [S]
+    const int64_t* n_rows;     // [S] plan rows (split: nTp + dynamic)
+
+    __device__ __forceinline__ uint32_t id(int s, int64_t v) const { return ids[id_off[s] + v]; }
+    // the plan's smallest id (the reference's row 0)
+    __device__ __forceinline__ uint32_t first(int s) const {
+        if (nTp > 0 && st_valid[s] > 0)
+            return n_rows[s] > nTp ? min(ids[id_off[s]], ids[id_off[s] + nTp]) : ids[id_off[s]];
+        return ids[id_off[s] + (nTp > 0 ? nTp : 0)];
+    }
+    __device__ __forceinline__ bool valid(int s, int64_t v) const {
+        return v < n_rows[s] && !(nTp > 0 && v >= st_valid[s] && v < nTp);
+    }
+    __device__ __forceinline__ const uint16_t* row(int s, int64_t v, int dim) const {
+        if (v < nTp) return Wst + v * dim;
+        const int64_t rr = row_off[s] + v - nTp;
+        return W + (row_ids ? static_cast<int64_t>(row_ids[rr]) : rr) * static_cast<int64_t>(dim);
+    }
+};
+
+__device__ __forceinline__ void write_result(unsigned long long best, uint32_t first_id,
+                                             int64_t pos, uint32_t* __restrict__ out_ids,
                                              float* __restrict__ out_max) {
-    const uint32_t r = 0xFFFFFFFFu - static_cast<uint32_t>(best);
-    out_ids[pos] = best ? ids[r] : 0xFFFFFFFFu;
+    const uint32_t id = best == kNanRow0Key ? first_id : 0xFFFFFFFFu - static_cast<uint32_t>(best);
+    out_ids[pos] = best ? id : 0xFFFFFFFFu;
     if (out_max)
         out_max[pos] = (best >> 32) == 0xFFFFFFFFu ? __int_as_float(0x7FC00000)
                                                    : float_of_ord(static_cast<uint32_t>(best >> 32));
@@ -643,8 +693,7 @@ __device__ __forceinline__ void write_result(unsigned long long best,
 // stats: [0] certified directly [1] recomputed [2] all-rows [3] non-finite
 // [4] all-rows list length [5] max |S_s| [6] pair count [7] rec_list length.
 __global__ void __launch_bounds__(256)
-certify_kernel(int P, int S, const int64_t* __restrict__ n_rows,
-               const uint32_t* __restrict__ plan_ids, const int64_t* __restrict__ id_off,
+certify_kernel(int P, int S, const RowMap map,
                const float* __restrict__ top_val, const uint32_t* __restrict__ top_row,
                const uint8_t* __restrict__ flags, int nsplit, const float* __restrict__ hnorm,
                const unsigned int* __restrict__ wmax_bits, float c_rel,
@@ -663,7 +712,7 @@ certify_kernel(int P, int S, const int64_t* __restrict__ n_rows,
         const int64_t pos = base + grp;
         const bool live = pos < npos;
         const int s = live ? static_cast<int>(pos / P) : 0;
-        const int64_t nrows = live ? n_rows[s] : 0;
+        const int64_t nrows = live ? map.n_rows[s] : 0;
         const bool work = live && nrows > 0;
         float thr = FLT_MAX;
         bool all = false, flg = false;
@@ -731,7 +780,7 @@ certify_kernel(int P, int S, const int64_t* __restrict__ n_rows,
         // the single candidate is the reference argmax (value within 2B of
         // nothing else); the lane holding it writes the result
         if (work && !all && ncand == 1 && mine == 1)
-            write_result(make_key(one_v, one_r, true, false), plan_ids + id_off[s], pos, out_ids,
+            write_result(make_key(one_v, map.id(s, one_r), true, false), 0u, pos, out_ids,
                          out_max);
     }
     __syncthreads();
@@ -768,9 +817,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 __global__ void __launch_bounds__(kPairWarps * 32, 1)
-recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, int P,
-                       int dim, const int64_t* __restrict__ row_off,
-                       const uint32_t* __restrict__ row_ids,
+recompute_pairs_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, int dim,
                        const unsigned int* __restrict__ stats, const uint2* __restrict__ pairs,
                        unsigned long long* __restrict__ pos_keys) {
     extern __shared__ __align__(16) uint8_t psmem[];
@@ -788,7 +835,7 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restric
 
     // issue side: row pointers of the task whose segments are being prefetched
     int64_t iss_task = -1;
-    const uint16_t* iss_w = W;
+    const uint16_t* iss_w = H;
     const uint16_t* iss_h = H;
     bool iss_act = false;
     auto issue = [&](int64_t u) {
@@ -799,9 +846,7 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restric
             const int64_t i = (first + k * nw) * 32 + lane;
             iss_act = i < count;
             const uint2 pr = iss_act ? pairs[i] : make_uint2(0u, 0u);
-            const int64_t rr = row_off[iss_act ? pr.x / P : 0] + pr.y;
-            iss_w = W + (row_ids ? static_cast<int64_t>(row_ids[iss_act ? rr : 0]) : rr) *
-                            static_cast<int64_t>(dim);
+            iss_w = iss_act ? map.row(static_cast<int>(pr.x / P), pr.y, dim) : H;
             iss_h = H + static_cast<int64_t>(pr.x) * dim;
         }
         uint8_t* slot = ring + static_cast<int>(u % kRing) * 64 * kSegStride;
@@ -850,7 +895,9 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restric
             const int64_t i = (first + k * nw) * 32 + lane;
             if (i < count) {
                 const uint2 pr = pairs[i];
-                atomicMax(&pos_keys[pr.x], make_key(acc, pr.y, true, pr.y == 0));
+                const int s = static_cast<int>(pr.x / P);
+                const uint32_t id = map.id(s, pr.y);
+                atomicMax(&pos_keys[pr.x], make_key(acc, id, true, acc != acc && id == map.first(s)));
             }
             acc = 0.0f;
         }
@@ -859,8 +906,7 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const uint16_t* __restric
 }
 
 // Phase C — ids of the recomputed positions from their folded keys.
-__global__ void rec_finalize_kernel(int P, const int64_t* __restrict__ id_off,
-                                    const uint32_t* __restrict__ plan_ids,
+__global__ void rec_finalize_kernel(int P, const RowMap map,
                                     const unsigned int* __restrict__ stats,
                                     const uint32_t* __restrict__ rec_list,
                                     const unsigned long long* __restrict__ pos_keys,
@@ -869,7 +915,9 @@ __global__ void rec_finalize_kernel(int P, const int64_t* __restrict__ id_off,
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t pos = rec_list[e];
-        write_result(pos_keys[pos], plan_ids + id_off[pos / P], pos, out_ids, out_max);
+        const unsigned long long k = pos_keys[pos];
+        write_result(k, k == kNanRow0Key ? map.first(static_cast<int>(pos / P)) : 0u, pos, out_ids,
+                     out_max);
     }
 }
 
@@ -877,9 +925,7 @@ __global__ void rec_finalize_kernel(int P, const int64_t* __restrict__ id_off,
 // (position, 32-row chunk), one row chain per lane, max key per position.
 // stats[4] = list length, stats[5] = max |S_s| (plan_wmax_kernel).
 __global__ void __launch_bounds__(256)
-all_rows_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, int P, int dim,
-                const int64_t* __restrict__ n_rows, const int64_t* __restrict__ row_off,
-                const uint32_t* __restrict__ row_ids,
+all_rows_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, int dim,
                 const unsigned int* __restrict__ stats, const int64_t* __restrict__ all_list,
                 unsigned long long* __restrict__ all_keys) {
     const int lane = threadIdx.x & 31;
@@ -893,11 +939,10 @@ all_rows_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, 
         const int64_t pos = all_list[e];
         const int s = static_cast<int>(pos / P);
         unsigned long long best = 0;
-        if (r < n_rows[s]) {
-            const int64_t rr = row_off[s] + r;
-            const float v = exact_dot_bf16(W + (row_ids ? static_cast<int64_t>(row_ids[rr]) : rr) * dim,
-                                           H + pos * dim, dim);
-            best = make_key(v, static_cast<uint32_t>(r), true, r == 0);
+        if (map.valid(s, r)) {
+            const float v = exact_dot_bf16(map.row(s, r, dim), H + pos * dim, dim);
+            const uint32_t id = map.id(s, r);
+            best = make_key(v, id, true, v != v && id == map.first(s));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -908,8 +953,7 @@ all_rows_kernel(const uint16_t* __restrict__ H, const uint16_t* __restrict__ W, 
     }
 }
 
-__global__ void all_finalize_kernel(int P, const int64_t* __restrict__ id_off,
-                                    const uint32_t* __restrict__ plan_ids,
+__global__ void all_finalize_kernel(int P, const RowMap map,
                                     const unsigned int* __restrict__ stats,
                                     const int64_t* __restrict__ all_list,
                                     const unsigned long long* __restrict__ all_keys,
@@ -918,7 +962,9 @@ __global__ void all_finalize_kernel(int P, const int64_t* __restrict__ id_off,
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t pos = all_list[e];
-        write_result(all_keys[e], plan_ids + id_off[pos / P], pos, out_ids, out_max);
+        const unsigned long long k = all_keys[e];
+        write_result(k, k == kNanRow0Key ? map.first(static_cast<int>(pos / P)) : 0u, pos, out_ids,
+                     out_max);
     }
 }
 
@@ -1136,15 +1182,23 @@ extern "C" svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int3
 
 namespace svt {
 namespace {
+// static/dynamic split of the plans (svt_prefill_score_split)
+struct SplitArgs {
+    const void* Wst = nullptr;         // the static rows [n_static, dim]
+    int64_t n_static = 0;
+    const int64_t* st_valid = nullptr;  // [S]
+};
+
 // W: the gathered sub-heads (row_ids == nullptr; rows row_off[s] + r) or the
-// full head (row_ids = plan ids; rows row_ids[row_off[s] + r], TMA gather4)
+// full head (row_ids = plan ids; rows row_ids[row_off[s] + r], TMA gather4);
+// split: W holds the dynamic rows and sp the static ones
 svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_rows,
                               const int64_t* d_row_offsets, const int64_t* d_n_rows,
                               const uint32_t* row_ids, const uint32_t* d_plan_ids,
                               const int64_t* d_id_offsets, const float* d_head_row_norms,
                               int32_t sequences, int32_t positions, int32_t dim,
                               uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
-                              svt_stream stream) {
+                              svt_stream stream, const SplitArgs& sp = SplitArgs()) {
     const void* d_subheads = W;
     const int64_t total_sub_rows = w_rows;
     using namespace svt;
@@ -1176,11 +1230,28 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
         return SVT_ERR_CONFIG;
     }
 
-    CUtensorMap mapH, mapW;
+    CUtensorMap mapH, mapW, mapS;
     if (svt_status s = make_map(&mapH, d_hidden, static_cast<uint64_t>(npos), dim, BM)) return s;
-    if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows), dim,
+    if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows > 0 ? total_sub_rows : 1), dim,
                                 row_ids ? 1u : (pair ? BN / 2 : BN)))
         return s;
+    const int64_t nTp = sp.Wst ? (sp.n_static + BN - 1) / BN * BN : 0;
+    mapS = mapW;
+    if (sp.Wst) {
+        if (svt_status s = make_map(&mapS, sp.Wst, static_cast<uint64_t>(sp.n_static), dim,
+                                    pair ? BN / 2 : BN))
+            return s;
+    }
+    RowMap rmap;
+    rmap.W = static_cast<const uint16_t*>(d_subheads);
+    rmap.Wst = static_cast<const uint16_t*>(sp.Wst);
+    rmap.row_off = d_row_offsets;
+    rmap.row_ids = row_ids;
+    rmap.nTp = nTp;
+    rmap.st_valid = sp.st_valid;
+    rmap.ids = d_plan_ids;
+    rmap.id_off = d_id_offsets;
+    rmap.n_rows = d_n_rows;
 
     const char* mode_env = getenv("SVT_PREFILL_MODE");  // profiling switches (PrefillParams::mode)
     const int mode = mode_env ? atoi(mode_env) : 0;
@@ -1206,7 +1277,8 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
         SVT_LAUNCH_CHECK("norms_kernel");
         // chunks per sequence: enough for any plan the sub-head rows can hold
         // (chunks past a plan's end are skipped)
-        const int cps = static_cast<int>((total_sub_rows + kWmaxChunk - 1) / kWmaxChunk) + 1;
+        const int cps =
+            static_cast<int>((total_sub_rows + nTp + kWmaxChunk - 1) / kWmaxChunk) + 1;
         const int64_t items = static_cast<int64_t>(sequences) * cps;
         plan_wmax_kernel<<<static_cast<int>(items < sm_count() * 8 ? items : sm_count() * 8), 256, 0,
                            side->stream>>>(d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows,
@@ -1226,6 +1298,8 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     p.n_rows = d_n_rows;
     p.row_off = d_row_offsets;
     p.plan_ids = row_ids;
+    p.nTp = nTp;
+    p.st_valid = sp.st_valid;
     p.top_val = top_val;
     p.top_row = top_row;
     p.flags = flags;
@@ -1245,13 +1319,13 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<2>, mapH, mapW, p));
+        SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<2>, mapH, mapW, mapS, p));
     } else {
         using G = Geo<1>;
         SVT_CUDA_TRY(cudaFuncSetAttribute(prefill_gemm_kernel<1>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
         prefill_gemm_kernel<1><<<sequences * (positions / BM) * ns, kGemmThreads, G::kSmem, st>>>(
-            mapH, mapW, p);
+            mapH, mapW, mapS, p);
     }
     SVT_LAUNCH_CHECK("prefill_gemm_kernel");
 
@@ -1261,24 +1335,22 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     const int64_t warps = (npos + 3) / 4;
     const int64_t blocks = (warps + 7) / 8;
     certify_kernel<<<static_cast<int>(blocks < sm_count() * 8 ? blocks : sm_count() * 8), 256, 0,
-                     st>>>(positions, sequences, d_n_rows, d_plan_ids, d_id_offsets, top_val, top_row,
+                     st>>>(positions, sequences, rmap, top_val, top_row,
                            flags, ns, hnorm, wmax, static_cast<float>(c) * 1.0001f, d_out_ids,
                            d_out_max, stats, all_list, all_keys, pairs, rec_list, pos_keys);
     SVT_LAUNCH_CHECK("certify_kernel");
     SVT_CUDA_TRY(cudaFuncSetAttribute(recompute_pairs_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
     recompute_pairs_kernel<<<sm_count(), kPairWarps * 32, kPairSmem, st>>>(
-        static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads), positions,
-        dim, d_row_offsets, row_ids, stats, pairs, pos_keys);
+        static_cast<const uint16_t*>(d_hidden), rmap, positions, dim, stats, pairs, pos_keys);
     SVT_LAUNCH_CHECK("recompute_pairs_kernel");
-    rec_finalize_kernel<<<sm_count(), 256, 0, st>>>(positions, d_id_offsets, d_plan_ids, stats,
+    rec_finalize_kernel<<<sm_count(), 256, 0, st>>>(positions, rmap, stats,
                                                     rec_list, pos_keys, d_out_ids, d_out_max);
     SVT_LAUNCH_CHECK("rec_finalize_kernel");
-    all_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(
-        static_cast<const uint16_t*>(d_hidden), static_cast<const uint16_t*>(d_subheads),
-        positions, dim, d_n_rows, d_row_offsets, row_ids, stats, all_list, all_keys);
+    all_rows_kernel<<<sm_count() * 8, 256, 0, st>>>(static_cast<const uint16_t*>(d_hidden), rmap,
+                                                    positions, dim, stats, all_list, all_keys);
     SVT_LAUNCH_CHECK("all_rows_kernel");
-    all_finalize_kernel<<<64, 256, 0, st>>>(positions, d_id_offsets, d_plan_ids, stats, all_list,
+    all_finalize_kernel<<<64, 256, 0, st>>>(positions, rmap, stats, all_list,
                                             all_keys, d_out_ids, d_out_max);
     SVT_LAUNCH_CHECK("all_finalize_kernel");
     return SVT_OK;
@@ -1313,4 +1385,125 @@ extern "C" svt_status svt_prefill_score_fused(const void* d_hidden, const void* 
     return svt::prefill_score_impl(d_hidden, d_head, head_rows, d_id_offsets, d_n_rows, d_plan_ids,
                                    d_plan_ids, d_id_offsets, d_head_row_norms, sequences, positions,
                                    dim, d_out_ids, d_out_max, d_workspace, stream);
+}
+
+// ---- static/dynamic split of the plans ----------------------------------------
+// A hybrid plan is T ∪ D_s (select, selector.cpp:16-43): every sequence shares
+// the static rows T. Scoring them from one static row block (gathered once,
+// L2-resident) and gathering only D_s \ T per sequence halves the gather and
+// the sub-head traffic. Plan row order becomes [T (padded to the N tile),
+// D_s \ T]; the keys carry head ids, so ties still resolve to the lower id
+// (the reference's earlier plan row).
+namespace svt {
+namespace {
+__device__ __forceinline__ bool in_words(const uint64_t* words, size_t universe, uint32_t id) {
+    return id < universe && ((words[id >> 6] >> (id & 63)) & 1ull);
+}
+
+// one CTA per sequence: plan ids -> dynamic ids (plan order), the virtual
+// plan [static ids, padding, dynamic ids] and its counters. A plan that does
+// not contain all of T (an explicit plan, a failed select) keeps every row
+// dynamic and masks the static block (st_valid = 0).
+__global__ void __launch_bounds__(256)
+split_plans_kernel(const uint32_t* __restrict__ active, const int64_t* __restrict__ act_off,
+                   const int64_t* __restrict__ n_active, const uint64_t* __restrict__ words,
+                   size_t universe, const uint32_t* __restrict__ st_ids, int64_t nT, int64_t nTp,
+                   uint32_t* __restrict__ dyn_ids, int64_t* __restrict__ n_dyn,
+                   uint32_t* __restrict__ vids, int64_t* __restrict__ vid_off,
+                   int64_t* __restrict__ vrows, int64_t* __restrict__ st_valid) {
+    __shared__ int64_t red[8];
+    const int s = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = n_active[s];
+    const uint32_t* plan = active + act_off[s];
+    const int64_t voff = act_off[s] + static_cast<int64_t>(s) * nTp;
+    // does the plan contain all of T? (plan ids are distinct)
+    int64_t c = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += in_words(words, universe, plan[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if (lane == 0) red[warp] = c;
+    __syncthreads();
+    int64_t cnt = 0;
+    for (int w = 0; w < 8; ++w) cnt += red[w];
+    const bool valid = nT > 0 && cnt == nT;
+    __syncthreads();
+    // order-preserving compaction of the dynamic ids
+    int64_t out = 0;
+    for (int64_t b = 0; b < n; b += blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        const uint32_t id = i < n ? plan[i] : 0u;
+        const bool keep = i < n && !(valid && in_words(words, universe, id));
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
+        if (lane == 0) red[warp] = __popc(m);
+        __syncthreads();
+        int64_t before = 0, total = 0;
+        for (int w = 0; w < 8; ++w) {
+            before += w < warp ? red[w] : 0;
+            total += red[w];
+        }
+        if (keep) {
+            const int64_t at = out + before + __popc(m & ((1u << lane) - 1u));
+            dyn_ids[act_off[s] + at] = id;
+            vids[voff + nTp + at] = id;
+        }
+        out += total;
+        __syncthreads();
+    }
+    for (int64_t v = threadIdx.x; v < nTp; v += blockDim.x)
+        vids[voff + v] = st_ids[v < nT ? v : nT - 1];
+    if (threadIdx.x == 0) {
+        n_dyn[s] = out;
+        vrows[s] = n > 0 ? nTp + out : 0;
+        st_valid[s] = valid ? nT : 0;
+        vid_off[s] = voff;
+    }
+}
+}  // namespace
+}  // namespace svt
+
+extern "C" svt_status svt_prefill_split_plans(const uint32_t* d_active_ids, const int64_t* d_act_off,
+                                              const int64_t* d_n_active, int32_t sequences,
+                                              const uint64_t* d_static_words, size_t universe,
+                                              const uint32_t* d_static_ids, int64_t n_static,
+                                              uint32_t* d_dyn_ids, int64_t* d_n_dyn,
+                                              uint32_t* d_vids, int64_t* d_vid_offsets,
+                                              int64_t* d_vrows, int64_t* d_static_valid,
+                                              svt_stream stream) {
+    using namespace svt;
+    if (sequences <= 0) return SVT_OK;
+    if (n_static <= 0) {
+        set_error("the static/dynamic split needs a non-empty static set");
+        return SVT_ERR_CONFIG;
+    }
+    const int64_t nTp = (n_static + BN - 1) / BN * BN;
+    split_plans_kernel<<<sequences, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_active_ids, d_act_off, d_n_active, d_static_words, universe, d_static_ids, n_static, nTp,
+        d_dyn_ids, d_n_dyn, d_vids, d_vid_offsets, d_vrows, d_static_valid);
+    SVT_LAUNCH_CHECK("split_plans_kernel");
+    return SVT_OK;
+}
+
+extern "C" int64_t svt_prefill_static_pad(int64_t n_static) {
+    return (n_static + svt::BN - 1) / svt::BN * svt::BN;
+}
+
+extern "C" svt_status svt_prefill_score_split(
+    const void* d_hidden, const void* d_static_rows, int64_t n_static,
+    const int64_t* d_static_valid, const void* d_dyn_rows, int64_t total_dyn_rows,
+    const int64_t* d_dyn_offsets, const int64_t* d_vrows, const uint32_t* d_vids,
+    const int64_t* d_vid_offsets, const float* d_head_row_norms, int32_t sequences,
+    int32_t positions, int32_t dim, uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
+    svt_stream stream) {
+    if (n_static <= 0 || n_static > 0x7FFFFFFF) {
+        svt::set_error("the static/dynamic split needs 1 <= n_static < 2^31");
+        return SVT_ERR_CONFIG;
+    }
+    svt::SplitArgs sp;
+    sp.Wst = d_static_rows;
+    sp.n_static = n_static;
+    sp.st_valid = d_static_valid;
+    return svt::prefill_score_impl(d_hidden, d_dyn_rows, total_dyn_rows, d_dyn_offsets, d_vrows,
+                                   nullptr, d_vids, d_vid_offsets, d_head_row_norms, sequences,
+                                   positions, dim, d_out_ids, d_out_max, d_workspace, stream, sp);
 }

@@ -28,6 +28,7 @@ class PrefillScorer:
                  positions: int, stream=None, fused: bool = False):
         n_rows = np.diff(id_offsets).astype(np.int64)
         self.fused = fused
+        self.split = False
         self._setup(head, positions, len(id_offsets) - 1, 0 if fused else int(n_rows.sum()),
                     stream)
         self.n_rows = torch.from_numpy(n_rows).cuda()
@@ -42,17 +43,42 @@ class PrefillScorer:
 
     @classmethod
     def from_batch(cls, head: HeadMatrix, tb, positions: int, stream=None,
-                   fused: bool = False) -> "PrefillScorer":
+                   fused: bool = False, split: bool = False) -> "PrefillScorer":
         """fused=True: no sub-heads; the GEMM gathers the plan rows from the
-        head itself (svt_prefill_score_fused, TMA tile::gather4)."""
+        head itself (svt_prefill_score_fused, TMA tile::gather4).
+        split=True (a batch built by select over a static set): the static
+        rows are gathered once and shared by every sequence, only each
+        plan's dynamic rows are gathered (svt_prefill_score_split)."""
+        if fused and split:
+            raise _lib.ConfigError("the fused and split scorers are exclusive")
         self = cls.__new__(cls)
         self.fused = fused
+        self.split = False
         self._setup(head, positions, tb.B, 0 if fused else int(tb.act_off_h[-1]), stream)
         self.n_rows = tb.n_active            # device int64 [S]
         self.row_off = tb.act_off            # device int64 [S+1] (capacity offsets)
         self.id_off = tb.act_off
         self.plan_ids = tb.active
         self._tb = tb
+        if split:
+            words = getattr(tb, "_words", None)
+            if words is None:
+                raise _lib.ConfigError("the split scorer needs a batch built from a static set")
+            w = words.cpu().numpy().view(np.uint64)
+            bits = np.unpackbits(w.view(np.uint8), bitorder="little")[: tb.V]
+            st = np.flatnonzero(bits).astype(np.uint32)
+            if st.size:
+                self.split = True
+                self.nT = int(st.size)
+                self.nTp = int(_lib.lib.svt_prefill_static_pad(self.nT))
+                self.st_ids = torch.from_numpy(st.view(np.int32)).cuda()
+                self.st_rows = torch.empty((self.nT, self.d), dtype=torch.bfloat16, device="cuda")
+                S = tb.B
+                self.dyn_ids = torch.empty(max(1, self.total), dtype=torch.int32, device="cuda")
+                self.vids = torch.empty(max(1, self.total + S * self.nTp), dtype=torch.int32,
+                                        device="cuda")
+                self.split_meta = torch.zeros((4, max(1, S)), dtype=torch.int64, device="cuda")
+                self.n_dyn, self.vid_off, self.vrows, self.st_valid = self.split_meta
         self.regather()
         return self
 
@@ -62,6 +88,21 @@ class PrefillScorer:
         if self.fused:
             return
         tb = self._tb
+        if self.split:
+            st = _stream(self.stream)
+            call("svt_prefill_split_plans", tb.active.data_ptr(), tb.act_off.data_ptr(),
+                 tb.n_active.data_ptr(), tb.B, tb._words.data_ptr(), tb.V,
+                 self.st_ids.data_ptr(), self.nT, self.dyn_ids.data_ptr(), self.n_dyn.data_ptr(),
+                 self.vids.data_ptr(), self.vid_off.data_ptr(), self.vrows.data_ptr(),
+                 self.st_valid.data_ptr(), st)
+            call("svt_gather_rows", self.head.data.data_ptr(), self.head.storage,
+                 self.head.rows(), self.d, self.st_ids.data_ptr(), self.nT,
+                 self.st_rows.data_ptr(), self.bad.data_ptr(), st)
+            call("svt_gather_plans", self.head.data.data_ptr(), self.head.storage,
+                 self.head.rows(), self.d, self.dyn_ids.data_ptr(), tb.act_off.data_ptr(),
+                 self.n_dyn.data_ptr(), tb.B, self.total, self.sub.data_ptr(),
+                 self.bad.data_ptr(), st)
+            return
         call("svt_gather_plans", self.head.data.data_ptr(), self.head.storage, self.head.rows(),
              self.d, tb.active.data_ptr(), tb.act_off.data_ptr(), tb.n_active.data_ptr(), tb.B,
              self.total, self.sub.data_ptr(), self.bad.data_ptr(), _stream(self.stream))
@@ -87,6 +128,14 @@ class PrefillScorer:
             call("svt_prefill_score_fused", hidden.data_ptr(), self.head.data.data_ptr(),
                  self.head.rows(), self.n_rows.data_ptr(), self.plan_ids.data_ptr(),
                  self.id_off.data_ptr(), self.head.row_norms.data_ptr(), self.S, self.P, self.d,
+                 out_ids.data_ptr(), None if out_max is None else out_max.data_ptr(),
+                 self.ws.data_ptr(), _stream(self.stream))
+            return out_ids
+        if self.split:
+            call("svt_prefill_score_split", hidden.data_ptr(), self.st_rows.data_ptr(), self.nT,
+                 self.st_valid.data_ptr(), self.sub.data_ptr(), self.total,
+                 self.row_off.data_ptr(), self.vrows.data_ptr(), self.vids.data_ptr(),
+                 self.vid_off.data_ptr(), self.head.row_norms.data_ptr(), self.S, self.P, self.d,
                  out_ids.data_ptr(), None if out_max is None else out_max.data_ptr(),
                  self.ws.data_ptr(), _stream(self.stream))
             return out_ids

@@ -573,6 +573,64 @@ def test_prefill_from_device_batch_matches_reference(th, fused):
     assert int(sc.bad.item()) == 0
 
 
+@pytest.mark.parametrize("case,nT", [("random", 600), ("random", 512), ("duplicate_rows", 600),
+                                     ("nonfinite", 300)])
+def test_prefill_split_matches_reference(th, prefill_tuning, case, nT):
+    """Static/dynamic split (svt_prefill_split_plans + svt_prefill_score_split):
+    the shared static rows scored from one block, only D_s \\ T gathered per
+    sequence; ids equal the reference greedy over each full plan. Covers the
+    static padding (|T| not a multiple of the N tile), ties between static
+    and dynamic rows (duplicated head rows: the lower id wins), non-finite
+    logits (NaN at the plan's smallest id), an empty prompt, and a plan
+    rewritten to miss part of T (its static block is masked, every row
+    dynamic)."""
+    from paper_2508_15229_b200 import prefill, synth
+
+    V, d, S, P = 5000, 128, 4, 256
+    rng = np.random.default_rng(nT * 7 + len(case))
+    if case == "duplicate_rows":
+        base = synth.round_bf16(rng.uniform(-1, 1, (150, d)).astype(np.float32))
+        head = th.HeadMatrix.from_host(base[np.arange(V) % 150], dtype_bytes=2,
+                                       storage=th.SVT_BF16)
+    else:
+        head = th.HeadMatrix.random(V, d, 0xBEEF + nT, storage=th.SVT_BF16)
+    W = head.to_host()
+    t_ids = rng.choice(V, nT, replace=False)
+    words = words_from_ids(t_ids, V)
+    prompts = [rng.integers(0, V, L).astype(np.uint32) for L in (400, 0, 1300, 90)]
+    off = np.zeros(S + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in prompts])
+    flat = np.concatenate(prompts) if off[-1] else np.zeros(1, np.uint32)
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), nT, V,
+                                torch.from_numpy(flat.view(np.int32)).cuda(), off)
+    plans = [orc.select(prompts[s], words, V, V).active_ids for s in range(S)]
+    # request 3: a plan that misses part of T (explicit rows)
+    p3 = plans[3][::2].copy()
+    o3 = int(tb.act_off_h[3])
+    tb.active[o3: o3 + p3.size].copy_(torch.from_numpy(p3.view(np.int32)))
+    tb.n_active[3] = p3.size
+    plans[3] = p3
+    sc = prefill.PrefillScorer.from_batch(head, tb, P, split=True)
+    assert sc.split
+    assert sc.st_valid.cpu().tolist() == [nT, nT, nT, 0]
+    hid = synth.round_bf16(rng.uniform(-1, 1, (S * P, d)).astype(np.float32))
+    if case == "nonfinite":
+        hid[::5] *= np.float32(3e38)
+        hid[7, :] = np.float32(np.inf)
+        hid = synth.round_bf16(hid)
+    out = torch.empty(S * P, dtype=torch.int32, device="cuda")
+    mx = torch.empty(S * P, dtype=torch.float32, device="cuda")
+    sc.score(torch.from_numpy(hid).cuda().to(torch.bfloat16), out, mx)
+    got = out.cpu().numpy().view(np.uint32)
+    for s in range(S):
+        sub = orc.gather(W, plans[s])
+        for p in range(P):
+            want, _ = orc.greedy_step(sub, hid[s * P + p], plans[s])
+            assert got[s * P + p] == want, (case, s, p)
+    assert int(sc.bad.item()) == 0
+    print("split stats", sc.stats())
+
+
 # ---- certified batch-1 decode over row-major rows (cfg1 latency path) ----------
 def _rows_decoder(th, head, ids, materialize=True, **kw):
     d_ids = torch.from_numpy(np.ascontiguousarray(ids, np.uint32).view(np.int32)).cuda()
