@@ -970,32 +970,32 @@ __global__ void all_finalize_kernel(int P, const RowMap map,
 
 // per-sequence max row norm from a per-head row-norm table (computed once
 // per head) through the plan ids
-// Work item = (sequence, 2048-row chunk of its plan): large plans (a shared
-// subset of up to |V| rows scored as one sequence) spread over the grid
-// instead of one block walking 128k dependent norm lookups.
+// Blocks (chunk lane x, sequence y): block x walks chunks x, x + gridDim.x, ...
+// of 2048 rows of its sequence's plan, so large plans (a shared subset of up
+// to |V| rows scored as one sequence) spread over many blocks instead of one
+// block walking 128k dependent norm lookups, and short plans cost one block.
 constexpr int kWmaxChunk = 2048;
+constexpr int kWmaxLanes = 32;
 __global__ void plan_wmax_kernel(const float* __restrict__ head_norm,
                                  const uint32_t* __restrict__ plan_ids,
                                  const int64_t* __restrict__ id_off,
-                                 const int64_t* __restrict__ n_rows, int S, int chunks_per_seq,
+                                 const int64_t* __restrict__ n_rows,
                                  unsigned int* __restrict__ wmax_bits,
                                  unsigned int* __restrict__ stats) {
-    const int64_t items = static_cast<int64_t>(S) * chunks_per_seq;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int s = static_cast<int>(it / chunks_per_seq);
-        const int64_t c0 = (it - static_cast<int64_t>(s) * chunks_per_seq) * kWmaxChunk;
-        const int64_t n = n_rows[s];
-        if (c0 == 0 && threadIdx.x == 0) atomicMax(&stats[5], static_cast<unsigned int>(n));
-        if (c0 >= n) continue;
+    const int s = blockIdx.y;
+    const int64_t n = n_rows[s];
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&stats[5], static_cast<unsigned int>(n));
+    const uint32_t* ids = plan_ids + id_off[s];
+    float m = 0.0f;
+    for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * kWmaxChunk; c0 < n;
+         c0 += static_cast<int64_t>(gridDim.x) * kWmaxChunk) {
         const int64_t c1 = min(n, c0 + kWmaxChunk);
-        const uint32_t* ids = plan_ids + id_off[s];
-        float m = 0.0f;
 #pragma unroll 4
         for (int64_t r = c0 + threadIdx.x; r < c1; r += blockDim.x) m = fmaxf(m, head_norm[ids[r]]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
-        if ((threadIdx.x & 31) == 0) atomicMax(&wmax_bits[s], __float_as_uint(m));
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0f) atomicMax(&wmax_bits[s], __float_as_uint(m));
 }
 
 // ---- host: tensor maps via the driver entry point (no libcuda link) --------
@@ -1225,8 +1225,8 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     unsigned long long* pos_keys = reinterpret_cast<unsigned long long*>(ws + L.pos_keys);
     uint32_t* rec_list = reinterpret_cast<uint32_t*>(ws + L.rec_list);
     uint2* pairs = reinterpret_cast<uint2*>(ws + L.pairs);
-    if (npos > 0xFFFFFFFFll) {
-        set_error("prefill scoring supports at most 2^32 positions per call");
+    if (npos > 0xFFFFFFFFll || sequences > 65535) {
+        set_error("prefill scoring supports at most 2^32 positions and 65535 sequences per call");
         return SVT_ERR_CONFIG;
     }
 
@@ -1275,14 +1275,9 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
         norms_kernel<<<sm_count() * 4, 256, 0, side->stream>>>(
             static_cast<const uint16_t*>(d_hidden), npos, dim, hnorm);
         SVT_LAUNCH_CHECK("norms_kernel");
-        // chunks per sequence: enough for any plan the sub-head rows can hold
-        // (chunks past a plan's end are skipped)
-        const int cps =
-            static_cast<int>((total_sub_rows + nTp + kWmaxChunk - 1) / kWmaxChunk) + 1;
-        const int64_t items = static_cast<int64_t>(sequences) * cps;
-        plan_wmax_kernel<<<static_cast<int>(items < sm_count() * 8 ? items : sm_count() * 8), 256, 0,
+        plan_wmax_kernel<<<dim3(kWmaxLanes, static_cast<unsigned>(sequences)), 256, 0,
                            side->stream>>>(d_head_row_norms, d_plan_ids, d_id_offsets, d_n_rows,
-                                           sequences, cps, wmax, stats);
+                                           wmax, stats);
         SVT_LAUNCH_CHECK("plan_wmax_kernel");
     }
     if (side->join) SVT_CUDA_TRY(cudaEventRecord(side->join, side->stream));
