@@ -9,6 +9,7 @@
 // Buffers grow monotonically and are reused, so a steady decode loop does no
 // allocation; the greedy workspace is zeroed once and left zeroed by every
 // launch.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -58,6 +59,7 @@ struct svt_session {
     cudaGraphExec_t graph_exec = nullptr;
     cudaGraphNode_t node_h2d = nullptr, node_d2h = nullptr;
     std::unordered_map<const void*, bool> pinned_cache;
+    std::unordered_map<const void*, void*> mapped_cache;  // pinned host -> device alias
     bool weights_stable = false;  // set after the first decode step following a prepare
 
     int64_t* n_active_d() { return d_meta; }
@@ -113,6 +115,52 @@ bool pinned_cached(svt_session* s, const void* p) {
     return v;
 }
 
+// the device alias of mapped pinned host memory (UVA: page-locked memory is
+// mapped), nullptr for anything else; memoised like pinned_cached
+void* mapped_cached(svt_session* s, const void* p) {
+    auto it = s->mapped_cache.find(p);
+    if (it != s->mapped_cache.end()) return it->second;
+    if (s->mapped_cache.size() > 4096) s->mapped_cache.clear();
+    void* v = nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess) {
+        if (a.type == cudaMemoryTypeHost) v = a.devicePointer;
+    } else {
+        cudaGetLastError();
+    }
+    s->mapped_cache.emplace(p, v);
+    return v;
+}
+
+// Copies a step's hidden states from mapped pinned host memory into the
+// session's device buffer. It releases its dependents first, so the decode
+// GEMV launched behind it (PDL) streams its first weight stages from HBM
+// while these PCIe reads are in flight, then waits for the copy to complete.
+__global__ void __launch_bounds__(256) pull_hidden_kernel(const float* __restrict__ src,
+                                                          size_t src_ld, float* __restrict__ dst,
+                                                          size_t dst_ld, int rows, int dim) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const bool vec = (dim % 4 == 0) && (src_ld % 4 == 0) && (dst_ld % 4 == 0) &&
+                     (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (vec) {
+        const int q = dim / 4;
+        const int64_t n = static_cast<int64_t>(rows) * q;
+        for (int64_t i = t0; i < n; i += stride) {
+            const int64_t r = i / q, c = i - r * q;
+            reinterpret_cast<float4*>(dst + r * dst_ld)[c] =
+                reinterpret_cast<const float4*>(src + r * src_ld)[c];
+        }
+    } else {
+        const int64_t n = static_cast<int64_t>(rows) * dim;
+        for (int64_t i = t0; i < n; i += stride) {
+            const int64_t r = i / dim, c = i - r * dim;
+            dst[r * dst_ld + c] = src[r * src_ld + c];
+        }
+    }
+}
+
 void drop_graph(svt_session* s) {
     if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
     if (s->graph) cudaGraphDestroy(s->graph);
@@ -120,6 +168,7 @@ void drop_graph(svt_session* s) {
     s->graph = nullptr;
     s->node_h2d = s->node_d2h = nullptr;
     s->pinned_cache.clear();  // host buffers may have been freed and reused
+    s->mapped_cache.clear();
 }
 
 
@@ -378,6 +427,37 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
     const size_t B = static_cast<size_t>(s->batch);
     if (B == 0) return SVT_OK;
     cudaStream_t q = s->stream;
+    // zero-copy path (SVT_SESSION_ZERO_COPY=1, mapped pinned buffers): a pull
+    // kernel reads the hidden states over PCIe while the PDL-launched GEMV
+    // already streams weights, and the finalize writes the ids (and maxima)
+    // straight into host memory. Measured at cfg2 it is no faster than the
+    // step graph (88 vs 86 us per call: the GEMV's pre-wait prefetch covers
+    // ~1 us of the ~6 us PCIe read), so the graph stays the default.
+    const char* zc_env = getenv("SVT_SESSION_ZERO_COPY");
+    const bool zero_copy = zc_env != nullptr && atoi(zc_env) != 0;
+    void* dh = zero_copy ? mapped_cached(s, h_hidden) : nullptr;
+    void* dout = dh ? mapped_cached(s, h_out_ids) : nullptr;
+    void* dmax = (dout && h_out_max) ? mapped_cached(s, h_out_max) : nullptr;
+    if (dh && dout && (!h_out_max || dmax)) {
+        for (int32_t b = 0; b < s->batch; ++b)
+            if (s->n_active[b] == 0) {
+                set_error("greedy step over an empty sub-head");
+                return SVT_ERR_INTEGRITY;
+            }
+        pull_hidden_kernel<<<32, 256, 0, q>>>(static_cast<const float*>(dh), host_ld, s->d_hidden,
+                                               s->ld, s->batch, static_cast<int>(s->dim));
+        SVT_LAUNCH_CHECK("pull_hidden_kernel");
+        // the weights were gathered before the pull kernel (a full
+        // dependency), so the GEMV may always prefetch them early
+        s->weights_stable = true;
+        svt_status st = svt_greedy_interleaved(
+            s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req, s->d_active, s->batch,
+            s->max_groups, s->d_hidden, s->ld, 0, 1, SVT_WEIGHTS_STABLE,
+            static_cast<uint32_t*>(dout), static_cast<float*>(dmax), nullptr, s->d_ws, q);
+        if (st) return st;
+        SVT_CUDA_TRY(cudaStreamSynchronize(q));
+        return SVT_OK;
+    }
     // (graph memcpy nodes can only be re-pointed when 1-D: contiguous rows)
     if (!h_out_max && host_ld == s->dim && s->ld == s->dim && pinned_cached(s, h_hidden) &&
         pinned_cached(s, h_out_ids)) {

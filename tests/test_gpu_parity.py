@@ -839,12 +839,18 @@ def test_vocab_sharded_certified_batch1(th):
             assert int(got[0]) == int(want), (G, want, got)
 
 
-def test_session_step_graph_pinned_buffers(th):
-    """Pinned contiguous host buffers take the per-session step graph (H2D ->
-    GEMV -> finalize -> D2H, memcpy nodes re-pointed per call): ids equal the
-    batched engine across steps with different buffers, a pageable call in
-    between, and a re-prepare with another batch (the graph is rebuilt)."""
+@pytest.mark.parametrize("zero_copy", ["1", "0"], ids=["zero_copy", "step_graph"])
+def test_session_step_graph_pinned_buffers(th, monkeypatch, zero_copy):
+    """Pinned host buffers take the zero-copy step (a pull kernel reads the
+    hidden states over PCIe while the PDL-launched GEMV streams weights; the
+    finalize writes the ids into host memory) or, with
+    SVT_SESSION_ZERO_COPY=0, the per-session step graph (H2D -> GEMV ->
+    finalize -> D2H, memcpy nodes re-pointed per call): ids equal the batched
+    engine across steps with different buffers, a pageable call in between,
+    strided pinned rows with the maxima, and a re-prepare with another batch."""
     from paper_2508_15229_b200 import session
+
+    monkeypatch.setenv("SVT_SESSION_ZERO_COPY", zero_copy)
 
     V, d = 151936, 896
     for B, steps in ((8, 3), (5, 2)):
@@ -863,6 +869,16 @@ def test_session_step_graph_pinned_buffers(th):
                     tb.greedy(torch.from_numpy(hid[t]).cuda(), o)
                     assert torch.equal(outs[t], o.cpu()), (B, rep, t)
                     assert np.array_equal(s.greedy(hid[t]), o.cpu().numpy().view(np.uint32))
+                    # strided pinned rows (ld > d) with pinned maxima
+                    wide = torch.zeros((B, d + 64), dtype=torch.float32).pin_memory()
+                    wide[:, :d] = torch.from_numpy(hid[t])
+                    ids2 = torch.empty(B, dtype=torch.int32).pin_memory()
+                    mx2 = torch.empty(B, dtype=torch.float32).pin_memory()
+                    s.greedy(wide, ids2, mx2)
+                    assert torch.equal(ids2, o.cpu()), (B, rep, t, "strided")
+                    mref = torch.empty(B, dtype=torch.float32, device="cuda")
+                    tb.greedy(torch.from_numpy(hid[t]).cuda(), o, mref)
+                    assert torch.equal(mx2, mref.cpu()), (B, rep, t, "max")
 
 
 @pytest.mark.parametrize("fused", [False, True])
