@@ -790,15 +790,22 @@ certify_kernel(int P, int S, const RowMap map,
 // Phase B — exact reference-order dot products of the candidate pairs, one
 // pair per lane (32 pairs per warp task). Row segments (kSegElems elements
 // of w and h for each of the warp's 32 pairs) are staged global -> shared by
-// the whole warp with cp.async (LDGSTS, 16 B per lane; two rows' 256-byte
+// the whole warp with cp.async (LDGSTS, 16 B per lane; four rows' 128-byte
 // segments per instruction = full 128-byte lines) into a kRing-deep ring,
 // streamed back to back across tasks, so each serial f32 chain reads shared
-// memory while later segments are in flight. Keys fold into pos_keys with a
-// 64-bit atomicMax (larger value, then lower row, NaN rules of make_key).
-constexpr int kSegElems = 128;                      // 256 B of bf16 per row per segment
+// memory while later segments are in flight. The serial f32 add chains are
+// latency-bound, so the ring trades depth for chains in flight: 8 warps x 3
+// slots of 64-element segments (117 us for 60k pairs at d = 3072) against
+// 2 warps x 6 slots of 128 (185 us). Unit, segment and slot indices advance
+// incrementally (no 64-bit divisions on the per-segment path). Keys fold
+// into pos_keys with a 64-bit atomicMax (larger value, then lower id, NaN
+// rules of make_key).
+constexpr int kSegElems = 64;                       // 128 B of bf16 per row per segment
 constexpr int kSegStride = kSegElems * 2 + 16;      // padded rows: conflict-free LDS.128
-constexpr int kRing = 6;
-constexpr int kPairWarps = 2;
+constexpr int kRing = 3;
+constexpr int kPairWarps = 8;
+constexpr int kSegChunks = kSegElems / 8;           // 16-byte chunks per row segment
+constexpr int kRowsPerCopy = 32 / kSegChunks;       // rows one warp-wide cp.async covers
 constexpr int kPairSmem = kPairWarps * kRing * 64 * kSegStride;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
@@ -833,29 +840,34 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, 
     const int nseg = (dim + kSegElems - 1) / kSegElems;
     const int64_t units = mytasks * nseg;  // (task, segment) units, streamed back to back
 
-    // issue side: row pointers of the task whose segments are being prefetched
-    int64_t iss_task = -1;
+    // issue side: the next unit (task ik, segment iseg) into ring slot islot,
+    // and the row pointers of task ik
+    int64_t ik = 0;
+    int iseg = 0, islot = 0;
     const uint16_t* iss_w = H;
     const uint16_t* iss_h = H;
     bool iss_act = false;
-    auto issue = [&](int64_t u) {
-        const int64_t k = u / nseg;
-        const int seg = static_cast<int>(u - k * nseg);
-        if (k != iss_task) {
-            iss_task = k;
-            const int64_t i = (first + k * nw) * 32 + lane;
+    auto issue = [&]() {
+        if (iseg == 0) {
+            const int64_t i = (first + ik * nw) * 32 + lane;
             iss_act = i < count;
             const uint2 pr = iss_act ? pairs[i] : make_uint2(0u, 0u);
             iss_w = iss_act ? map.row(static_cast<int>(pr.x / P), pr.y, dim) : H;
             iss_h = H + static_cast<int64_t>(pr.x) * dim;
         }
-        uint8_t* slot = ring + static_cast<int>(u % kRing) * 64 * kSegStride;
+        const int seg = iseg;
+        uint8_t* slot = ring + islot * 64 * kSegStride;
+        if (++iseg == nseg) {
+            iseg = 0;
+            ++ik;
+        }
+        if (++islot == kRing) islot = 0;
         const int e0 = seg * kSegElems;
         const int nch = min(kSegElems, dim - e0) / 8;  // 16-byte chunks per row
-        const int half = lane >> 4, ch = lane & 15;
+        const int half = lane / kSegChunks, ch = lane % kSegChunks;
 #pragma unroll 4
-        for (int r2 = 0; r2 < 16; ++r2) {
-            const int row = 2 * r2 + half;  // pair index whose row this lane copies
+        for (int r2 = 0; r2 < 32 / kRowsPerCopy; ++r2) {
+            const int row = kRowsPerCopy * r2 + half;  // pair index whose row this lane copies
             const uint16_t* w = reinterpret_cast<const uint16_t*>(
                 __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(iss_w), row));
             const uint16_t* h = reinterpret_cast<const uint16_t*>(
@@ -866,17 +878,18 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, 
         }
     };
     for (int64_t u = 0; u < kRing; ++u) {
-        if (u < units) issue(u);
+        if (u < units) issue();
         cp_async_commit();  // one group per unit (empty past the end) keeps the count aligned
     }
 
     float acc = 0.0f;
+    int64_t k = 0;
+    int seg = 0, cslot = 0;
     for (int64_t u = 0; u < units; ++u) {
-        const int64_t k = u / nseg;
-        const int seg = static_cast<int>(u - k * nseg);
         cp_async_wait<kRing - 1>();  // this lane's copies of unit u have landed
         __syncwarp();                // ... and every other lane's
-        const uint8_t* slot = ring + static_cast<int>(u % kRing) * 64 * kSegStride;
+        const uint8_t* slot = ring + cslot * 64 * kSegStride;
+        if (++cslot == kRing) cslot = 0;
         const uint4* sw = reinterpret_cast<const uint4*>(slot + lane * kSegStride);
         const uint4* sh = reinterpret_cast<const uint4*>(slot + (32 + lane) * kSegStride);
         const int nch = min(kSegElems, dim - seg * kSegElems) / 8;
@@ -889,7 +902,7 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, 
             for (int e = 0; e < 8; ++e) acc = ref_mac(acc, wa[e], ha[e]);
         }
         __syncwarp();  // every lane is done with this slot before it is refilled
-        if (u + kRing < units) issue(u + kRing);
+        if (u + kRing < units) issue();
         cp_async_commit();
         if (seg == nseg - 1) {
             const int64_t i = (first + k * nw) * 32 + lane;
@@ -900,6 +913,10 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, 
                 atomicMax(&pos_keys[pr.x], make_key(acc, id, true, acc != acc && id == map.first(s)));
             }
             acc = 0.0f;
+        }
+        if (++seg == nseg) {
+            seg = 0;
+            ++k;
         }
     }
     cp_async_wait<0>();
