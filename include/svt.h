@@ -413,13 +413,19 @@ svt_status svt_prefill_score_split(const void* d_hidden, const void* d_static_ro
  * out_max of svt_prefill_score: the exact reference logit for recomputed
  * positions, the tensor-core logit for positions certified directly. */
 svt_status svt_prefill_set_tuning(int32_t pair, int32_t nsplit);
-/* Split count a svt_prefill_score call over (sequences, positions) uses with
- * the current tuning. nsplit 0 (the default) is automatic: 2, raised (up to
- * 128) until the GEMM grid covers every SM — e.g. a shared-subset decode
- * batch scored as ONE sequence of `batch` positions. */
+/* Split count a svt_prefill_score call over (sequences, positions) starts
+ * from with the current tuning. nsplit 0 (the default) is automatic: 2,
+ * raised (up to 128) until the GEMM grid covers every SM — e.g. a
+ * shared-subset decode batch scored as ONE sequence of `batch` positions. A
+ * call then caps it at the N tiles its sub-head rows allow; the count it used
+ * is in the workspace at svt_prefill_meta_offset. */
 int32_t svt_prefill_effective_nsplit(int32_t sequences, int32_t positions);
 void svt_prefill_get_tuning(int32_t* pair, int32_t* nsplit);
 void svt_prefill_offsets(int32_t sequences, int32_t positions, int64_t* out4);
+/* Byte offset in the workspace of an i32 holding the N-range splits the last
+ * svt_prefill_score* call used (the automatic count, capped by the N tiles a
+ * plan can have: the top-8 records are [S*P][that count][8]). */
+int64_t svt_prefill_meta_offset(int32_t sequences, int32_t positions);
 /* Upward-rounded L2 norm of each row of a bf16 matrix (dim % 8 == 0). */
 svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int32_t dim, float* d_out,
                               svt_stream stream);

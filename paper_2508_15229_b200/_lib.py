@@ -115,6 +115,7 @@ _SIGS = {
     "svt_prefill_get_tuning": ([_vp, _vp], None),
     "svt_prefill_effective_nsplit": ([_i32, _i32], _i32),
     "svt_prefill_offsets": ([_i32, _i32, _vp], None),
+    "svt_prefill_meta_offset": ([_i32, _i32], _i64),
     "svt_shard_combine": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),

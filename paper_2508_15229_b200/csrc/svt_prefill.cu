@@ -700,8 +700,10 @@ certify_kernel(int P, int S, const RowMap map,
                uint32_t* __restrict__ out_ids, float* __restrict__ out_max,
                unsigned int* __restrict__ stats, int64_t* __restrict__ all_list,
                unsigned long long* __restrict__ all_keys, uint2* __restrict__ pairs,
-               uint32_t* __restrict__ rec_list, unsigned long long* __restrict__ pos_keys) {
+               uint32_t* __restrict__ rec_list, unsigned long long* __restrict__ pos_keys,
+               int32_t* __restrict__ meta) {
     const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) meta[0] = nsplit;
     __shared__ unsigned cnt[4];  // block-local counters, flushed once per block
     if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -832,8 +834,64 @@ recompute_pairs_kernel(const uint16_t* __restrict__ H, const RowMap map, int P, 
     // slot layout: rows 0-31 = w of pairs 0-31, rows 32-63 = h of pairs 0-31
     uint8_t* ring = psmem + warp * kRing * 64 * kSegStride;
     const int64_t count = stats[6];
-    const int64_t ntasks = (count + 31) / 32;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kPairWarps;
+    if (count <= nw) {
+        // few pairs (small shared-plan batches): latency mode, one warp per
+        // pair. The warp pulls the pair's w and h rows into its ring region
+        // in one go (pieces of kPiece elements); all lanes form the exact f32
+        // products (bf16 x bf16 fits f32: __fmul_rn is the reference's
+        // product), then lane 0 runs the add chain over them, 4 per LDS.128.
+        constexpr int kPiece = kRing * 64 * kSegStride / 8 / 8 * 8;  // w + h + product bytes
+        const int64_t i = static_cast<int64_t>(blockIdx.x) * kPairWarps + warp;
+        if (i >= count) return;
+        const uint2 pr = pairs[i];
+        const int s = static_cast<int>(pr.x / P);
+        const uint16_t* w = map.row(s, pr.y, dim);
+        const uint16_t* h = H + static_cast<int64_t>(pr.x) * dim;
+        float acc = 0.0f;
+        for (int e0 = 0; e0 < dim; e0 += kPiece) {
+            const int n = min(kPiece, dim - e0);  // a multiple of 8 (dim % 64 == 0)
+            for (int c = lane; c < n / 8; c += 32) {
+                cp_async16(ring + c * 16, w + e0 + c * 8, true);
+                cp_async16(ring + 2 * n + c * 16, h + e0 + c * 8, true);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncwarp();
+            float4* prod = reinterpret_cast<float4*>(ring + 4 * n);
+            {
+                const uint4* sw = reinterpret_cast<const uint4*>(ring);
+                const uint4* sh = reinterpret_cast<const uint4*>(ring + 2 * n);
+                for (int c = lane; c < n / 8; c += 32) {
+                    float wa[8], ha[8];
+                    Chunk<SVT_BF16>::widen(sw[c], wa);
+                    Chunk<SVT_BF16>::widen(sh[c], ha);
+                    prod[2 * c] = make_float4(__fmul_rn(wa[0], ha[0]), __fmul_rn(wa[1], ha[1]),
+                                              __fmul_rn(wa[2], ha[2]), __fmul_rn(wa[3], ha[3]));
+                    prod[2 * c + 1] = make_float4(__fmul_rn(wa[4], ha[4]), __fmul_rn(wa[5], ha[5]),
+                                                  __fmul_rn(wa[6], ha[6]), __fmul_rn(wa[7], ha[7]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll 8
+                for (int c = 0; c < n / 4; ++c) {
+                    const float4 q = prod[c];
+                    acc = __fadd_rn(acc, q.x);
+                    acc = __fadd_rn(acc, q.y);
+                    acc = __fadd_rn(acc, q.z);
+                    acc = __fadd_rn(acc, q.w);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            const uint32_t id = map.id(s, pr.y);
+            atomicMax(&pos_keys[pr.x], make_key(acc, id, true, acc != acc && id == map.first(s)));
+        }
+        return;
+    }
+    const int64_t ntasks = (count + 31) / 32;
     const int64_t first = static_cast<int64_t>(blockIdx.x) * kPairWarps + warp;
     if (first >= ntasks) return;
     const int64_t mytasks = (ntasks - first + nw - 1) / nw;
@@ -1108,7 +1166,7 @@ namespace {
 // Workspace layout for (S, P, nsplit); every region 256-byte aligned.
 struct PrefillLayout {
     size_t top_val, top_row, hnorm, wmax, flags, stats, dbg, all_list, all_keys, pos_keys,
-        rec_list, pairs, end;
+        rec_list, pairs, meta, end;
     PrefillLayout(int64_t S, int64_t P, int64_t ns) {
         const int64_t npos = S * P;
         size_t o = 0;
@@ -1129,6 +1187,7 @@ struct PrefillLayout {
         pos_keys = take(npos * 8);
         rec_list = take(npos * 4);
         pairs = take(npos * ns * TOPK * 8);
+        meta = take(8 * 4);  // [0] the N-range splits of the last call
         end = o;
     }
 };
@@ -1158,15 +1217,24 @@ SideStream* side_stream() {
 }  // namespace
 }  // namespace svt
 
-extern "C" size_t svt_prefill_workspace_bytes(int32_t sequences, int32_t positions) {
-    using namespace svt;
-    // room for every split count a call with the current tuning can use
+namespace svt {
+namespace {
+// the split count the workspace layout is sized for: every count a call with
+// the current tuning can use (a call may use fewer, see prefill_score_impl)
+int alloc_nsplit(int64_t S, int64_t P) {
     int ns = kMaxSplit;
     for (bool pr : {false, true}) {
-        const int e = effective_nsplit(sequences, positions, pr);
+        const int e = effective_nsplit(S, P, pr);
         ns = e > ns ? e : ns;
     }
-    return PrefillLayout(sequences, positions, ns).end;
+    return ns;
+}
+}  // namespace
+}  // namespace svt
+
+extern "C" size_t svt_prefill_workspace_bytes(int32_t sequences, int32_t positions) {
+    using namespace svt;
+    return PrefillLayout(sequences, positions, alloc_nsplit(sequences, positions)).end;
 }
 
 extern "C" int32_t svt_prefill_effective_nsplit(int32_t sequences, int32_t positions) {
@@ -1174,13 +1242,16 @@ extern "C" int32_t svt_prefill_effective_nsplit(int32_t sequences, int32_t posit
 }
 
 extern "C" void svt_prefill_offsets(int32_t sequences, int32_t positions, int64_t* out) {
-    const svt::PrefillLayout L(sequences, positions,
-                               svt::effective_nsplit(sequences, positions,
-                                                     svt::use_pair(positions)));
+    const svt::PrefillLayout L(sequences, positions, svt::alloc_nsplit(sequences, positions));
     out[0] = static_cast<int64_t>(L.top_val);
     out[1] = static_cast<int64_t>(L.top_row);
     out[2] = static_cast<int64_t>(L.stats);
     out[3] = static_cast<int64_t>(L.dbg);
+}
+
+extern "C" int64_t svt_prefill_meta_offset(int32_t sequences, int32_t positions) {
+    return static_cast<int64_t>(
+        svt::PrefillLayout(sequences, positions, svt::alloc_nsplit(sequences, positions)).meta);
 }
 
 extern "C" svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int32_t dim,
@@ -1229,8 +1300,16 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     uint8_t* ws = static_cast<uint8_t*>(d_workspace);
     // the CTA pair (cta_group::2) needs 256-position M tiles
     const bool pair = use_pair(positions);
-    const int ns = effective_nsplit(sequences, positions, pair);
-    const PrefillLayout L(sequences, positions, ns);
+    // N-range splits: automatic, but never more than a plan can have N tiles
+    // (a small shared plan would otherwise leave most splits empty and make
+    // the certification walk them); the layout keeps the allocation's stride
+    int ns = effective_nsplit(sequences, positions, pair);
+    if (!row_ids) {
+        const int64_t rows_bound = w_rows + (sp.Wst ? (sp.n_static + BN - 1) / BN * BN : 0);
+        const int64_t tiles = (rows_bound + BN - 1) / BN;
+        if (tiles < ns) ns = static_cast<int>(tiles > 0 ? tiles : 1);
+    }
+    const PrefillLayout L(sequences, positions, alloc_nsplit(sequences, positions));
     float* top_val = reinterpret_cast<float*>(ws + L.top_val);
     uint32_t* top_row = reinterpret_cast<uint32_t*>(ws + L.top_row);
     float* hnorm = reinterpret_cast<float*>(ws + L.hnorm);
@@ -1349,7 +1428,8 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     certify_kernel<<<static_cast<int>(blocks < sm_count() * 8 ? blocks : sm_count() * 8), 256, 0,
                      st>>>(positions, sequences, rmap, top_val, top_row,
                            flags, ns, hnorm, wmax, static_cast<float>(c) * 1.0001f, d_out_ids,
-                           d_out_max, stats, all_list, all_keys, pairs, rec_list, pos_keys);
+                           d_out_max, stats, all_list, all_keys, pairs, rec_list, pos_keys,
+                           reinterpret_cast<int32_t*>(ws + L.meta));
     SVT_LAUNCH_CHECK("certify_kernel");
     SVT_CUDA_TRY(cudaFuncSetAttribute(recompute_pairs_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));

@@ -167,7 +167,8 @@ class PrefillScorer:
         """Partial top-8 records of the last score(): (values f32
         [S*P, nsplit*8], plan rows u32-as-int32 [S*P, nsplit*8])."""
         npos = self.S * self.P
-        ns = _lib.lib.svt_prefill_effective_nsplit(self.S, self.P)
+        mo = _lib.lib.svt_prefill_meta_offset(self.S, self.P)
+        ns = int(self.ws[mo: mo + 4].view(torch.int32).item())  # splits the last call used
         o = self._offsets()
         v = self.ws[o[0]: o[0] + npos * ns * 32].view(torch.float32).view(npos, ns * 8)
         r = self.ws[o[1]: o[1] + npos * ns * 32].view(torch.int32).view(npos, ns * 8)
