@@ -431,8 +431,10 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
     // kernel reads the hidden states over PCIe while the PDL-launched GEMV
     // already streams weights, and the finalize writes the ids (and maxima)
     // straight into host memory. Measured at cfg2 it is no faster than the
-    // step graph (88 vs 86 us per call: the GEMV's pre-wait prefetch covers
-    // ~1 us of the ~6 us PCIe read), so the graph stays the default.
+    // step graph (82-88 vs 82-86 us per call): the pull kernel's PCIe reads
+    // take ~8.8 us for 229 KB at any grid from 32 to 296 CTAs (ncu), and the
+    // GEMV's pre-wait prefetch covers only its first ring stages of that, so
+    // the graph stays the default.
     const char* zc_env = getenv("SVT_SESSION_ZERO_COPY");
     const bool zero_copy = zc_env != nullptr && atoi(zc_env) != 0;
     void* dh = zero_copy ? mapped_cached(s, h_hidden) : nullptr;
