@@ -48,20 +48,23 @@ constexpr int BM = 128, BN = 256, BK = 64, TOPK = 8;
 constexpr int kMaxSplit = 8;  // N-range splits per M tile (partial top-8 records per position)
 constexpr int kTileA = BM * BK * 2;  // 16 KB: this CTA's 128 positions x 64 K
 constexpr int kGemmThreads = 192;
-constexpr uint32_t kTmemCols = 512;  // two 128 x 256 f32 accumulators
+constexpr int kBNSmall = 64;  // N tile for small problems (few N tiles: more CTAs busy)
 
 // Per-CTA-group-size geometry: NCTA = 1 (cta_group::1, M=128) or 2
-// (cta_group::2 CTA pair, M=256; each CTA holds half of the N=256 B tile)
-template <int NCTA>
+// (cta_group::2 CTA pair, M=256; each CTA holds half of the TBN-row B tile),
+// N tile TBN = 256 (BN), or kBNSmall when a launch has too few N tiles to
+// fill the SMs
+template <int NCTA, int TBN = BN>
 struct Geo {
-    static constexpr int kTileB = (BN / NCTA) * BK * 2;  // this CTA's B rows
+    static constexpr int kTileB = (TBN / NCTA) * BK * 2;  // this CTA's B rows
+    static constexpr uint32_t kTmemCols = 2 * TBN < 32 ? 32u : 2u * TBN;  // two accumulators
     static constexpr int kStage = kTileA + kTileB;
     static constexpr int kStages = NCTA == 1 ? 4 : 6;
     static constexpr int kEpiStage = 64 * 128 * 4;  // 64 columns x 128 positions (f32), insertion path
     static constexpr int kSmem = kStages * kStage + kEpiStage + 1024 /*align*/ + 256 /*barriers*/;
     // kind::f16 instruction descriptor: D f32, A/B bf16, both K-major
     static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) |
-                                       (uint32_t(BN >> 3) << 17) |
+                                       (uint32_t(TBN >> 3) << 17) |
                                        (uint32_t((BM * NCTA) >> 4) << 24);
 };
 
@@ -254,12 +257,13 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
 // MMA time. TMA completions land on the leader's full barriers; MMA commits
 // are multicast to both CTAs' empty / accumulator-full barriers; both CTAs'
 // epilogue warps release the accumulator on the leader's barrier.
-template <int NCTA>
+template <int NCTA, int TBN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
                     const __grid_constant__ CUtensorMap tmW,
                     const __grid_constant__ CUtensorMap tmS, const PrefillParams p) {
-    using G = Geo<NCTA>;
+    using G = Geo<NCTA, TBN>;
+    constexpr int BN = TBN;  // this instantiation's N tile
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-align the ring (TMA 128B swizzle + UMMA descriptors); the offset is
     // the same in both CTAs of a pair
@@ -312,7 +316,7 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc<NCTA>(tmem_slot, kTmemCols);
+    if (warp == 1) tmem_alloc<NCTA>(tmem_slot, G::kTmemCols);
     tc_fence_before();
     if constexpr (NCTA == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
@@ -535,6 +539,10 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
                             hi &= hi - 1;
                         }
                         float cv = epi[j * 128 + row];
+                        // the mask was taken against the 8th best before this
+                        // chunk; skip values it has risen past since (a fresh
+                        // record would otherwise insert all 64)
+                        if (!(cv > tv[TOPK - 1])) continue;
                         uint32_t cr = static_cast<uint32_t>(col0 + j);
 #pragma unroll
                         for (int i = 0; i < TOPK; ++i) {
@@ -575,7 +583,7 @@ prefill_gemm_kernel(const __grid_constant__ CUtensorMap tmH,
     if constexpr (NCTA == 2) cluster_sync_all(); else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<NCTA>(tmem_base, kTmemCols);
+        tmem_dealloc<NCTA>(tmem_base, G::kTmemCols);
     }
 }
 
@@ -1270,6 +1278,28 @@ extern "C" svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int3
 
 namespace svt {
 namespace {
+template <int NCTA, int TBN>
+cudaError_t launch_gemm(const CUtensorMap& mH, const CUtensorMap& mW, const CUtensorMap& mS,
+                        const PrefillParams& p, int grid, cudaStream_t st) {
+    using G = Geo<NCTA, TBN>;
+    cudaError_t e = cudaFuncSetAttribute(prefill_gemm_kernel<NCTA, TBN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = G::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = NCTA;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = NCTA == 2 ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<NCTA, TBN>, mH, mW, mS, p);
+}
+
 // static/dynamic split of the plans (svt_prefill_score_split)
 struct SplitArgs {
     const void* Wst = nullptr;         // the static rows [n_static, dim]
@@ -1303,10 +1333,20 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     // N-range splits: automatic, but never more than a plan can have N tiles
     // (a small shared plan would otherwise leave most splits empty and make
     // the certification walk them); the layout keeps the allocation's stride
+    // The N tile: 256, or kBNSmall when the 256-row tiles of the whole launch
+    // would keep fewer than half the SMs busy (a small shared plan scored as
+    // one sequence: 4 tiles at |S| = 1k use 8 of 148 SMs)
     int ns = effective_nsplit(sequences, positions, pair);
+    int tbn = BN;
     if (!row_ids) {
         const int64_t rows_bound = w_rows + (sp.Wst ? (sp.n_static + BN - 1) / BN * BN : 0);
-        const int64_t tiles = (rows_bound + BN - 1) / BN;
+        const int ncta = pair ? 2 : 1;
+        const int64_t groups = static_cast<int64_t>(sequences) * (positions / (BM * ncta));
+        const char* small_env = getenv("SVT_PREFILL_SMALL_N");  // 0: always 256 (A/B, tests)
+        const bool small_ok = small_env == nullptr || atoi(small_env) != 0;
+        if (small_ok && groups * ((rows_bound + BN - 1) / BN) * ncta < sm_count() / 2)
+            tbn = kBNSmall;
+        const int64_t tiles = (rows_bound + tbn - 1) / tbn;
         if (tiles < ns) ns = static_cast<int>(tiles > 0 ? tiles : 1);
     }
     const PrefillLayout L(sequences, positions, alloc_nsplit(sequences, positions));
@@ -1329,13 +1369,13 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     CUtensorMap mapH, mapW, mapS;
     if (svt_status s = make_map(&mapH, d_hidden, static_cast<uint64_t>(npos), dim, BM)) return s;
     if (svt_status s = make_map(&mapW, d_subheads, static_cast<uint64_t>(total_sub_rows > 0 ? total_sub_rows : 1), dim,
-                                row_ids ? 1u : (pair ? BN / 2 : BN)))
+                                row_ids ? 1u : static_cast<uint32_t>(pair ? tbn / 2 : tbn)))
         return s;
     const int64_t nTp = sp.Wst ? (sp.n_static + BN - 1) / BN * BN : 0;
     mapS = mapW;
     if (sp.Wst) {
         if (svt_status s = make_map(&mapS, sp.Wst, static_cast<uint64_t>(sp.n_static), dim,
-                                    pair ? BN / 2 : BN))
+                                    static_cast<uint32_t>(pair ? tbn / 2 : tbn)))
             return s;
     }
     RowMap rmap;
@@ -1394,29 +1434,14 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     p.top_val = top_val;
     p.top_row = top_row;
     p.flags = flags;
-    if (pair) {
-        using G = Geo<2>;
-        SVT_CUDA_TRY(cudaFuncSetAttribute(prefill_gemm_kernel<2>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(sequences * (positions / BM) * ns));
-        cfg.blockDim = dim3(kGemmThreads);
-        cfg.dynamicSmemBytes = G::kSmem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, prefill_gemm_kernel<2>, mapH, mapW, mapS, p));
-    } else {
-        using G = Geo<1>;
-        SVT_CUDA_TRY(cudaFuncSetAttribute(prefill_gemm_kernel<1>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
-        prefill_gemm_kernel<1><<<sequences * (positions / BM) * ns, kGemmThreads, G::kSmem, st>>>(
-            mapH, mapW, mapS, p);
+    {
+        const int grid = sequences * (positions / BM) * ns;
+        const cudaError_t e =
+            pair ? (tbn == BN ? launch_gemm<2, BN>(mapH, mapW, mapS, p, grid, st)
+                              : launch_gemm<2, kBNSmall>(mapH, mapW, mapS, p, grid, st))
+                 : (tbn == BN ? launch_gemm<1, BN>(mapH, mapW, mapS, p, grid, st)
+                              : launch_gemm<1, kBNSmall>(mapH, mapW, mapS, p, grid, st));
+        if (e != cudaSuccess) return cuda_status(e, "prefill_gemm_kernel launch");
     }
     SVT_LAUNCH_CHECK("prefill_gemm_kernel");
 

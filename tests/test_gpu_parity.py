@@ -444,12 +444,16 @@ def test_certified_near_ties_recompute(th):
     assert int(a.item()) == want and int(c.item()) == want
 
 
-@pytest.fixture(params=[(1, 4), (0, 1), (1, 3), (0, 8)], ids=lambda t: f"pair{t[0]}_split{t[1]}")
-def prefill_tuning(request):
+@pytest.fixture(params=[(1, 4, "1"), (0, 1, "1"), (1, 3, "0"), (0, 8, "0"), (1, 0, "1")],
+                ids=lambda t: f"pair{t[0]}_split{t[1]}_smallN{t[2]}")
+def prefill_tuning(request, monkeypatch):
+    """GEMM tuning: CTA pair or single CTA, N splits (0 = automatic), and
+    whether launches with few 256-row N tiles may switch to 64-row tiles."""
     from paper_2508_15229_b200 import prefill
 
     old = prefill.PrefillScorer.tuning()
-    prefill.PrefillScorer.set_tuning(*request.param)
+    prefill.PrefillScorer.set_tuning(request.param[0], request.param[1])
+    monkeypatch.setenv("SVT_PREFILL_SMALL_N", request.param[2])
     yield request.param
     prefill.PrefillScorer.set_tuning(*old)
 
