@@ -1334,8 +1334,10 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     // (a small shared plan would otherwise leave most splits empty and make
     // the certification walk them); the layout keeps the allocation's stride
     // The N tile: 256, or kBNSmall when the 256-row tiles of the whole launch
-    // would keep fewer than half the SMs busy (a small shared plan scored as
-    // one sequence: 4 tiles at |S| = 1k use 8 of 148 SMs)
+    // would keep fewer than a quarter of the SMs busy (a small shared plan
+    // scored as one sequence: 4 tiles at |S| = 1k use 8 of 148 SMs). A tile's
+    // K loop costs about the same at N = 64 as at 256, so this only pays
+    // when it turns idle SMs into working ones.
     int ns = effective_nsplit(sequences, positions, pair);
     int tbn = BN;
     if (!row_ids) {
@@ -1344,7 +1346,7 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
         const int64_t groups = static_cast<int64_t>(sequences) * (positions / (BM * ncta));
         const char* small_env = getenv("SVT_PREFILL_SMALL_N");  // 0: always 256 (A/B, tests)
         const bool small_ok = small_env == nullptr || atoi(small_env) != 0;
-        if (small_ok && groups * ((rows_bound + BN - 1) / BN) * ncta < sm_count() / 2)
+        if (small_ok && groups * ((rows_bound + BN - 1) / BN) * ncta < sm_count() / 4)
             tbn = kBNSmall;
         const int64_t tiles = (rows_bound + tbn - 1) / tbn;
         if (tiles < ns) ns = static_cast<int>(tiles > 0 ? tiles : 1);
