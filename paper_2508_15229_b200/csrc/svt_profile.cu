@@ -152,6 +152,20 @@ __device__ __forceinline__ void add_input(const ProfParams& p, const CtaState& c
     }
 }
 
+// df[id] += 1: the CTA-local slot if it holds (or can claim) this id
+__device__ __forceinline__ void df_add(const ProfParams& p, const CtaState& c, uint32_t id) {
+    const uint32_t slot = (id * 2654435761u) >> (32 - kDfSlotsLog);
+    uint32_t k = c.df_key[slot];
+    if (k == kEmpty) {
+        k = atomicCAS(&c.df_key[slot], kEmpty, id);
+        if (k == kEmpty) k = id;
+    }
+    if (k == id)
+        atomicAdd(&c.df_cnt[slot], 1u);
+    else
+        atomicAdd(&p.df[id], 1u);
+}
+
 // one output occurrence
 __device__ __forceinline__ void add_output(const ProfParams& p, const CtaState& c, uint32_t id,
                                            unsigned long long& copied, unsigned long long& n_out,
@@ -162,29 +176,25 @@ __device__ __forceinline__ void add_output(const ProfParams& p, const CtaState& 
     if (!(atomicOr(&c.bout[id >> 5], m) & m)) {
         ++n_out;
         n_dcopy += in ? 1 : 0;
-        // df: the CTA-local slot if it holds (or can claim) this id
-        const uint32_t slot = (id * 2654435761u) >> (32 - kDfSlotsLog);
-        uint32_t k = c.df_key[slot];
-        if (k == kEmpty) {
-            k = atomicCAS(&c.df_key[slot], kEmpty, id);
-            if (k == kEmpty) k = id;
-        }
-        if (k == id)
-            atomicAdd(&c.df_cnt[slot], 1u);
-        else
-            atomicAdd(&p.df[id], 1u);
+        df_add(p, c, id);
         if (!(p.out_union[id >> 5] & m)) atomicOr(&p.out_union[id >> 5], m);
     }
 }
 
-__device__ __forceinline__ void finish_doc(const ProfParams& p, int64_t doc, int64_t n_occ,
-                                           unsigned long long v[4]) {
-    if (threadIdx.x == 0) {
+__device__ __forceinline__ void finish_doc_lane0(const ProfParams& p, int64_t doc,
+                                                 int64_t n_occ, const unsigned long long v[4],
+                                                 int writer) {
+    if (writer == 0) {
         p.err_kind[doc] = 0;
         p.distinct_input[doc] = static_cast<uint32_t>(v[0]);
         p.overlap_occ[doc] = static_cast<double>(v[1]) / static_cast<double>(n_occ);
         p.overlap_dist[doc] = static_cast<double>(v[3]) / static_cast<double>(v[2]);
     }
+}
+
+__device__ __forceinline__ void finish_doc(const ProfParams& p, int64_t doc, int64_t n_occ,
+                                           unsigned long long v[4]) {
+    finish_doc_lane0(p, doc, n_occ, v, static_cast<int>(threadIdx.x));
 }
 
 __device__ __forceinline__ void report(const ProfParams& p, int64_t doc, int64_t bad_in,
@@ -197,12 +207,161 @@ __device__ __forceinline__ void report(const ProfParams& p, int64_t doc, int64_t
     }
 }
 
+// ---- the warp path: one warp per document ------------------------------------
+// Documents of up to kWarpIn inputs and kWarpOut outputs (the common case)
+// are profiled by one warp each, with the distinct-input and distinct-output
+// sets as open-addressing hash tables in the warp's shared memory (load
+// factor <= 1/2, first occurrence = the atomicCAS that claimed the slot).
+// No block barriers; the ids stay in registers.
+constexpr int kWarpIn = 512, kWarpOut = 256;
+constexpr int kInLog = 10, kOutLog = 9;  // 1024 / 512 slots
+constexpr int kPWarps = 8;
+constexpr size_t kWarpTables = static_cast<size_t>(kPWarps) * ((1u << kInLog) + (1u << kOutLog)) * 4;
+// + the CTA's own input / output union bitmaps (2 x V bits) when they fit;
+// they are OR-ed into the global unions once per CTA
+size_t warp_smem(int64_t nwords32, bool cta_unions) {
+    return kWarpTables + 2 * 4 * kDfSlots + (cta_unions ? 2 * 4 * static_cast<size_t>(nwords32) : 0);
+}
+
+__device__ __forceinline__ bool warp_fits(int64_t li, int64_t lo) {
+    return li <= kWarpIn && lo <= kWarpOut;
+}
+// true when `id` was not in the table (this call inserted it)
+template <int LOG>
+__device__ __forceinline__ bool hash_insert(uint32_t* t, uint32_t id) {
+    uint32_t s = (id * 2654435761u) >> (32 - LOG);
+    while (true) {
+        const uint32_t old = atomicCAS(&t[s], kEmpty, id);
+        if (old == kEmpty) return true;
+        if (old == id) return false;
+        s = (s + 1) & ((1u << LOG) - 1);
+    }
+}
+template <int LOG>
+__device__ __forceinline__ bool hash_contains(const uint32_t* t, uint32_t id) {
+    uint32_t s = (id * 2654435761u) >> (32 - LOG);
+    while (true) {
+        const uint32_t v = t[s];
+        if (v == id) return true;
+        if (v == kEmpty) return false;
+        s = (s + 1) & ((1u << LOG) - 1);
+    }
+}
+
+__global__ void __launch_bounds__(kPWarps * 32) profile_warp_kernel(ProfParams p,
+                                                                   int cta_unions) {
+    extern __shared__ uint32_t wsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* df_key = wsm;
+    uint32_t* df_cnt = wsm + kDfSlots;
+    uint32_t* tin = wsm + 2 * kDfSlots + warp * ((1 << kInLog) + (1 << kOutLog));
+    uint32_t* tout = tin + (1 << kInLog);
+    // unions: the CTA's bitmaps in shared memory, or the global ones
+    uint32_t* uin = cta_unions ? wsm + 2 * kDfSlots + kWarpTables / 4 : p.in_union;
+    uint32_t* uout = cta_unions ? uin + p.nwords32 : p.out_union;
+    for (int i = threadIdx.x; i < kDfSlots; i += blockDim.x) {
+        df_key[i] = kEmpty;
+        df_cnt[i] = 0u;
+    }
+    if (cta_unions)
+        for (int64_t i = threadIdx.x; i < 2 * p.nwords32; i += blockDim.x) uin[i] = 0u;
+    for (int i = lane; i < (1 << kInLog) + (1 << kOutLog); i += 32) tin[i] = kEmpty;
+    __syncthreads();
+    const CtaState c = {nullptr, nullptr, df_key, df_cnt};
+    constexpr int kIn = kWarpIn / 32, kOut = kWarpOut / 32;
+    for (int64_t doc = static_cast<int64_t>(blockIdx.x) * kPWarps + warp; doc < p.n_docs;
+         doc += static_cast<int64_t>(gridDim.x) * kPWarps) {
+        const int64_t ia = p.in_off[doc], ib = p.in_off[doc + 1];
+        const int64_t oa = p.out_off[doc], ob = p.out_off[doc + 1];
+        if (!warp_fits(ib - ia, ob - oa)) continue;  // the block kernel's document
+        uint32_t vin[kIn], vout[kOut];
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) {
+            const int64_t i = ia + k * 32 + lane;
+            vin[k] = i < ib ? p.in_ids[i] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kOut; ++k) {
+            const int64_t i = oa + k * 32 + lane;
+            vout[k] = i < ob ? p.out_ids[i] : 0u;
+        }
+        // ---- validation (reference order: input ids, output ids, empty) ------
+        int64_t bad_in = INT64_MAX, bad_out = INT64_MAX;
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) {
+            const int64_t i = ia + k * 32 + lane;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, i < ib && static_cast<int64_t>(vin[k]) >= p.V);
+            if (m && bad_in == INT64_MAX) bad_in = ia + k * 32 + __ffs(m) - 1;
+        }
+#pragma unroll
+        for (int k = 0; k < kOut; ++k) {
+            const int64_t i = oa + k * 32 + lane;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, i < ob && static_cast<int64_t>(vout[k]) >= p.V);
+            if (m && bad_out == INT64_MAX) bad_out = oa + k * 32 + __ffs(m) - 1;
+        }
+        if (bad_in != INT64_MAX) bad_out = INT64_MAX;
+        if (bad_in != INT64_MAX || bad_out != INT64_MAX || ob == oa) {
+            if (lane == 0) {
+                p.err_kind[doc] = bad_in != INT64_MAX ? 1 : bad_out != INT64_MAX ? 2 : 3;
+                p.err_id[doc] = bad_in != INT64_MAX    ? p.in_ids[bad_in]
+                                : bad_out != INT64_MAX ? p.out_ids[bad_out]
+                                                       : 0u;
+            }
+            continue;
+        }
+        unsigned long long v[4] = {0, 0, 0, 0};  // n_in, copied, n_out, n_dcopy
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) {
+            if (ia + k * 32 + lane < ib && hash_insert<kInLog>(tin, vin[k])) {
+                const uint32_t id = vin[k], m = 1u << (id & 31);
+                ++v[0];
+                if (!(uin[id >> 5] & m)) atomicOr(&uin[id >> 5], m);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kOut; ++k) {
+            if (oa + k * 32 + lane >= ob) continue;
+            const uint32_t id = vout[k], m = 1u << (id & 31);
+            const bool in = hash_contains<kInLog>(tin, id);
+            v[1] += in ? 1 : 0;
+            if (hash_insert<kOutLog>(tout, id)) {
+                ++v[2];
+                v[3] += in ? 1 : 0;
+                df_add(p, c, id);
+                if (!(uout[id >> 5] & m)) atomicOr(&uout[id >> 5], m);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xFFFFFFFFu, v[k], o);
+        finish_doc_lane0(p, doc, ob - oa, v, lane);
+        __syncwarp();
+        for (int i = lane; i < (1 << kInLog) + (1 << kOutLog); i += 32) tin[i] = kEmpty;
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kDfSlots; i += blockDim.x)
+        if (df_cnt[i]) atomicAdd(&p.df[df_key[i]], df_cnt[i]);
+    if (cta_unions)
+        for (int64_t i = threadIdx.x; i < p.nwords32; i += blockDim.x) {
+            if (uin[i]) atomicOr(&p.in_union[i], uin[i]);
+            if (uout[i]) atomicOr(&p.out_union[i], uout[i]);
+        }
+}
+
+// ---- the block path: documents past the warp path's sizes ---------------------
+// One CTA per document, V-bit shared-memory bitmaps. The CTA scans a chunk of
+// kProfThreads documents at a time for the ones the warp path skipped.
 __global__ void __launch_bounds__(kProfThreads) profile_kernel(ProfParams p) {
     extern __shared__ uint32_t bits[];  // [0, nwords32): input set, [nwords32, 2x): output set
     __shared__ unsigned long long red[kProfThreads / 32];
     __shared__ unsigned long long red4[4][kProfThreads / 32];
     __shared__ uint32_t df_key[kDfSlots];
     __shared__ uint32_t df_cnt[kDfSlots];
+    __shared__ int64_t s_docs[kProfThreads];
+    __shared__ int s_n;
     const CtaState c = {bits, bits + p.nwords32, df_key, df_cnt};
     for (int64_t w = threadIdx.x; w < 2 * p.nwords32; w += kProfThreads) bits[w] = 0u;
     for (int i = threadIdx.x; i < kDfSlots; i += kProfThreads) {
@@ -210,98 +369,104 @@ __global__ void __launch_bounds__(kProfThreads) profile_kernel(ProfParams p) {
         df_cnt[i] = 0u;
     }
     __syncthreads();
-    const int64_t G = gridDim.x;
-    DocOff off = load_off(p, blockIdx.x);
-    DocIds ids = load_ids(p, off);
-    DocOff off_next = load_off(p, blockIdx.x + G);
-    for (int64_t doc = blockIdx.x; doc < p.n_docs; doc += G) {
-        // prefetch: the next document's ids, the one after's offsets
-        const DocIds ids_next = load_ids(p, off_next);
-        const DocOff off_next2 = load_off(p, doc + 2 * G);
-        const int64_t ia = off.ia, ib = off.ib, oa = off.oa, ob = off.ob;
-        if (fits(off)) {
-            // ---- validation (reference order: input ids, output ids, empty) --
-            unsigned long long bi = ~0ull, bo = ~0ull;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kProfThreads; base < p.n_docs;
+         base += static_cast<int64_t>(gridDim.x) * kProfThreads) {
+        const int64_t d = base + threadIdx.x;
+        const bool mine =
+            d < p.n_docs &&
+            !warp_fits(p.in_off[d + 1] - p.in_off[d], p.out_off[d + 1] - p.out_off[d]);
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        if (mine) s_docs[atomicAdd(&s_n, 1)] = d;
+        __syncthreads();
+        const int n_long = s_n;
+        for (int q = 0; q < n_long; ++q) {
+            const int64_t doc = s_docs[q];
+            const DocOff off = load_off(p, doc);
+            const DocIds ids = load_ids(p, off);
+            const int64_t ia = off.ia, ib = off.ib, oa = off.oa, ob = off.ob;
+            if (fits(off)) {
+                // ---- validation (reference order: input ids, output ids, empty) --
+                unsigned long long bi = ~0ull, bo = ~0ull;
 #pragma unroll
-            for (int k = kRin - 1; k >= 0; --k) {
-                const int64_t i = ia + threadIdx.x + k * kProfThreads;
-                if (i < ib && static_cast<int64_t>(ids.in[k]) >= p.V) bi = i;
-            }
+                for (int k = kRin - 1; k >= 0; --k) {
+                    const int64_t i = ia + threadIdx.x + k * kProfThreads;
+                    if (i < ib && static_cast<int64_t>(ids.in[k]) >= p.V) bi = i;
+                }
 #pragma unroll
-            for (int k = kRout - 1; k >= 0; --k) {
-                const int64_t i = oa + threadIdx.x + k * kProfThreads;
-                if (i < ob && static_cast<int64_t>(ids.out[k]) >= p.V) bo = i;
-            }
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                for (int k = kRout - 1; k >= 0; --k) {
+                    const int64_t i = oa + threadIdx.x + k * kProfThreads;
+                    if (i < ob && static_cast<int64_t>(ids.out[k]) >= p.V) bo = i;
+                }
+                const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long x = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
-                const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, bo, o);
-                bi = x < bi ? x : bi;
-                bo = y < bo ? y : bo;
-            }
-            if (lane == 0) {
-                red4[0][warp] = bi;
-                red4[1][warp] = bo;
-            }
-            __syncthreads();
-            for (int i = 0; i < kProfThreads / 32; ++i) {
-                bi = red4[0][i] < bi ? red4[0][i] : bi;
-                bo = red4[1][i] < bo ? red4[1][i] : bo;
-            }
-            __syncthreads();  // (red4 is reused below)
-            const int64_t bad_in = bi == ~0ull ? INT64_MAX : static_cast<int64_t>(bi);
-            const int64_t bad_out =
-                bad_in != INT64_MAX || bo == ~0ull ? INT64_MAX : static_cast<int64_t>(bo);
-            if (bad_in != INT64_MAX || bad_out != INT64_MAX || ob == oa) {
-                report(p, doc, bad_in, bad_out);
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long x = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+                    const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, bo, o);
+                    bi = x < bi ? x : bi;
+                    bo = y < bo ? y : bo;
+                }
+                if (lane == 0) {
+                    red4[0][warp] = bi;
+                    red4[1][warp] = bo;
+                }
+                __syncthreads();
+                for (int i = 0; i < kProfThreads / 32; ++i) {
+                    bi = red4[0][i] < bi ? red4[0][i] : bi;
+                    bo = red4[1][i] < bo ? red4[1][i] : bo;
+                }
+                __syncthreads();  // (red4 is reused below)
+                const int64_t bad_in = bi == ~0ull ? INT64_MAX : static_cast<int64_t>(bi);
+                const int64_t bad_out =
+                    bad_in != INT64_MAX || bo == ~0ull ? INT64_MAX : static_cast<int64_t>(bo);
+                if (bad_in != INT64_MAX || bad_out != INT64_MAX || ob == oa) {
+                    report(p, doc, bad_in, bad_out);
+                } else {
+                    unsigned long long v[4] = {0, 0, 0, 0};  // n_in, copied, n_out, n_dcopy
+#pragma unroll
+                    for (int k = 0; k < kRin; ++k)
+                        if (ia + threadIdx.x + k * kProfThreads < ib) add_input(p, c, ids.in[k], v[0]);
+                    __syncthreads();
+#pragma unroll
+                    for (int k = 0; k < kRout; ++k)
+                        if (oa + threadIdx.x + k * kProfThreads < ob)
+                            add_output(p, c, ids.out[k], v[1], v[2], v[3]);
+                    block_sum4(v, red4);
+                    finish_doc(p, doc, ob - oa, v);
+                    // clear only the words this document touched
+#pragma unroll
+                    for (int k = 0; k < kRin; ++k)
+                        if (ia + threadIdx.x + k * kProfThreads < ib) c.bin[ids.in[k] >> 5] = 0u;
+#pragma unroll
+                    for (int k = 0; k < kRout; ++k)
+                        if (oa + threadIdx.x + k * kProfThreads < ob) c.bout[ids.out[k] >> 5] = 0u;
+                    __syncthreads();
+                }
             } else {
-                unsigned long long v[4] = {0, 0, 0, 0};  // n_in, copied, n_out, n_dcopy
-#pragma unroll
-                for (int k = 0; k < kRin; ++k)
-                    if (ia + threadIdx.x + k * kProfThreads < ib) add_input(p, c, ids.in[k], v[0]);
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < kRout; ++k)
-                    if (oa + threadIdx.x + k * kProfThreads < ob)
-                        add_output(p, c, ids.out[k], v[1], v[2], v[3]);
-                block_sum4(v, red4);
-                finish_doc(p, doc, ob - oa, v);
-                // clear only the words this document touched
-#pragma unroll
-                for (int k = 0; k < kRin; ++k)
-                    if (ia + threadIdx.x + k * kProfThreads < ib) c.bin[ids.in[k] >> 5] = 0u;
-#pragma unroll
-                for (int k = 0; k < kRout; ++k)
-                    if (oa + threadIdx.x + k * kProfThreads < ob) c.bout[ids.out[k] >> 5] = 0u;
-                __syncthreads();
-            }
-        } else {
-            // ---- a long document: straight from global memory ------------------
-            const int64_t bad_in = first_bad(p.in_ids, ia, ib, p.V, red);
-            const int64_t bad_out =
-                bad_in == INT64_MAX ? first_bad(p.out_ids, oa, ob, p.V, red) : INT64_MAX;
-            if (bad_in != INT64_MAX || bad_out != INT64_MAX || ob == oa) {
-                report(p, doc, bad_in, bad_out);
-            } else {
-                unsigned long long v[4] = {0, 0, 0, 0};
-                for (int64_t i = ia + threadIdx.x; i < ib; i += kProfThreads)
-                    add_input(p, c, p.in_ids[i], v[0]);
-                __syncthreads();
-                for (int64_t i = oa + threadIdx.x; i < ob; i += kProfThreads)
-                    add_output(p, c, p.out_ids[i], v[1], v[2], v[3]);
-                block_sum4(v, red4);
-                finish_doc(p, doc, ob - oa, v);
-                for (int64_t i = ia + threadIdx.x; i < ib; i += kProfThreads)
-                    c.bin[p.in_ids[i] >> 5] = 0u;
-                for (int64_t i = oa + threadIdx.x; i < ob; i += kProfThreads)
-                    c.bout[p.out_ids[i] >> 5] = 0u;
-                __syncthreads();
+                // ---- a long document: straight from global memory ------------------
+                const int64_t bad_in = first_bad(p.in_ids, ia, ib, p.V, red);
+                const int64_t bad_out =
+                    bad_in == INT64_MAX ? first_bad(p.out_ids, oa, ob, p.V, red) : INT64_MAX;
+                if (bad_in != INT64_MAX || bad_out != INT64_MAX || ob == oa) {
+                    report(p, doc, bad_in, bad_out);
+                } else {
+                    unsigned long long v[4] = {0, 0, 0, 0};
+                    for (int64_t i = ia + threadIdx.x; i < ib; i += kProfThreads)
+                        add_input(p, c, p.in_ids[i], v[0]);
+                    __syncthreads();
+                    for (int64_t i = oa + threadIdx.x; i < ob; i += kProfThreads)
+                        add_output(p, c, p.out_ids[i], v[1], v[2], v[3]);
+                    block_sum4(v, red4);
+                    finish_doc(p, doc, ob - oa, v);
+                    for (int64_t i = ia + threadIdx.x; i < ib; i += kProfThreads)
+                        c.bin[p.in_ids[i] >> 5] = 0u;
+                    for (int64_t i = oa + threadIdx.x; i < ob; i += kProfThreads)
+                        c.bout[p.out_ids[i] >> 5] = 0u;
+                    __syncthreads();
+                }
             }
         }
-        off = off_next;
-        ids = ids_next;
-        off_next = off_next2;
+        __syncthreads();
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kDfSlots; i += kProfThreads)
@@ -368,12 +533,29 @@ extern "C" svt_status svt_profile_batch(size_t vocab_size, const uint32_t* d_inp
                   vocab_size);
         return SVT_ERR_CONFIG;
     }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // documents up to kWarpIn / kWarpOut ids: one warp each
+    {
+        const bool cta_unions = warp_smem(p.nwords32, true) <= 200 * 1024;
+        const size_t wsmem = warp_smem(p.nwords32, cta_unions);
+        SVT_CUDA_TRY(cudaFuncSetAttribute(profile_warp_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(wsmem)));
+        const int per_sm = static_cast<int>((228 * 1024) / (wsmem + 1024));
+        const int64_t cap = static_cast<int64_t>(sm_count()) * (per_sm > 0 ? per_sm : 1);
+        const int64_t want = (n_docs + kPWarps - 1) / kPWarps;
+        profile_warp_kernel<<<static_cast<int>(want < cap ? want : cap), kPWarps * 32, wsmem,
+                              st>>>(p, cta_unions ? 1 : 0);
+        SVT_LAUNCH_CHECK("profile_warp_kernel");
+    }
+    // longer documents: one CTA each, V-bit bitmaps
     SVT_CUDA_TRY(cudaFuncSetAttribute(profile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
-    const int per_sm = static_cast<int>((228 * 1024) / (smem + 2048 + 2 * 4 * kDfSlots));
+    const int per_sm = static_cast<int>((228 * 1024) / (smem + 4096 + 2 * 4 * kDfSlots));
     const int64_t cap = static_cast<int64_t>(sm_count()) * (per_sm > 0 ? per_sm : 1);
-    const int grid = static_cast<int>(n_docs < cap ? n_docs : cap);
-    profile_kernel<<<grid, kProfThreads, smem, static_cast<cudaStream_t>(stream)>>>(p);
+    const int64_t chunks = (n_docs + kProfThreads - 1) / kProfThreads;
+    const int grid = static_cast<int>(chunks < cap ? chunks : cap);
+    profile_kernel<<<grid, kProfThreads, smem, st>>>(p);
     SVT_LAUNCH_CHECK("profile_kernel");
     return SVT_OK;
 }
