@@ -531,9 +531,9 @@ svt_status svt_tolerance_filter(const uint64_t* d_candidate_words,
                                 const uint32_t* d_df, size_t n_df, int64_t doc_count, double tau,
                                 uint64_t* d_kept_words, uint32_t* d_pruned, int64_t* d_n_pruned,
                                 uint64_t* d_pruned_df_sum, svt_stream stream);
-/* (f3) Profiler::add (profiler.cpp:56-97) over a CSR batch of documents, one
- * CTA per document with its distinct-input / distinct-output sets as shared-
- * memory bitmaps. Accumulates into d_df (u32 [V]) and the two union bitmaps
+/* (f3) Profiler::add (profiler.cpp:56-97) over a CSR batch of documents: a
+ * warp per document (up to 512 inputs / 256 outputs; shared-memory hash
+ * sets), a CTA per longer document (shared-memory bitmaps). Accumulates into d_df (u32 [V]) and the two union bitmaps
  * (ceil(V/64) words, OR); writes per document (submission order)
  * distinct_input, overlap_occurrence, overlap_distinct (exact integer
  * quotients, equal to the reference's doubles) and d_err_kind: 0 ok, 1 an

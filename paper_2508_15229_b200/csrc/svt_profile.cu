@@ -10,13 +10,16 @@
 //   an input id >= V (IntegrityError naming the first one), then an output
 //   id >= V, then an empty output (ParseError).
 //
-// B200 form: one CTA per document (grid-stride over a batch); the document's
-// distinct-input and distinct-output sets are two V-bit bitmaps in shared
-// memory (32 KB each at V = 256,000), filled with shared-memory atomicOr whose
-// return value says "first occurrence". Corpus-level state (df counts and the
-// two unions) is updated with global atomics only on first occurrences, so
-// the result does not depend on document order (the per-document ratios are
-// exact integer quotients, identical to the reference's doubles).
+// B200 form: documents of up to 512 inputs / 256 outputs take one warp each,
+// with the document's distinct-input and distinct-output sets as hash tables
+// in the warp's shared memory (the atomicCAS that claims a slot is the first
+// occurrence). Longer documents take one CTA each, with the two sets as V-bit
+// bitmaps in shared memory (32 KB each at V = 256,000) filled by atomicOr
+// whose return value says "first occurrence". Corpus-level state (df counts
+// and the two unions) changes only on first occurrences, through CTA-local
+// caches flushed with global atomics, so the result does not depend on
+// document order (the per-document ratios are exact integer quotients,
+// identical to the reference's doubles).
 #include "svt_common.cuh"
 
 namespace svt {
