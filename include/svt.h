@@ -519,8 +519,9 @@ svt_status svt_plan_from_json(const char* text, size_t len, const char* origin, 
 /* ------------------------------------------------------------------------
  * (f4) Tolerance filter of the static builder (static_builder.cpp:79-121),
  * on the GPU: the non-protected candidates ordered by (df, id) lose the
- * longest prefix whose df total stays within tau * doc_count. One CTA finds
- * the cut by value (radix select on the df threshold, no sort) and writes
+ * longest prefix whose df total stays within tau * doc_count. The cut is
+ * found by value (radix select on the df threshold, no sort; a cooperative
+ * multi-CTA launch, one CTA for small universes) and the call writes
  * kept = candidates \ pruned (ceil(universe/64) words) and the pruned ids
  * ascending (capacity |candidates|); *d_n_pruned and *d_pruned_df_sum are
  * device scalars. d_always_keep_words may be NULL; df beyond n_df counts 0.

@@ -21,6 +21,7 @@
 // Edge cases follow the reference's comparison: budget < 0 prunes nothing,
 // NaN / +inf budget prunes every prunable id; df beyond the df array is 0.
 #include <cmath>
+#include <cstdlib>
 
 #include "svt_common.cuh"
 
@@ -231,6 +232,199 @@ __global__ void __launch_bounds__(kTolThreads, 1) tolerance_kernel(TolParams p) 
     }
 }
 
+
+// ---- the multi-CTA form (one cooperative launch, G co-resident CTAs) ---------
+// Same algorithm, the id range split into G contiguous slices. The radix
+// levels add per-CTA histograms into a global one and meet at a grid
+// barrier; every CTA then derives the same pick. The output pass needs, per
+// CTA, the ids with df < v* and df == v* before its slice (a scan of G counts
+// after a barrier), so pruned ids land in id order. The scratch (histograms,
+// counts, barrier counter) lives in the kept-words output, zeroed by the host
+// and overwritten only after the last barrier.
+struct TolScratch {
+    unsigned long long hist[4][kBuckets];
+    unsigned long long bar;
+    unsigned long long cnt[1];  // [2 * G]: df < v*, df == v* per CTA
+};
+constexpr size_t tol_scratch_bytes(int G) {
+    return sizeof(unsigned long long) * (4 * kBuckets + 1 + 2 * static_cast<size_t>(G));
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1ull);
+        while (*reinterpret_cast<volatile unsigned long long*>(bar) < target) __nanosleep(32);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTolThreads, 1) tolerance_multi_kernel(TolParams p) {
+    extern __shared__ unsigned long long hist[];  // [warp][bucket] df sums
+    __shared__ uint64_t red[kTolWarps];
+    __shared__ uint64_t s_below, s_before_lt, s_before_eq;
+    __shared__ uint32_t s_prefix;
+    __shared__ int s_all;
+    TolScratch* sc = reinterpret_cast<TolScratch*>(p.kept);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int G = gridDim.x, cta = blockIdx.x;
+    // this CTA's words [w0, w1)
+    const int64_t per = (p.nwords + G - 1) / G;
+    const int64_t w0 = min(p.nwords, per * cta), w1 = min(p.nwords, w0 + per);
+    const int64_t id_lo = w0 * 64, id_hi = w1 * 64;
+    unsigned long long nbar = 0;
+
+    uint64_t vstar, S = 0;
+    if (p.mode == 1) {
+        vstar = 0;
+    } else if (p.mode == 2) {
+        vstar = 1ull << 33;
+    } else {
+        if (t == 0) {
+            s_below = 0;
+            s_prefix = 0;
+            s_all = 0;
+        }
+        unsigned long long* mine = hist + warp * kBuckets;
+        for (int level = 0; level < 4; ++level) {
+            const int shift = 24 - 8 * level;
+            const uint64_t hi_mask =
+                level == 0 ? 0ull : (0xFFFFFFFFull << (shift + 8)) & 0xFFFFFFFFull;
+            for (int i = t; i < kTolWarps * kBuckets; i += kTolThreads) hist[i] = 0ull;
+            __syncthreads();
+            const uint64_t prefix = s_prefix;
+            for (int64_t base = id_lo; base < id_hi; base += 4 * kTolThreads) {
+                uint64_t d[4];
+                bool in[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t id = base + k * kTolThreads + t;
+                    in[k] = id < id_hi && ((prunable_word(p, id >> 6) >> (id & 63)) & 1ull);
+                    d[k] = in[k] ? df_of(p, id) : 0ull;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool m = in[k] && (d[k] & hi_mask) == prefix;
+                    hist_add(mine, m, static_cast<uint32_t>((d[k] >> shift) & 0xFF), d[k]);
+                }
+            }
+            __syncthreads();
+            if (t < kBuckets) {
+                unsigned long long sum = 0;
+                for (int w = 0; w < kTolWarps; ++w) sum += hist[w * kBuckets + t];
+                if (sum) atomicAdd(&sc->hist[level][t], sum);
+            }
+            grid_barrier(&sc->bar, static_cast<unsigned long long>(G) * ++nbar);
+            if (t == 0) {
+                uint64_t below = s_below;
+                int pick = -1;
+                for (int b = 0; b < kBuckets; ++b) {
+                    const uint64_t h = __ldcg(&sc->hist[level][b]);
+                    if (below + h > p.B) {
+                        pick = b;
+                        break;
+                    }
+                    below += h;
+                }
+                if (pick < 0)
+                    s_all = 1;
+                else
+                    s_prefix =
+                        static_cast<uint32_t>(prefix | (static_cast<uint64_t>(pick) << shift));
+                s_below = below;
+            }
+            __syncthreads();
+            if (s_all) break;
+        }
+        vstar = s_all ? (1ull << 32) : static_cast<uint64_t>(s_prefix);
+        S = s_below;
+    }
+    uint64_t j = 0;
+    if (p.mode == 0 && vstar <= 0xFFFFFFFFull && vstar > 0) j = (p.B - S) / vstar;
+
+    // ---- counts before this slice ----------------------------------------------
+    uint64_t n_lt = 0, n_eq = 0;
+    for (int64_t id = id_lo + t; id < id_hi; id += kTolThreads) {
+        if (!((prunable_word(p, id >> 6) >> (id & 63)) & 1ull)) continue;
+        const uint64_t d = df_of(p, id);
+        n_lt += d < vstar ? 1 : 0;
+        n_eq += d == vstar ? 1 : 0;
+    }
+    uint64_t tot_lt = 0, tot_eq = 0;
+    block_excl_scan(n_lt, red, &tot_lt);
+    block_excl_scan(n_eq, red, &tot_eq);
+    if (t == 0) {
+        sc->cnt[2 * cta] = tot_lt;
+        sc->cnt[2 * cta + 1] = tot_eq;
+    }
+    grid_barrier(&sc->bar, static_cast<unsigned long long>(G) * ++nbar);
+    if (t == 0) {
+        uint64_t blt = 0, beq = 0;
+        for (int c = 0; c < cta; ++c) {
+            blt += __ldcg(&sc->cnt[2 * c]);
+            beq += __ldcg(&sc->cnt[2 * c + 1]);
+        }
+        s_before_lt = blt;
+        s_before_eq = beq;
+    }
+    // every CTA has its prefix before the kept words (the scratch) are written
+    grid_barrier(&sc->bar, static_cast<unsigned long long>(G) * ++nbar);
+    const uint64_t eq_before = s_before_eq;
+    uint64_t out_at = s_before_lt + (eq_before < j ? eq_before : j);
+    uint64_t eq_seen = eq_before, dsum = 0;
+    for (int64_t base = id_lo; base < id_hi; base += kChunk) {
+        const int64_t id0 = base + static_cast<int64_t>(t) * kItems;
+        const bool live = id0 < id_hi;
+        const uint64_t cw = live ? __ldg(p.cand + (id0 >> 6)) : 0ull;
+        const uint64_t pw = live ? prunable_word(p, id0 >> 6) : 0ull;
+        const uint32_t pbits = static_cast<uint32_t>((pw >> (id0 & 63)) & 0xFFu);
+        uint64_t d[kItems];
+        uint32_t ne = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            d[k] = (pbits >> k) & 1u ? df_of(p, id0 + k) : 0ull;
+            ne += ((pbits >> k) & 1u) && d[k] == vstar ? 1u : 0u;
+        }
+        uint64_t eq_tot = 0;
+        uint64_t eq_rank = eq_seen + block_excl_scan(ne, red, &eq_tot);
+        uint32_t cut = 0;
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            if (!((pbits >> k) & 1u)) continue;
+            if (d[k] < vstar) {
+                cut |= 1u << k;
+            } else if (d[k] == vstar) {
+                if (eq_rank < j) cut |= 1u << k;
+                ++eq_rank;
+            }
+        }
+        uint64_t cut_tot = 0;
+        uint64_t pos = out_at + block_excl_scan(__popc(cut), red, &cut_tot);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k)
+            if ((cut >> k) & 1u) {
+                p.pruned[pos++] = static_cast<uint32_t>(id0 + k);
+                dsum += d[k];
+            }
+        uint64_t pm = static_cast<uint64_t>(cut) << (id0 & 63);
+        pm |= __shfl_xor_sync(0xFFFFFFFFu, pm, 1);
+        pm |= __shfl_xor_sync(0xFFFFFFFFu, pm, 2);
+        pm |= __shfl_xor_sync(0xFFFFFFFFu, pm, 4);
+        if ((lane & 7) == 0 && live) p.kept[id0 >> 6] = cw & ~pm;
+        out_at += cut_tot;
+        eq_seen += eq_tot;
+    }
+    uint64_t dsum_tot = 0;
+    block_excl_scan(dsum, red, &dsum_tot);
+    const uint64_t my_cuts = out_at - (s_before_lt + (eq_before < j ? eq_before : j));
+    if (t == 0) {
+        if (my_cuts) atomicAdd(reinterpret_cast<unsigned long long*>(p.n_pruned), my_cuts);
+        if (dsum_tot) atomicAdd(reinterpret_cast<unsigned long long*>(p.df_sum), dsum_tot);
+    }
+}
+
 }  // namespace
 }  // namespace svt
 
@@ -271,9 +465,38 @@ extern "C" svt_status svt_tolerance_filter(const uint64_t* d_candidate_words,
         p.mode = 0;
         p.B = static_cast<uint64_t>(std::floor(budget));
     }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // many CTAs (one cooperative launch) when the kept words can hold the
+    // scratch for at least 8 of them; one CTA otherwise (small universes)
+    const char* env = getenv("SVT_TOLERANCE_CTAS");  // A/B and tests: force a CTA count
+    int G = sm_count();
+    const size_t kept_bytes = static_cast<size_t>(p.nwords) * 8;
+    while (G > 1 && tol_scratch_bytes(G) > kept_bytes) G /= 2;
+    if (G < 8) G = 1;
+    if (env) G = atoi(env) > 0 ? atoi(env) : 1;
+    if (G > 1 && tol_scratch_bytes(G) > kept_bytes) G = 1;
+    if (G > 1) {
+        int per_sm = 0;
+        SVT_CUDA_TRY(cudaFuncSetAttribute(tolerance_multi_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kTolSmem)));
+        SVT_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tolerance_multi_kernel,
+                                                                   kTolThreads, kTolSmem));
+        if (per_sm * sm_count() < G) G = 1;
+    }
+    if (G > 1) {
+        SVT_CUDA_TRY(cudaMemsetAsync(d_kept_words, 0, tol_scratch_bytes(G), st));
+        SVT_CUDA_TRY(cudaMemsetAsync(d_n_pruned, 0, sizeof(int64_t), st));
+        SVT_CUDA_TRY(cudaMemsetAsync(d_pruned_df_sum, 0, sizeof(uint64_t), st));
+        void* args[] = {&p};
+        SVT_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tolerance_multi_kernel),
+                                                 dim3(G), dim3(kTolThreads), args, kTolSmem, st));
+        SVT_LAUNCH_CHECK("tolerance_multi_kernel");
+        return SVT_OK;
+    }
     SVT_CUDA_TRY(cudaFuncSetAttribute(tolerance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kTolSmem)));
-    tolerance_kernel<<<1, kTolThreads, kTolSmem, static_cast<cudaStream_t>(stream)>>>(p);
+    tolerance_kernel<<<1, kTolThreads, kTolSmem, st>>>(p);
     SVT_LAUNCH_CHECK("tolerance_kernel");
     return SVT_OK;
 }

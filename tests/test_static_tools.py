@@ -169,10 +169,13 @@ def test_oracle_profiler_matches_reference():
 
 # ---- GPU --------------------------------------------------------------------------
 @pytest.mark.gpu
-def test_gpu_tolerance_filter_matches_oracle():
+@pytest.mark.parametrize("ctas", [None, "3", "1"], ids=["auto", "3ctas", "1cta"])
+def test_gpu_tolerance_filter_matches_oracle(monkeypatch, ctas):
     from paper_2508_15229_b200 import corpus
     from paper_2508_15229_b200.tailored_head import TokenSet
 
+    if ctas is not None:  # the multi-CTA cooperative kernel or the single-CTA one
+        monkeypatch.setenv("SVT_TOLERANCE_CTAS", ctas)
     for cand, keep, U, df, M, tau in tol_cases():
         st, kept, pruned, s = tol(ORC, "orc_", cand, keep, U, df, M, tau)
         c = TokenSet(U)
