@@ -6,7 +6,8 @@
 // prefix whose running df total stays within tau * doc_count is pruned
 // (the loop breaks at the first id with double(cumulative + df) > budget).
 //
-// Instead of sorting, one CTA finds the prefix by value:
+// Instead of sorting, the prefix is found by value (the multi-CTA form is at
+// the end of the file; this is the one-CTA form):
 //   S(v) = sum of df over prunable ids with df < v is non-decreasing in v,
 //   so v* = max{v : S(v) <= B} (B = floor(budget)) is the smallest df value
 //   x with S(x) + x * count(x) > B. It is found by a 4-level radix select on
