@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="interleaved", choices=["interleaved", "fused"])
+    ap.add_argument("--mode", default="interleaved", choices=["interleaved", "split", "fused"])
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--no-secondary", action="store_true")
@@ -186,6 +186,10 @@ class Job:
         self.out = torch.empty((steps, B), dtype=torch.int32, device="cuda")
         self.torch = torch
         self.rdec = None
+        self.sdec = None
+        if B > 1:
+            # shared static rows: scored once per step for the whole batch
+            self.sdec = th.SplitDecoder(self.tb, self.head)
         if B == 1:
             # batch-1 latency path: row-major sub-head + certified decode
             n = int(self.tb.n_active[0].item())
@@ -199,11 +203,16 @@ class Job:
         elif mode == "rows":
             self.rdec.stream = tb.stream
             self.rdec.gather()
+        elif mode == "split":
+            self.sdec.stream = tb.stream
+            self.sdec.prepare()
         for t in range(self.steps):
             if dec_events is not None:
                 dec_events[t][0].record()
             if mode == "rows":
                 self.rdec.greedy(self.hidden[t][0], self.out[t])
+            elif mode == "split":
+                self.sdec.greedy(self.hidden[t], self.out[t])
             else:
                 tb.greedy(self.hidden[t], self.out[t], fused=(mode == "fused"))
             if dec_events is not None:
@@ -214,9 +223,13 @@ class Job:
         # exact-order GEMV and its programmatic-dependent argmax finalize
         if mode == "rows":  # select + layout + row gather + one launch per token
             return 3 + self.steps
+        if mode == "split":  # + split + dynamic layout + gather; static, GEMV, finalize, combine
+            return 5 + 4 * self.steps
         return 2 + (1 if mode == "interleaved" else 0) + 2 * self.steps
 
-    def decode_bytes(self):
+    def decode_bytes(self, mode="interleaved"):
+        if mode == "split":
+            return self.sdec.algorithmic_decode_bytes(self.esize, self.cfg["d"])
         return self.tb.algorithmic_decode_bytes(self.esize, self.cfg["d"])
 
 
@@ -238,15 +251,22 @@ def capture_job(job, mode, torch):
         elif mode == "rows":
             job.rdec.stream = s
             job.rdec.gather()
+        elif mode == "split":
+            job.sdec.stream = s
+            job.sdec.prepare()
     with torch.cuda.graph(decode, stream=s):
         for t in range(job.steps):
             if mode == "rows":
                 job.rdec.greedy(job.hidden[t][0], job.out[t])
+            elif mode == "split":
+                job.sdec.greedy(job.hidden[t], job.out[t])
             else:
                 job.tb.greedy(job.hidden[t], job.out[t], fused=(mode == "fused"))
     job.tb.stream = None
     if job.rdec is not None:
         job.rdec.stream = None
+    if job.sdec is not None:
+        job.sdec.stream = None
     return s, prep, decode
 
 
@@ -941,6 +961,21 @@ def secondary(args, torch, th, synth):
     gbs = job.decode_bytes() / (dec_avg / 1e3) / 1e9
     out["cfg2_fused"] = {"tokens_per_s": args.batch * args.decode_steps * 5 / (ms / 1e3),
                          "decode_us": dec_avg * 1e3, "decode_gbs": gbs, "frac": gbs / peak}
+    ref_out = None
+    ms_i, dec_i, _ = time_job(job, "interleaved", 5, 2, torch, None, 1)
+    ref_out = job.out.cpu().numpy().copy()
+    ms, dec_ms, _ = time_job(job, "split", 5, 2, torch, None, 1)
+    dec_avg = sum(dec_ms) / len(dec_ms)
+    out["cfg2_split"] = {
+        "tokens_per_s": args.batch * args.decode_steps * 5 / (ms / 1e3),
+        "decode_us": dec_avg * 1e3,
+        "interleaved_decode_us": sum(dec_i) / len(dec_i) * 1e3,
+        "hbm_bytes_per_decode": job.decode_bytes("split"),
+        "unsplit_bytes_per_decode": job.decode_bytes("interleaved"),
+        "ids_match_interleaved": bool(np.array_equal(job.out.cpu().numpy(), ref_out)),
+        "what": "static rows T scored once per step for all requests (exact chains, "
+                "FP32-issue bound, side stream) + exact GEMV over each request's D_b \\ T "
+                "(HBM bound) + combine; svt_greedy_split"}
     del job
     torch.cuda.empty_cache()
     out["cfg3_prefill"] = prefill_secondary(torch, th, synth)

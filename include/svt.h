@@ -273,6 +273,45 @@ svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_
                             float* d_out_max, uint64_t* d_out_keys, void* d_workspace,
                             svt_stream stream);
 
+/* Split greedy decode: a batch of hybrid plans S_b = T ∪ D_b (select,
+ * selector.cpp:16-43) with the static rows T read once per step for the
+ * whole batch (greedy_step per request, head.cpp:203-217, same ids).
+ * svt_decode_split_plans splits the capacity-CSR plans of
+ * svt_select_batched into the dynamic ids D_b \ T (plan order, at
+ * d_act_off[b], count d_n_dyn[b]), d_static_valid[b] (n_static, or 0 when a
+ * plan misses part of T: its rows are then all dynamic), d_first_ids[b] (the
+ * plan's smallest id) and d_dyn_starts[b] (1 when that id is dynamic).
+ * svt_greedy_split then runs, per step:
+ *   the static half: exact reference-order logits of every static row for
+ *     every request, from d_static_sub (T gathered once by
+ *     svt_gather_interleaved as a single plan; n_static rows, ids
+ *     d_static_ids ascending), on a side stream;
+ *   the dynamic half: the exact-order GEMV over d_dyn_sub (the D_b \ T
+ *     sub-heads, svt_gather_interleaved over d_dyn_ids with the group
+ *     records of svt_plan_layout on d_n_dyn);
+ *   a combine: larger value, then lower id; a NaN at the plan's smallest id
+ *     wins (the reference's row-0 rule).
+ * d_workspace: svt_greedy_split_workspace_bytes(batch, max_groups), zeroed
+ * once before the first call (each call leaves its static keys at zero).
+ * flags: SVT_WEIGHTS_STABLE as for svt_greedy_interleaved. */
+svt_status svt_decode_split_plans(const uint32_t* d_active_ids, const int64_t* d_act_off,
+                                  const int64_t* d_n_active, int32_t batch,
+                                  const uint64_t* d_static_words, size_t universe,
+                                  const uint32_t* d_static_ids, int64_t n_static,
+                                  uint32_t* d_dyn_ids, int64_t* d_n_dyn, int64_t* d_static_valid,
+                                  uint32_t* d_first_ids, uint8_t* d_dyn_starts,
+                                  svt_stream stream);
+size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups);
+svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, int64_t n_static, size_t dim,
+                            const uint32_t* d_static_ids, const int64_t* d_static_valid,
+                            const uint32_t* d_first_ids, const void* d_dyn_sub,
+                            const int64_t* d_group_begin, const void* d_group_meta,
+                            const uint32_t* d_dyn_ids, const int64_t* d_n_dyn,
+                            const uint8_t* d_dyn_starts, int32_t batch, int64_t max_groups,
+                            const float* d_hidden, size_t hidden_ld, int32_t flags,
+                            uint32_t* d_out_ids, float* d_out_max, void* d_workspace,
+                            svt_stream stream);
+
 /* Certified greedy decode (latency-bound small batches, e.g. batch 1): a
  * split-K FFMA pass over the interleaved sub-heads streams at full HBM
  * bandwidth and yields f_r with a rigorous bound |f_r - ref_r| <= B_r

@@ -230,7 +230,7 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
                                 int32_t batch, int64_t max_groups, const float* hidden,
                                 size_t ld, uint32_t row_base, int32_t plan_start, int32_t flags,
                                 uint32_t* out_ids, float* out_max, uint64_t* out_keys, void* ws,
-                                svt_stream stream) {
+                                svt_stream stream, const uint8_t* plan_start_req = nullptr) {
     if (svt_status s = check_dtype(dt)) return s;
     if (svt_status s = need_device()) return s;
     if (batch <= 0) return SVT_OK;
@@ -253,9 +253,11 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
     p.out_keys = reinterpret_cast<unsigned long long*>(out_keys);
     p.row_base = row_base;
     p.plan_start = plan_start;
+    p.plan_start_req = plan_start_req;
     p.weights_stable = (flags & SVT_WEIGHTS_STABLE) ? 1 : 0;
     return gemv_run(src, MODE_ARGMAX, dt, p, static_cast<cudaStream_t>(stream));
 }
+
 
 svt_status svt_greedy_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
                                   const int64_t* d_group_begin, const void* d_group_meta,
@@ -310,6 +312,21 @@ svt_status svt_greedy_step(const void* d_subhead, svt_dtype dt, size_t rows, siz
 }
 
 }  // extern "C"
+
+namespace svt {
+// the split decode's dynamic half (svt_split_decode.cu): interleaved
+// sub-heads with a per-request plan-start flag
+svt_status greedy_interleaved_req(const void* d_sub, svt_dtype dt, size_t dim,
+                                  const int64_t* gb, const void* meta, const uint32_t* ids,
+                                  int32_t batch, int64_t max_groups, const float* hidden,
+                                  size_t ld, int32_t flags, const uint8_t* plan_start_req,
+                                  uint32_t* out_ids, uint64_t* out_keys, void* ws,
+                                  cudaStream_t st) {
+    return greedy_common(SRC_INTERLEAVED, d_sub, dt, 0, dim, gb, meta, ids, batch, max_groups,
+                         hidden, ld, 0, 0, flags, out_ids, nullptr, out_keys, ws, st,
+                         plan_start_req);
+}
+}  // namespace svt
 
 // ---- cross-shard combine ------------------------------------------------------
 namespace svt {

@@ -71,8 +71,9 @@ __device__ __forceinline__ void group_epilogue(const GemvParams& p, const GroupM
     if constexpr (MODE == MODE_LOGITS) {
         if (valid) p.logits[lbase + row] = acc;
     } else {
-        const unsigned long long key = make_key(
-            acc, p.row_base + static_cast<uint32_t>(row), valid, p.plan_start != 0 && row == 0);
+        const bool start = p.plan_start_req ? p.plan_start_req[m.b] != 0 : p.plan_start != 0;
+        const unsigned long long key =
+            make_key(acc, p.row_base + static_cast<uint32_t>(row), valid, start && row == 0);
         const unsigned long long kmax = warp_max_u64(key);
         if (lane == 0) p.gkeys[g] = kmax;
     }

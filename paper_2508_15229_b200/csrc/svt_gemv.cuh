@@ -44,6 +44,10 @@ struct GemvParams {
     unsigned long long* out_keys;
     uint32_t row_base;
     int32_t plan_start;
+    // per request: plan row 0 of this request's rows is the whole plan's row
+    // 0 (split decode: the dynamic rows start the plan only when their first
+    // id is below every static id); nullptr: plan_start for all requests
+    const uint8_t* plan_start_req;
     int32_t stages;
     int32_t weights_stable;  // sub-head / rows not written by the kernel this launch depends on
     int64_t single_rows;

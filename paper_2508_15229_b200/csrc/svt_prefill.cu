@@ -1529,7 +1529,8 @@ split_plans_kernel(const uint32_t* __restrict__ active, const int64_t* __restric
                    size_t universe, const uint32_t* __restrict__ st_ids, int64_t nT, int64_t nTp,
                    uint32_t* __restrict__ dyn_ids, int64_t* __restrict__ n_dyn,
                    uint32_t* __restrict__ vids, int64_t* __restrict__ vid_off,
-                   int64_t* __restrict__ vrows, int64_t* __restrict__ st_valid) {
+                   int64_t* __restrict__ vrows, int64_t* __restrict__ st_valid,
+                   uint32_t* __restrict__ first_ids, uint8_t* __restrict__ dyn_starts) {
     __shared__ int64_t red[8];
     const int s = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1564,18 +1565,22 @@ split_plans_kernel(const uint32_t* __restrict__ active, const int64_t* __restric
         if (keep) {
             const int64_t at = out + before + __popc(m & ((1u << lane) - 1u));
             dyn_ids[act_off[s] + at] = id;
-            vids[voff + nTp + at] = id;
+            if (vids) vids[voff + nTp + at] = id;
         }
         out += total;
         __syncthreads();
     }
-    for (int64_t v = threadIdx.x; v < nTp; v += blockDim.x)
-        vids[voff + v] = st_ids[v < nT ? v : nT - 1];
+    if (vids)
+        for (int64_t v = threadIdx.x; v < nTp; v += blockDim.x)
+            vids[voff + v] = st_ids[v < nT ? v : nT - 1];
     if (threadIdx.x == 0) {
         n_dyn[s] = out;
-        vrows[s] = n > 0 ? nTp + out : 0;
+        if (vrows) vrows[s] = n > 0 ? nTp + out : 0;
         st_valid[s] = valid ? nT : 0;
-        vid_off[s] = voff;
+        if (vid_off) vid_off[s] = voff;
+        // the plan's first (smallest) id, and whether the dynamic rows hold it
+        if (first_ids) first_ids[s] = n > 0 ? plan[0] : 0xFFFFFFFFu;
+        if (dyn_starts) dyn_starts[s] = (n > 0 && out > 0 && dyn_ids[act_off[s]] == plan[0]) ? 1 : 0;
     }
 }
 }  // namespace
@@ -1598,7 +1603,27 @@ extern "C" svt_status svt_prefill_split_plans(const uint32_t* d_active_ids, cons
     const int64_t nTp = (n_static + BN - 1) / BN * BN;
     split_plans_kernel<<<sequences, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         d_active_ids, d_act_off, d_n_active, d_static_words, universe, d_static_ids, n_static, nTp,
-        d_dyn_ids, d_n_dyn, d_vids, d_vid_offsets, d_vrows, d_static_valid);
+        d_dyn_ids, d_n_dyn, d_vids, d_vid_offsets, d_vrows, d_static_valid, nullptr, nullptr);
+    SVT_LAUNCH_CHECK("split_plans_kernel");
+    return SVT_OK;
+}
+
+extern "C" svt_status svt_decode_split_plans(const uint32_t* d_active_ids, const int64_t* d_act_off,
+                                             const int64_t* d_n_active, int32_t batch,
+                                             const uint64_t* d_static_words, size_t universe,
+                                             const uint32_t* d_static_ids, int64_t n_static,
+                                             uint32_t* d_dyn_ids, int64_t* d_n_dyn,
+                                             int64_t* d_static_valid, uint32_t* d_first_ids,
+                                             uint8_t* d_dyn_starts, svt_stream stream) {
+    using namespace svt;
+    if (batch <= 0) return SVT_OK;
+    if (n_static <= 0) {
+        set_error("the static/dynamic split needs a non-empty static set");
+        return SVT_ERR_CONFIG;
+    }
+    split_plans_kernel<<<batch, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_active_ids, d_act_off, d_n_active, d_static_words, universe, d_static_ids, n_static, 0,
+        d_dyn_ids, d_n_dyn, nullptr, nullptr, nullptr, d_static_valid, d_first_ids, d_dyn_starts);
     SVT_LAUNCH_CHECK("split_plans_kernel");
     return SVT_OK;
 }

@@ -1,0 +1,290 @@
+// svt_split_decode.cu — batched greedy decode over hybrid plans with the
+// static rows shared (the cfg2 decode step).
+//
+// Reference: every request b runs greedy_step(gather(W, S_b), h_b, S_b)
+// (head.cpp:176-217) over its own plan S_b = T ∪ D_b (select,
+// selector.cpp:16-43): the |T| static rows are gathered and streamed once per
+// request. Here they are read once per step for the whole batch:
+//   * static half: static_rows_kernel computes the exact reference-order
+//     logit (acc = fadd_rn(acc, fmul_rn(w, h)), ascending k) of every static
+//     row for every request — the rows come from one shared lane-interleaved
+//     block (L2-resident), each warp dots one 32-row group with RB hidden
+//     states — and folds (value, id) keys per request with a 64-bit atomicMax;
+//   * dynamic half: the exact-order GEMV (svt_gemv.cu) over the requests'
+//     D_b \ T sub-heads, one (value, row) record per request; its rows' first
+//     is the plan's first row only when flagged per request (NaN rule);
+//   * combine: the larger (value, ~id) key wins per request. Ids order the
+//     plan, so ties resolve to the lower id as the reference scan's earlier
+//     row; a NaN at the plan's first row (the smallest id, in either half)
+//     wins outright.
+// The static half runs on a side stream beside the dynamic GEMV: one is
+// FP32-issue bound on L2-resident rows, the other HBM bound.
+#include <cstdlib>
+
+#include "svt_common.cuh"
+#include "svt_gemv.cuh"
+
+namespace svt {
+svt_status greedy_interleaved_req(const void* d_sub, svt_dtype dt, size_t dim, const int64_t* gb,
+                                  const void* meta, const uint32_t* ids, int32_t batch,
+                                  int64_t max_groups, const float* hidden, size_t ld,
+                                  int32_t flags, const uint8_t* plan_start_req,
+                                  uint32_t* out_ids, uint64_t* out_keys, void* ws,
+                                  cudaStream_t st);
+namespace {
+
+constexpr int kRB = 2;        // requests per warp (independent chains per lane)
+constexpr int kSWarps = 8;    // warps per CTA
+constexpr int kAhead = 8;     // row chunks in flight per lane
+
+struct StaticParams {
+    const uint8_t* sub;        // lane-interleaved static rows (svt_gather_interleaved layout)
+    int64_t n_static;
+    int32_t nchunks;           // 16-byte chunks per row
+    int32_t dim;
+    const uint32_t* st_ids;    // [n_static] ascending
+    const float* hidden;
+    int64_t ld;
+    int32_t B;
+    const int64_t* st_valid;   // [B] static rows in the request's plan (n_static or 0)
+    const uint32_t* first_ids; // [B] the plan's smallest id
+    unsigned long long* keys;  // [B] (value, ~id) keys, zero on entry
+};
+
+template <int DT>
+__global__ void __launch_bounds__(kSWarps * 32) static_rows_kernel(const StaticParams p) {
+    using CK = Chunk<DT>;
+    constexpr int E = CK::E;
+    extern __shared__ __align__(16) float sh_h[];  // [kRB][nchunks * E] hidden states
+    const int lane = threadIdx.x & 31;
+    const int64_t ngroups = (p.n_static + 31) / 32;
+    const int64_t gblk = (ngroups + kSWarps - 1) / kSWarps;
+    // CTA = (request block, kSWarps consecutive groups): its warps share the
+    // block's hidden states, staged once in shared memory
+    const int b0 = static_cast<int>(blockIdx.x / gblk) * kRB;
+    const int64_t g = (blockIdx.x % gblk) * kSWarps + (threadIdx.x >> 5);
+    const int hlen = p.nchunks * E;  // a multiple of 4
+    {
+        // 16-byte cp.async for the whole float4s of each row, scalar tail, zeros past dim
+        const int q4 = hlen / 4, full4 = p.dim / 4;
+        for (int i = threadIdx.x; i < kRB * q4; i += blockDim.x) {
+            const int r = i / q4, q = i - r * q4;
+            const int b = b0 + r;
+            float* dst = sh_h + r * hlen + 4 * q;
+            if (b < p.B && q < full4) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
+                             "l"(p.hidden + static_cast<int64_t>(b) * p.ld + 4 * q)
+                             : "memory");
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int k = 4 * q + e;
+                    dst[e] = (b < p.B && k < p.dim)
+                                 ? __ldg(p.hidden + static_cast<int64_t>(b) * p.ld + k)
+                                 : 0.0f;
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    if (g >= ngroups) return;
+    const uint4* src = reinterpret_cast<const uint4*>(p.sub) + g * p.nchunks * 32 + lane;
+    float acc[kRB];
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) acc[r] = 0.0f;
+    // the rows stream from L2: keep kAhead chunk loads in flight per lane
+    uint4 wbuf[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u)
+        wbuf[u] = u < p.nchunks ? __ldg(src + u * 32) : make_uint4(0u, 0u, 0u, 0u);
+    for (int c0 = 0; c0 < p.nchunks; c0 += kAhead) {
+#pragma unroll
+        for (int u = 0; u < kAhead; ++u) {
+            const int c = c0 + u;
+            if (c >= p.nchunks) break;
+            float w[E];
+            CK::widen(wbuf[u], w);
+            if (c + kAhead < p.nchunks) wbuf[u] = __ldg(src + (c + kAhead) * 32);
+            const int e0 = c * E;
+            float hv[kRB][E];
+#pragma unroll
+            for (int r = 0; r < kRB; ++r)
+#pragma unroll
+                for (int q = 0; q < E / 4; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(sh_h + r * hlen + e0 + 4 * q);
+                    hv[r][4 * q] = v.x;
+                    hv[r][4 * q + 1] = v.y;
+                    hv[r][4 * q + 2] = v.z;
+                    hv[r][4 * q + 3] = v.w;
+                }
+            if (e0 + E <= p.dim) {
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+#pragma unroll
+                    for (int r = 0; r < kRB; ++r) acc[r] = ref_mac(acc[r], w[e], hv[r][e]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (e0 + e < p.dim)
+#pragma unroll
+                        for (int r = 0; r < kRB; ++r) acc[r] = ref_mac(acc[r], w[e], hv[r][e]);
+            }
+        }
+    }
+    const int64_t row = g * 32 + lane;
+    const bool live = row < p.n_static;
+    const uint32_t id = live ? p.st_ids[row] : 0u;
+#pragma unroll
+    for (int r = 0; r < kRB; ++r) {
+        const int b = b0 + r;
+        if (b >= p.B) break;  // (warp-uniform)
+        const bool valid = live && p.st_valid[b] > 0;
+        const unsigned long long k =
+            warp_max_u64(make_key(acc[r], id, valid, acc[r] != acc[r] && id == p.first_ids[b]));
+        if (lane == 0 && k) atomicMax(&p.keys[b], k);
+    }
+}
+
+// per request: the dynamic record {key lo, key hi, id, max} (plan-row key of
+// the GEMV) against the static (value, ~id) key; the static keys are reset
+// for the next step
+__global__ void split_combine_kernel(const uint4* __restrict__ rec,
+                                     unsigned long long* __restrict__ keys,
+                                     const uint32_t* __restrict__ first_ids,
+                                     const int64_t* __restrict__ n_dyn, int B,
+                                     uint32_t* __restrict__ out_ids, float* __restrict__ out_max) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const unsigned long long ks = keys[b];
+    keys[b] = 0ull;
+    unsigned long long kd = 0ull;
+    if (n_dyn[b] > 0) {
+        const uint4 r = rec[b];
+        const unsigned long long k = (static_cast<unsigned long long>(r.y) << 32) | r.x;
+        kd = k == kNanRow0Key ? kNanRow0Key
+                              : (k ? (static_cast<unsigned long long>(r.y) << 32) |
+                                         static_cast<unsigned long long>(0xFFFFFFFFu - r.z)
+                                   : 0ull);
+    }
+    const unsigned long long k = ks > kd ? ks : kd;
+    uint32_t id = 0xFFFFFFFFu;
+    float mx = __int_as_float(0x7FC00000);
+    if (k == kNanRow0Key) {
+        id = first_ids[b];
+    } else if (k) {
+        id = 0xFFFFFFFFu - static_cast<uint32_t>(k);
+        mx = float_of_ord(static_cast<uint32_t>(k >> 32));
+    }
+    out_ids[b] = id;
+    if (out_max) out_max[b] = mx;
+}
+
+struct SplitSide {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SplitSide* split_side() {
+    static SplitSide per_dev[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    SplitSide& s = per_dev[dev];
+    if (!s.stream) {
+        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+    }
+    return &s;
+}
+
+}  // namespace
+}  // namespace svt
+
+extern "C" size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups) {
+    const size_t b = static_cast<size_t>(batch > 0 ? batch : 0);
+    // static keys | dynamic records | GEMV group keys
+    return ((b * 8 + 255) & ~size_t(255)) + ((b * 16 + 255) & ~size_t(255)) +
+           svt_greedy_workspace_bytes(batch, max_groups);
+}
+
+extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, int64_t n_static,
+                                       size_t dim, const uint32_t* d_static_ids,
+                                       const int64_t* d_static_valid, const uint32_t* d_first_ids,
+                                       const void* d_dyn_sub, const int64_t* d_group_begin,
+                                       const void* d_group_meta, const uint32_t* d_dyn_ids,
+                                       const int64_t* d_n_dyn, const uint8_t* d_dyn_starts,
+                                       int32_t batch, int64_t max_groups, const float* d_hidden,
+                                       size_t hidden_ld, int32_t flags, uint32_t* d_out_ids,
+                                       float* d_out_max, void* d_workspace, svt_stream stream) {
+    using namespace svt;
+    if (batch <= 0) return SVT_OK;
+    if (dt != SVT_F32 && dt != SVT_BF16 && dt != SVT_F16) {
+        set_error("split decode: unsupported dtype %d", static_cast<int>(dt));
+        return SVT_ERR_CONFIG;
+    }
+    if (hidden_ld % 4 || hidden_ld < dim || (reinterpret_cast<uintptr_t>(d_hidden) & 15)) {
+        set_error("split decode: hidden rows must be 16-byte aligned (ld %% 4 == 0, ld >= dim)");
+        return SVT_ERR_CONFIG;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* ws = static_cast<uint8_t*>(d_workspace);
+    const size_t b = static_cast<size_t>(batch);
+    auto* keys = reinterpret_cast<unsigned long long*>(ws);
+    auto* rec = reinterpret_cast<uint64_t*>(ws + ((b * 8 + 255) & ~size_t(255)));
+    void* gws = ws + ((b * 8 + 255) & ~size_t(255)) + ((b * 16 + 255) & ~size_t(255));
+
+    // static half on the side stream (the keys are zero: initial workspace
+    // state or reset by the previous combine)
+    SplitSide* side = getenv("SVT_SPLIT_SERIAL") ? nullptr : split_side();
+    cudaStream_t ss = side ? side->stream : st;
+    if (side) {
+        SVT_CUDA_TRY(cudaEventRecord(side->fork, st));
+        SVT_CUDA_TRY(cudaStreamWaitEvent(ss, side->fork, 0));
+    }
+    if (n_static > 0) {
+        StaticParams p;
+        p.sub = static_cast<const uint8_t*>(d_static_sub);
+        p.n_static = n_static;
+        p.nchunks = static_cast<int32_t>((dim * static_cast<size_t>(esize_of(dt)) + 15) / 16);
+        p.dim = static_cast<int32_t>(dim);
+        p.st_ids = d_static_ids;
+        p.hidden = d_hidden;
+        p.ld = static_cast<int64_t>(hidden_ld);
+        p.B = batch;
+        p.st_valid = d_static_valid;
+        p.first_ids = d_first_ids;
+        p.keys = keys;
+        const int64_t gblk = ((n_static + 31) / 32 + kSWarps - 1) / kSWarps;
+        const int grid = static_cast<int>(gblk * ((batch + kRB - 1) / kRB));
+        const size_t smem = static_cast<size_t>(kRB) * p.nchunks * (dt == SVT_F32 ? 4 : 8) * 4;
+        if (smem > 200 * 1024) {
+            set_error("split decode: hidden size %zu too large for the static half", dim);
+            return SVT_ERR_CONFIG;
+        }
+        auto launch = [&](auto kern) -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            kern<<<grid, kSWarps * 32, smem, ss>>>(p);
+            return cudaGetLastError();
+        };
+        const cudaError_t e = dt == SVT_F32    ? launch(static_rows_kernel<SVT_F32>)
+                              : dt == SVT_BF16 ? launch(static_rows_kernel<SVT_BF16>)
+                                               : launch(static_rows_kernel<SVT_F16>);
+        if (e != cudaSuccess) return cuda_status(e, "static_rows_kernel");
+        SVT_LAUNCH_CHECK("static_rows_kernel");
+    }
+    if (side) SVT_CUDA_TRY(cudaEventRecord(side->join, ss));
+    // dynamic half: requests without dynamic rows have no group (record untouched)
+    if (svt_status s = greedy_interleaved_req(d_dyn_sub, dt, dim, d_group_begin, d_group_meta,
+                                              d_dyn_ids, batch, max_groups, d_hidden, hidden_ld,
+                                              flags, d_dyn_starts, d_out_ids, rec, gws, st))
+        return s;
+    if (side) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
+    split_combine_kernel<<<(batch + 127) / 128, 128, 0, st>>>(
+        reinterpret_cast<const uint4*>(rec), keys, d_first_ids, d_n_dyn, batch, d_out_ids,
+        d_out_max);
+    SVT_LAUNCH_CHECK("split_combine_kernel");
+    return SVT_OK;
+}

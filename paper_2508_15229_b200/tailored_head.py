@@ -31,7 +31,7 @@ __all__ = [
     "Error", "ConfigError", "ParseError", "IntegrityError", "TokenSet", "SelectionPlan",
     "HeadMatrix", "select", "remap_out", "union_plans", "gather", "logits", "greedy_step",
     "memory_report", "simulate", "breakeven_rows", "TailoredBatch", "SVT_F32", "SVT_F16",
-    "SVT_BF16", "dtype_of", "torch_dtype",
+    "SVT_BF16", "dtype_of", "torch_dtype", "SplitDecoder",
 ]
 
 _TORCH = {SVT_F32: torch.float32, SVT_F16: torch.float16, SVT_BF16: torch.bfloat16}
@@ -353,6 +353,100 @@ def plan_from_json(text: str, origin: str = "<mem>") -> SelectionPlan:
     call("svt_plan_from_json", raw, len(raw), origin.encode(), ids.ctypes.data, ids.size,
          C.byref(n), C.byref(ns), C.byref(nd), C.byref(full))
     return SelectionPlan(ids[: n.value].copy(), ns.value, nd.value, full.value)
+
+class SplitDecoder:
+    """Batched greedy decode over a select()-built batch with the static rows
+    shared (svt_decode_split_plans + svt_greedy_split).
+
+    Each plan is T ∪ D_b; the static rows T are gathered once into one
+    lane-interleaved block and scored for every request from it (exact
+    reference-order chains), only D_b \\ T is gathered per request and
+    streamed by the exact-order GEMV, and the two halves meet in a (value,
+    id) combine. Ids are those of ``TailoredBatch.greedy`` over the full
+    plans. :meth:`prepare` re-splits and re-gathers after ``tb.run_select()``.
+    """
+
+    def __init__(self, tb: "TailoredBatch", head: HeadMatrix, stream=None):
+        words = getattr(tb, "_words", None)
+        if words is None:
+            raise ConfigError("the split decoder needs a batch built by select over a static set")
+        self.tb, self.head, self.stream = tb, head, stream
+        B, V, d = tb.B, tb.V, head.dim()
+        w = words.cpu().numpy().view(np.uint64)
+        bits = np.unpackbits(w.view(np.uint8), bitorder="little")[:V]
+        st = np.flatnonzero(bits).astype(np.uint32)
+        if st.size == 0:
+            raise ConfigError("the split decoder needs a non-empty static set")
+        self.nT = int(st.size)
+        dev = "cuda"
+        self.st_ids = torch.from_numpy(st.view(np.int32)).to(dev)
+        # the static block: T as one plan, lane-interleaved
+        self.st_groups = (self.nT + 31) // 32
+        self.st_gb = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.st_gm = torch.zeros((self.st_groups, 8), dtype=torch.int32, device=dev)
+        n_st = torch.tensor([self.nT], dtype=torch.int64, device=dev)
+        off0 = torch.zeros(2, dtype=torch.int64, device=dev)
+        call("svt_plan_layout", n_st.data_ptr(), off0.data_ptr(), 1, self.st_gb.data_ptr(),
+             self.st_gm.data_ptr(), self.st_groups, _stream(stream))
+        self.st_sub = torch.empty(
+            max(16, _lib.lib.svt_subhead_bytes(head.storage, d, self.st_groups)),
+            dtype=torch.uint8, device=dev)
+        self.bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        call("svt_gather_interleaved", head.data.data_ptr(), head.storage, head.rows(), d,
+             self.st_ids.data_ptr(), self.st_gb.data_ptr(), self.st_gm.data_ptr(), 1,
+             self.st_groups, self.st_sub.data_ptr(), self.bad.data_ptr(), _stream(stream))
+        # the dynamic halves (capacity layout of the batch's plans)
+        self.dyn_ids = torch.empty_like(tb.active)
+        self.meta = torch.zeros((2, max(B, 1)), dtype=torch.int64, device=dev)
+        self.n_dyn, self.st_valid = self.meta
+        self.first_ids = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
+        self.dyn_starts = torch.zeros(max(B, 1), dtype=torch.uint8, device=dev)
+        self.max_groups = tb.max_groups
+        self.gb = torch.zeros(B + 1, dtype=torch.int64, device=dev)
+        self.gm = torch.zeros((max(1, self.max_groups), 8), dtype=torch.int32, device=dev)
+        self.sub = torch.empty(
+            max(16, _lib.lib.svt_subhead_bytes(head.storage, d, self.max_groups)),
+            dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_split_workspace_bytes(B, self.max_groups)),
+                              dtype=torch.uint8, device=dev)
+        self._stable = False
+        self.prepare()
+
+    def prepare(self):
+        """Split the batch's current plans and gather their dynamic rows."""
+        tb, head, st = self.tb, self.head, _stream(self.stream)
+        call("svt_decode_split_plans", tb.active.data_ptr(), tb.act_off.data_ptr(),
+             tb.n_active.data_ptr(), tb.B, tb._words.data_ptr(), tb.V, self.st_ids.data_ptr(),
+             self.nT, self.dyn_ids.data_ptr(), self.n_dyn.data_ptr(), self.st_valid.data_ptr(),
+             self.first_ids.data_ptr(), self.dyn_starts.data_ptr(), st)
+        call("svt_plan_layout", self.n_dyn.data_ptr(), tb.act_off.data_ptr(), tb.B,
+             self.gb.data_ptr(), self.gm.data_ptr(), self.max_groups, st)
+        call("svt_gather_interleaved", head.data.data_ptr(), head.storage, head.rows(),
+             head.dim(), self.dyn_ids.data_ptr(), self.gb.data_ptr(), self.gm.data_ptr(), tb.B,
+             self.max_groups, self.sub.data_ptr(), self.bad.data_ptr(), st)
+        self._stable = False
+        return self
+
+    def greedy(self, hidden: torch.Tensor, out_ids: torch.Tensor,
+               out_max: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """hidden: [B, ld] float32 on the device (ld % 4 == 0, ld >= dim)."""
+        flags = SVT_WEIGHTS_STABLE if self._stable else 0
+        self._stable = True
+        h = self.head
+        call("svt_greedy_split", self.st_sub.data_ptr(), h.storage, self.nT, h.dim(),
+             self.st_ids.data_ptr(), self.st_valid.data_ptr(), self.first_ids.data_ptr(),
+             self.sub.data_ptr(), self.gb.data_ptr(), self.gm.data_ptr(), self.dyn_ids.data_ptr(),
+             self.n_dyn.data_ptr(), self.dyn_starts.data_ptr(), self.tb.B, self.max_groups,
+             hidden.data_ptr(), hidden.stride(0), flags, out_ids.data_ptr(), _ptr(out_max),
+             self.ws.data_ptr(), _stream(self.stream))
+        return out_ids
+
+    def algorithmic_decode_bytes(self, esize: int, dim: int) -> int:
+        """Bytes one split decode step must move from HBM: the static block
+        once, each request's dynamic rows, the hidden states and the outputs."""
+        nd = self.n_dyn.cpu().numpy()
+        return (self.nT + int(nd.sum())) * dim * esize + self.tb.B * (dim * 4 + 8)
+
 
 class RowDecoder:
     """Batch-1 greedy decode over ONE plan (BASELINE cfg1): the plan's rows

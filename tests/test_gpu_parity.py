@@ -635,6 +635,64 @@ def test_prefill_split_matches_reference(th, prefill_tuning, case, nT):
     print("split stats", sc.stats())
 
 
+@pytest.mark.parametrize("case", ["random_bf16", "random_f32_d100", "duplicate_rows", "nonfinite",
+                                  "bf16_d100"])
+def test_split_decode_matches_reference(th, case):
+    """Split decode (svt_decode_split_plans + svt_greedy_split): the static rows
+    scored once for the whole batch, the dynamic rows per request; ids and the
+    exact winning logit equal the reference greedy_step over each full plan
+    (head.cpp:203-217), across steps and a re-select. Covers ties between
+    static and dynamic rows (duplicated head rows: the lower id wins), NaN
+    logits (the plan's smallest id wins, static or dynamic), empty prompts,
+    a prompt inside T, partial 16-byte chunks (d = 100) and f32 heads."""
+    V, B = 20000, 7
+    d = 100 if case.endswith("d100") else 256
+    storage = th.SVT_F32 if "f32" in case else th.SVT_BF16
+    rng = np.random.default_rng(len(case) * 13 + d)
+    if case == "duplicate_rows":
+        base = bf16_np(rng.uniform(-1, 1, (120, d)).astype(np.float32))
+        head = th.HeadMatrix.from_host(base[np.arange(V) % 120], dtype_bytes=2, storage=storage)
+    else:
+        head = th.HeadMatrix.random(V, d, 0xD00D + d, storage=storage)
+    W = head.to_host()
+    t_ids = rng.choice(V, 333, replace=False)
+    words = words_from_ids(t_ids, V)
+    lens = [200, 0, 50, 300, 1, 120, 64]
+    prompts = [rng.integers(0, V, L).astype(np.uint32) for L in lens]
+    prompts[4] = np.array([int(np.sort(t_ids)[5])], np.uint32)  # entirely inside T
+    prompts[6][0] = 0  # id 0 makes the dynamic rows start this plan
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in prompts])
+    d_prompts = torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda()
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), 333, V, d_prompts,
+                                off)
+    dec = th.SplitDecoder(tb, head)
+    ld = (d + 3) // 4 * 4
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    mx = torch.empty(B, dtype=torch.float32, device="cuda")
+    for rnd in range(2):
+        for t in range(3):
+            h = bf16_np(rng.uniform(-1, 1, (B, d)).astype(np.float32))
+            if case == "nonfinite":
+                h[t % B] *= np.float32(3e38)
+                h[(t + 3) % B, :] = np.float32(np.inf)
+            hl = np.zeros((B, ld), np.float32)
+            hl[:, :d] = h
+            dec.greedy(torch.from_numpy(hl).cuda(), out, mx)
+            got = out.cpu().numpy().view(np.uint32)
+            gmx = mx.cpu().numpy()
+            for b in range(B):
+                plan = orc.select(prompts[b], words, V, V).active_ids
+                want, wmax = orc.greedy_step(W[plan], h[b], plan)
+                assert got[b] == want, (case, rnd, t, b)
+                assert (np.isnan(wmax) and np.isnan(gmx[b])) or gmx[b] == wmax, (case, b)
+        prompts = [rng.integers(0, V, L).astype(np.uint32) for L in lens]
+        d_prompts.copy_(torch.from_numpy(np.concatenate(prompts).view(np.int32)))
+        tb.run_select()
+        dec.prepare()
+    assert int(dec.bad.item()) == 0
+
+
 # ---- certified batch-1 decode over row-major rows (cfg1 latency path) ----------
 def _rows_decoder(th, head, ids, materialize=True, **kw):
     d_ids = torch.from_numpy(np.ascontiguousarray(ids, np.uint32).view(np.int32)).cuda()
