@@ -62,6 +62,29 @@ struct svt_session {
     std::unordered_map<const void*, void*> mapped_cache;  // pinned host -> device alias
     bool weights_stable = false;  // set after the first decode step following a prepare
 
+    // split decode (svt_greedy_split): the static rows gathered once per
+    // prepare into their own block, d_sub / d_group_req / group_begin then
+    // hold the requests' dynamic rows only
+    bool split = false;
+    int64_t n_st = 0, st_groups = 0;
+    uint32_t* d_st_ids = nullptr;
+    size_t cap_st = 0;
+    svt::GroupMeta* d_st_meta = nullptr;
+    size_t cap_st_groups = 0;
+    uint8_t* d_st_sub = nullptr;
+    size_t cap_st_sub = 0;
+    int64_t* d_st_small = nullptr;  // {n_st, 0, 0, group_begin[2]}
+    uint32_t* d_dyn_ids = nullptr;
+    size_t cap_dyn = 0;
+    int64_t* d_split_meta = nullptr;  // n_dyn | st_valid | first_ids (u32) | dyn_starts (u8)
+    size_t cap_split_meta = 0;
+    uint8_t* d_split_ws = nullptr;
+    size_t cap_split_ws = 0;
+    int64_t* n_dyn_d() { return d_split_meta; }
+    int64_t* st_valid_d() { return d_split_meta + cap_batch; }
+    uint32_t* first_ids_d() { return reinterpret_cast<uint32_t*>(d_split_meta + 2 * cap_batch); }
+    uint8_t* dyn_starts_d() { return reinterpret_cast<uint8_t*>(d_split_meta + 3 * cap_batch); }
+
     int64_t* n_active_d() { return d_meta; }
     int64_t* n_static_d() { return d_meta + cap_batch; }
     int64_t* n_dynamic_d() { return d_meta + 2 * cap_batch; }
@@ -87,7 +110,8 @@ svt_status grow(T** p, size_t* cap, size_t need) {
 void free_all(svt_session* s) {
     void* dev[] = {s->d_words, s->d_inputs, s->d_in_off, s->d_act_off, s->d_meta, s->d_active,
                    s->d_group_req, s->d_sub, s->d_hidden, s->d_out_ids, s->d_out_max, s->d_ws,
-                   s->d_bad};
+                   s->d_bad, s->d_st_ids, s->d_st_meta, s->d_st_sub, s->d_st_small,
+                   s->d_dyn_ids, s->d_split_meta, s->d_split_ws};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {s->h_hidden, s->h_ids, s->h_max};
@@ -194,6 +218,69 @@ svt_status ensure_batch(svt_session* s, size_t B) {
     SVT_CUDA_TRY(cudaMallocHost(&s->h_max, nb * sizeof(float)));
     s->cap_batch = nb;
     return SVT_OK;
+}
+
+// the split half of prepare: static ids (host, from the words), the static
+// block (one plan, lane-interleaved), the requests' dynamic ids and flags
+svt_status prepare_split(svt_session* s, const uint64_t* h_words, int64_t n_static,
+                         cudaStream_t q) {
+    const size_t B = static_cast<size_t>(s->batch);
+    std::vector<uint32_t> ids;
+    ids.reserve(static_cast<size_t>(n_static));
+    const size_t nw = (s->rows + 63) / 64;
+    for (size_t w = 0; w < nw; ++w)
+        for (uint64_t m = h_words[w]; m; m &= m - 1)
+            ids.push_back(static_cast<uint32_t>(w * 64 + __builtin_ctzll(m)));
+    s->n_st = n_static;
+    s->st_groups = (n_static + 31) / 32;
+    svt_status st = grow(&s->d_st_ids, &s->cap_st, ids.size());
+    if (!st) st = grow(&s->d_st_meta, &s->cap_st_groups, static_cast<size_t>(s->st_groups));
+    if (!st)
+        st = grow(&s->d_st_sub, &s->cap_st_sub,
+                  svt_subhead_bytes(s->dt, s->dim, static_cast<int64_t>(s->cap_st_groups)));
+    if (!st && !s->d_st_small) {
+        size_t cap = 0;
+        st = grow(&s->d_st_small, &cap, 8);
+    }
+    if (!st) st = grow(&s->d_dyn_ids, &s->cap_dyn, static_cast<size_t>(s->act_off[B]));
+    if (!st && s->cap_split_meta < 4 * s->cap_batch) {
+        if (s->d_split_meta) cudaFree(s->d_split_meta);
+        s->d_split_meta = nullptr;
+        s->cap_split_meta = 0;
+        st = grow(&s->d_split_meta, &s->cap_split_meta, 4 * s->cap_batch);
+    }
+    const size_t wsb = svt_greedy_split_workspace_bytes(s->batch, s->max_groups);
+    if (!st && (wsb > s->cap_split_ws || !s->d_split_ws)) {
+        if (s->d_split_ws) cudaFree(s->d_split_ws);
+        s->d_split_ws = nullptr;
+        s->cap_split_ws = 0;
+        st = grow(&s->d_split_ws, &s->cap_split_ws, wsb);
+        // the static keys start at zero (each split step leaves them at zero)
+        if (!st) {
+            const cudaError_t e = cudaMemset(s->d_split_ws, 0, s->cap_split_ws);
+            if (e != cudaSuccess) st = svt::cuda_status(e, "split workspace memset");
+        }
+    }
+    if (st) return st;
+    const int64_t small[3] = {n_static, 0, 0};
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_st_small, small, sizeof(small), cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_st_ids, ids.data(), ids.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, q));
+    st = svt_plan_layout(s->d_st_small, s->d_st_small + 1, 1, s->d_st_small + 3, s->d_st_meta,
+                         s->st_groups, q);
+    if (!st)
+        st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim, s->d_st_ids,
+                                    s->d_st_small + 3, s->d_st_meta, 1, s->st_groups,
+                                    s->d_st_sub, s->d_bad, q);
+    if (!st)
+        st = svt_decode_split_plans(s->d_active, s->d_act_off, s->n_active_d(), s->batch,
+                                    s->d_words, s->rows, s->d_st_ids, n_static, s->d_dyn_ids,
+                                    s->n_dyn_d(), s->st_valid_d(), s->first_ids_d(),
+                                    s->dyn_starts_d(), q);
+    // (the host copy of `ids` must outlive the async H2D: synchronise here;
+    // prepare ends with a synchronisation anyway)
+    if (!st) SVT_CUDA_TRY(cudaStreamSynchronize(q));
+    return st;
 }
 
 }  // namespace
@@ -336,13 +423,17 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
     st = svt_select_batched(s->d_words, static_universe, s->rows, s->d_inputs, s->d_in_off, batch,
                             s->d_active, s->d_act_off, s->n_active_d(), s->n_static_d(),
                             s->n_dynamic_d(), s->first_bad_d(), q);
+    // split decode for batches over a non-empty static set (SVT_SESSION_SPLIT=0: off)
+    const char* split_env = getenv("SVT_SESSION_SPLIT");
+    s->split = n_static > 0 && batch >= 2 && (split_env == nullptr || atoi(split_env) != 0);
+    if (!st && s->split) st = prepare_split(s, h_static_words, n_static, q);
     if (!st)
-        st = svt_plan_layout(s->n_active_d(), s->d_act_off, batch, s->group_begin_d(), s->d_group_req,
-                             s->max_groups, q);
+        st = svt_plan_layout(s->split ? s->n_dyn_d() : s->n_active_d(), s->d_act_off, batch,
+                             s->group_begin_d(), s->d_group_req, s->max_groups, q);
     if (!st)
-        st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim, s->d_active,
-                                    s->group_begin_d(), s->d_group_req, batch,
-                                    s->max_groups, s->d_sub, s->d_bad, q);
+        st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim,
+                                    s->split ? s->d_dyn_ids : s->d_active, s->group_begin_d(),
+                                    s->d_group_req, batch, s->max_groups, s->d_sub, s->d_bad, q);
     if (st) return st;
     std::vector<int64_t> meta(4 * B);
     SVT_CUDA_TRY(cudaMemcpyAsync(meta.data(), s->n_active_d(), B * sizeof(int64_t),
@@ -413,6 +504,12 @@ svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size
     // must not prefetch them ahead of the dependency wait
     const int32_t flags = s->weights_stable ? SVT_WEIGHTS_STABLE : 0;
     s->weights_stable = true;
+    if (s->split)
+        return svt_greedy_split(s->d_st_sub, s->dt, s->n_st, s->dim, s->d_st_ids, s->st_valid_d(),
+                                s->first_ids_d(), s->d_sub, s->group_begin_d(), s->d_group_req,
+                                s->d_dyn_ids, s->n_dyn_d(), s->dyn_starts_d(), s->batch,
+                                s->max_groups, d_hidden, hidden_ld, flags, d_out_ids, d_out_max,
+                                s->d_split_ws, s->stream);
     return svt_greedy_interleaved(s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req,
                                   s->d_active, s->batch, s->max_groups, d_hidden, hidden_ld, 0, 1,
                                   flags, d_out_ids, d_out_max, nullptr, s->d_ws, s->stream);
@@ -452,10 +549,9 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
         // the weights were gathered before the pull kernel (a full
         // dependency), so the GEMV may always prefetch them early
         s->weights_stable = true;
-        svt_status st = svt_greedy_interleaved(
-            s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req, s->d_active, s->batch,
-            s->max_groups, s->d_hidden, s->ld, 0, 1, SVT_WEIGHTS_STABLE,
-            static_cast<uint32_t*>(dout), static_cast<float*>(dmax), nullptr, s->d_ws, q);
+        svt_status st = svt_session_greedy_device(s, s->d_hidden, s->ld,
+                                                  static_cast<uint32_t*>(dout),
+                                                  static_cast<float*>(dmax));
         if (st) return st;
         SVT_CUDA_TRY(cudaStreamSynchronize(q));
         return SVT_OK;

@@ -35,7 +35,7 @@ namespace {
 
 constexpr int kRB = 2;        // requests per warp (independent chains per lane)
 constexpr int kSWarps = 8;    // warps per CTA
-constexpr int kAhead = 8;     // row chunks in flight per lane
+constexpr int kPieceChunks = 96;  // row chunks staged per piece (~96 KB of shared memory)
 
 struct StaticParams {
     const uint8_t* sub;        // lane-interleaved static rows (svt_gather_interleaved layout)
@@ -51,87 +51,118 @@ struct StaticParams {
     unsigned long long* keys;  // [B] (value, ~id) keys, zero on entry
 };
 
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return static_cast<unsigned long long>(__float_as_uint(lo)) |
+           (static_cast<unsigned long long>(__float_as_uint(hi)) << 32);
+}
+
 template <int DT>
 __global__ void __launch_bounds__(kSWarps * 32) static_rows_kernel(const StaticParams p) {
     using CK = Chunk<DT>;
     constexpr int E = CK::E;
-    extern __shared__ __align__(16) float sh_h[];  // [kRB][nchunks * E] hidden states
-    const int lane = threadIdx.x & 31;
-    const int64_t ngroups = (p.n_static + 31) / 32;
-    const int64_t gblk = (ngroups + kSWarps - 1) / kSWarps;
-    // CTA = (request block, kSWarps consecutive groups): its warps share the
-    // block's hidden states, staged once in shared memory
-    const int b0 = static_cast<int>(blockIdx.x / gblk) * kRB;
-    const int64_t g = (blockIdx.x % gblk) * kSWarps + (threadIdx.x >> 5);
-    const int hlen = p.nchunks * E;  // a multiple of 4
-    {
-        // 16-byte cp.async for the whole float4s of each row, scalar tail, zeros past dim
-        const int q4 = hlen / 4, full4 = p.dim / 4;
-        for (int i = threadIdx.x; i < kRB * q4; i += blockDim.x) {
-            const int r = i / q4, q = i - r * q4;
-            const int b = b0 + r;
-            float* dst = sh_h + r * hlen + 4 * q;
-            if (b < p.B && q < full4) {
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
-                             "l"(p.hidden + static_cast<int64_t>(b) * p.ld + 4 * q)
-                             : "memory");
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int k = 4 * q + e;
-                    dst[e] = (b < p.B && k < p.dim)
-                                 ? __ldg(p.hidden + static_cast<int64_t>(b) * p.ld + k)
-                                 : 0.0f;
-                }
-            }
-        }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    if (g >= ngroups) return;
-    const uint4* src = reinterpret_cast<const uint4*>(p.sub) + g * p.nchunks * 32 + lane;
+    constexpr int kReq = kSWarps * kRB;  // requests per CTA
+    // CTA = (row group g, block of kReq requests): the group's rows and the
+    // block's hidden states are staged once in shared memory and every warp
+    // (kRB requests each) reads both from there
+    extern __shared__ __align__(16) uint8_t ssm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nqb = (p.B + kReq - 1) / kReq;
+    const int64_t g = blockIdx.x / nqb;
+    const int qb = static_cast<int>(blockIdx.x - g * nqb) * kReq;
+    // the K range in pieces of kPieceChunks chunks: stage the group's rows
+    // and the block's hidden states for the piece, then every warp chains on
+    const int pc = p.nchunks < kPieceChunks ? p.nchunks : kPieceChunks;
+    const int hlen = pc * E;  // hidden floats per request per piece (a multiple of 4)
+    uint4* sw = reinterpret_cast<uint4*>(ssm);                                    // [pc][32]
+    float* sh_h = reinterpret_cast<float*>(ssm + static_cast<size_t>(pc) * 512);  // [kReq][hlen]
+    const uint4* src = reinterpret_cast<const uint4*>(p.sub) + g * p.nchunks * 32;
+    const int b0 = qb + warp * kRB;
+    const float* hw = sh_h + warp * kRB * hlen;
     float acc[kRB];
 #pragma unroll
     for (int r = 0; r < kRB; ++r) acc[r] = 0.0f;
-    // the rows stream from L2: keep kAhead chunk loads in flight per lane
-    uint4 wbuf[kAhead];
-#pragma unroll
-    for (int u = 0; u < kAhead; ++u)
-        wbuf[u] = u < p.nchunks ? __ldg(src + u * 32) : make_uint4(0u, 0u, 0u, 0u);
-    for (int c0 = 0; c0 < p.nchunks; c0 += kAhead) {
-#pragma unroll
-        for (int u = 0; u < kAhead; ++u) {
-            const int c = c0 + u;
-            if (c >= p.nchunks) break;
-            float w[E];
-            CK::widen(wbuf[u], w);
-            if (c + kAhead < p.nchunks) wbuf[u] = __ldg(src + (c + kAhead) * 32);
-            const int e0 = c * E;
-            float hv[kRB][E];
-#pragma unroll
-            for (int r = 0; r < kRB; ++r)
-#pragma unroll
-                for (int q = 0; q < E / 4; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(sh_h + r * hlen + e0 + 4 * q);
-                    hv[r][4 * q] = v.x;
-                    hv[r][4 * q + 1] = v.y;
-                    hv[r][4 * q + 2] = v.z;
-                    hv[r][4 * q + 3] = v.w;
-                }
-            if (e0 + E <= p.dim) {
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-#pragma unroll
-                    for (int r = 0; r < kRB; ++r) acc[r] = ref_mac(acc[r], w[e], hv[r][e]);
+    for (int c0 = 0; c0 < p.nchunks; c0 += pc) {
+        const int nc = p.nchunks - c0 < pc ? p.nchunks - c0 : pc;
+        for (int i = threadIdx.x; i < nc * 32; i += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sw + i)),
+                         "l"(src + c0 * 32 + i)
+                         : "memory");
+        const int q4 = nc * E / 4;
+        for (int i = threadIdx.x; i < kReq * q4; i += blockDim.x) {
+            const int r = i / q4, q = i - r * q4;
+            const int b = qb + r;
+            const int k0 = c0 * E + 4 * q;  // element index in the row
+            float* dst = sh_h + r * hlen + 4 * q;
+            if (b < p.B && k0 + 4 <= p.dim) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
+                             "l"(p.hidden + static_cast<int64_t>(b) * p.ld + k0)
+                             : "memory");
             } else {
 #pragma unroll
-                for (int e = 0; e < E; ++e)
-                    if (e0 + e < p.dim)
-#pragma unroll
-                        for (int r = 0; r < kRB; ++r) acc[r] = ref_mac(acc[r], w[e], hv[r][e]);
+                for (int e = 0; e < 4; ++e)
+                    dst[e] = (b < p.B && k0 + e < p.dim)
+                                 ? __ldg(p.hidden + static_cast<int64_t>(b) * p.ld + k0 + e)
+                                 : 0.0f;
             }
         }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        if (b0 < p.B) {
+            // full chunks: no bounds checks, addresses as base + immediate
+            const int left = p.dim - c0 * E;
+            const int nfull = left >= nc * E ? nc : (left > 0 ? left / E : 0);
+            const uint4* wp = sw + lane;
+#pragma unroll 4
+            for (int c = 0; c < nfull; ++c) {
+                float w[E];
+                CK::widen(wp[c * 32], w);
+                float hv[kRB][E];
+#pragma unroll
+                for (int r = 0; r < kRB; ++r)
+#pragma unroll
+                    for (int q = 0; q < E / 4; ++q) {
+                        const float4 v = reinterpret_cast<const float4*>(hw + r * hlen)[c * (E / 4) + q];
+                        hv[r][4 * q] = v.x;
+                        hv[r][4 * q + 1] = v.y;
+                        hv[r][4 * q + 2] = v.z;
+                        hv[r][4 * q + 3] = v.w;
+                    }
+                if constexpr (kRB == 2) {
+                    // the two requests' chains advance in one FADD2 (add.rn.f32x2:
+                    // two independent round-to-nearest adds); the products stay
+                    // scalar __fmul_rn so nothing contracts into an FMA
+                    unsigned long long a2 = pack2(acc[0], acc[1]);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const unsigned long long p2 =
+                            pack2(__fmul_rn(w[e], hv[0][e]), __fmul_rn(w[e], hv[1][e]));
+                        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a2) : "l"(p2));
+                    }
+                    acc[0] = __uint_as_float(static_cast<uint32_t>(a2));
+                    acc[1] = __uint_as_float(static_cast<uint32_t>(a2 >> 32));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+#pragma unroll
+                        for (int r = 0; r < kRB; ++r) acc[r] = ref_mac(acc[r], w[e], hv[r][e]);
+                }
+            }
+            // the row's last, partial chunk (dim not a multiple of E)
+            for (int c = nfull; c < nc; ++c) {
+                float w[E];
+                CK::widen(wp[c * 32], w);
+                const int e0 = c * E;
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if ((c0 + c) * E + e < p.dim)
+#pragma unroll
+                        for (int r = 0; r < kRB; ++r)
+                            acc[r] = ref_mac(acc[r], w[e], hw[r * hlen + e0 + e]);
+            }
+        }
+        __syncthreads();  // the piece's buffers are refilled next
     }
+    if (b0 >= p.B) return;
     const int64_t row = g * 32 + lane;
     const bool live = row < p.n_static;
     const uint32_t id = live ? p.st_ids[row] : 0u;
@@ -255,10 +286,13 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         p.st_valid = d_static_valid;
         p.first_ids = d_first_ids;
         p.keys = keys;
-        const int64_t gblk = ((n_static + 31) / 32 + kSWarps - 1) / kSWarps;
-        const int grid = static_cast<int>(gblk * ((batch + kRB - 1) / kRB));
-        const size_t smem = static_cast<size_t>(kRB) * p.nchunks * (dt == SVT_F32 ? 4 : 8) * 4;
-        if (smem > 200 * 1024) {
+        constexpr int kReq = kSWarps * kRB;
+        const int64_t ngroups = (n_static + 31) / 32;
+        const int grid = static_cast<int>(ngroups * ((batch + kReq - 1) / kReq));
+        const int pc = p.nchunks < kPieceChunks ? p.nchunks : kPieceChunks;
+        const size_t smem = static_cast<size_t>(pc) * 512 +
+                            static_cast<size_t>(kReq) * pc * (dt == SVT_F32 ? 4 : 8) * 4;
+        if (smem > 220 * 1024) {
             set_error("split decode: hidden size %zu too large for the static half", dim);
             return SVT_ERR_CONFIG;
         }

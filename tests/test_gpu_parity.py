@@ -901,8 +901,9 @@ def test_vocab_sharded_certified_batch1(th):
             assert int(got[0]) == int(want), (G, want, got)
 
 
+@pytest.mark.parametrize("split", ["1", "0"], ids=["split", "unsplit"])
 @pytest.mark.parametrize("zero_copy", ["1", "0"], ids=["zero_copy", "step_graph"])
-def test_session_step_graph_pinned_buffers(th, monkeypatch, zero_copy):
+def test_session_step_graph_pinned_buffers(th, monkeypatch, zero_copy, split):
     """Pinned host buffers take the zero-copy step (a pull kernel reads the
     hidden states over PCIe while the PDL-launched GEMV streams weights; the
     finalize writes the ids into host memory) or, with
@@ -913,6 +914,7 @@ def test_session_step_graph_pinned_buffers(th, monkeypatch, zero_copy):
     from paper_2508_15229_b200 import session
 
     monkeypatch.setenv("SVT_SESSION_ZERO_COPY", zero_copy)
+    monkeypatch.setenv("SVT_SESSION_SPLIT", split)  # shared static rows, or every row per request
 
     V, d = 151936, 896
     for B, steps in ((8, 3), (5, 2)):
