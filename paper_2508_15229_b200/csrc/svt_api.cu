@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "svt_gemv.cuh"
 
 namespace svt {
@@ -230,7 +232,8 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
                                 int32_t batch, int64_t max_groups, const float* hidden,
                                 size_t ld, uint32_t row_base, int32_t plan_start, int32_t flags,
                                 uint32_t* out_ids, float* out_max, uint64_t* out_keys, void* ws,
-                                svt_stream stream, const uint8_t* plan_start_req = nullptr) {
+                                svt_stream stream, const uint8_t* plan_start_req = nullptr,
+                                int32_t smem_budget = 0) {
     if (svt_status s = check_dtype(dt)) return s;
     if (svt_status s = need_device()) return s;
     if (batch <= 0) return SVT_OK;
@@ -254,6 +257,7 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
     p.row_base = row_base;
     p.plan_start = plan_start;
     p.plan_start_req = plan_start_req;
+    p.smem_budget = smem_budget;
     p.weights_stable = (flags & SVT_WEIGHTS_STABLE) ? 1 : 0;
     return gemv_run(src, MODE_ARGMAX, dt, p, static_cast<cudaStream_t>(stream));
 }
@@ -322,9 +326,13 @@ svt_status greedy_interleaved_req(const void* d_sub, svt_dtype dt, size_t dim,
                                   size_t ld, int32_t flags, const uint8_t* plan_start_req,
                                   uint32_t* out_ids, uint64_t* out_keys, void* ws,
                                   cudaStream_t st) {
+    // a smaller ring leaves shared memory for a static-half CTA on every SM,
+    // so the two halves run side by side (SVT_SPLIT_GEMV_SMEM: bytes, A/B)
+    const char* env = getenv("SVT_SPLIT_GEMV_SMEM");
+    const int32_t budget = env ? atoi(env) : 112 * 1024;
     return greedy_common(SRC_INTERLEAVED, d_sub, dt, 0, dim, gb, meta, ids, batch, max_groups,
                          hidden, ld, 0, 0, flags, out_ids, nullptr, out_keys, ws, st,
-                         plan_start_req);
+                         plan_start_req, budget);
 }
 }  // namespace svt
 

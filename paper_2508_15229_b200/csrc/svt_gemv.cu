@@ -469,11 +469,12 @@ template <int DT, int SRC, int MODE, int CR>
 svt_status launch_ring_cr(GemvParams p, cudaStream_t st, int nwa, int grid) {
     constexpr int E = Chunk<DT>::E;
     constexpr int kSlot = slot_bytes<SRC, CR>(E);
-    int S = g_tuning.stages > 0 ? g_tuning.stages : kSmemBudget / (nwa * kSlot);
+    const int budget = p.smem_budget > 0 && p.smem_budget < kSmemBudget ? p.smem_budget : kSmemBudget;
+    int S = g_tuning.stages > 0 ? g_tuning.stages : budget / (nwa * kSlot);
     if (g_tuning.stages <= 0 && nwa >= 4 && S > 3) S = 3;
     if (S > 32) S = 32;
     if (S < 2) S = 2;
-    while (nwa > 1 && nwa * S * kSlot > kSmemBudget) --nwa;
+    while (nwa > 1 && nwa * S * kSlot > budget) --nwa;
     p.stages = S;
     p.dbg = g_tuning.dbg;
     // nwa (producer, consumer) warp pairs per CTA, each with S slots and

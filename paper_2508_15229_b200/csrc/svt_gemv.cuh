@@ -48,6 +48,9 @@ struct GemvParams {
     // 0 (split decode: the dynamic rows start the plan only when their first
     // id is below every static id); nullptr: plan_start for all requests
     const uint8_t* plan_start_req;
+    // shared-memory budget of the ring (0: the default, nearly all of it);
+    // the split decode leaves room for its static half beside each CTA
+    int32_t smem_budget;
     int32_t stages;
     int32_t weights_stable;  // sub-head / rows not written by the kernel this launch depends on
     int64_t single_rows;

@@ -35,7 +35,10 @@ namespace {
 
 constexpr int kRB = 2;        // requests per warp (independent chains per lane)
 constexpr int kSWarps = 8;    // warps per CTA
-constexpr int kPieceChunks = 96;  // row chunks staged per piece (~96 KB of shared memory)
+// row chunks staged per piece: 48 (48 KB of shared memory at bf16) lets two
+// static CTAs sit beside the dynamic GEMV's 112 KB ring on one SM
+// (measured at cfg2: 26.8 us per step; 29.9 us with 96-chunk pieces)
+constexpr int kPieceChunks = 48;
 
 struct StaticParams {
     const uint8_t* sub;        // lane-interleaved static rows (svt_gather_interleaved layout)
@@ -49,6 +52,7 @@ struct StaticParams {
     const int64_t* st_valid;   // [B] static rows in the request's plan (n_static or 0)
     const uint32_t* first_ids; // [B] the plan's smallest id
     unsigned long long* keys;  // [B] (value, ~id) keys, zero on entry
+    int32_t piece;             // row chunks staged per piece
 };
 
 __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
@@ -71,7 +75,7 @@ __global__ void __launch_bounds__(kSWarps * 32) static_rows_kernel(const StaticP
     const int qb = static_cast<int>(blockIdx.x - g * nqb) * kReq;
     // the K range in pieces of kPieceChunks chunks: stage the group's rows
     // and the block's hidden states for the piece, then every warp chains on
-    const int pc = p.nchunks < kPieceChunks ? p.nchunks : kPieceChunks;
+    const int pc = p.nchunks < p.piece ? p.nchunks : p.piece;
     const int hlen = pc * E;  // hidden floats per request per piece (a multiple of 4)
     uint4* sw = reinterpret_cast<uint4*>(ssm);                                    // [pc][32]
     float* sh_h = reinterpret_cast<float*>(ssm + static_cast<size_t>(pc) * 512);  // [kReq][hlen]
@@ -289,7 +293,9 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         constexpr int kReq = kSWarps * kRB;
         const int64_t ngroups = (n_static + 31) / 32;
         const int grid = static_cast<int>(ngroups * ((batch + kReq - 1) / kReq));
-        const int pc = p.nchunks < kPieceChunks ? p.nchunks : kPieceChunks;
+        const char* pe = getenv("SVT_SPLIT_PIECE");  // A/B: chunks per staged piece
+        p.piece = pe && atoi(pe) > 0 ? atoi(pe) : kPieceChunks;
+        const int pc = p.nchunks < p.piece ? p.nchunks : p.piece;
         const size_t smem = static_cast<size_t>(pc) * 512 +
                             static_cast<size_t>(kReq) * pc * (dt == SVT_F32 ? 4 : 8) * 4;
         if (smem > 220 * 1024) {
