@@ -131,19 +131,26 @@ __global__ void __launch_bounds__(kSWarps * 32) static_rows_kernel(const StaticP
                         hv[r][4 * q + 2] = v.z;
                         hv[r][4 * q + 3] = v.w;
                     }
-                if constexpr (kRB == 2) {
-                    // the two requests' chains advance in one FADD2 (add.rn.f32x2:
+                if constexpr (kRB % 2 == 0) {
+                    // two requests' chains advance in one FADD2 (add.rn.f32x2:
                     // two independent round-to-nearest adds); the products stay
                     // scalar __fmul_rn so nothing contracts into an FMA
-                    unsigned long long a2 = pack2(acc[0], acc[1]);
+                    unsigned long long a2[kRB / 2];
 #pragma unroll
-                    for (int e = 0; e < E; ++e) {
-                        const unsigned long long p2 =
-                            pack2(__fmul_rn(w[e], hv[0][e]), __fmul_rn(w[e], hv[1][e]));
-                        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a2) : "l"(p2));
+                    for (int r = 0; r < kRB / 2; ++r) a2[r] = pack2(acc[2 * r], acc[2 * r + 1]);
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+#pragma unroll
+                        for (int r = 0; r < kRB / 2; ++r) {
+                            const unsigned long long p2 = pack2(__fmul_rn(w[e], hv[2 * r][e]),
+                                                                __fmul_rn(w[e], hv[2 * r + 1][e]));
+                            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(a2[r]) : "l"(p2));
+                        }
+#pragma unroll
+                    for (int r = 0; r < kRB / 2; ++r) {
+                        acc[2 * r] = __uint_as_float(static_cast<uint32_t>(a2[r]));
+                        acc[2 * r + 1] = __uint_as_float(static_cast<uint32_t>(a2[r] >> 32));
                     }
-                    acc[0] = __uint_as_float(static_cast<uint32_t>(a2));
-                    acc[1] = __uint_as_float(static_cast<uint32_t>(a2 >> 32));
                 } else {
 #pragma unroll
                     for (int e = 0; e < E; ++e)
