@@ -1159,6 +1159,31 @@ def run_sweep(args, torch, rank):
                         flops = None
                     reps = 4 if nbytes < (4 << 30) else 2
                     ms = _graph_ms(torch, fn, reps, flush, sink)
+                    if mode == "shared" and B > 1:
+                        # the shared subset as the static set of a split decode
+                        # (every row static, no dynamic rows): exact chains from
+                        # one shared block; reported when faster
+                        wd = torch.from_numpy(synth.words_of(shared_ids, V).view(np.int64)).cuda()
+                        tbs = th.TailoredBatch.build(
+                            wd, k, V, torch.zeros(1, dtype=torch.int32, device="cuda"),
+                            np.zeros(B + 1, np.int64))
+                        sd = th.SplitDecoder(tbs, head)
+                        hs = torch.zeros((B, (d + 3) // 4 * 4), dtype=torch.float32,
+                                         device="cuda")
+                        hs[:, :d] = hid
+                        keep += [tbs, sd, hs, wd]
+
+                        def fn_split(s, sd=sd, hs=hs):
+                            sd.stream = s
+                            sd.greedy(hs, out)
+                        ms_split = _graph_ms(torch, fn_split, reps, flush, sink)
+                        rec["alt_path_us"] = {rec["path"]: ms * 1e3,
+                                              "svt_greedy_split (shared rows, exact)": ms_split * 1e3}
+                        if ms_split < ms:
+                            ms = ms_split
+                            rec["path"] = "svt_greedy_split (shared rows, exact)"
+                            nbytes = k * d * wb + B * (d * 4 + 8)
+                            flops = None
                     rec["us_per_step"] = ms * 1e3
                     rec["tokens_per_s"] = B / (ms / 1e3)
                     rec["algorithmic_bytes"] = nbytes

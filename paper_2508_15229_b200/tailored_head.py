@@ -401,7 +401,17 @@ class SplitDecoder:
         self.n_dyn, self.st_valid = self.meta
         self.first_ids = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
         self.dyn_starts = torch.zeros(max(B, 1), dtype=torch.uint8, device=dev)
+        # dynamic rows per request <= its plan capacity (any plan missing part
+        # of T keeps every row dynamic); when that capacity's sub-heads would
+        # be huge, size for select-built plans (T inside every plan: at most
+        # capacity - |T| dynamic rows) and check the static-valid flags
         self.max_groups = tb.max_groups
+        self._strict = False
+        if _lib.lib.svt_subhead_bytes(head.storage, d, self.max_groups) > (4 << 30):
+            caps = np.diff(tb.act_off_h)
+            self.max_groups = max(1, int(sum((max(0, int(c) - self.nT) + 31) // 32
+                                              for c in caps)))
+            self._strict = True
         self.gb = torch.zeros(B + 1, dtype=torch.int64, device=dev)
         self.gm = torch.zeros((max(1, self.max_groups), 8), dtype=torch.int32, device=dev)
         self.sub = torch.empty(
@@ -419,6 +429,9 @@ class SplitDecoder:
              tb.n_active.data_ptr(), tb.B, tb._words.data_ptr(), tb.V, self.st_ids.data_ptr(),
              self.nT, self.dyn_ids.data_ptr(), self.n_dyn.data_ptr(), self.st_valid.data_ptr(),
              self.first_ids.data_ptr(), self.dyn_starts.data_ptr(), st)
+        if self._strict and bool((self.st_valid[: tb.B] == 0).any()):
+            raise IntegrityError("split decode sized for select-built plans: a plan is missing "
+                                 "static rows")
         call("svt_plan_layout", self.n_dyn.data_ptr(), tb.act_off.data_ptr(), tb.B,
              self.gb.data_ptr(), self.gm.data_ptr(), self.max_groups, st)
         call("svt_gather_interleaved", head.data.data_ptr(), head.storage, head.rows(),
