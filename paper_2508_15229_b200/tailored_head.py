@@ -429,7 +429,8 @@ class SplitDecoder:
              tb.n_active.data_ptr(), tb.B, tb._words.data_ptr(), tb.V, self.st_ids.data_ptr(),
              self.nT, self.dyn_ids.data_ptr(), self.n_dyn.data_ptr(), self.st_valid.data_ptr(),
              self.first_ids.data_ptr(), self.dyn_starts.data_ptr(), st)
-        if self._strict and bool((self.st_valid[: tb.B] == 0).any()):
+        if (self._strict and not torch.cuda.is_current_stream_capturing()
+                and self._flags_missing_static(st)):
             raise IntegrityError("split decode sized for select-built plans: a plan is missing "
                                  "static rows")
         call("svt_plan_layout", self.n_dyn.data_ptr(), tb.act_off.data_ptr(), tb.B,
@@ -439,6 +440,11 @@ class SplitDecoder:
              self.max_groups, self.sub.data_ptr(), self.bad.data_ptr(), st)
         self._stable = False
         return self
+
+    def _flags_missing_static(self, st) -> bool:
+        # (host check of the split's static-valid flags, on the split's stream)
+        _lib.lib.svt_stream_synchronize(st)
+        return bool((self.st_valid[: self.tb.B] == 0).any())
 
     def greedy(self, hidden: torch.Tensor, out_ids: torch.Tensor,
                out_max: Optional[torch.Tensor] = None) -> torch.Tensor:
