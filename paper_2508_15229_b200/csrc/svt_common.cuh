@@ -238,6 +238,15 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
 namespace svt {
 void set_error(const char* fmt, ...);
 svt_status cuda_status(cudaError_t e, const char* what);
+
+// A side stream (+ fork / join events) per (device, calling stream): kernels
+// forked beside a caller's stream never share events with another caller's
+// concurrent work. Created on first use, kept for the process.
+struct SideStream {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream_for(cudaStream_t main);
 int sm_count();
 }  // namespace svt
 

@@ -1204,29 +1204,6 @@ struct PrefillLayout {
 
 namespace svt {
 namespace {
-// One side stream + fork/join events per device (created on first use).
-struct SideStream {
-    cudaStream_t stream = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-SideStream* side_stream() {
-    static SideStream per_dev[64];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    SideStream& s = per_dev[dev];
-    if (!s.stream) {
-        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess)
-            return nullptr;
-    }
-    return &s;
-}
-}  // namespace
-}  // namespace svt
-
-namespace svt {
-namespace {
 // the split count the workspace layout is sized for: every count a call with
 // the current tuning can use (a call may use fewer, see prefill_score_impl)
 int alloc_nsplit(int64_t S, int64_t P) {
@@ -1399,7 +1376,7 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     // certification: fork them onto a side stream so they overlap the
     // tensor-bound GEMM; joined before certify_kernel (graph-capture safe)
     static const bool serial = getenv("SVT_PREFILL_SERIAL") != nullptr;  // A/B switch
-    SideStream* side = (serial || (mode & 16)) ? nullptr : side_stream();
+    SideStream* side = (serial || (mode & 16)) ? nullptr : side_stream_for(st);
     SideStream inline_side;
     if (!side) {
         inline_side.stream = st;

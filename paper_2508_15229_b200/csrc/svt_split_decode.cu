@@ -20,6 +20,9 @@
 // The static half runs on a side stream beside the dynamic GEMV: one is
 // FP32-issue bound on L2-resident rows, the other HBM bound.
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "svt_common.cuh"
 #include "svt_gemv.cuh"
@@ -222,25 +225,26 @@ __global__ void split_combine_kernel(const uint4* __restrict__ rec,
     if (out_max) out_max[b] = mx;
 }
 
-struct SplitSide {
-    cudaStream_t stream = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-SplitSide* split_side() {
-    static SplitSide per_dev[64];
+}  // namespace
+
+SideStream* side_stream_for(cudaStream_t main) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, SideStream> streams;
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    SplitSide& s = per_dev[dev];
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    SideStream& s = streams[{dev, main}];
     if (!s.stream) {
         if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess)
+            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            streams.erase({dev, main});
             return nullptr;
+        }
     }
     return &s;
 }
-
-}  // namespace
 }  // namespace svt
 
 extern "C" size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups) {
@@ -278,7 +282,7 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
 
     // static half on the side stream (the keys are zero: initial workspace
     // state or reset by the previous combine)
-    SplitSide* side = getenv("SVT_SPLIT_SERIAL") ? nullptr : split_side();
+    SideStream* side = getenv("SVT_SPLIT_SERIAL") ? nullptr : side_stream_for(st);
     cudaStream_t ss = side ? side->stream : st;
     if (side) {
         SVT_CUDA_TRY(cudaEventRecord(side->fork, st));
