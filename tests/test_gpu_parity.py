@@ -693,6 +693,44 @@ def test_split_decode_matches_reference(th, case):
     assert int(dec.bad.item()) == 0
 
 
+def test_split_decode_two_streams(th):
+    """Two split decoders on two streams, launched back to back without a
+    host sync between them: each stream's static half runs on its own side
+    stream and joins its own caller (no shared events), so both batches get
+    the reference ids."""
+    V, d, B = 12000, 256, 5
+    head = th.HeadMatrix.random(V, d, 0xAB, storage=th.SVT_BF16)
+    W = head.to_host()
+    rng = np.random.default_rng(77)
+    decs, hids, refs = [], [], []
+    for j in range(2):
+        words = words_from_ids(rng.choice(V, 250 + 50 * j, replace=False), V)
+        prompts = [rng.integers(0, V, 150).astype(np.uint32) for _ in range(B)]
+        off = np.zeros(B + 1, np.int64)
+        off[1:] = np.cumsum([len(q) for q in prompts])
+        tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(),
+                                    250 + 50 * j, V,
+                                    torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda(),
+                                    off)
+        decs.append(th.SplitDecoder(tb, head))
+        h = bf16_np(rng.uniform(-1, 1, (B, d)).astype(np.float32))
+        hids.append(torch.from_numpy(h).cuda())
+        refs.append([orc.greedy_step(W[orc.select(prompts[b], words, V, V).active_ids], h[b],
+                                     orc.select(prompts[b], words, V, V).active_ids)[0]
+                     for b in range(B)])
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty(B, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for rep in range(4):
+        for j in range(2):
+            decs[j].stream = streams[j]
+            with torch.cuda.stream(streams[j]):
+                decs[j].greedy(hids[j], outs[j])
+    torch.cuda.synchronize()
+    for j in range(2):
+        assert outs[j].cpu().numpy().view(np.uint32).tolist() == refs[j], j
+
+
 # ---- certified batch-1 decode over row-major rows (cfg1 latency path) ----------
 def _rows_decoder(th, head, ids, materialize=True, **kw):
     d_ids = torch.from_numpy(np.ascontiguousarray(ids, np.uint32).view(np.int32)).cuda()
