@@ -7,9 +7,10 @@
 // request. Here they are read once per step for the whole batch:
 //   * static half: static_rows_kernel computes the exact reference-order
 //     logit (acc = fadd_rn(acc, fmul_rn(w, h)), ascending k) of every static
-//     row for every request — the rows come from one shared lane-interleaved
-//     block (L2-resident), each warp dots one 32-row group with RB hidden
-//     states — and folds (value, id) keys per request with a 64-bit atomicMax;
+//     row for every request. A CTA stages one 32-row group of the shared
+//     lane-interleaved block (L2-resident) and 16 hidden states in shared
+//     memory; each warp chains two requests per lane (FADD2) and folds
+//     (value, ~id) keys per request with a 64-bit atomicMax;
 //   * dynamic half: the exact-order GEMV (svt_gemv.cu) over the requests'
 //     D_b \ T sub-heads, one (value, row) record per request; its rows' first
 //     is the plan's first row only when flagged per request (NaN rule);
@@ -17,8 +18,9 @@
 //     plan, so ties resolve to the lower id as the reference scan's earlier
 //     row; a NaN at the plan's first row (the smallest id, in either half)
 //     wins outright.
-// The static half runs on a side stream beside the dynamic GEMV: one is
-// FP32-issue bound on L2-resident rows, the other HBM bound.
+// The static half runs on a side stream beside the dynamic GEMV (its ring
+// capped at 112 KB so two static CTAs fit on each SM): one is FP32-issue
+// bound on L2-resident rows, the other HBM bound.
 #include <cstdlib>
 #include <map>
 #include <mutex>
