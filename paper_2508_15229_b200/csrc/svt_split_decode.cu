@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kSWarps * 32) static_rows_kernel(const StaticP
             const int left = p.dim - c0 * E;
             const int nfull = left >= nc * E ? nc : (left > 0 ? left / E : 0);
             const uint4* wp = sw + lane;
-#pragma unroll 4
+#pragma unroll 8
             for (int c = 0; c < nfull; ++c) {
                 float w[E];
                 CK::widen(wp[c * 32], w);
