@@ -59,7 +59,9 @@ __device__ __forceinline__ bool exp_in_range(uint32_t bits) {
 template <int DT>
 __device__ __forceinline__ bool hidden_fma_safe(float h) {
     const uint32_t b = __float_as_uint(h);
-    constexpr uint32_t low = DT == SVT_BF16 ? 0xFFu : 0x3FFu;
+    // f32 carries 24 significant bits; zeroing the low 8 (bf16 W: 16 + 8)
+    // or low 11 (f16 W: 13 + 11) mantissa bits makes w*h exact
+    constexpr uint32_t low = DT == SVT_BF16 ? 0xFFu : 0x7FFu;
     return exp_in_range(b) && (b & low) == 0u;
 }
 // weight element of a 16-byte chunk (storage bits) inside the safe range
@@ -191,6 +193,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
         "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// L2 prefetch of a contiguous range (a hint: it never makes stale data
+// visible, L2 being the point of coherence), 16-byte granular
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -222,6 +230,23 @@ __device__ __forceinline__ unsigned long long atom_exch_relaxed_u64(unsigned lon
                  : "l"(p), "l"(v)
                  : "memory");
     return old;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {

@@ -64,6 +64,7 @@ constexpr int kMaxCand = 1024;   // tail candidate list
 constexpr int kPiece = 2048;     // bytes per exact-recompute piece
 constexpr unsigned kOverflow = 0xFFFFFFFFu;
 constexpr unsigned kBad = 0xFFFFFFFEu;  // record count: a non-finite value in the CTA
+constexpr int kPollLimit = 256;  // fast finalize: polls before it falls back to the grid dependency
 
 // Per-CTA record: the CTA's max lo and its rows with hi >= it (inline up to
 // two, with their remapped ids; more go to the gcand list, kOverflow means
@@ -645,6 +646,493 @@ __global__ void __launch_bounds__(32, 16) greedy_rows_finalize_kernel(SmallParam
     if (lane == 0) atomicAdd(&p.ctrl[nw_code == 0 ? 4 : 5], 1u);
 }
 
+
+// ===========================================================================
+// Small plans: every row of a CTA resident at once (<= 32 rows per CTA) —
+// the batch-1 decode of BASELINE cfg1 (|S| ~ 2.55k rows of 8 KB).
+//
+// Why a second kernel: at cfg1 the warp-per-row kernel above spends ~2.5 us
+// per token AFTER h arrives, replicating h through shared memory into every
+// warp's registers (15 x 8 KB per SM) and reading every row from shared
+// memory on the critical path; its finalize is a full grid dependency
+// behind the rows grid. Here:
+//  * 16 compute warps in 4 row groups; thread (group g, t in 0..127) owns
+//    chunks t, t+128, ... of every row of its group, so h is read once per
+//    group-thread (16 floats) instead of once per warp-row.
+//  * Rows are stable across decode steps (SVT_ROWS_WEIGHTS_STABLE): a
+//    control warp issues one bulk copy per row BEFORE the programmatic
+//    dependency wait, and the compute warps move them into registers as
+//    they land — also before h exists. After the wait only h (8 KB, one
+//    bulk copy, prefetched into L2 beforehand) and the FFMAs remain.
+//  * Reductions: a transpose-halving shuffle reduce (2 x rows-per-group
+//    values per thread, one value per lane at the end), then four warp
+//    partials per group summed in a fixed order by the control warp, one
+//    lane per row: bound, lo/hi, the CTA's candidates.
+//  * Hand-off without a grid dependency: each CTA publishes a tagged
+//    32-byte record of four 64-bit words (each single-copy atomic and
+//    carrying the launch's 8-bit tag). The one-warp finalize polls them.
+//    Values in the words are 24-bit orderable keys rounded outward (L down,
+//    hi up), so the certification only ever keeps more candidates. A CTA
+//    with more than two candidates also writes its list and releases it
+//    (fence) before its record; nothing else is written, so consecutive
+//    launches never race on unfenced scratch.
+//  * The finalize reserves enough shared memory that it can only run on
+//    the SM the rows grid leaves free (grid = SMs - 1): its polls never
+//    queue behind a rows CTA's bulk-copy stream.
+// ===========================================================================
+constexpr int kFNG = 4;                      // row groups per CTA
+constexpr int kFWPG = 4;                     // compute warps per group
+constexpr int kFCompute = kFNG * kFWPG;      // 16
+constexpr int kFThreads = (kFCompute + 1) * 32;  // + the control warp
+constexpr int kFTPG = kFWPG * 32;            // chunk stride inside a group
+constexpr int kFMaxRows = 32;                // rows per CTA: one control lane each
+constexpr int kFMaxGrid = 160;  // >= SMs - 1 rows CTAs (B200: 147)
+
+struct alignas(32) FRec {
+    unsigned long long w[4];
+};
+
+struct FastParams {
+    const uint8_t* W;
+    int64_t row_bytes;
+    const uint32_t* src_ids;  // nullptr: row k is W row k
+    int64_t n;
+    int32_t dim;
+    int32_t flags;
+    const float* h;
+    const uint32_t* plan_ids;
+    uint32_t row_base;
+    int32_t plan_start;
+    uint32_t* out_id;
+    float* out_max;
+    uint4* out_key;
+    unsigned* ctrl;   // [4]/[5] statistics, [8] epoch counter in [0, 255)
+    FRec* frec;       // [kFMaxGrid]
+    uint2* cand;      // [kFMaxGrid][kFMaxRows] {global row, hi bits} (> 2 candidates)
+    float c_rel;
+    float eta;
+    int32_t grid;
+    int32_t extra;
+    int64_t per_cta;
+    int32_t fin_in_grid;  // 1: the finalizer is the grid's last CTA; 0: its own launch
+    unsigned long long* dbg;  // per CTA 8 %globaltimer stamps (svt_rows_set_debug)
+};
+
+__device__ __forceinline__ int64_t frow_begin(const FastParams& p, int c) {
+    return p.per_cta * c + (c < p.extra ? c : p.extra);
+}
+__device__ __forceinline__ const uint8_t* frow_ptr(const FastParams& p, int64_t r) {
+    const int64_t src = p.src_ids ? static_cast<int64_t>(__ldg(p.src_ids + r)) : r;
+    return p.W + src * p.row_bytes;
+}
+__device__ __forceinline__ unsigned ord24_down(float v) { return ord_of(v) >> 8; }
+__device__ __forceinline__ unsigned ord24_up_of(unsigned o) {
+    const unsigned long long u = (static_cast<unsigned long long>(o) + 255ull) >> 8;
+    return static_cast<unsigned>(u > 0xFFFFFFull ? 0xFFFFFFull : u);
+}
+// epoch counter -> the launch's tag in [1, 255]; a zeroed record never matches
+__device__ __forceinline__ unsigned long long tag_of(unsigned e) {
+    return static_cast<unsigned long long>(e % 255u + 1u);
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+#define SVT_FSTAMP(k) \
+    if (p.dbg) p.dbg[blockIdx.x * 128 + (k)] = gtimer()
+
+template <int RPG>
+struct FPad {  // 2 * RPG values padded to a power of two <= 32
+    static constexpr int P = 2 * RPG <= 2 ? 2 : 2 * RPG <= 4 ? 4 : 2 * RPG <= 8 ? 8
+                           : 2 * RPG <= 16 ? 16 : 32;
+    static constexpr int LOG = P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : 5;
+};
+
+template <int DT, int CPT, int RPG>
+__device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm) {
+    constexpr int E = Chunk<DT>::E;
+    constexpr int P = FPad<RPG>::P, LOG = FPad<RPG>::LOG;
+    __shared__ uint64_t s_bar[kFMaxRows];
+    __shared__ uint64_t s_hbar;
+    __shared__ __align__(16) unsigned s_epoch[4];
+    __shared__ float s_red[kFNG][kFWPG][P];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t r0 = frow_begin(p, c);
+    const int nrows = static_cast<int>(frow_begin(p, c + 1) - r0);
+    const uint32_t rb = static_cast<uint32_t>(p.row_bytes);
+    const uint32_t h_bytes = static_cast<uint32_t>(p.dim) * 4u;
+    uint8_t* ring = dsm;
+    float* s_h = reinterpret_cast<float*>(dsm + static_cast<size_t>(kFNG * RPG) * rb);
+    const bool early = (p.flags & SVT_ROWS_WEIGHTS_STABLE) != 0;
+    if (tid == kFCompute * 32) {
+        SVT_FSTAMP(0);
+        for (int i = 0; i < nrows; ++i) mbar_init(&s_bar[i], 1);
+        mbar_init(&s_hbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kFCompute) {
+        // ---- control warp: copies, dependency, h, then the CTA record ----
+        uint32_t my_id = 0u;
+        const uint64_t pol = policy_evict_first();
+        auto issue_rows = [&]() {
+            if (lane < nrows) {
+                mbar_arrive_expect_tx(&s_bar[lane], rb);
+                bulk_g2s(ring + static_cast<size_t>(lane) * rb, frow_ptr(p, r0 + lane), rb,
+                         &s_bar[lane], pol);
+                my_id = p.plan_ids ? __ldg(p.plan_ids + r0 + lane)
+                                   : p.row_base + static_cast<uint32_t>(r0 + lane);
+            }
+        };
+        if (early) issue_rows();
+        if (lane == 0) bulk_prefetch_l2(p.h, h_bytes);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;");
+        if (lane == 0) SVT_FSTAMP(1);
+        if (!early) issue_rows();
+        if (lane == 0) {
+            // h and the epoch counter (written by the previous finalize) in
+            // one transaction group: no LSU round trip on the critical path
+            mbar_arrive_expect_tx(&s_hbar, h_bytes + 16u);
+            bulk_g2s(s_h, p.h, h_bytes, &s_hbar, policy_evict_last());
+            bulk_g2s(s_epoch, p.ctrl + 8, 16u, &s_hbar, policy_evict_last());
+        }
+        named_bar_sync(1, kFThreads);  // every group's warp partials are in s_red
+        const unsigned epoch = s_epoch[0];  // s_hbar completed before the compute warps arrived
+        if (lane == 0) SVT_FSTAMP(3);
+        // lane j <-> row j: group j % 4, slot j / 4
+        const bool act = lane < nrows;
+        float f = 0.0f, a = 0.0f;
+        if (act) {
+            const int g = lane % kFNG, k = lane / kFNG;
+#pragma unroll
+            for (int w = 0; w < kFWPG; ++w) {
+                f += s_red[g][w][2 * k];
+                a += s_red[g][w][2 * k + 1];
+            }
+        }
+        const bool bad = act && (!isfinite(f) || !isfinite(a));
+        const float bnd = __fadd_ru(__fmul_ru(p.c_rel, a), p.eta);
+        float lo = __fsub_rd(f, bnd);
+        const float hi = __fadd_ru(f, bnd);
+        if (!(lo == lo) || !act) lo = -FLT_MAX;
+        float L = lo;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xFFFFFFFFu, L, o));
+        if (lane == 0) SVT_FSTAMP(5);
+        const bool anybad = __any_sync(0xFFFFFFFFu, bad);
+        const bool cand = act && hi >= L;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, cand);
+        const unsigned cnt = __popc(m);
+        const unsigned oh = cand ? ord_of(hi) : 0u;
+        const unsigned h1 = __reduce_max_sync(0xFFFFFFFFu, oh);
+        const int l1 = __ffs(__ballot_sync(0xFFFFFFFFu, cand && oh == h1)) - 1;
+        const unsigned oh2 = (cand && lane != l1) ? oh : 0u;
+        const unsigned h2 = __reduce_max_sync(0xFFFFFFFFu, oh2);
+        const unsigned m2 = __ballot_sync(0xFFFFFFFFu, cand && lane != l1 && oh2 == h2);
+        const int l2 = m2 ? __ffs(m2) - 1 : l1;
+        const uint32_t id1 = __shfl_sync(0xFFFFFFFFu, my_id, l1 < 0 ? 0 : l1);
+        const uint32_t id2 = __shfl_sync(0xFFFFFFFFu, my_id, l2 < 0 ? 0 : l2);
+        const unsigned code = anybad ? 1u : (cnt > 2 ? 2u : 0u);
+        if (code == 2u && cand) {  // the full list, released before the record
+            const unsigned pos = __popc(m & ((1u << lane) - 1u));
+            p.cand[static_cast<size_t>(c) * kFMaxRows + pos] =
+                make_uint2(static_cast<uint32_t>(r0 + lane), __float_as_uint(hi));
+        }
+        __syncwarp();
+        if (lane == 0) SVT_FSTAMP(6);
+        if (lane == 0) {
+            if (code == 2u) fence_acq_rel_gpu();
+            const unsigned long long tag = tag_of(epoch) << 56;
+            const unsigned long long l24 = ord24_down(L);
+            const unsigned long long hi1 = ord24_up_of(h1);
+            const unsigned long long hi2 = cnt >= 2 ? ord24_up_of(h2) : 0ull;
+            const unsigned long long row1 = static_cast<unsigned>(l1 < 0 ? 0 : l1) & 0xFFFFu;
+            const unsigned long long row2 = cnt >= 2 ? (static_cast<unsigned>(l2) & 0xFFFFu)
+                                                     : 0xFFFFull;
+            FRec* fr = p.frec + c;
+            st_relaxed_u64(&fr->w[0], tag | l24 << 32 | hi2 << 8 | code);
+            st_relaxed_u64(&fr->w[1], tag | hi1 << 32 | id1);
+            st_relaxed_u64(&fr->w[2], tag | row1 << 32 | row2 << 16);
+            st_relaxed_u64(&fr->w[3], tag | static_cast<unsigned long long>(cnt) << 32 | id2);
+            SVT_FSTAMP(4);
+        }
+        return;
+    }
+    // ---- compute warps ------------------------------------------------------
+    const int g = warp / kFWPG, wig = warp % kFWPG, tg = wig * 32 + lane;
+    uint4 wv[RPG][CPT];
+#pragma unroll
+    for (int k = 0; k < RPG; ++k) {
+        const int i = k * kFNG + g;
+        if (i < nrows) {
+            mbar_wait_parity(&s_bar[i], 0u);
+#pragma unroll
+            for (int q = 0; q < CPT; ++q)
+                wv[k][q] = *reinterpret_cast<const uint4*>(ring + static_cast<size_t>(i) * rb +
+                                                           static_cast<size_t>(tg + q * kFTPG) * 16);
+        } else {
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) wv[k][q] = make_uint4(0u, 0u, 0u, 0u);
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;");
+    mbar_wait_parity(&s_hbar, 0u);
+    if (warp == 0 && lane == 0) SVT_FSTAMP(2);
+    float hv[CPT][E];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(s_h + (tg + q * kFTPG) * E + e);
+            hv[q][e] = x.x;
+            hv[q][e + 1] = x.y;
+            hv[q][e + 2] = x.z;
+            hv[q][e + 3] = x.w;
+        }
+    }
+    float v[P];
+#pragma unroll
+    for (int k = 0; k < RPG; ++k) {
+        float f0 = 0.0f, f1 = 0.0f, a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            float w[E];
+            Chunk<DT>::widen(wv[k][q], w);
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+                f0 = __fmaf_rn(w[e], hv[q][e], f0);
+                a0 = __fmaf_rn(fabsf(w[e]), fabsf(hv[q][e]), a0);
+                f1 = __fmaf_rn(w[e + 1], hv[q][e + 1], f1);
+                a1 = __fmaf_rn(fabsf(w[e + 1]), fabsf(hv[q][e + 1]), a1);
+            }
+        }
+        v[2 * k] = f0 + f1;
+        v[2 * k + 1] = a0 + a1;
+    }
+#pragma unroll
+    for (int j = 2 * RPG; j < P; ++j) v[j] = 0.0f;
+    // transpose-halving: after LOG steps lane l holds value (l >> (5-LOG)) & (P-1)
+#pragma unroll
+    for (int s = 0; s < LOG; ++s) {
+        const int o = 16 >> s;
+        const int m = P >> (s + 1);
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < m; ++j) {
+            const float send = up ? v[j] : v[j + m];
+            const float keep = up ? v[j + m] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, o);
+        }
+    }
+#pragma unroll
+    for (int o = (16 >> LOG); o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xFFFFFFFFu, v[0], o);
+    if ((lane & ((32 >> LOG) - 1)) == 0) s_red[g][wig][(lane >> (5 - LOG)) & (P - 1)] = v[0];
+    named_bar_arrive(1, kFThreads);
+}
+
+// ---- the grid's last CTA: one warp polls the tagged records and decides ------
+template <int DT>
+__device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t* fsmem, unsigned* sn) {
+    unsigned& s_n = *sn;
+    const int lane = threadIdx.x;
+    const int G = p.grid;
+    unsigned* s_list = reinterpret_cast<unsigned*>(fsmem);                     // [kMaxCand]
+    uint8_t* s_buf = fsmem + kMaxCand * 4;                                     // 2 pieces
+    float* s_h = reinterpret_cast<float*>(fsmem + kMaxCand * 4 + 2 * kPiece);  // [dim]
+    if (lane == 0) s_n = 0;
+    constexpr int kPer = kFMaxGrid / 32;
+    // written by the previous launch's finalize, complete before the wait
+    const unsigned epoch = ld_relaxed_u32(p.ctrl + 8);
+    const unsigned long long tag = tag_of(epoch);
+    unsigned long long w0[kPer], w1[kPer], w2[kPer], w3[kPer];
+    bool seen = false;
+    const unsigned long long t_start = gtimer();
+    for (int it = 0; !seen; ++it) {
+        // every load of a round is issued before any result is used
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            if (32 * q < G) {
+                const FRec* fr = p.frec + min(lane + 32 * q, G - 1);
+                w0[q] = ld_relaxed_u64(&fr->w[0]);
+                w1[q] = ld_relaxed_u64(&fr->w[1]);
+                w2[q] = ld_relaxed_u64(&fr->w[2]);
+                w3[q] = ld_relaxed_u64(&fr->w[3]);
+            }
+        }
+        bool mine = true;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+            if (32 * q < G)
+                mine = mine && (w0[q] >> 56) == tag && (w1[q] >> 56) == tag &&
+                       (w2[q] >> 56) == tag && (w3[q] >> 56) == tag;
+        seen = __all_sync(0xFFFFFFFFu, mine);
+        if (!seen && it >= kPollLimit) {
+            // rows CTAs still streaming (large rows, a busy GPU): back off;
+            // after 2 s something is wrong (a record never came) — report
+            // an invalid id instead of hanging the device
+            __nanosleep(256);
+            if (__shfl_sync(0xFFFFFFFFu, gtimer() - t_start, 0) > 2000000000ull) {
+                if (lane == 0) {
+                    *p.out_id = 0xFFFFFFFFu;
+                    atomicAdd(&p.ctrl[6], 1u);
+                    p.ctrl[8] = (epoch + 1u) % 255u;
+                }
+                return;
+            }
+        }
+    }
+    if (p.dbg && lane == 0) p.dbg[124] = gtimer();
+    unsigned l24 = 0u, code = 0u;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        if (32 * q < G && lane + 32 * q < G) {
+            l24 = max(l24, static_cast<unsigned>(w0[q] >> 32) & 0xFFFFFFu);
+            code |= static_cast<unsigned>(w0[q] & 0xFFu);
+        }
+    }
+    l24 = __reduce_max_sync(0xFFFFFFFFu, l24);
+    code = __reduce_or_sync(0xFFFFFFFFu, code);
+    // candidates from the records: hi1 / hi2 >= L (outward-rounded keys)
+    unsigned nhit = 0u, id = 0u;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+        if (32 * q < G && lane + 32 * q < G) {
+            const unsigned hi1 = static_cast<unsigned>(w1[q] >> 32) & 0xFFFFFFu;
+            const unsigned hi2 = static_cast<unsigned>(w0[q] >> 8) & 0xFFFFFFu;
+            if (hi1 >= l24) {
+                ++nhit;
+                id = static_cast<unsigned>(w1[q]);
+            }
+            if (hi2 >= l24 && (static_cast<unsigned>(w3[q] >> 32) & 0xFFFFu) >= 2u) ++nhit;
+        }
+    }
+    const unsigned total = __reduce_add_sync(0xFFFFFFFFu, nhit);
+    const bool want_exact = p.out_max || p.out_key;
+    unsigned recomputed = 0u;
+    if (code == 0u && total == 1u && !want_exact) {
+        // one row can reach the largest lower bound: the reference argmax
+        if (nhit) *p.out_id = id;
+    } else {
+        recomputed = 1u;
+        const bool all = (code & 1u) != 0u;
+        if (!all) {
+            if (code & 2u) fence_acq_rel_gpu();  // acquire the released lists
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int cc = lane + 32 * q;
+                if (32 * q >= G || cc >= G) continue;
+                const int64_t b = frow_begin(p, cc);
+                const unsigned ccode = static_cast<unsigned>(w0[q] & 0xFFu);
+                const unsigned cnt = static_cast<unsigned>(w3[q] >> 32) & 0xFFFFu;
+                if (ccode == 0u) {
+                    if ((static_cast<unsigned>(w1[q] >> 32) & 0xFFFFFFu) >= l24) {
+                        const unsigned k = atomicAdd(&s_n, 1u);
+                        if (k < kMaxCand)
+                            s_list[k] = static_cast<unsigned>(b) +
+                                        (static_cast<unsigned>(w2[q] >> 32) & 0xFFFFu);
+                    }
+                    if (cnt >= 2u && (static_cast<unsigned>(w0[q] >> 8) & 0xFFFFFFu) >= l24) {
+                        const unsigned k = atomicAdd(&s_n, 1u);
+                        if (k < kMaxCand)
+                            s_list[k] = static_cast<unsigned>(b) +
+                                        (static_cast<unsigned>(w2[q] >> 16) & 0xFFFFu);
+                    }
+                } else {
+                    for (unsigned e = 0; e < cnt && e < static_cast<unsigned>(kFMaxRows); ++e) {
+                        const uint2 ce = __ldcg(p.cand + static_cast<size_t>(cc) * kFMaxRows + e);
+                        if (ord24_up_of(ord_of(__uint_as_float(ce.y))) >= l24) {
+                            const unsigned k = atomicAdd(&s_n, 1u);
+                            if (k < kMaxCand) s_list[k] = ce.x;
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const unsigned n = s_n;
+        const bool every = all || n == 0 || n > static_cast<unsigned>(kMaxCand);
+        if (!every && n == 1u && !want_exact) {
+            // one row left once the lists are filtered by the global bar
+            if (lane == 0) {
+                const uint32_t r = s_list[0];
+                *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+                if (p.dbg) p.dbg[126] = gtimer();
+                p.ctrl[8] = (epoch + 1u) % 255u;
+                atomicAdd(&p.ctrl[4], 1u);
+            }
+            return;
+        }
+        for (int e = lane * 4; e < p.dim; e += 32 * 4)
+            *reinterpret_cast<float4*>(s_h + e) = __ldg(reinterpret_cast<const float4*>(p.h + e));
+        __syncwarp();
+        const int64_t nwork = every ? p.n : static_cast<int64_t>(n);
+        unsigned long long best = 0ull;
+        for (int64_t i = 0; i < nwork; ++i) {
+            const int64_t r = every ? i : static_cast<int64_t>(s_list[i]);
+            const float v = exact_row_warp<DT>(frow_ptr(p, r), p.row_bytes, s_h, s_buf, lane);
+            const unsigned long long key =
+                make_key(v, static_cast<uint32_t>(r), true, p.plan_start && r == 0);
+            best = key > best ? key : best;
+        }
+        if (lane == 0) {
+            const unsigned long long k = best;
+            const uint32_t r = 0xFFFFFFFFu - static_cast<uint32_t>(k);
+            uint32_t oid = 0xFFFFFFFFu;
+            float mx = __int_as_float(0x7FC00000);
+            unsigned long long gk = 0ull;
+            if (k != 0ull) {
+                oid = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
+                if (k != kNanRow0Key) mx = float_of_ord(static_cast<uint32_t>(k >> 32));
+                gk = k == kNanRow0Key ? k
+                                      : (k & 0xFFFFFFFF00000000ull) | (0xFFFFFFFFu - (p.row_base + r));
+            }
+            *p.out_id = oid;
+            if (p.out_max) *p.out_max = mx;
+            if (p.out_key)
+                *p.out_key = make_uint4(static_cast<uint32_t>(gk), static_cast<uint32_t>(gk >> 32),
+                                        oid, __float_as_uint(mx));
+        }
+    }
+    if (lane == 0) {
+        if (p.dbg) p.dbg[126] = gtimer();
+        p.ctrl[8] = (epoch + 1u) % 255u;
+        atomicAdd(&p.ctrl[recomputed ? 5 : 4], 1u);
+    }
+}
+
+// the finalize as its own one-warp grid (a programmatic dependent of the rows
+// grid; it polls instead of waiting, and its shared-memory reservation keeps
+// it on the SM the rows grid leaves free)
+template <int DT>
+__global__ void __launch_bounds__(32, 1) rows_fast_fin_kernel(FastParams p) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    extern __shared__ __align__(128) uint8_t fsm[];
+    __shared__ unsigned s_n;
+    if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
+    rows_fast_finalize<DT>(p, fsm, &s_n);
+}
+
+template <int DT, int CPT, int RPG>
+__global__ void __launch_bounds__(kFThreads, 1) rows_fast_kernel(FastParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    if (blockIdx.x == p.grid) {
+        // the finalizer: dispatched after every rows CTA (highest index), on
+        // the SM they leave free
+        if (threadIdx.x >= 32) return;
+        __shared__ unsigned s_n;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;");
+        if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
+        rows_fast_finalize<DT>(p, dsm, &s_n);
+        return;
+    }
+    rows_fast_cta<DT, CPT, RPG>(p, dsm);
+}
+
 unsigned long long* g_rows_dbg = nullptr;
 
 double gamma_n(double n) {
@@ -687,6 +1175,88 @@ svt_status launch_rows(SmallParams p, int grid, cudaStream_t st) {
     return SVT_OK;
 }
 
+template <int DT, int CPT, int RPG>
+svt_status launch_rows_fast(FastParams p, cudaStream_t st) {
+    size_t smem = static_cast<size_t>(kFNG * RPG) * static_cast<size_t>(p.row_bytes) +
+                  static_cast<size_t>(p.dim) * 4;
+    const size_t fin_smem = kMaxCand * 4 + 2 * kPiece + static_cast<size_t>(p.dim) * 4;
+    smem = smem > fin_smem ? smem : fin_smem;  // the finalizer's recompute buffers
+    auto kern = rows_fast_kernel<DT, CPT, RPG>;
+    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    // rows CTAs (+ the finalizer CTA, last index, in one-launch mode)
+    cfg.gridDim = dim3(static_cast<unsigned>(p.grid + (p.fin_in_grid ? 1 : 0)));
+    cfg.blockDim = dim3(kFThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    if (p.fin_in_grid) return SVT_OK;
+    size_t fsmem = fin_smem;
+    const size_t sm_smem = 228 * 1024;
+    if (smem < sm_smem && sm_smem - smem > fsmem) fsmem = sm_smem - smem;
+    if (fsmem > 200 * 1024) fsmem = 200 * 1024;
+    auto fin = rows_fast_fin_kernel<DT>;
+    SVT_CUDA_TRY(cudaFuncSetAttribute(fin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(fsmem)));
+    cudaLaunchConfig_t fc = {};
+    fc.gridDim = dim3(1);
+    fc.blockDim = dim3(32);
+    fc.dynamicSmemBytes = fsmem;
+    fc.stream = st;
+    fc.attrs = attr;
+    fc.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&fc, fin, p));
+    return SVT_OK;
+}
+
+template <int DT, int CPT>
+svt_status pick_rpg(FastParams p, int rpg, cudaStream_t st) {
+    if (rpg <= 1) return launch_rows_fast<DT, CPT, 1>(p, st);
+    if (rpg <= 2) return launch_rows_fast<DT, CPT, 2>(p, st);
+    if (rpg <= 3) return launch_rows_fast<DT, CPT, 3>(p, st);
+    if constexpr (CPT <= 4) {
+        if (rpg <= 5) return launch_rows_fast<DT, CPT, 5>(p, st);
+    }
+    if constexpr (CPT <= 2) {
+        if (rpg <= 8) return launch_rows_fast<DT, CPT, 8>(p, st);
+    }
+    return SVT_ERR_CONFIG;
+}
+
+// The small-plan kernel when the shape fits (every row of a CTA resident,
+// 16-byte chunks a multiple of 128 per row, <= 20 chunks per thread in
+// registers); returns false to fall back to the streaming kernel.
+bool rows_fast_eligible(int64_t n, size_t row_bytes, size_t dim, int* grid_out, int* rpg_out,
+                        int* cpt_out) {
+    if (const char* v = getenv("SVT_ROWS_FAST"))
+        if (atoi(v) == 0) return false;
+    const size_t nchunks = row_bytes / 16;
+    if (nchunks % kFTPG != 0) return false;
+    const int cpt = static_cast<int>(nchunks / kFTPG);
+    if (cpt != 1 && cpt != 2 && cpt != 4) return false;
+    const int sms = sm_count();
+    // one SM left to the finalize once the plan covers the GPU
+    int grid = static_cast<int>(n < sms - 1 ? n : sms - 1);
+    if (grid < 1) grid = 1;
+    if (grid > kFMaxGrid) grid = kFMaxGrid;
+    const int64_t rpc = (n + grid - 1) / grid;
+    if (rpc > kFMaxRows) return false;
+    const int rpg = static_cast<int>((rpc + kFNG - 1) / kFNG);
+    const int rpg_t = rpg <= 3 ? rpg : rpg <= 5 ? 5 : 8;
+    if (rpg_t * cpt > 20 || (cpt == 4 && rpg_t > 5)) return false;
+    if (static_cast<size_t>(kFNG * rpg_t) * row_bytes + dim * 4 > 200 * 1024) return false;
+    *grid_out = grid;
+    *rpg_out = rpg_t;
+    *cpt_out = cpt;
+    return true;
+}
+
 }  // namespace
 }  // namespace svt
 
@@ -694,10 +1264,21 @@ extern "C" void svt_rows_set_debug(void* d_stamps) {
     svt::g_rows_dbg = static_cast<unsigned long long*>(d_stamps);
 }
 
+namespace {
+size_t rows_stream_ws_bytes(size_t rows) {
+    using namespace svt;
+    const size_t b = 256 + static_cast<size_t>(kMaxGrid) * sizeof(Rec) +
+                     static_cast<size_t>(kMaxGrid) * kCapG * 8 + (rows > 0 ? rows : 1) * 4;
+    return (b + 255) / 256 * 256;
+}
+}  // namespace
+
 extern "C" size_t svt_greedy_rows_workspace_bytes(size_t rows) {
     using namespace svt;
-    return 256 + static_cast<size_t>(kMaxGrid) * sizeof(Rec) +
-           static_cast<size_t>(kMaxGrid) * kCapG * 8 + (rows > 0 ? rows : 1) * 4;
+    // streaming-kernel area, then the small-plan kernel's tagged records and
+    // candidate lists (disjoint: a workspace may serve both kernels)
+    return rows_stream_ws_bytes(rows) + static_cast<size_t>(kFMaxGrid) * sizeof(FRec) +
+           static_cast<size_t>(kFMaxGrid) * kFMaxRows * sizeof(uint2);
 }
 
 extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
@@ -767,6 +1348,58 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
                       (1.0 - gamma_n(n_fast)) * 1.0001;
     p.c_rel = static_cast<float>(cr) * (1.0f + FLT_EPSILON);
     p.eta = static_cast<float>((static_cast<double>(dim) + n_fast) * 4.0) * 1.40129846e-45f;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    {
+        int fgrid = 0, rpg = 0, cpt = 0;
+        if (!getenv("SVT_ROWS_GRID") &&
+            rows_fast_eligible(p.n, row_bytes, dim, &fgrid, &rpg, &cpt)) {
+            FastParams f = {};
+            f.W = p.W;
+            f.row_bytes = p.row_bytes;
+            f.src_ids = p.src_ids;
+            f.n = p.n;
+            f.dim = p.dim;
+            f.flags = flags;
+            f.h = d_hidden;
+            f.plan_ids = d_plan_ids;
+            f.row_base = row_base;
+            f.plan_start = plan_start;
+            f.out_id = d_out_id;
+            f.out_max = d_out_max;
+            f.out_key = static_cast<uint4*>(d_out_record);
+            f.ctrl = p.ctrl;
+            uint8_t* fb = static_cast<uint8_t*>(d_workspace) + rows_stream_ws_bytes(n_rows);
+            f.frec = reinterpret_cast<FRec*>(fb);
+            f.cand = reinterpret_cast<uint2*>(fb + kFMaxGrid * sizeof(FRec));
+            f.grid = fgrid;
+            f.per_cta = p.n / fgrid;
+            f.extra = static_cast<int32_t>(p.n % fgrid);
+            f.dbg = g_rows_dbg;
+            if (const char* v = getenv("SVT_ROWS_FIN")) f.fin_in_grid = atoi(v) != 0;
+            // fast-pass depth: CPT*E/2 FFMAs per accumulator (+1 combine), 5
+            // shuffle levels, 4 warp partials summed in order (+ slack)
+            const int Ef = dt == SVT_F32 ? 4 : 8;
+            const double nf = static_cast<double>(cpt * Ef / 2 + 1 + 5 + 4 + 2);
+            const double crf = (gamma_n(nf) + gamma_n(static_cast<double>(dim))) /
+                               (1.0 - gamma_n(nf)) * 1.0001;
+            f.c_rel = static_cast<float>(crf) * (1.0f + FLT_EPSILON);
+            f.eta = static_cast<float>((static_cast<double>(dim) + nf) * 4.0) * 1.40129846e-45f;
+            switch (dt) {
+                case SVT_F32:
+                    return cpt == 1   ? pick_rpg<SVT_F32, 1>(f, rpg, st)
+                           : cpt == 2 ? pick_rpg<SVT_F32, 2>(f, rpg, st)
+                                      : pick_rpg<SVT_F32, 4>(f, rpg, st);
+                case SVT_F16:
+                    return cpt == 1   ? pick_rpg<SVT_F16, 1>(f, rpg, st)
+                           : cpt == 2 ? pick_rpg<SVT_F16, 2>(f, rpg, st)
+                                      : pick_rpg<SVT_F16, 4>(f, rpg, st);
+                default:
+                    return cpt == 1   ? pick_rpg<SVT_BF16, 1>(f, rpg, st)
+                           : cpt == 2 ? pick_rpg<SVT_BF16, 2>(f, rpg, st)
+                                      : pick_rpg<SVT_BF16, 4>(f, rpg, st);
+            }
+        }
+    }
     int grid = sm_count();
     if (const char* v = getenv("SVT_ROWS_GRID")) grid = atoi(v);
     if (const char* v = getenv("SVT_ROWS_VARIANT")) p.variant = atoi(v);
@@ -790,7 +1423,6 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
             slots -= slots % kWarps;
     }
     p.slots = static_cast<int32_t>(slots < 1 ? 1 : slots);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     // h in registers when a lane's share is <= 64 values
     const int cpl = (p.nchunks + 31) / 32;
     switch (dt) {

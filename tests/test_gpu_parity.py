@@ -145,6 +145,28 @@ def test_logits_bitwise_against_oracle(th, storage):
         assert np.array_equal(bits(got), bits(want)), (rows, dim)
 
 
+@pytest.mark.parametrize("sig_bits", [12, 13, 14, 24])
+def test_f16_head_short_hidden_bitwise(th, sig_bits):
+    # f16 weights with full 11-bit significands against hidden values with
+    # 12..14 significant bits: 14 + 11 > 24, so w*h is not exact in f32 and
+    # the exact-FMA shortcut must not fire (the mask was 0x3FF)
+    rng = np.random.default_rng(0xF16 + sig_bits)
+    rows, dim = 300, 512
+    mant = rng.integers(0x3FF - 64, 0x400, (rows, dim)).astype(np.uint16)  # near-full significands
+    expo = rng.integers(13, 17, (rows, dim)).astype(np.uint16)
+    sign = rng.integers(0, 2, (rows, dim)).astype(np.uint16)
+    w = ((sign << 15) | (expo << 10) | mant).view(np.float16).astype(np.float32)
+    head = th.HeadMatrix.from_host(w, dtype_bytes=2, storage=th.SVT_F16)
+    h = rng.uniform(-2, 2, dim).astype(np.float32)
+    hb = h.view(np.uint32) | np.uint32((1 << 23) - 1)  # all-ones significand
+    hb &= ~np.uint32((1 << (24 - sig_bits)) - 1)
+    h = hb.view(np.float32)
+    want = orc.logits(w, h)
+    assert np.array_equal(bits(th.logits(head, h)), bits(want))
+    plan = th.SelectionPlan(np.arange(rows, dtype=np.uint32), 0, rows, rows)
+    assert th.greedy_step(head, h, plan) == orc.argmax_first(want)
+
+
 def test_sub_head_logits_equal_full_head_bitwise(th):
     # test_head.cpp:73-93 on the GPU: logits(gather(head, plan)) == logits(head)[plan]
     rng = np.random.default_rng(0x10617)
