@@ -686,6 +686,8 @@ constexpr int kFCompute = kFNG * kFWPG;      // 16
 constexpr int kFThreads = (kFCompute + 1) * 32;  // + the control warp
 constexpr int kFTPG = kFWPG * 32;            // chunk stride inside a group
 constexpr int kFMaxRows = 32;                // rows per CTA: one control lane each
+constexpr int kFinWarps = 1;      // polling warps of the finalize (4 staggered: no gain measured)
+constexpr int kFinStagger = 120;  // ns between their first polls
 constexpr int kFMaxGrid = 160;  // >= SMs - 1 rows CTAs (B200: 147)
 
 struct alignas(32) FRec {
@@ -715,6 +717,7 @@ struct FastParams {
     int32_t extra;
     int64_t per_cta;
     int32_t fin_in_grid;  // 1: the finalizer is the grid's last CTA; 0: its own launch
+    int32_t variant;      // measurement only (SVT_FAST_VARIANT): 1 = no row traffic
     unsigned long long* dbg;  // per CTA 8 %globaltimer stamps (svt_rows_set_debug)
 };
 
@@ -743,21 +746,57 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 #define SVT_FSTAMP(k) \
     if (p.dbg) p.dbg[blockIdx.x * 128 + (k)] = gtimer()
 
-template <int RPG>
-struct FPad {  // 2 * RPG values padded to a power of two <= 32
-    static constexpr int P = 2 * RPG <= 2 ? 2 : 2 * RPG <= 4 ? 4 : 2 * RPG <= 8 ? 8
-                           : 2 * RPG <= 16 ? 16 : 32;
+template <int V>
+struct FPad {  // V values padded to a power of two in [2, 32]
+    static constexpr int P = V <= 2 ? 2 : V <= 4 ? 4 : V <= 8 ? 8 : V <= 16 ? 16 : 32;
     static constexpr int LOG = P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : 5;
 };
+
+// Warp transpose-halving sum of P values per lane: LOG exchange steps each
+// halve the values a lane holds, then butterflies finish the 32-lane sum.
+// Lane l ends with the sum of value (l >> (5 - LOG)) & (P - 1); returns it.
+template <int P, int LOG>
+__device__ __forceinline__ float transpose_sum(float (&v)[P], int lane) {
+#pragma unroll
+    for (int s = 0; s < LOG; ++s) {
+        const int o = 16 >> s;
+        const int m = P >> (s + 1);
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < m; ++j) {
+            const float send = up ? v[j] : v[j + m];
+            const float keep = up ? v[j + m] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, o);
+        }
+    }
+#pragma unroll
+    for (int o = (16 >> LOG); o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xFFFFFFFFu, v[0], o);
+    return v[0];
+}
+
+// packed f32x2 FMA (FFMA2): two lanes of a pair in one issue slot
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float x, float y) {
+    return static_cast<unsigned long long>(__float_as_uint(x)) |
+           (static_cast<unsigned long long>(__float_as_uint(y)) << 32);
+}
+__device__ __forceinline__ float sum2(unsigned long long v) {
+    return __uint_as_float(static_cast<uint32_t>(v)) + __uint_as_float(static_cast<uint32_t>(v >> 32));
+}
 
 template <int DT, int CPT, int RPG>
 __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm) {
     constexpr int E = Chunk<DT>::E;
-    constexpr int P = FPad<RPG>::P, LOG = FPad<RPG>::LOG;
+    constexpr int PF = FPad<2 * RPG>::P, LF = FPad<2 * RPG>::LOG;
     __shared__ uint64_t s_bar[kFMaxRows];
     __shared__ uint64_t s_hbar;
     __shared__ __align__(16) unsigned s_epoch[4];
-    __shared__ float s_red[kFNG][kFWPG][P];
+    __shared__ float s_red[kFNG][kFWPG][PF];  // per warp: row dots, then row sums |w||h|
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
     const int64_t r0 = frow_begin(p, c);
@@ -787,12 +826,16 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
                                    : p.row_base + static_cast<uint32_t>(r0 + lane);
             }
         };
-        if (early) issue_rows();
+        if (p.variant & 1) {  // measurement: no row traffic (the chain alone)
+            if (lane < nrows) mbar_arrive(&s_bar[lane]);
+        } else if (early) {
+            issue_rows();
+        }
         if (lane == 0) bulk_prefetch_l2(p.h, h_bytes);
         asm volatile("griddepcontrol.wait;" ::: "memory");
         asm volatile("griddepcontrol.launch_dependents;");
         if (lane == 0) SVT_FSTAMP(1);
-        if (!early) issue_rows();
+        if (!early && !(p.variant & 1)) issue_rows();
         if (lane == 0) {
             // h and the epoch counter (written by the previous finalize) in
             // one transaction group: no LSU round trip on the critical path
@@ -810,8 +853,8 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
             const int g = lane % kFNG, k = lane / kFNG;
 #pragma unroll
             for (int w = 0; w < kFWPG; ++w) {
-                f += s_red[g][w][2 * k];
-                a += s_red[g][w][2 * k + 1];
+                f += s_red[g][w][k];
+                a += s_red[g][w][RPG + k];
             }
         }
         const bool bad = act && (!isfinite(f) || !isfinite(a));
@@ -868,7 +911,11 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
 #pragma unroll
     for (int k = 0; k < RPG; ++k) {
         const int i = k * kFNG + g;
-        if (i < nrows) {
+        if (p.variant & 1) {  // measurement: distinct synthetic rows, no traffic
+            const uint32_t b = __float_as_uint(exp2f(static_cast<float>(r0 + i) * 0.0145f));
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) wv[k][q] = make_uint4(b, b, b, b);
+        } else if (i < nrows) {
             mbar_wait_parity(&s_bar[i], 0u);
 #pragma unroll
             for (int q = 0; q < CPT; ++q)
@@ -879,66 +926,65 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
             for (int q = 0; q < CPT; ++q) wv[k][q] = make_uint4(0u, 0u, 0u, 0u);
         }
     }
-    asm volatile("griddepcontrol.launch_dependents;");
-    mbar_wait_parity(&s_hbar, 0u);
-    if (warp == 0 && lane == 0) SVT_FSTAMP(2);
-    float hv[CPT][E];
-#pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-#pragma unroll
-        for (int e = 0; e < E; e += 4) {
-            const float4 x = *reinterpret_cast<const float4*>(s_h + (tg + q * kFTPG) * E + e);
-            hv[q][e] = x.x;
-            hv[q][e + 1] = x.y;
-            hv[q][e + 2] = x.z;
-            hv[q][e + 3] = x.w;
-        }
-    }
-    float v[P];
+    if (p.dbg && lane == 0) atomicMax(&p.dbg[blockIdx.x * 128 + 7], gtimer());  // rows in registers
+    // widened weights as f32 pairs (f32: the storage words themselves)
+    constexpr int NP = CPT * E / 2;  // pairs per row per thread
+    unsigned long long w2[RPG][NP];
 #pragma unroll
     for (int k = 0; k < RPG; ++k) {
-        float f0 = 0.0f, f1 = 0.0f, a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
             float w[E];
             Chunk<DT>::widen(wv[k][q], w);
 #pragma unroll
-            for (int e = 0; e < E; e += 2) {
-                f0 = __fmaf_rn(w[e], hv[q][e], f0);
-                a0 = __fmaf_rn(fabsf(w[e]), fabsf(hv[q][e]), a0);
-                f1 = __fmaf_rn(w[e + 1], hv[q][e + 1], f1);
-                a1 = __fmaf_rn(fabsf(w[e + 1]), fabsf(hv[q][e + 1]), a1);
-            }
-        }
-        v[2 * k] = f0 + f1;
-        v[2 * k + 1] = a0 + a1;
-    }
-#pragma unroll
-    for (int j = 2 * RPG; j < P; ++j) v[j] = 0.0f;
-    // transpose-halving: after LOG steps lane l holds value (l >> (5-LOG)) & (P-1)
-#pragma unroll
-    for (int s = 0; s < LOG; ++s) {
-        const int o = 16 >> s;
-        const int m = P >> (s + 1);
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int j = 0; j < m; ++j) {
-            const float send = up ? v[j] : v[j + m];
-            const float keep = up ? v[j + m] : v[j];
-            v[j] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, o);
+            for (int e = 0; e < E; e += 2) w2[k][q * E / 2 + e / 2] = pack2(w[e], w[e + 1]);
         }
     }
+    asm volatile("griddepcontrol.launch_dependents;");
+    mbar_wait_parity(&s_hbar, 0u);
+    if (warp == 0 && lane == 0) SVT_FSTAMP(2);
+    unsigned long long h2[NP];
 #pragma unroll
-    for (int o = (16 >> LOG); o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xFFFFFFFFu, v[0], o);
-    if ((lane & ((32 >> LOG) - 1)) == 0) s_red[g][wig][(lane >> (5 - LOG)) & (P - 1)] = v[0];
+    for (int q = 0; q < CPT; ++q) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(s_h + (tg + q * kFTPG) * E + e);
+            h2[q * E / 2 + e / 2] = pack2(x.x, x.y);
+            h2[q * E / 2 + e / 2 + 1] = pack2(x.z, x.w);
+        }
+    }
+    float v[PF];
+#pragma unroll
+    for (int k = 0; k < RPG; ++k) {
+        // f: one FFMA2 per pair; a = sum |w||h|: FFMAs with free |.| operand
+        // modifiers (two chains)
+        unsigned long long acc = 0ull;
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            acc = ffma2(w2[k][j], h2[j], acc);
+            const uint32_t wl = static_cast<uint32_t>(w2[k][j]), wh = static_cast<uint32_t>(w2[k][j] >> 32);
+            const uint32_t hl = static_cast<uint32_t>(h2[j]), hh = static_cast<uint32_t>(h2[j] >> 32);
+            a0 = __fmaf_rn(fabsf(__uint_as_float(wl)), fabsf(__uint_as_float(hl)), a0);
+            a1 = __fmaf_rn(fabsf(__uint_as_float(wh)), fabsf(__uint_as_float(hh)), a1);
+        }
+        v[k] = sum2(acc);
+        v[RPG + k] = a0 + a1;
+    }
+#pragma unroll
+    for (int j = 2 * RPG; j < PF; ++j) v[j] = 0.0f;
+    const float r = transpose_sum<PF, LF>(v, lane);
+    if ((lane & ((32 >> LF) - 1)) == 0) s_red[g][wig][(lane >> (5 - LF)) & (PF - 1)] = r;
     named_bar_arrive(1, kFThreads);
 }
 
 // ---- the grid's last CTA: one warp polls the tagged records and decides ------
 template <int DT>
-__device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t* fsmem, unsigned* sn) {
+__device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t* fsmem, unsigned* sn,
+                                                   unsigned* claim) {
     unsigned& s_n = *sn;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
     const int G = p.grid;
     unsigned* s_list = reinterpret_cast<unsigned*>(fsmem);                     // [kMaxCand]
     uint8_t* s_buf = fsmem + kMaxCand * 4;                                     // 2 pieces
@@ -951,7 +997,12 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
     unsigned long long w0[kPer], w1[kPer], w2[kPer], w3[kPer];
     bool seen = false;
     const unsigned long long t_start = gtimer();
+    // several polling warps, staggered by a fraction of a load round trip,
+    // shorten the delay between the last record landing and its detection;
+    // the first warp to see every record claims the decision
+    if (wid > 0) __nanosleep(kFinStagger * wid);
     for (int it = 0; !seen; ++it) {
+        if (*reinterpret_cast<volatile unsigned*>(claim)) return;
         // every load of a round is issued before any result is used
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
@@ -970,12 +1021,20 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
                 mine = mine && (w0[q] >> 56) == tag && (w1[q] >> 56) == tag &&
                        (w2[q] >> 56) == tag && (w3[q] >> 56) == tag;
         seen = __all_sync(0xFFFFFFFFu, mine);
+        if (seen) {
+            unsigned won = 0u;
+            if (lane == 0) won = atomicCAS(claim, 0u, 1u) == 0u;
+            if (!__shfl_sync(0xFFFFFFFFu, won, 0)) return;
+        }
         if (!seen && it >= kPollLimit) {
             // rows CTAs still streaming (large rows, a busy GPU): back off;
             // after 2 s something is wrong (a record never came) — report
             // an invalid id instead of hanging the device
             __nanosleep(256);
             if (__shfl_sync(0xFFFFFFFFu, gtimer() - t_start, 0) > 2000000000ull) {
+                unsigned won = 0u;
+                if (lane == 0) won = atomicCAS(claim, 0u, 1u) == 0u;
+                if (!__shfl_sync(0xFFFFFFFFu, won, 0)) return;
                 if (lane == 0) {
                     *p.out_id = 0xFFFFFFFFu;
                     atomicAdd(&p.ctrl[6], 1u);
@@ -1016,6 +1075,10 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
     if (code == 0u && total == 1u && !want_exact) {
         // one row can reach the largest lower bound: the reference argmax
         if (nhit) *p.out_id = id;
+        if (p.variant & 4) {  // measurement: bare minimum exit
+            if (lane == 0) p.ctrl[8] = (epoch + 1u) % 255u;
+            return;
+        }
     } else {
         recomputed = 1u;
         const bool all = (code & 1u) != 0u;
@@ -1100,7 +1163,7 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
     if (lane == 0) {
         if (p.dbg) p.dbg[126] = gtimer();
         p.ctrl[8] = (epoch + 1u) % 255u;
-        atomicAdd(&p.ctrl[recomputed ? 5 : 4], 1u);
+        if (!(p.variant & 2)) atomicAdd(&p.ctrl[recomputed ? 5 : 4], 1u);
     }
 }
 
@@ -1108,12 +1171,14 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
 // grid; it polls instead of waiting, and its shared-memory reservation keeps
 // it on the SM the rows grid leaves free)
 template <int DT>
-__global__ void __launch_bounds__(32, 1) rows_fast_fin_kernel(FastParams p) {
+__global__ void __launch_bounds__(32 * kFinWarps, 1) rows_fast_fin_kernel(FastParams p) {
     asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ __align__(128) uint8_t fsm[];
-    __shared__ unsigned s_n;
+    __shared__ unsigned s_n, s_claim;
+    if (threadIdx.x == 0) s_claim = 0u;
+    __syncthreads();
     if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
-    rows_fast_finalize<DT>(p, fsm, &s_n);
+    rows_fast_finalize<DT>(p, fsm, &s_n, &s_claim);
 }
 
 template <int DT, int CPT, int RPG>
@@ -1123,11 +1188,13 @@ __global__ void __launch_bounds__(kFThreads, 1) rows_fast_kernel(FastParams p) {
         // the finalizer: dispatched after every rows CTA (highest index), on
         // the SM they leave free
         if (threadIdx.x >= 32) return;
-        __shared__ unsigned s_n;
+        __shared__ unsigned s_n, s_claim;
+        if (threadIdx.x == 0) s_claim = 0u;
+        __syncwarp();
         asm volatile("griddepcontrol.wait;" ::: "memory");
         asm volatile("griddepcontrol.launch_dependents;");
         if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
-        rows_fast_finalize<DT>(p, dsm, &s_n);
+        rows_fast_finalize<DT>(p, dsm, &s_n, &s_claim);
         return;
     }
     rows_fast_cta<DT, CPT, RPG>(p, dsm);
@@ -1206,7 +1273,7 @@ svt_status launch_rows_fast(FastParams p, cudaStream_t st) {
                                       static_cast<int>(fsmem)));
     cudaLaunchConfig_t fc = {};
     fc.gridDim = dim3(1);
-    fc.blockDim = dim3(32);
+    fc.blockDim = dim3(32 * kFinWarps);
     fc.dynamicSmemBytes = fsmem;
     fc.stream = st;
     fc.attrs = attr;
@@ -1376,6 +1443,7 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
             f.extra = static_cast<int32_t>(p.n % fgrid);
             f.dbg = g_rows_dbg;
             if (const char* v = getenv("SVT_ROWS_FIN")) f.fin_in_grid = atoi(v) != 0;
+            if (const char* v = getenv("SVT_FAST_VARIANT")) f.variant = atoi(v);
             // fast-pass depth: CPT*E/2 FFMAs per accumulator (+1 combine), 5
             // shuffle levels, 4 warp partials summed in order (+ slack)
             const int Ef = dt == SVT_F32 ? 4 : 8;

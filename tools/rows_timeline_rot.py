@@ -57,7 +57,8 @@ t0 = d[0, :G, 0][d[0, :G, 0] > 0].min()
 for k in range(K):
     x = d[k, :G, :8] - t0
     print(json.dumps({"k": k, "start_med": int(np.median(x[:, 0])), "start_max": int(x[:, 0].max()),
-                      "depwait_med": int(np.median(x[:, 1])), "h_med": int(np.median(x[:, 2])),
+                      "depwait_med": int(np.median(x[:, 1])), "rows_in_med": int(np.median(x[:, 7])),
+                      "rows_in_max": int(x[:, 7].max()), "h_med": int(np.median(x[:, 2])),
                       "reduced_med": int(np.median(x[:, 3])), "ctl_L_med": int(np.median(x[:, 5])),
                       "ctl_ids_med": int(np.median(x[:, 6])), "record_med": int(np.median(x[:, 4])),
                       "record_max": int(x[:, 4].max()),
