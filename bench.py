@@ -1,24 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the tailored LM-head path (BASELINE.json metric:
-"tailored LM-head tokens/s ... ; HBM GB/s vs roofline").
+"tailored LM-head tokens/s (Llama-3.2-1B shape); HBM GB/s vs roofline").
 
-Workload (BASELINE.json configs[1], the single-GPU throughput config):
-  Qwen2.5-0.5B-shaped head, V=151936, d=896, bf16 weights, B=64 requests per
-  GPU, each with its own plan S_b = T ∪ prompt_b (|T|=2048 static ids, 512-
-  token synthetic prompt), 64 greedy decode steps per request.
-One bench STEP = one full pass of the hot path over one request batch:
-  (a) select  -> plan layout -> (b) interleaved gather -> 64 x (c+d) fused
-  exact-order logits + argmax + remap.   tokens per step = B * 64.
-Inputs (head, static bitmap, prompts, 64 x B hidden states) are resident in
-HBM before the timed region. The per-step decode working set (Σ|S_b|·d·2 ≈
-293 MB) exceeds the 126 MB L2, so no explicit flush is needed ("inputs larger
-than L2").
+Headline workload (BASELINE.json configs[0], the config the metric is quoted
+on): cfg1, the Llama-3.2-1B-shaped tailored head (V=128,256, d=2,048, f32
+weights, random init), batch 1: one synthetic 512-token prompt + the 2,048-id
+static task vocab -> select -> gather -> 64 greedy decode tokens, all
+certified bit-exact against the reference (svt_greedy_certified_rows).
+One bench STEP = JOBS (8) such independent jobs: 8 x (select + row gather),
+then their 64 tokens token-interleaved (job 0 token 0, job 1 token 0, ...).
+Interleaving makes consecutive decode launches touch different 20.9 MB
+sub-heads whose total (8 x 20.9 MB = 167 MB) exceeds the 126 MB L2, so every
+token streams its sub-head from HBM ("inputs larger than L2"; no flush).
+tokens per step = 8 * 64. The warm figure (one job, its sub-head L2-resident
+across its 64 tokens) is reported beside it.
 
-N>1 (torchrun): batch-shard weak scaling — every rank runs its own 64
-requests (request seeds offset by rank); no collective on the data path.
+e2e: the same 8 jobs through the host-buffer C-ABI (svt_session_prepare_host
+per job, then svt_session_decode_host: one H2D of all hidden states, the
+interleaved decode, one D2H of the ids).
+
+N>1 (torchrun): batch-shard weak scaling — every rank runs its own 8 jobs
+(prompt seeds offset by rank); no collective on the data path.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
-unmodified reference TUs) on the host cores, same workload, rank 0 only.
+unmodified reference select / gather / greedy_step) on the host cores, the
+identical 8 jobs per step with every decode step run (rank 0 only).
+--workload cfg2|cfg3|cfg4|cfg5|embed|corpus: the other BASELINE configs.
 """
 from __future__ import annotations
 
@@ -54,9 +61,12 @@ def parse():
     ap.add_argument("--sweep-sizes", default="1024,4096,16384,65536,128256")
     ap.add_argument("--sweep-batches", default="1,32,256")
     ap.add_argument("--sweep-dtypes", default="bf16,f32")
-    ap.add_argument("--workload", default="cfg2",
-                    choices=["cfg2", "cfg3", "cfg4", "cfg5", "embed", "corpus"],
-                    help="cfg2: batch-shard tailored decode (headline); cfg3: batched "
+    ap.add_argument("--jobs", type=int, default=8,
+                    help="cfg1: independent batch-1 jobs per step (token-interleaved)")
+    ap.add_argument("--workload", default="cfg1",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "embed", "corpus"],
+                    help="cfg1: batch-1 tailored decode (headline); cfg2: batch-shard "
+                         "tailored decode, 64 requests per GPU; cfg3: batched "
                          "prefill-scoring on tcgen05 (Llama-3.2-3B shape, 256 seqs x 2048 "
                          "positions per GPU); cfg4: vocab-sharded full-vocab greedy "
                          "(Gemma-2-2B shape) with an NCCL record all-gather; cfg5: subset-size "
@@ -69,8 +79,9 @@ def parse():
 
 CFG2 = dict(workload="cfg2: Qwen2.5-0.5B-shaped tailored head, per-request plans",
             V=151936, d=896, static=2048, prompt_len=512, dtype="bf16")
-CFG1 = dict(workload="cfg1: Llama-3.2-1B-shaped tailored head, batch 1", V=128256, d=2048,
-            static=2048, prompt_len=512, dtype="f32")
+CFG1 = dict(workload="cfg1: Llama-3.2-1B-shaped tailored LM head (V=128256, d=2048, f32), "
+                     "batch 1: 512-token prompt + 2,048-token static task vocab, greedy decode "
+                     "64 tokens", V=128256, d=2048, static=2048, prompt_len=512, dtype="f32")
 CFG3 = dict(workload="cfg3: Llama-3.2-3B-shaped batched prefill-scoring over per-sequence "
                      "tailored heads (tcgen05)", V=128256, d=3072, static=2048, prompt_len=2048,
             positions=2048, dtype="bf16")
@@ -471,6 +482,8 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    if args.workload == "cfg1":
+        return run_reference_cfg1(args, threads)
     if args.workload == "cfg3":
         vals = []
         for k in range(args.warmup + args.steps):
@@ -517,6 +530,384 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------
+# cfg1 (the headline): JOBS independent batch-1 jobs per step
+# --------------------------------------------------------------------------
+class Cfg1Jobs:
+    """R independent cfg1 jobs on one device: the shared head (W =
+    HeadMatrix::random(V, d, 0x5EED), regenerated on the device), the static
+    bitmap, one prompt per job (seed 0x9A0 + rank*R + j), a B=1
+    TailoredBatch (select) and a RowDecoder (row gather + certified greedy)
+    per job, and every step's hidden state (rows t*R + j of
+    HeadMatrix::random(64*R, d, 0x41DD)) resident in HBM."""
+
+    def __init__(self, R, steps, rank, torch, th, synth, head=None):
+        V, d = CFG1["V"], CFG1["d"]
+        self.R, self.steps, self.torch = R, steps, torch
+        self.head = head if head is not None else th.HeadMatrix.random(V, d, synth.SEED_W,
+                                                                      storage=th.SVT_F32)
+        t_ids = synth.static_ids(V, CFG1["static"])
+        self.words_h = synth.words_of(t_ids, V)
+        self.words = torch.from_numpy(self.words_h.view(np.int64)).cuda()
+        self.prompts_h = [synth.prompt_ids(V, CFG1["prompt_len"], rank * R + j) for j in range(R)]
+        self.tbs, self.decs, self.n = [], [], []
+        for p in self.prompts_h:
+            off = np.array([0, len(p)], np.int64)
+            tb = th.TailoredBatch.build(self.words, CFG1["static"], V,
+                                        torch.from_numpy(p.view(np.int32)).cuda(), off)
+            n = int(tb.n_active[0].item())
+            self.tbs.append(tb)
+            self.decs.append(th.RowDecoder(self.head, tb.active[:n], n))
+            self.n.append(n)
+        m = steps * R * d
+        hid = torch.empty(m, dtype=torch.float32, device="cuda")
+        th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_F32, th.SVT_F32, 0, m,
+                     synth.SEED_H, None)
+        self.hidden = hid.view(steps, R, d)
+        self.out = torch.zeros((steps, R), dtype=torch.int32, device="cuda")
+
+    def set_stream(self, st):
+        for tb, rd in zip(self.tbs, self.decs):
+            tb.stream = st
+            rd.stream = st
+
+    def prep(self):
+        for tb, rd in zip(self.tbs, self.decs):
+            tb.run_select(layout=False)
+            rd.gather()
+
+    def decode(self, jobs=None):
+        jobs = range(self.R) if jobs is None else jobs
+        for t in range(self.steps):
+            for j in jobs:
+                self.decs[j].greedy(self.hidden[t, j], self.out[t, j])
+
+    def token_bytes(self):
+        """Algorithmic bytes of one decode launch: the plan's
+        rows (n x d x 4), h (d x 4), the plan ids for the remap (n x 4) and
+        the 8-byte result, averaged over the jobs."""
+        d = CFG1["d"]
+        return sum(n * d * 4 + d * 4 + n * 4 + 8 for n in self.n) / self.R
+
+    # launches per step: per job select + gather, per token the rows grid +
+    # its finalize
+    def launches_per_step(self):
+        return self.R * 2 + self.steps * self.R * 2
+
+    def stats(self):
+        fast = slow = 0
+        for rd in self.decs:
+            a, b = rd.stats()
+            fast, slow = fast + a, slow + b
+        return fast, slow
+
+
+def _capture(torch, fn, st):
+    with torch.cuda.stream(st):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        fn()
+    return g
+
+
+def time_cfg1(jobs, K, W, torch, dist, world):
+    """K steps = K x (prep graph: R x (select + gather); decode graph: the
+    R jobs' 64 tokens interleaved). CUDA events on the replay stream; the
+    decode graph's events give the per-token time (cold: see module doc)."""
+    s = torch.cuda.Stream()
+    jobs.set_stream(s)
+    prep = _capture(torch, jobs.prep, s)
+    dec = _capture(torch, jobs.decode, s)
+    with torch.cuda.stream(s):
+        for _ in range(W):
+            prep.replay()
+            dec.replay()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        with torch.cuda.stream(s):
+            a.record(s)
+            for k in range(K):
+                prep.replay()
+                ev[k][0].record(s)
+                dec.replay()
+                ev[k][1].record(s)
+            b.record(s)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = a.elapsed_time(b)
+    dec_ms = [x.elapsed_time(y) for (x, y) in ev]
+    if dist is not None and world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # warm: job 0 alone, its sub-head L2-resident across its 64 tokens
+    warm_g = _capture(torch, lambda: jobs.decode([0]), s)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            warm_g.replay()
+        x, y = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x.record(s)
+        for _ in range(10):
+            warm_g.replay()
+        y.record(s)
+    torch.cuda.synchronize()
+    warm_us = x.elapsed_time(y) / 10 / jobs.steps * 1e3
+    jobs.set_stream(None)
+    return ms, dec_ms, warm_us, clk.summary()
+
+
+def cfg1_e2e(jobs, K, W, torch, th, session_mod):
+    """The same R jobs through the host-buffer C-ABI: per step, per job
+    svt_session_prepare_host (H2D of the static bitmap + prompt, select,
+    row gather, one synchronisation), then one svt_session_decode_host over
+    the R sessions (H2D of all 64 x R hidden states from pinned memory, the
+    interleaved certified decode, D2H of the ids). Host-timed."""
+    R, steps, d, V = jobs.R, jobs.steps, CFG1["d"], CFG1["V"]
+    hid_h = jobs.hidden.cpu().pin_memory()
+    ids_h = torch.zeros((steps, R), dtype=torch.int32).pin_memory()
+    st = torch.cuda.Stream()
+    sess = [session_mod.Session(jobs.head, max_batch=1, stream=st) for _ in range(R)]
+    offs = [np.array([0, len(p)], np.int64) for p in jobs.prompts_h]
+
+    def one():
+        for j in range(R):
+            sess[j].prepare(jobs.words_h, V, jobs.prompts_h[j], offs[j])
+        session_mod.decode_host(sess, hid_h, steps, ids_h)
+
+    try:
+        for _ in range(W):
+            one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            one()
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+    finally:
+        for x in sess:
+            x.close()
+    h2d = R * (jobs.words_h.nbytes + jobs.prompts_h[0].nbytes + 16) + steps * R * d * 4
+    d2h = steps * R * 4 + R * 4 * 8  # ids + per-job plan counters / status words
+    ok = bool(np.array_equal(ids_h.numpy(), jobs.out.cpu().numpy()))
+    return R * steps * K / sec, h2d, d2h, ok, sec / K
+
+
+def cfg1_cpu_reference(R, threads, steps=64):
+    """The reference (oracle/_ref) on the host cores for the cfg1 jobs: every
+    decode step run (ref_jobs_run). Returns a dict for one job on 1 thread
+    (the reference's own single-threaded path, select / gather / greedy
+    reported separately) and for the R jobs on `threads` threads (jobs over
+    threads; spare threads split each job's logits into contiguous row
+    slices). Falls back to the C restatement ("port", 1 job,
+    1 thread) when oracle/_ref is absent."""
+    from oracle import oracle as O
+    from paper_2508_15229_b200 import synth
+
+    V, d = CFG1["V"], CFG1["d"]
+    words = synth.words_of(synth.static_ids(V, CFG1["static"]), V)
+    prompts = [synth.prompt_ids(V, CFG1["prompt_len"], j) for j in range(R)]
+    off = np.zeros(R + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in prompts])
+    flat = np.concatenate(prompts)
+    hid = synth.head_random(steps * R, d, synth.SEED_H).reshape(steps, R, d)
+    if not O.ref_available():
+        orc = O.c_oracle()
+        W = orc.head_random(V, d, synth.SEED_W)
+        t0 = time.perf_counter()
+        plan = orc.select(prompts[0], words, V, V).active_ids
+        t1 = time.perf_counter()
+        sub = orc.gather(W, plan)
+        t2 = time.perf_counter()
+        for t in range(steps):
+            orc.greedy_step(sub, hid[t, 0], plan)
+        t3 = time.perf_counter()
+        one = {"select_ms": (t1 - t0) * 1e3, "gather_ms": (t2 - t1) * 1e3,
+               "greedy_ms_per_token": (t3 - t2) / steps * 1e3, "threads": 1,
+               "tokens_per_s": steps / (t3 - t0)}
+        return {"kind": "port", "one_job_1_thread": one, "jobs_n_threads": None,
+                "cpu_model": _cpu_model()}
+    R_ = O.ref_lib()
+    h = R_.L.ref_head_new_random(V, d, synth.SEED_W, 4)
+    try:
+        ids1, ph1, wall1 = R_.jobs_run(h, words, V, flat[:off[1]], off[:2], hid[:, :1].copy(),
+                                       steps, 1)
+        idsn, phn, walln = R_.jobs_run(h, words, V, flat, off, hid, steps, threads)
+    finally:
+        R_.L.ref_head_free(h)
+    one = {"select_ms": ph1[0] * 1e3, "gather_ms": ph1[1] * 1e3,
+           "greedy_ms_per_token": ph1[2] / steps * 1e3, "threads": 1,
+           "tokens_per_s": steps / wall1}
+    many = {"jobs": R, "threads": threads, "wall_ms": walln * 1e3,
+            "select_ms_sum": phn[0] * 1e3, "gather_ms_sum": phn[1] * 1e3,
+            "greedy_ms_per_token": phn[2] / (steps * R) * 1e3,
+            "tokens_per_s": R * steps / walln}
+    return {"kind": "reference", "one_job_1_thread": one, "jobs_n_threads": many,
+            "cpu_model": _cpu_model(), "ids": idsn, "ids_one": ids1}
+
+
+def cfg1_config(R, steps, world):
+    """The cfg1 config block, identical in both arms."""
+    return {"workload": CFG1["workload"], "V": CFG1["V"], "d": CFG1["d"], "batch": 1,
+            "prompt_len": CFG1["prompt_len"], "static_vocab": CFG1["static"],
+            "decode_steps": steps, "jobs_per_step": R,
+            "step": f"{R} independent jobs: {R} x (select + gather), then their {steps} greedy "
+                    f"tokens (token-interleaved on the GPU)",
+            "l2": f"inputs larger than L2: {R} sub-heads of ~20.9 MB (no flush)",
+            "parallelism": f"batch-shard x{world}"}
+
+
+def run_reference_cfg1(args, threads):
+    """--impl reference at cfg1: the identical step (args.jobs jobs x 64
+    tokens, every decode step run) through the reference's own select /
+    gather / greedy_step (oracle/_ref) on the host cores."""
+    from oracle import oracle as O
+    from paper_2508_15229_b200 import synth
+
+    R, steps = args.jobs, args.decode_steps
+    V, d = CFG1["V"], CFG1["d"]
+    words = synth.words_of(synth.static_ids(V, CFG1["static"]), V)
+    prompts = [synth.prompt_ids(V, CFG1["prompt_len"], j) for j in range(R)]
+    off = np.zeros(R + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in prompts])
+    flat = np.concatenate(prompts)
+    hid = synth.head_random(steps * R, d, synth.SEED_H).reshape(steps, R, d)
+    kind = "reference" if O.ref_available() else "port"
+    walls, phases = [], None
+    if kind == "reference":
+        RL = O.ref_lib()
+        h = RL.L.ref_head_new_random(V, d, synth.SEED_W, 4)
+        try:
+            for k in range(args.warmup + args.steps):
+                _, ph, wall = RL.jobs_run(h, words, V, flat, off, hid, steps, threads)
+                if k >= args.warmup:
+                    walls.append(wall)
+                    phases = ph
+        finally:
+            RL.L.ref_head_free(h)
+    else:
+        orc = O.c_oracle()
+        W = orc.head_random(V, d, synth.SEED_W)
+        threads = 1
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            for j in range(R):
+                plan = orc.select(prompts[j], words, V, V).active_ids
+                sub = orc.gather(W, plan)
+                for t in range(steps):
+                    orc.greedy_step(sub, hid[t, j], plan)
+            if k >= args.warmup:
+                walls.append(time.perf_counter() - t0)
+    wall = statistics.median(walls)
+    v = R * steps / wall
+    c = {"value": v, "unit": UNIT, "cores": min(threads, os.cpu_count() or 1), "kind": kind,
+         "cpu_model": _cpu_model(),
+         "sample": f"the identical step: {R} cfg1 jobs x {steps} tokens, every decode step run, "
+                   f"{threads} host threads (jobs over threads, spare threads split each job's "
+                   f"logits into row slices)"}
+    if phases is not None:
+        c["phases_ms_summed_over_jobs"] = {"select": phases[0] * 1e3, "gather": phases[1] * 1e3,
+                                           "greedy": phases[2] * 1e3}
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded splitmix64 streams, SURVEY §8d); random-init head",
+        "config": cfg1_config(R, steps, args.gpus),
+        "cpu_baseline": c,
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_cfg1(args, torch, dist, world, rank):
+    from paper_2508_15229_b200 import session as session_mod
+    from paper_2508_15229_b200 import synth
+    from paper_2508_15229_b200 import tailored_head as th
+
+    R, steps = args.jobs, args.decode_steps
+    jobs = Cfg1Jobs(R, steps, rank, torch, th, synth)
+    ms, dec_ms, warm_us, clocks = time_cfg1(jobs, args.steps, args.warmup, torch, dist, world)
+    tokens = R * steps * args.steps * world
+    value = tokens / (ms / 1000.0)
+    tok_us = sum(dec_ms) / len(dec_ms) / (R * steps) * 1e3
+    bpt = jobs.token_bytes()
+    peak, peak_kind = load_peaks()
+    achieved = bpt / (tok_us / 1e6) / 1e9
+    warm_gbs = bpt / (warm_us / 1e6) / 1e9
+    fast, slow = jobs.stats()
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": load_traffic("rows_fast_cfg1"),
+        "kernel": "rows_fast_kernel<f32,4,5> + rows_fast_fin_kernel<f32> "
+                  "(svt_greedy_certified_rows, one decode token)",
+        "bytes_per_launch": bpt, "avg_launch_us": tok_us,
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "l2": "cold: consecutive launches read different sub-heads (8 x 20.9 MB > 126 MB L2)",
+        "timing": "CUDA events around the decode graph (R x 64 launches) of every step; "
+                  "per-launch time = graph time / (R x 64), including the finalize",
+        "decode_share_of_step": sum(dec_ms) / ms if world == 1 else None,
+        "warm": {"us_per_token": warm_us, "gbs": warm_gbs, "frac": warm_gbs / peak,
+                 "what": "job 0 alone: its 20.9 MB sub-head stays in L2 across its 64 tokens"},
+        "certified": {"direct": fast, "exact_recompute": slow},
+    }
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded splitmix64 streams, SURVEY §8d); random-init head",
+        "config": cfg1_config(R, steps, world),
+        "plan_rows": jobs.n,
+        "launch": "CUDA graph replay (prep graph + decode graph per step)",
+        "roofline": roofline,
+        "gpu_launches": jobs.launches_per_step() * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_e2e:
+        e2e_v, h2d, d2h, ok, sec = cfg1_e2e(jobs, max(4, args.steps // 2), 2, torch, th,
+                                            session_mod)
+        result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                         "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
+                         "api": "svt_session_prepare_host x R + svt_session_decode_host "
+                                "(host buffers)", "ids_match_device_path": ok}
+    ids_dev = jobs.out.cpu().numpy().view(np.uint32).copy()
+    head = jobs.head
+    del jobs
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_secondary:
+        result["secondary"] = secondary(args, torch, th, synth)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        c = cfg1_cpu_reference(R, os.cpu_count() or 1, steps)
+        many, one = c["jobs_n_threads"], c["one_job_1_thread"]
+        base = {"kind": c["kind"], "cpu_model": c["cpu_model"], "one_job_1_thread": one}
+        if many is not None:
+            base.update({"value": many["tokens_per_s"], "unit": UNIT, "cores": many["threads"],
+                         "jobs_n_threads": many,
+                         "ids_match_gpu": bool(np.array_equal(c["ids"], ids_dev)),
+                         "sample": f"the identical step ({R} cfg1 jobs x {steps} tokens, every "
+                                   f"decode step run) on {many['threads']} host threads: jobs "
+                                   f"over threads, spare threads split each job's logits into "
+                                   f"row slices; one_job_1_thread = the reference's own "
+                                   f"single-threaded path"})
+        else:
+            base.update({"value": one["tokens_per_s"], "unit": UNIT, "cores": 1,
+                         "sample": "one cfg1 job (C restatement, 1 thread)"})
+        result["cpu_baseline"] = base
+    del head
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+# --------------------------------------------------------------------------
 def main():
     args = parse()
     if args.impl == "reference":
@@ -546,6 +937,13 @@ def main():
         return run_embed(args, torch, rank)
     if args.workload == "corpus":
         return run_corpus(args, torch, rank)
+    if args.workload == "cfg1":
+        return run_cfg1(args, torch, dist, world, rank)
+    return run_cfg2(args, torch, dist, world, rank)
+
+
+def run_cfg2(args, torch, dist, world, rank):
+    """cfg2 (Qwen2.5-0.5B shape, bf16, B=64 per GPU, per-request plans)."""
     from paper_2508_15229_b200 import session as session_mod
     from paper_2508_15229_b200 import synth
     from paper_2508_15229_b200 import tailored_head as th
@@ -625,8 +1023,6 @@ def main():
         result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": d2h, "api": "svt_session_* (host buffers)",
                          "ids_match_device_path": ok}
-    if rank == 0 and world == 1 and not args.no_secondary:
-        result["secondary"] = secondary(args, torch, th, synth)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_reference(CFG2, B, 2, os.cpu_count() or 1)
     if dist is not None:
@@ -723,10 +1119,11 @@ def run_vocab_shard(args, torch, dist, world, rank):
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
         "gpu_launches": 3 * steps * args.steps, "clocks": clk.summary(),
     }
-    if rank == 0:
+    if rank == 0 and not getattr(args, "quiet", False):
         print(json.dumps(result), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    return result
 
 
 def prefill_fused():
@@ -970,53 +1367,58 @@ def cfg1_cold(job, torch, K=64):
 
 
 def secondary(args, torch, th, synth):
-    """cfg1 (Llama-3.2-1B shape, batch 1, fp32) and the fused and interleaved
-    (unsplit) variants of cfg2."""
+    """The other BASELINE configs in the default run (full lines: --workload
+    cfg2|cfg3|cfg4|cfg5|embed): cfg2 split and unsplit decode, cfg3
+    prefill-scoring, cfg4 at G=1, a cfg5 subset-size summary, and the
+    offloaded embedding."""
+    import copy
+
     out = {}
-    job = Job(CFG1, 1, 64, 0, torch, th, synth)
-    ref_ids = None
-    for mode in ("rows", "interleaved"):
-        ms, dec_ms, _ = time_job(job, mode, 10, 3, torch, None, 1)
-        dec_avg = sum(dec_ms) / len(dec_ms)
-        peak, _ = load_peaks()
-        gbs = job.decode_bytes() / (dec_avg / 1e3) / 1e9
-        ids = job.out.cpu().numpy().copy()
-        out["cfg1_" + mode] = {"tokens_per_s": 64 * 10 / (ms / 1e3),
-                               "decode_us_per_token": dec_avg * 1e3,
-                               "decode_tokens_per_s": 1e3 / dec_avg,
-                               "decode_gbs": gbs, "frac": gbs / peak,
-                               "plan_rows": int(job.tb.n_active[0].item()),
-                               "l2": "warm: the 20.9 MB sub-head stays in L2 between tokens"}
-        if ref_ids is None:
-            ref_ids = ids
-        else:
-            out["cfg1_" + mode]["ids_match_rows"] = bool(np.array_equal(ids, ref_ids))
-    out["cfg1_rows"]["cold"] = cfg1_cold(job, torch)
-    out["cfg1_rows"]["certified_stats"] = list(job.rdec.stats())
-    del job
-    torch.cuda.empty_cache()
-    job = Job(CFG2, args.batch, args.decode_steps, 0, torch, th, synth)
-    ms, dec_ms, _ = time_job(job, "fused", 5, 2, torch, None, 1)
-    dec_avg = sum(dec_ms) / len(dec_ms)
     peak, _ = load_peaks()
-    gbs = job.decode_bytes() / (dec_avg / 1e3) / 1e9
-    out["cfg2_fused"] = {"tokens_per_s": args.batch * args.decode_steps * 5 / (ms / 1e3),
-                         "decode_us": dec_avg * 1e3, "decode_gbs": gbs, "frac": gbs / peak}
+    job = Job(CFG2, 64, 64, 0, torch, th, synth)
     ms_s, dec_s, _ = time_job(job, "split", 5, 2, torch, None, 1)
     split_out = job.out.cpu().numpy().copy()
+    dec_avg = sum(dec_s) / len(dec_s)
+    sb = job.decode_bytes("split")
+    out["cfg2_split"] = {"tokens_per_s": 64 * 64 * 5 / (ms_s / 1e3), "decode_us": dec_avg * 1e3,
+                         "decode_gbs": sb / (dec_avg / 1e3) / 1e9,
+                         "frac": sb / (dec_avg / 1e3) / 1e9 / peak,
+                         "what": "64 requests, per-request plans; static rows scored once per "
+                                 "step (svt_greedy_split); L2 flushed before every job step"}
     ms, dec_ms, _ = time_job(job, "interleaved", 5, 2, torch, None, 1)
     dec_avg = sum(dec_ms) / len(dec_ms)
     gbs = job.decode_bytes("interleaved") / (dec_avg / 1e3) / 1e9
     out["cfg2_interleaved"] = {
-        "tokens_per_s": args.batch * args.decode_steps * 5 / (ms / 1e3),
-        "decode_us": dec_avg * 1e3, "decode_gbs": gbs, "frac": gbs / peak,
-        "split_decode_us": sum(dec_s) / len(dec_s) * 1e3,
+        "tokens_per_s": 64 * 64 * 5 / (ms / 1e3), "decode_us": dec_avg * 1e3,
+        "decode_gbs": gbs, "frac": gbs / peak,
         "ids_match_split": bool(np.array_equal(job.out.cpu().numpy(), split_out)),
         "what": "every plan row streamed per request by the exact-order GEMV "
                 "(gemv_ring_kernel<bf16,INTERLEAVED,argmax>): HBM-bound, no shared rows"}
     del job
     torch.cuda.empty_cache()
     out["cfg3_prefill"] = prefill_secondary(torch, th, synth)
+    torch.cuda.empty_cache()
+    a = copy.copy(args)
+    a.quiet, a.steps, a.warmup, a.decode_steps, a.batch = True, 3, 2, 16, 1
+    r = run_vocab_shard(a, torch, None, 1, 0)
+    out["cfg4_g1"] = {"tokens_per_s": r["value"], "ms_per_token": r["ms_per_step"] / 16,
+                      "roofline": r["roofline"], "what": "full V=256,000 x 2,304 bf16 head, "
+                      "batch 1, one shard (G=1); G=2/4/8: --workload cfg4 under torchrun"}
+    torch.cuda.empty_cache()
+    a = copy.copy(args)
+    a.quiet, a.sweep_sizes, a.sweep_batches, a.sweep_dtypes = True, "1024,16384,128256", "1,256", "bf16"
+    r = run_sweep(a, torch, 0)
+    out["cfg5_summary"] = [{k: x.get(k) for k in ("dtype", "batch", "subset", "mode", "path",
+                                                  "us_per_step", "tokens_per_s", "gbs",
+                                                  "hbm_frac", "tflops", "tensor_frac",
+                                                  "speedup_vs_full_vocab")}
+                           for x in r["sweep"]]
+    torch.cuda.empty_cache()
+    a = copy.copy(args)
+    a.quiet = True
+    r = run_embed(a, torch, 0)
+    out["embed"] = {"roofline": r["roofline"], "tokens_per_s_zero_copy": r["value"],
+                    "results": r["results"]}
     torch.cuda.empty_cache()
     return out
 
@@ -1213,7 +1615,8 @@ def run_sweep(args, torch, rank):
                         rec["tflops"] = flops / (ms / 1e3) / 1e12
                         rec["tensor_frac"] = rec["tflops"] / tpeak
                     rows.append(rec)
-                    print(json.dumps(rec), file=sys.stderr, flush=True)
+                    if not getattr(args, "quiet", False):
+                        print(json.dumps(rec), file=sys.stderr, flush=True)
                     del keep
                     torch.cuda.empty_cache()
         del head
@@ -1235,8 +1638,9 @@ def run_sweep(args, torch, rank):
                          "l2": "256 MB read-flush before every step (subtracted)"},
               "peaks": {"hbm_gbs": peak, "hbm_source": peak_kind, "bf16_tflops": tpeak},
               "sweep": rows}
-    if rank == 0:
+    if rank == 0 and not getattr(args, "quiet", False):
         print(json.dumps(result), flush=True)
+    return result
 
 
 def run_embed(args, torch, rank):
@@ -1383,8 +1787,9 @@ def run_embed(args, torch, rank):
                            "peak_source": "pinned H2D cudaMemcpy of 256 MB, measured in this run",
                            "kernel": "embed_zero_copy_kernel"},
               "results": res}
-    if rank == 0:
+    if rank == 0 and not getattr(args, "quiet", False):
         print(json.dumps(result), flush=True)
+    return result
 
 
 def run_corpus(args, torch, rank):

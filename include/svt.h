@@ -624,6 +624,15 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
 svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size_t hidden_ld,
                                      uint32_t* d_out_ids, float* d_out_max);
 svt_stream svt_session_stream(svt_session* s);
+/* `steps` decode steps of n prepared sessions sharing one stream (and one
+ * hidden dimension), with HOST buffers: one H2D of every step's hidden
+ * states, the steps run token-interleaved on the device (step t: every
+ * session's greedy step in order), one D2H of the ids, one synchronisation.
+ * h_hidden: [steps][sum of batches][dim] f32; h_out_ids: [steps][sum of
+ * batches]. A batch-1 session runs the certified rows kernel (gathered once
+ * per prepare); larger batches the split / interleaved decode. */
+svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessions,
+                                   const float* h_hidden, int32_t steps, uint32_t* h_out_ids);
 
 #ifdef __cplusplus
 }

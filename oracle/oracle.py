@@ -287,6 +287,23 @@ class _RefLib:
         L.ref_batch_greedy.argtypes = [C.c_void_p, _f32p, _sz, C.c_int, C.c_int, _u32p]
         L.ref_slice_argmax.argtypes = [C.c_void_p, _sz, _sz, _f32p, _P(C.c_uint32),
                                        _P(C.c_float)]
+        L.ref_jobs_run.argtypes = [C.c_void_p, _u64p, _sz, _u32p, _i64p, C.c_int, _f32p,
+                                   C.c_int, C.c_int, _u32p, _P(C.c_double), _P(C.c_double)]
+
+    def jobs_run(self, head, words, V, flat, off, hidden, steps, threads):
+        """ref_jobs_run: J = len(off) - 1 cfg1 jobs (select -> gather ->
+        `steps` greedy steps each) on `threads` host threads. Returns (ids
+        [steps][J], (select, gather, decode) seconds summed over jobs, wall s)."""
+        J = len(off) - 1
+        ids = np.zeros((steps, J), np.uint32)
+        ph = (C.c_double * 3)()
+        wall = C.c_double()
+        self._chk(self.L.ref_jobs_run(head, np.ascontiguousarray(words, np.uint64), V,
+                                      np.ascontiguousarray(flat, np.uint32),
+                                      np.ascontiguousarray(off, np.int64), J,
+                                      np.ascontiguousarray(hidden, np.float32), steps, threads,
+                                      ids, ph, C.byref(wall)))
+        return ids, tuple(ph), wall.value
 
     def _chk(self, st):
         if st:

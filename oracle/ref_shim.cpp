@@ -12,6 +12,7 @@
 // host cores (batch-sharded over std::thread, each thread calling the
 // unmodified reference functions — SURVEY §8d "CPU timing beside it").
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -293,6 +294,88 @@ int ref_slice_argmax(void* head, size_t r0, size_t r1, const float* hidden, uint
             if (s[i] > s[k]) k = i;
         *best = static_cast<uint32_t>(r0 + k);
         *best_val = s[k];
+    });
+}
+
+// BASELINE cfg1 jobs on the host cores: job j = select(prompt_j, T) ->
+// gather -> `steps` greedy steps on hidden[t][j] (the reference functions
+// themselves, all steps run). Jobs are spread over the threads; when there
+// are more threads than jobs, each job's logits are split into contiguous
+// row slices (one gather per slice: per-row order preserved),
+// the slices' first maxima combined in slice order with the reference's
+// strict `>` and the winner remapped with remap_out. phase_s receives the
+// select / gather / decode seconds summed over jobs, wall_s the wall time.
+int ref_jobs_run(void* head, const uint64_t* static_words, size_t universe,
+                 const uint32_t* prompt_ids, const int64_t* prompt_off, int J,
+                 const float* hidden, int steps, int threads, uint32_t* out_ids,
+                 double* phase_s, double* wall_s) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        const auto& W = *static_cast<HeadMatrix*>(head);
+        const TokenSet T = words_to_set(static_words, universe);
+        const size_t d = W.dim();
+        const int workers = std::max(1, std::min(threads, J));
+        const int slices = std::max(1, threads / std::max(1, J));
+        std::vector<double> ph(static_cast<size_t>(J) * 3, 0.0);
+        const auto w0 = clk::now();
+        parallel_for(J, workers, [&](int j) {
+            auto t0 = clk::now();
+            const auto n = static_cast<size_t>(prompt_off[j + 1] - prompt_off[j]);
+            const SelectionPlan plan =
+                select(std::span<const TokenId>(prompt_ids + prompt_off[j], n), T, W.rows());
+            auto t1 = clk::now();
+            const size_t S = plan.active_ids.size();
+            const int ns = static_cast<int>(std::min<size_t>(static_cast<size_t>(slices), S));
+            std::vector<HeadMatrix> subs;
+            std::vector<size_t> base;
+            if (ns <= 1) {
+                subs.push_back(gather(W, plan));
+                base.push_back(0);
+            } else {
+                subs.resize(static_cast<size_t>(ns));
+                for (int k = 0; k < ns; ++k) {
+                    const size_t a = S * static_cast<size_t>(k) / static_cast<size_t>(ns);
+                    const size_t b = S * static_cast<size_t>(k + 1) / static_cast<size_t>(ns);
+                    SelectionPlan sl;
+                    sl.active_ids.assign(plan.active_ids.begin() + static_cast<long>(a),
+                                         plan.active_ids.begin() + static_cast<long>(b));
+                    sl.full_vocab_size = plan.full_vocab_size;
+                    subs[static_cast<size_t>(k)] = gather(W, sl);
+                    base.push_back(a);
+                }
+            }
+            auto t2 = clk::now();
+            for (int t = 0; t < steps; ++t) {
+                const float* h = hidden + (static_cast<size_t>(t) * J + j) * d;
+                uint32_t& out = out_ids[static_cast<size_t>(t) * J + j];
+                if (ns <= 1) {
+                    out = greedy_step(subs[0], std::span<const float>(h, d), plan);
+                    continue;
+                }
+                std::vector<size_t> arg(static_cast<size_t>(ns));
+                std::vector<float> val(static_cast<size_t>(ns));
+                parallel_for(ns, ns, [&](int k) {
+                    const auto sc = logits(subs[static_cast<size_t>(k)], std::span<const float>(h, d));
+                    size_t best = 0;
+                    for (size_t i = 1; i < sc.size(); ++i)
+                        if (sc[i] > sc[best]) best = i;
+                    arg[static_cast<size_t>(k)] = best;
+                    val[static_cast<size_t>(k)] = sc[best];
+                });
+                size_t bk = 0;
+                for (int k = 1; k < ns; ++k)
+                    if (val[static_cast<size_t>(k)] > val[bk]) bk = static_cast<size_t>(k);
+                out = remap_out(plan, base[bk] + arg[bk]);
+            }
+            auto t3 = clk::now();
+            ph[static_cast<size_t>(j) * 3 + 0] = std::chrono::duration<double>(t1 - t0).count();
+            ph[static_cast<size_t>(j) * 3 + 1] = std::chrono::duration<double>(t2 - t1).count();
+            ph[static_cast<size_t>(j) * 3 + 2] = std::chrono::duration<double>(t3 - t2).count();
+        });
+        *wall_s = std::chrono::duration<double>(clk::now() - w0).count();
+        phase_s[0] = phase_s[1] = phase_s[2] = 0.0;
+        for (int j = 0; j < J; ++j)
+            for (int k = 0; k < 3; ++k) phase_s[k] += ph[static_cast<size_t>(j) * 3 + k];
     });
 }
 

@@ -131,6 +131,7 @@ _SIGS = {
     "svt_session_greedy_host": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
     "svt_session_greedy_device": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
     "svt_session_stream": ([_vp], _vp),
+    "svt_session_decode_host": ([_vp, C.c_int32, _vp, C.c_int32, _vp], C.c_int),
     "svt_plan_to_json": ([_vp, _sz, _sz, _sz, _sz, _i32, _vp, _sz, _vp], C.c_int),
     "svt_plans_to_jsonl": ([_vp, _vp, _vp, _vp, _vp, _i32, _sz, _vp, _sz, _vp], C.c_int),
     "svt_plan_from_json": ([C.c_char_p, _sz, C.c_char_p, _vp, _sz, _vp, _vp, _vp, _vp], C.c_int),

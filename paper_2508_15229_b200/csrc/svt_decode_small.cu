@@ -940,7 +940,10 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
             for (int e = 0; e < E; e += 2) w2[k][q * E / 2 + e / 2] = pack2(w[e], w[e + 1]);
         }
     }
-    asm volatile("griddepcontrol.launch_dependents;");
+    // (no launch_dependents here: a CTA counts as triggered once ANY of its
+    // threads executes it, and the dependents (this step's finalize) must
+    // not start before the control warp has passed the dependency wait —
+    // the finalize reads the epoch the previous finalize wrote)
     mbar_wait_parity(&s_hbar, 0u);
     if (warp == 0 && lane == 0) SVT_FSTAMP(2);
     unsigned long long h2[NP];

@@ -85,6 +85,19 @@ struct svt_session {
     uint32_t* first_ids_d() { return reinterpret_cast<uint32_t*>(d_split_meta + 2 * cap_batch); }
     uint8_t* dyn_starts_d() { return reinterpret_cast<uint8_t*>(d_split_meta + 3 * cap_batch); }
 
+    // batch-1 sessions (BASELINE cfg1): the plan's rows gathered row-major
+    // once per prepare, every step on the certified rows kernel
+    bool rows_mode = false;
+    uint8_t* d_rows = nullptr;
+    size_t cap_rows = 0;
+    uint8_t* d_rows_ws = nullptr;
+    size_t cap_rows_ws = 0;
+    // svt_session_decode_host staging: [steps][batch rows] hidden states, ids
+    float* d_multi = nullptr;
+    size_t cap_multi = 0;
+    uint32_t* d_multi_ids = nullptr;
+    size_t cap_multi_ids = 0;
+
     int64_t* n_active_d() { return d_meta; }
     int64_t* n_static_d() { return d_meta + cap_batch; }
     int64_t* n_dynamic_d() { return d_meta + 2 * cap_batch; }
@@ -111,7 +124,8 @@ void free_all(svt_session* s) {
     void* dev[] = {s->d_words, s->d_inputs, s->d_in_off, s->d_act_off, s->d_meta, s->d_active,
                    s->d_group_req, s->d_sub, s->d_hidden, s->d_out_ids, s->d_out_max, s->d_ws,
                    s->d_bad, s->d_st_ids, s->d_st_meta, s->d_st_sub, s->d_st_small,
-                   s->d_dyn_ids, s->d_split_meta, s->d_split_ws};
+                   s->d_dyn_ids, s->d_split_meta, s->d_split_ws, s->d_rows, s->d_rows_ws,
+                   s->d_multi, s->d_multi_ids};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {s->h_hidden, s->h_ids, s->h_max};
@@ -426,11 +440,14 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
     // split decode for batches over a non-empty static set (SVT_SESSION_SPLIT=0: off)
     const char* split_env = getenv("SVT_SESSION_SPLIT");
     s->split = n_static > 0 && batch >= 2 && (split_env == nullptr || atoi(split_env) != 0);
+    // batch 1: row-major gather + the certified rows kernel (SVT_SESSION_ROWS=0: off)
+    const char* rows_env = getenv("SVT_SESSION_ROWS");
+    s->rows_mode = batch == 1 && (rows_env == nullptr || atoi(rows_env) != 0);
     if (!st && s->split) st = prepare_split(s, h_static_words, n_static, q);
-    if (!st)
+    if (!st && !s->rows_mode)
         st = svt_plan_layout(s->split ? s->n_dyn_d() : s->n_active_d(), s->d_act_off, batch,
                              s->group_begin_d(), s->d_group_req, s->max_groups, q);
-    if (!st)
+    if (!st && !s->rows_mode)
         st = svt_gather_interleaved(s->head, s->dt, s->rows, s->dim,
                                     s->split ? s->d_dyn_ids : s->d_active, s->group_begin_d(),
                                     s->d_group_req, batch, s->max_groups, s->d_sub, s->d_bad, q);
@@ -460,6 +477,31 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
             set_error("internal: plan capacity exceeded for request %zu", b);
             s->batch = 0;
             return SVT_ERR_RUNTIME;
+        }
+    }
+    if (s->rows_mode && s->n_active[0] > 0) {
+        // the plan size is known now: gather its rows row-major (stream-
+        // ordered before every later step), workspace zeroed once
+        const size_t n = static_cast<size_t>(s->n_active[0]);
+        const size_t bytes = n * s->dim * svt_dtype_size(s->dt) + 16;
+        st = grow(&s->d_rows, &s->cap_rows, bytes);
+        const size_t wsb = svt_greedy_rows_workspace_bytes(n);
+        if (!st && (wsb > s->cap_rows_ws || !s->d_rows_ws)) {
+            if (s->d_rows_ws) cudaFree(s->d_rows_ws);
+            s->d_rows_ws = nullptr;
+            s->cap_rows_ws = 0;
+            st = grow(&s->d_rows_ws, &s->cap_rows_ws, wsb);
+            if (!st) {
+                const cudaError_t e = cudaMemset(s->d_rows_ws, 0, s->cap_rows_ws);
+                if (e != cudaSuccess) st = svt::cuda_status(e, "rows workspace memset");
+            }
+        }
+        if (!st)
+            st = svt_gather_rows(s->head, s->dt, s->rows, s->dim, s->d_active, n, s->d_rows,
+                                 s->d_bad, q);
+        if (st) {
+            s->batch = 0;
+            return st;
         }
     }
     return SVT_OK;
@@ -504,6 +546,12 @@ svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size
     // must not prefetch them ahead of the dependency wait
     const int32_t flags = s->weights_stable ? SVT_WEIGHTS_STABLE : 0;
     s->weights_stable = true;
+    if (s->rows_mode) {
+        const size_t n = static_cast<size_t>(s->n_active[0]);
+        return svt_greedy_certified_rows(s->d_rows, s->dt, n, s->dim, nullptr, n, d_hidden,
+                                         s->d_active, 0u, 1, flags, d_out_ids, d_out_max,
+                                         nullptr, s->d_rows_ws, s->stream);
+    }
     if (s->split)
         return svt_greedy_split(s->d_st_sub, s->dt, s->n_st, s->dim, s->d_st_ids, s->st_valid_d(),
                                 s->first_ids_d(), s->d_sub, s->group_begin_d(), s->d_group_req,
@@ -626,7 +674,8 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
         SVT_CUDA_TRY(cudaMemcpyAsync(s->d_hidden, s->h_hidden, B * s->ld * sizeof(float),
                                      cudaMemcpyHostToDevice, q));
     }
-    svt_status st = svt_session_greedy_device(s, s->d_hidden, s->ld, s->d_out_ids, s->d_out_max);
+    svt_status st = svt_session_greedy_device(s, s->d_hidden, s->ld, s->d_out_ids,
+                                              h_out_max ? s->d_out_max : nullptr);
     if (st) return st;
     const bool direct = is_pinned(h_out_ids);
     SVT_CUDA_TRY(cudaMemcpyAsync(direct ? h_out_ids : s->h_ids, s->d_out_ids, B * sizeof(uint32_t),
@@ -637,6 +686,55 @@ svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t
     SVT_CUDA_TRY(cudaStreamSynchronize(q));
     if (!direct) std::memcpy(h_out_ids, s->h_ids, B * sizeof(uint32_t));
     if (h_out_max) std::memcpy(h_out_max, s->h_max, B * sizeof(float));
+    return SVT_OK;
+}
+
+svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessions,
+                                   const float* h_hidden, int32_t steps, uint32_t* h_out_ids) {
+    if (!sessions || n_sessions <= 0 || !sessions[0]) {
+        set_error("no sessions");
+        return SVT_ERR_CONFIG;
+    }
+    if (steps < 0) {
+        set_error("negative step count");
+        return SVT_ERR_CONFIG;
+    }
+    svt_session* s0 = sessions[0];
+    size_t rows = 0;  // hidden rows per step (the sessions' batches, in order)
+    for (int32_t i = 0; i < n_sessions; ++i) {
+        svt_session* si = sessions[i];
+        if (!si || si->stream != s0->stream || si->dim != s0->dim) {
+            set_error("decode_host: sessions must share one stream and one hidden dimension");
+            return SVT_ERR_CONFIG;
+        }
+        if (si->dim % 4 != 0) {
+            set_error("decode_host: hidden dimension must be a multiple of 4");
+            return SVT_ERR_CONFIG;
+        }
+        rows += static_cast<size_t>(si->batch);
+    }
+    if (steps == 0 || rows == 0) return SVT_OK;
+    const size_t dim = s0->dim, total = static_cast<size_t>(steps) * rows;
+    svt_status st = grow(&s0->d_multi, &s0->cap_multi, total * dim);
+    if (!st) st = grow(&s0->d_multi_ids, &s0->cap_multi_ids, total);
+    if (st) return st;
+    cudaStream_t q = s0->stream;
+    SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi, h_hidden, total * dim * sizeof(float),
+                                 cudaMemcpyHostToDevice, q));
+    for (int32_t t = 0; t < steps; ++t) {
+        size_t off = static_cast<size_t>(t) * rows;
+        for (int32_t i = 0; i < n_sessions; ++i) {
+            svt_session* si = sessions[i];
+            if (si->batch == 0) continue;
+            st = svt_session_greedy_device(si, s0->d_multi + off * dim, dim,
+                                           s0->d_multi_ids + off, nullptr);
+            if (st) return st;
+            off += static_cast<size_t>(si->batch);
+        }
+    }
+    SVT_CUDA_TRY(cudaMemcpyAsync(h_out_ids, s0->d_multi_ids, total * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, q));
+    SVT_CUDA_TRY(cudaStreamSynchronize(q));
     return SVT_OK;
 }
 

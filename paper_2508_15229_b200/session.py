@@ -66,3 +66,23 @@ class Session:
             out_max.data_ptr() if hasattr(out_max, "data_ptr") else out_max.ctypes.data)
         call("svt_session_greedy_host", self.h, ptr, ld, optr, mptr)
         return out_ids
+
+
+def decode_host(sessions, hidden, steps: int, out_ids=None):
+    """svt_session_decode_host: `steps` token-interleaved decode steps over
+    prepared sessions sharing one stream. hidden: host [steps][sum B][dim]
+    float32 (a pinned torch tensor or a numpy array); returns the ids
+    [steps][sum B] (uint32 numpy array or the given buffer)."""
+    rows = sum(s.B for s in sessions)
+    arr = (C.c_void_p * len(sessions))(*[s.h.value for s in sessions])
+    if hasattr(hidden, "data_ptr"):
+        hptr = hidden.data_ptr()
+    else:
+        hidden = np.ascontiguousarray(hidden, np.float32)
+        hptr = hidden.ctypes.data
+    if out_ids is None:
+        out_ids = np.empty((steps, rows), np.uint32)
+    optr = out_ids.data_ptr() if hasattr(out_ids, "data_ptr") else out_ids.ctypes.data
+    call("svt_session_decode_host", arr, len(sessions), hptr, steps, optr)
+    return out_ids
+

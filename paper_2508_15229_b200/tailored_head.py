@@ -668,13 +668,18 @@ class TailoredBatch:
         self._stable = False
         return self
 
-    def run_select(self):
+    def run_select(self, layout: bool = True):
+        """select (a) for every request; ``layout=False`` skips the row-group
+        layout the interleaved paths use (row-major / batch-1 decoders)."""
         self._stable = False
         call("svt_select_batched", self._words.data_ptr(), self.V, self.V,
              self._prompts.data_ptr(), self._prompt_off.data_ptr(), self.B,
              self.active.data_ptr(), self.act_off.data_ptr(), self.n_active.data_ptr(),
              self.n_static.data_ptr(), self.n_dynamic.data_ptr(), self.first_bad_d.data_ptr(),
              _stream(self.stream))
+        if not layout:
+            self._first_bad_h = None
+            return
         call("svt_plan_layout", self.n_active.data_ptr(), self.act_off.data_ptr(), self.B,
              self.group_begin.data_ptr(), self.group_meta.data_ptr(), self.max_groups,
              _stream(self.stream))

@@ -788,6 +788,95 @@ def test_rows_certified_cfg1_shape(th, materialize):
     assert fast + slow == hid.shape[0] + 3 and slow >= 3
 
 
+def test_rows_cfg1_all_64_steps_graph_and_exact_logits(th):
+    """cfg1 at full shape, all 64 decode steps: (i) back-to-back in CUDA
+    graphs (programmatic launches, no host sync between tokens) for two
+    jobs token-interleaved and for one job alone, replayed twice — ids equal
+    the reference greedy_step; (ii) every step's exact winning logit equals
+    the reference's bit for bit."""
+    from paper_2508_15229_b200 import synth
+
+    V, d, steps = 128256, 2048, 64
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_F32, 2, 512, 2048, steps)
+    W = head.to_host()
+    plans = [orc.select(prompts[j], words, V, V).active_ids for j in range(2)]
+    subs = [orc.gather(W, p) for p in plans]
+    want = np.zeros((steps, 2), np.uint32)
+    wmax = np.zeros((steps, 2), np.float32)
+    for j in range(2):
+        for t in range(steps):
+            want[t, j], wmax[t, j] = orc.greedy_step(subs[j], hid[t][j], plans[j])
+    decs = [_rows_decoder(th, head, plans[j]) for j in range(2)]
+    hd = torch.from_numpy(np.ascontiguousarray(hid, np.float32)).cuda()
+    out = torch.full((steps, 2), -1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.Stream()
+    for dcd in decs:
+        dcd.stream = st
+
+    def run(jobs):
+        for t in range(steps):
+            for j in jobs:
+                decs[j].greedy(hd[t, j], out[t, j])
+
+    for jobs in ([0, 1], [0]):
+        with torch.cuda.stream(st):
+            run(jobs)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            run(jobs)
+        for _ in range(2):
+            out.fill_(-1)
+            with torch.cuda.stream(st):
+                g.replay()
+            torch.cuda.synchronize()
+            got = out.cpu().numpy().view(np.uint32)
+            assert np.array_equal(got[:, jobs], want[:, jobs]), jobs
+    for dcd in decs:
+        dcd.stream = None
+    for t in range(steps):
+        for j in range(2):
+            gid, gmax = _rows_greedy(decs[j], hid[t][j], want_max=True)
+            assert gid == want[t, j] and bits([gmax])[0] == bits([wmax[t, j]])[0], (t, j)
+
+
+def test_session_batch1_rows_and_decode_host(th):
+    """Batch-1 sessions run the certified rows kernel (row-major gather per
+    prepare); svt_session_decode_host over three sessions sharing a stream
+    (batches 1, 1 and 3) equals the reference for every step, and a single
+    session's per-step host call agrees."""
+    from paper_2508_15229_b200 import session
+
+    V, d, steps = 128256, 2048, 5
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_F32, 5, 512, 2048, steps)
+    W = head.to_host()
+    plans = [orc.select(prompts[j], words, V, V).active_ids for j in range(5)]
+    subs = [orc.gather(W, p) for p in plans]
+    want = np.array([[orc.greedy_step(subs[j], hid[t][j], plans[j])[0] for j in range(5)]
+                     for t in range(steps)], np.uint32)
+    st = torch.cuda.Stream()
+    groups = [[0], [1], [2, 3, 4]]
+    sess = [session.Session(head, max_batch=len(g), stream=st) for g in groups]
+    try:
+        for s_, g in zip(sess, groups):
+            off = np.zeros(len(g) + 1, np.int64)
+            off[1:] = np.cumsum([len(prompts[j]) for j in g])
+            s_.prepare(words, V, np.concatenate([prompts[j] for j in g]), off)
+        ids = session.decode_host(sess, np.ascontiguousarray(hid, np.float32), steps)
+        assert np.array_equal(ids, want)
+        ids2 = session.decode_host(sess, torch.from_numpy(hid).pin_memory(), steps)
+        assert np.array_equal(ids2, want)
+        for t in range(steps):
+            assert int(sess[0].greedy(hid[t][:1])[0]) == want[t, 0]
+        mx = np.zeros(1, np.float32)
+        got = sess[1].greedy(hid[0][1:2], out_max=mx)
+        assert int(got[0]) == want[0, 1]
+        assert bits(mx)[0] == bits([orc.greedy_step(subs[1], hid[0][1], plans[1])[1]])[0]
+    finally:
+        for s_ in sess:
+            s_.close()
+
+
 @pytest.mark.parametrize("V,d,storage,n", [(151936, 896, "bf16", 2600), (256000, 2304, "bf16", 4000),
                                            (5000, 256, "f16", 700), (3000, 64, "f32", 300),
                                            (9000, 8192, "f32", 333), (40000, 1024, "bf16", 40000)])
