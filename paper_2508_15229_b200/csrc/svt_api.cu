@@ -152,6 +152,7 @@ svt_status svt_stream_create(svt_stream* out) {
     return SVT_OK;
 }
 svt_status svt_stream_destroy(svt_stream stream) {
+    if (stream) svt::release_side_stream(static_cast<cudaStream_t>(stream));
     if (stream) SVT_CUDA_TRY(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
     return SVT_OK;
 }

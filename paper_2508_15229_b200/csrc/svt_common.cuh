@@ -266,12 +266,14 @@ svt_status cuda_status(cudaError_t e, const char* what);
 
 // A side stream (+ fork / join events) per (device, calling stream): kernels
 // forked beside a caller's stream never share events with another caller's
-// concurrent work. Created on first use, kept for the process.
+// concurrent work. Created on first use; released with the calling stream
+// (release_side_stream: svt_stream_destroy, svt_session_destroy).
 struct SideStream {
     cudaStream_t stream = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream* side_stream_for(cudaStream_t main);
+void release_side_stream(cudaStream_t main);
 int sm_count();
 }  // namespace svt
 

@@ -362,7 +362,10 @@ svt_status svt_session_destroy(svt_session* s) {
     cudaStreamSynchronize(s->stream);
     drop_graph(s);
     free_all(s);
-    if (s->own_stream) cudaStreamDestroy(s->stream);
+    if (s->own_stream) {
+        svt::release_side_stream(s->stream);
+        cudaStreamDestroy(s->stream);
+    }
     delete s;
     return SVT_OK;
 }

@@ -229,23 +229,50 @@ __global__ void split_combine_kernel(const uint4* __restrict__ rec,
 
 }  // namespace
 
+namespace {
+std::mutex g_side_mu;
+std::map<std::pair<int, cudaStream_t>, SideStream> g_side;
+
+void destroy_side(SideStream& s) {
+    if (s.join) cudaEventDestroy(s.join);
+    if (s.fork) cudaEventDestroy(s.fork);
+    if (s.stream) cudaStreamDestroy(s.stream);
+    s = SideStream{};
+}
+}  // namespace
+
 SideStream* side_stream_for(cudaStream_t main) {
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, SideStream> streams;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
-    SideStream& s = streams[{dev, main}];
+    std::lock_guard<std::mutex> lock(g_side_mu);
+    SideStream& s = g_side[{dev, main}];
     if (!s.stream) {
         if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();
-            streams.erase({dev, main});
+            destroy_side(s);  // whatever was created before the failure
+            g_side.erase({dev, main});
             return nullptr;
         }
     }
     return &s;
+}
+
+// Drop the side streams forked from `main` (every device): called before the
+// caller destroys `main`, so sessions and streams that come and go do not
+// grow the map. Work already queued on the side stream completes first.
+void release_side_stream(cudaStream_t main) {
+    std::lock_guard<std::mutex> lock(g_side_mu);
+    for (auto it = g_side.begin(); it != g_side.end();) {
+        if (it->first.second == main) {
+            if (it->second.stream) cudaStreamSynchronize(it->second.stream);
+            destroy_side(it->second);
+            it = g_side.erase(it);
+        } else {
+            ++it;
+        }
+    }
 }
 }  // namespace svt
 
@@ -325,15 +352,24 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         const cudaError_t e = dt == SVT_F32    ? launch(static_rows_kernel<SVT_F32>)
                               : dt == SVT_BF16 ? launch(static_rows_kernel<SVT_BF16>)
                                                : launch(static_rows_kernel<SVT_F16>);
-        if (e != cudaSuccess) return cuda_status(e, "static_rows_kernel");
+        if (e != cudaSuccess) {
+            cudaMemsetAsync(keys, 0, b * 8, ss);
+            return cuda_status(e, "static_rows_kernel");
+        }
         SVT_LAUNCH_CHECK("static_rows_kernel");
     }
     if (side) SVT_CUDA_TRY(cudaEventRecord(side->join, ss));
     // dynamic half: requests without dynamic rows have no group (record untouched)
     if (svt_status s = greedy_interleaved_req(d_dyn_sub, dt, dim, d_group_begin, d_group_meta,
                                               d_dyn_ids, batch, max_groups, d_hidden, hidden_ld,
-                                              flags, d_dyn_starts, d_out_ids, rec, gws, st))
+                                              flags, d_dyn_starts, d_out_ids, rec, gws, st)) {
+        // the combine will not run: join the side stream and restore the
+        // zero static keys it would have left, so a retry on this workspace
+        // does not fold into stale keys
+        if (side) cudaStreamWaitEvent(st, side->join, 0);
+        cudaMemsetAsync(keys, 0, b * 8, st);
         return s;
+    }
     if (side) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
     split_combine_kernel<<<(batch + 127) / 128, 128, 0, st>>>(
         reinterpret_cast<const uint4*>(rec), keys, d_first_ids, d_n_dyn, batch, d_out_ids,

@@ -24,6 +24,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "svt_common.cuh"
 
 namespace svt {
@@ -240,27 +242,20 @@ __global__ void __launch_bounds__(kTolThreads, 1) tolerance_kernel(TolParams p) 
 // barrier; every CTA then derives the same pick. The output pass needs, per
 // CTA, the ids with df < v* and df == v* before its slice (a scan of G counts
 // after a barrier), so pruned ids land in id order. The scratch (histograms,
-// counts, barrier counter) lives in the kept-words output, zeroed by the host
-// and overwritten only after the last barrier.
+// counts) lives in the kept-words output, zeroed by the host and overwritten
+// only after the last barrier. The barriers are the cooperative launch's own
+// grid barrier (cooperative_groups): their state lives outside every buffer
+// this kernel writes, so a CTA that leaves the last barrier and starts
+// writing kept words can never disturb a CTA still waiting in it.
 struct TolScratch {
     unsigned long long hist[4][kBuckets];
-    unsigned long long bar;
     unsigned long long cnt[1];  // [2 * G]: df < v*, df == v* per CTA
 };
 constexpr size_t tol_scratch_bytes(int G) {
-    return sizeof(unsigned long long) * (4 * kBuckets + 1 + 2 * static_cast<size_t>(G));
+    return sizeof(unsigned long long) * (4 * kBuckets + 2 * static_cast<size_t>(G));
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1ull);
-        while (*reinterpret_cast<volatile unsigned long long*>(bar) < target) __nanosleep(32);
-        __threadfence();
-    }
-    __syncthreads();
-}
+__device__ __forceinline__ void grid_barrier() { cooperative_groups::this_grid().sync(); }
 
 __global__ void __launch_bounds__(kTolThreads, 1) tolerance_multi_kernel(TolParams p) {
     extern __shared__ unsigned long long hist[];  // [warp][bucket] df sums
@@ -275,8 +270,6 @@ __global__ void __launch_bounds__(kTolThreads, 1) tolerance_multi_kernel(TolPara
     const int64_t per = (p.nwords + G - 1) / G;
     const int64_t w0 = min(p.nwords, per * cta), w1 = min(p.nwords, w0 + per);
     const int64_t id_lo = w0 * 64, id_hi = w1 * 64;
-    unsigned long long nbar = 0;
-
     uint64_t vstar, S = 0;
     if (p.mode == 1) {
         vstar = 0;
@@ -317,7 +310,7 @@ __global__ void __launch_bounds__(kTolThreads, 1) tolerance_multi_kernel(TolPara
                 for (int w = 0; w < kTolWarps; ++w) sum += hist[w * kBuckets + t];
                 if (sum) atomicAdd(&sc->hist[level][t], sum);
             }
-            grid_barrier(&sc->bar, static_cast<unsigned long long>(G) * ++nbar);
+            grid_barrier();
             if (t == 0) {
                 uint64_t below = s_below;
                 int pick = -1;
@@ -360,7 +353,7 @@ __global__ void __launch_bounds__(kTolThreads, 1) tolerance_multi_kernel(TolPara
         sc->cnt[2 * cta] = tot_lt;
         sc->cnt[2 * cta + 1] = tot_eq;
     }
-    grid_barrier(&sc->bar, static_cast<unsigned long long>(G) * ++nbar);
+    grid_barrier();
     if (t == 0) {
         uint64_t blt = 0, beq = 0;
         for (int c = 0; c < cta; ++c) {
@@ -371,7 +364,7 @@ __global__ void __launch_bounds__(kTolThreads, 1) tolerance_multi_kernel(TolPara
         s_before_eq = beq;
     }
     // every CTA has its prefix before the kept words (the scratch) are written
-    grid_barrier(&sc->bar, static_cast<unsigned long long>(G) * ++nbar);
+    grid_barrier();
     const uint64_t eq_before = s_before_eq;
     uint64_t out_at = s_before_lt + (eq_before < j ? eq_before : j);
     uint64_t eq_seen = eq_before, dsum = 0;
