@@ -61,6 +61,8 @@ size_t svt_dtype_size(svt_dtype dt);
 /* Device memory and stream plumbing, so an FFI host (cgo, JNI, ctypes, the
  * C++ drop-in) needs no CUDA runtime of its own. */
 svt_status svt_set_device(int device);
+/* The calling thread's current device (per-thread state of the C++ drop-in). */
+svt_status svt_get_device(int* device);
 svt_status svt_device_alloc(void** d_ptr, size_t bytes);
 svt_status svt_device_free(void* d_ptr);
 svt_status svt_host_alloc_pinned(void** h_ptr, size_t bytes);

@@ -55,6 +55,7 @@ _SIGS = {
     "svt_device_count": ([], C.c_int),
     "svt_dtype_size": ([C.c_int], _sz),
     "svt_set_device": ([C.c_int], C.c_int),
+    "svt_get_device": ([C.POINTER(C.c_int)], C.c_int),
     "svt_device_alloc": ([C.POINTER(_vp), _sz], C.c_int),
     "svt_device_free": ([_vp], C.c_int),
     "svt_host_alloc_pinned": ([C.POINTER(_vp), _sz], C.c_int),

@@ -96,10 +96,23 @@ def build_dropin_test(force=False):
     return out
 
 
+def build_dropin_bench(force=False):
+    """C++ drop-in timing at cfg1 (tests/cpp/bench_dropin_cfg1.cpp)."""
+    src = os.path.join(ROOT, "tests", "cpp", "bench_dropin_cfg1.cpp")
+    out = os.path.join(LIB, "bench_dropin_cfg1")
+    deps = [src, os.path.join(LIB, "libsubvocab_b200.so")]
+    if force or _stale(out, deps):
+        cxx = os.environ.get("CXX", "g++")
+        _run([cxx, "-std=c++20", "-O2", "-I", INCLUDE, src, "-o", out, "-L", LIB,
+              "-lsubvocab_b200", "-lsvt", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_all(force=False):
     build_svt(force)
     build_dropin(force)
     build_dropin_test(force)
+    build_dropin_bench(force)
 
 
 if __name__ == "__main__":

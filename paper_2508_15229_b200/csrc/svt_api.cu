@@ -103,6 +103,11 @@ svt_status svt_set_device(int device) {
     SVT_CUDA_TRY(cudaSetDevice(device));
     return SVT_OK;
 }
+svt_status svt_get_device(int* device) {
+    if (svt_status s = need_device()) return s;
+    SVT_CUDA_TRY(cudaGetDevice(device));
+    return SVT_OK;
+}
 svt_status svt_device_alloc(void** d_ptr, size_t bytes) {
     if (svt_status s = need_device()) return s;
     SVT_CUDA_TRY(cudaMalloc(d_ptr, bytes ? bytes : 16));
