@@ -1037,88 +1037,121 @@ CFG4 = dict(workload="cfg4: Gemma-2-2B-shaped head, vocab-sharded full-vocab gre
 
 
 def run_vocab_shard(args, torch, dist, world, rank):
-    """cfg4: rows of the full V=256000 x 2304 bf16 head split contiguously
-    over the ranks (each rank materialises only its slice); one decode step =
-    local exact GEMV + argmax record -> NCCL all-gather -> combine. Strong
+    """cfg4: the full V=256000 x 2304 bf16 head, vocab-sharded: the plan is
+    cut into contiguous ascending slices over the ranks. Identity plan (the
+    headline of this workload): each rank materialises only its rows. One
+    decode step = svt_sharded_greedy (certified rows kernel with an exact
+    shard record -> ncclAllGather of the 16-byte records over NVLink on a
+    communicator made through svt_nccl_* -> combine); the 64 steps of a
+    bench step replay as ONE CUDA graph. A tailored plan (select over 2,048
+    static ids + a 512-token prompt, the same slices) is timed beside it
+    ("identity plan plus one tailored plan"). Strong
     scaling (total work fixed)."""
     from paper_2508_15229_b200 import sharded, synth
     from paper_2508_15229_b200 import tailored_head as th
 
     V, d = CFG4["V"], CFG4["d"]
-    B = args.batch if args.batch != 64 else 1
+    steps = args.decode_steps
     r0, r1 = sharded.shard_ranges(V, world)[rank]
     local = torch.empty((r1 - r0, d), dtype=torch.bfloat16, device="cuda")
     th._lib.call("svt_head_random", local.data_ptr(), th.SVT_BF16, th.SVT_BF16, r0 * d,
                  (r1 - r0) * d, synth.SEED_W, None)
     head = th.HeadMatrix(0, d, 2, th.SVT_BF16, data=local)
-    vs = sharded.VocabShardedHead(head, B)
-    vs.shard = sharded.RowShard(head, r0, r1, B, plan_start=(rank == 0), local_rows=local)
-    steps = args.decode_steps
-    ld = (d + 3) // 4 * 4
-    hid = torch.empty(steps * B * d, dtype=torch.float32, device="cuda")
-    th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_F32, th.SVT_BF16, 0, steps * B * d,
+    # NCCL communicator through the C-ABI; ranks sharing one GPU under the
+    # gloo backend (tools/multirank_smoke.sh) cannot form one, so they
+    # all-gather the records through torch.distributed instead (no graph)
+    use_nccl = world == 1 or dist.get_backend() == "nccl"
+    comm = sharded.NcclComm(world, rank) if use_nccl else None
+    hid = torch.empty(steps * d, dtype=torch.float32, device="cuda")
+    th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_F32, th.SVT_BF16, 0, steps * d,
                  synth.SEED_H, None)
-    hidden = torch.zeros((steps, B, ld), dtype=torch.float32, device="cuda")
-    hidden[:, :, :d] = hid.view(steps, B, d)
-    out = torch.empty((steps, B), dtype=torch.int32, device="cuda")
+    hidden = hid.view(steps, d)
+    out = torch.full((steps,), -1, dtype=torch.int32, device="cuda")
+    if use_nccl:
+        dec = sharded.ShardedDecoder(head, comm, n_plan=V, local_rows=True)
+        g = dec.graph(hidden, out).replay
+    else:
+        vs = sharded.VocabShardedHead(head, 1)
+        vs.shard = sharded.RowShard(head, r0, r1, 1, plan_start=(rank == 0), local_rows=local)
+        hpad = torch.zeros((steps, 1, (d + 3) // 4 * 4), dtype=torch.float32, device="cuda")
+        hpad[:, 0, :d] = hidden
 
-    def run(evs=None):
-        for t in range(steps):
-            if evs is not None:
-                evs[t][0].record()
-            vs.step(hidden[t])
-            if evs is not None:
-                evs[t][1].record()
-            out[t].copy_(vs.out[:B])
+        def g():
+            for t in range(steps):
+                vs.step(hpad[t])
+                out[t:t + 1].copy_(vs.out[:1])
 
-    for _ in range(args.warmup):
-        run()
-    torch.cuda.synchronize()
-    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in range(steps)] for _ in range(args.steps)]
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    def timed(graph, reps, warm):
+        for _ in range(warm):
+            graph()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        for k in range(args.steps):
-            run(evs[k])
+        for _ in range(reps):
+            graph()
         b.record()
         torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    ms = a.elapsed_time(b)
-    step_ms = [x.elapsed_time(y) for row in evs for (x, y) in row]
-    if dist is not None and world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    tokens = B * steps * args.steps
-    per_rank_bytes = (r1 - r0) * d * 2 + B * (d * 4 + 16)
-    step_avg = sum(step_ms) / len(step_ms)
+        if dist is not None:
+            dist.barrier()
+        ms = a.elapsed_time(b)
+        if dist is not None and world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ms = timed(g, args.steps, args.warmup)
+    tokens = steps * args.steps
+    per_rank_bytes = (r1 - r0) * d * 2 + d * 4 + 16
+    tok_us = ms * 1e3 / tokens
     peak, peak_kind = load_peaks()
-    achieved = per_rank_bytes / (step_avg / 1e3) / 1e9
+    achieved = per_rank_bytes / tok_us / 1e3
+    # the tailored plan over the same ranks (each rank gathers its slice's rows
+    # from a full head it generates locally)
+    full = torch.empty((V, d), dtype=torch.bfloat16, device="cuda")
+    th._lib.call("svt_head_random", full.data_ptr(), th.SVT_BF16, th.SVT_BF16, 0, V * d,
+                 synth.SEED_W, None)
+    fhead = th.HeadMatrix(0, d, 2, th.SVT_BF16, data=full)
+    tb = th.TailoredBatch.select_only(synth.words_of(synth.static_ids(V, 2048), V), V,
+                                      [synth.prompt_ids(V, 512, 0)])
+    plan = tb.plan(0).active_ids
+    tailored = None
+    if use_nccl:
+        tdec = sharded.ShardedDecoder(fhead, comm, plan_ids=plan)
+        tout = torch.full((steps,), -1, dtype=torch.int32, device="cuda")
+        tms = timed(tdec.graph(hidden, tout).replay, args.steps, args.warmup)
+        tailored = {"plan_rows": int(plan.size), "tokens_per_s": tokens / (tms / 1e3),
+                    "us_per_token": tms * 1e3 / tokens, "per_rank_rows": tdec.n,
+                    "what": "select(2,048 static + 512-token prompt) plan, contiguous plan "
+                            "slices per rank, same graph-captured step"}
+    del full
     result = {
         "metric": METRIC, "value": tokens / (ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded splitmix64); random-init head",
-        "config": {"workload": CFG4["workload"], "V": V, "d": d, "batch": B,
+        "config": {"workload": CFG4["workload"], "V": V, "d": d, "batch": 1,
                    "decode_steps": steps, "parallelism": f"vocab-shard x{world}",
-                   "step": f"{steps} decode tokens; each = per-rank greedy over its row slice "
-                           "(certified split-K at batch 1, exact-order GEMV otherwise) -> exact "
-                           "(max, id) record -> NCCL all-gather -> combine",
+                   "step": f"{steps} decode tokens in one CUDA graph; each = svt_sharded_greedy: "
+                           "certified rows kernel over the rank's slice (exact (max, id) record) "
+                           "-> ncclAllGather -> combine",
                    "l2": "per-rank slice > L2 at G<=8 (1.18 GB / G), no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": ("svt_greedy_certified_rows (exact shard record)" if vs.shard.certified
-                                else "gemv_ring_kernel<bf16,ROWS,argmax> + finalize") +
-                               " + all-gather + combine",
-                     "bytes_per_launch": per_rank_bytes, "avg_launch_us": step_avg * 1e3,
+                     "kernel": "svt_sharded_greedy = rows_fast/greedy_rows kernel (exact shard "
+                               "record) + ncclAllGather + svt_shard_combine",
+                     "bytes_per_launch": per_rank_bytes, "avg_launch_us": tok_us,
+                     "timing": "CUDA events around graph replays; per token = time / tokens",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+        "tailored_plan": tailored,
         "gpu_launches": 3 * steps * args.steps, "clocks": clk.summary(),
     }
+    if comm is not None:
+        comm.close()
     if rank == 0 and not getattr(args, "quiet", False):
         print(json.dumps(result), flush=True)
     if dist is not None:
@@ -1402,8 +1435,10 @@ def secondary(args, torch, th, synth):
     a.quiet, a.steps, a.warmup, a.decode_steps, a.batch = True, 3, 2, 16, 1
     r = run_vocab_shard(a, torch, None, 1, 0)
     out["cfg4_g1"] = {"tokens_per_s": r["value"], "ms_per_token": r["ms_per_step"] / 16,
-                      "roofline": r["roofline"], "what": "full V=256,000 x 2,304 bf16 head, "
-                      "batch 1, one shard (G=1); G=2/4/8: --workload cfg4 under torchrun"}
+                      "roofline": r["roofline"], "tailored_plan": r["tailored_plan"],
+                      "what": "full V=256,000 x 2,304 bf16 head, batch 1, one shard (G=1), "
+                      "svt_sharded_greedy on a one-rank NCCL communicator, 16 steps per CUDA "
+                      "graph; G=2/4/8: --workload cfg4 under torchrun"}
     torch.cuda.empty_cache()
     a = copy.copy(args)
     a.quiet, a.sweep_sizes, a.sweep_batches, a.sweep_dtypes = True, "1024,16384,128256", "1,256", "bf16"

@@ -206,6 +206,22 @@ svt_status svt_logits_interleaved(const void* d_sub, svt_dtype dt, size_t dim,
                                   size_t hidden_ld, float* d_out, const int64_t* d_out_offsets,
                                   svt_stream stream);
 
+/* Top-k over each request's plan (north_star (d); the reference has argmax
+ * only, head.cpp:203-217). Defined as the k largest keys (value descending,
+ * ties to the lower plan row = lower id, -0.0 == +0.0, NaN rows after every
+ * number except a NaN at plan row 0, which ranks first when plan_start) —
+ * entry 0 is greedy_step's id. Input: exact logits in plan order (request b:
+ * d_logits[d_logit_offsets[b] + k], k < d_n_rows[b], e.g. from
+ * svt_logits_interleaved), so values are the reference's bit for bit.
+ * Output [batch][k]: global ids (through d_ids + d_id_offsets[b]; NULL:
+ * plan rows) and values; entries past a plan's size are 0xFFFFFFFF / NaN.
+ * 1 <= k <= 256. */
+svt_status svt_topk_logits(const float* d_logits, const int64_t* d_logit_offsets,
+                           const int64_t* d_n_rows, const uint32_t* d_ids,
+                           const int64_t* d_id_offsets, int32_t batch, int32_t k,
+                           int32_t plan_start, uint32_t* d_out_ids, float* d_out_vals,
+                           svt_stream stream);
+
 /* Single-plan greedy over a row-major sub-head (the exact greedy_step
  * signature shape: sub-head rows are the plan's rows in order, d_plan_ids
  * remaps the winner). d_out_id/d_out_max are single elements; d_workspace
@@ -481,6 +497,35 @@ svt_status svt_row_norms_bf16(const void* d_rows, int64_t nrows, int32_t dim, fl
  * contiguous and ascending. */
 svt_status svt_shard_combine(const void* d_records, int32_t shards, int32_t batch,
                              uint32_t* d_out_ids, float* d_out_max, svt_stream stream);
+
+/* Vocab-sharded greedy step over NCCL (SURVEY §8b "svt_sharded_greedy(...,
+ * ncclComm_t)", §8e). This rank holds a contiguous ascending slice of the
+ * plan: plan rows [row_base, row_base + n_rows) — rows of d_rows (row-major,
+ * head_rows of them) taken in place, or through d_src_ids (plan slice ids
+ * into a full head). d_plan_ids: the slice's global vocabulary ids (a
+ * tailored plan), or NULL for the identity plan (id = row_base + row).
+ * Batch 1 (BASELINE cfg4). One call = certified rows kernel with an exact
+ * shard record -> ncclAllGather of G 16-byte records on `nccl_comm`
+ * (ncclComm_t; NULL only when world == 1) -> svt_shard_combine; every rank
+ * gets the reference's id (head.cpp:203-217 over the whole plan) in
+ * d_out_id (and its exact logit in d_out_max, optional). Stream-ordered and
+ * graph-capturable; flags: SVT_ROWS_WEIGHTS_STABLE as for
+ * svt_greedy_certified_rows. Workspace: svt_sharded_workspace_bytes,
+ * 256-byte aligned, zeroed once before the first call. NCCL is resolved at
+ * run time (the process's loaded libnccl, else dlopen("libnccl.so.2")). */
+size_t svt_sharded_workspace_bytes(size_t n_rows, int32_t world);
+svt_status svt_sharded_greedy(const void* d_rows, svt_dtype dt, size_t head_rows, size_t dim,
+                              const uint32_t* d_src_ids, size_t n_rows, const float* d_hidden,
+                              const uint32_t* d_plan_ids, uint32_t row_base, int32_t flags,
+                              void* nccl_comm, int32_t world, uint32_t* d_out_id,
+                              float* d_out_max, void* d_workspace, svt_stream stream);
+/* Communicator plumbing for hosts without their own NCCL binding: rank 0
+ * makes the unique id (128 bytes), the host ships it to every rank, each
+ * rank initialises its communicator (one rank per GPU). */
+svt_status svt_nccl_get_unique_id(void* h_out, size_t bytes);
+svt_status svt_nccl_comm_init(void** out_comm, int32_t world, int32_t rank,
+                              const void* h_unique_id);
+svt_status svt_nccl_comm_destroy(void* comm);
 
 /* ------------------------------------------------------------------------
  * (e) Offloaded embedding lookup (the reference only models it:

@@ -86,6 +86,7 @@ class _COracle:
         L.orc_logits.argtypes = [_f32p, _sz, _sz, _f32p, _sz, _f32p]
         L.orc_greedy_step.argtypes = [_f32p, _sz, _sz, _f32p, _sz, _u32p, _sz, _P(C.c_uint32),
                                       _P(C.c_float)]
+        L.orc_topk.argtypes = [_f32p, _sz, _sz, _f32p, _sz, _u32p, _sz, _sz, _u32p, _f32p]
         L.orc_argmax_first.argtypes = [_f32p, _sz]
         L.orc_argmax_first.restype = _sz
         L.orc_memory_report.argtypes = [_sz, _sz, C.c_int, _sz] + [_P(C.c_uint64)] * 4 + [
@@ -216,6 +217,23 @@ class _COracle:
     def argmax_first(self, scores):
         s = np.ascontiguousarray(scores, np.float32)
         return self.L.orc_argmax_first(s, s.size)
+
+    def topk(self, sub, hidden, plan_ids, k):
+        """(ids, values) of the k best plan rows: value desc, id asc (not a
+        reference function; svt_oracle.c orc_topk)."""
+        sub = np.ascontiguousarray(sub, np.float32)
+        hidden = np.ascontiguousarray(hidden, np.float32)
+        plan_ids = np.ascontiguousarray(plan_ids, np.uint32)
+        rows, dim = sub.shape
+        ids = np.zeros(max(k, 1), np.uint32)
+        vals = np.zeros(max(k, 1), np.float32)
+        st = self.L.orc_topk(sub.reshape(-1) if sub.size else np.zeros(1, np.float32), rows, dim,
+                             hidden if hidden.size else np.zeros(1, np.float32), hidden.size,
+                             plan_ids if plan_ids.size else np.zeros(1, np.uint32), plan_ids.size,
+                             k, ids, vals)
+        if st:
+            raise OracleError(st)
+        return ids[:k], vals[:k]
 
     def memory_report(self, full, dim, dtype_bytes, plan):
         a, b, c, d = (C.c_uint64() for _ in range(4))

@@ -268,6 +268,49 @@ int orc_greedy_step(const float* sub, size_t rows, size_t dim, const float* hidd
     return orc_remap_out(plan_ids, plan_n, best, out_id); /* :216 */
 }
 
+/* top-k over a plan. NOT in the reference (it has the argmax scan only,
+ * head.cpp:212-215); defined per SURVEY Appendix A as a sort by (value desc,
+ * id asc), extended with the scan's NaN rules so that entry 0 is greedy_step's
+ * row: a NaN at plan row 0 ranks first (the scan never leaves row 0 then),
+ * every other NaN ranks after all numbers (the scan skips it), NaNs among
+ * themselves by lower row; -0.0 == +0.0 (IEEE compare). Selection by
+ * repeated scans over the reference-order logits (orc_logits). */
+static int topk_class(float v, size_t r) {
+    if (v != v) return r == 0 ? 2 : 0;
+    return 1;
+}
+static int topk_beats(const float* s, size_t a, size_t b) { /* a before b? */
+    const int ca = topk_class(s[a], a), cb = topk_class(s[b], b);
+    if (ca != cb) return ca > cb;
+    if (ca == 1 && s[a] != s[b]) return s[a] > s[b];
+    return a < b;
+}
+int orc_topk(const float* sub, size_t rows, size_t dim, const float* hidden, size_t hidden_len,
+             const uint32_t* plan_ids, size_t plan_n, size_t k, uint32_t* out_ids,
+             float* out_vals) {
+    if (rows != plan_n) return ORC_INTEGRITY;
+    float* s = (float*)malloc((rows ? rows : 1) * sizeof(float));
+    unsigned char* used = (unsigned char*)calloc(rows ? rows : 1, 1);
+    const int st = orc_logits(sub, rows, dim, hidden, hidden_len, s);
+    if (st) { free(s); free(used); return st; }
+    for (size_t j = 0; j < k; ++j) {
+        size_t best = rows;
+        for (size_t r = 0; r < rows; ++r)
+            if (!used[r] && (best == rows || topk_beats(s, r, best))) best = r;
+        if (best == rows) {
+            out_ids[j] = 0xFFFFFFFFu;
+            out_vals[j] = (float)NAN;
+            continue;
+        }
+        used[best] = 1;
+        out_ids[j] = plan_ids[best];
+        out_vals[j] = s[best];
+    }
+    free(s);
+    free(used);
+    return ORC_OK;
+}
+
 /* memory_report, head.cpp:219-237. */
 int orc_memory_report(size_t full_size, size_t dim, int dtype_bytes, size_t plan_size,
                       uint64_t* full_head, uint64_t* sub_head, uint64_t* emb_gpu,

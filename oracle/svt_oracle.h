@@ -87,6 +87,13 @@ int orc_greedy_step(const float* sub, size_t rows, size_t dim, const float* hidd
                     size_t hidden_len, const uint32_t* plan_ids, size_t plan_n,
                     uint32_t* out_id, float* out_max);
 
+/* top-k (value desc, id asc; NaN at plan row 0 first, other NaN last):
+ * NOT a reference function — defined per SURVEY Appendix A, entry 0 ==
+ * orc_greedy_step. Entries past `rows`: id 0xFFFFFFFF, NaN. */
+int orc_topk(const float* sub, size_t rows, size_t dim, const float* hidden, size_t hidden_len,
+             const uint32_t* plan_ids, size_t plan_n, size_t k, uint32_t* out_ids,
+             float* out_vals);
+
 /* argmax with the reference scan rule over a score vector (head.cpp:213-215). */
 size_t orc_argmax_first(const float* scores, size_t n);
 

@@ -123,6 +123,13 @@ _SIGS = {
     "svt_prefill_offsets": ([_i32, _i32, _vp], None),
     "svt_prefill_meta_offset": ([_i32, _i32], _i64),
     "svt_shard_combine": ([_vp, _i32, _i32, _vp, _vp, _vp], C.c_int),
+    "svt_topk_logits": ([_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp], C.c_int),
+    "svt_sharded_workspace_bytes": ([_sz, _i32], _sz),
+    "svt_sharded_greedy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _u32, _i32, _vp, _i32,
+                            _vp, _vp, _vp, _vp], C.c_int),
+    "svt_nccl_get_unique_id": ([_vp, _sz], C.c_int),
+    "svt_nccl_comm_init": ([C.POINTER(_vp), _i32, _i32, _vp], C.c_int),
+    "svt_nccl_comm_destroy": ([_vp], C.c_int),
     "svt_embed_lookup_zero_copy": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_embed_lookup_staged": ([_vp, C.c_int, _sz, _sz, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_session_create": ([C.POINTER(_vp), _vp, C.c_int, _sz, _sz, _i32, _i64, _vp], C.c_int),

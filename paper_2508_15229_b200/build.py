@@ -62,7 +62,7 @@ def build_svt(force=False):
         with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
             list(ex.map(compile_one, todo))
     if force or todo or _stale(out, objs):
-        _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", *objs, "-o", out, "-lcudart", "-ldl"])
     return out
 
 

@@ -831,6 +831,18 @@ class TailoredBatch:
                  self.act_off.data_ptr(), _stream(self.stream))
         return out
 
+    def topk(self, hidden: torch.Tensor, k: int, fused: bool = False):
+        """Top-k per request (svt_topk_logits over the exact logits): ids
+        [B, k] (global, remapped through the plans) and values [B, k], value
+        descending, ties to the lower id; entry 0 == greedy()'s id."""
+        lg = self.logits(hidden, fused=fused)
+        ids = torch.empty((self.B, k), dtype=torch.int32, device="cuda")
+        vals = torch.empty((self.B, k), dtype=torch.float32, device="cuda")
+        call("svt_topk_logits", lg.data_ptr(), self.act_off.data_ptr(), self.n_active.data_ptr(),
+             self.active.data_ptr(), self.act_off.data_ptr(), self.B, k, 1, ids.data_ptr(),
+             vals.data_ptr(), _stream(self.stream))
+        return ids, vals
+
     def algorithmic_decode_bytes(self, esize: int, dim: int) -> int:
         """Bytes one decode step must move: Σ_b |S_b|·d·b_W
         + d·4 (hidden) + 8 (id + max out)."""

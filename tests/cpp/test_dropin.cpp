@@ -252,6 +252,38 @@ TEST_CASE("head: greedy step decodes through the plan") {
     }
 }
 
+TEST_CASE("head: top-k extension (value desc, id asc; element 0 == greedy_step)") {
+    HeadMatrix sub(5, 1, 4);
+    sub.at(0, 0) = 1.0f;
+    sub.at(1, 0) = 3.0f;
+    sub.at(2, 0) = 2.0f;
+    sub.at(3, 0) = 3.0f;  // ties row 1: the lower id first
+    sub.at(4, 0) = -1.0f;
+    const SelectionPlan plan = plan_of({0, 2, 4, 6, 9}, 16);
+    const auto top = topk_step(sub, std::vector<float>{1.0f}, plan, 4);
+    CHECK((top == std::vector<TokenId>{2, 6, 4, 0}));
+    CHECK(topk_step(sub, std::vector<float>{1.0f}, plan, 9).size() == 5);
+    CHECK_THROWS_AS(topk_step(sub, std::vector<float>{1.0f}, plan, 0), ConfigError);
+    std::mt19937_64 rng(0x70CC);
+    for (int it = 0; it < 50; ++it) {
+        const HeadMatrix head = HeadMatrix::random(300, 16, rng());
+        std::vector<TokenId> picked;
+        for (TokenId r = 0; r < 300; ++r)
+            if (rng() & 1) picked.push_back(r);
+        if (picked.empty()) continue;
+        const SelectionPlan p = plan_of(picked, 300);
+        const auto h = rand_hidden(rng, 16);
+        const HeadMatrix g = gather(head, p);
+        const auto k = topk_step(g, h, p, 8);
+        CHECK(k.front() == greedy_step(g, h, p));
+        const auto lg = logits(g, h);
+        for (std::size_t j = 1; j < k.size(); ++j) {
+            const float a = lg[*p.global_to_local(k[j - 1])], b = lg[*p.global_to_local(k[j])];
+            CHECK((a > b || (a == b && k[j - 1] < k[j])));
+        }
+    }
+}
+
 TEST_CASE("head: memory report arithmetic") {
     const MemoryReport r = memory_report(128000, 2048, 2, 105);
     CHECK(r.sub_head_bytes == 430080);

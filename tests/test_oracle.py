@@ -205,3 +205,66 @@ def test_offload_model_matches_reference():
     for h in range(0, 0x10000, 7):
         assert orc.half_to_float(h) == ref.half_to_float(h) or (
             np.isnan(orc.half_to_float(h)) and np.isnan(ref.half_to_float(h)))
+
+
+# ---- top-k (north_star (d); defined, not in the reference) --------------------
+def _topk_brute(scores, ids, k):
+    """(value desc, id asc) with the scan's NaN rules, by Python sorting."""
+    s = np.asarray(scores, np.float32)
+
+    def rank(r):
+        v = float(s[r])
+        if np.isnan(v):
+            return (2, 0.0, r) if r == 0 else (0, 0.0, r)
+        return (1, v + 0.0, r)  # -0.0 == +0.0
+
+    order = sorted(range(len(s)), key=lambda r: (-rank(r)[0], -rank(r)[1], r))
+    return [int(ids[r]) for r in order[:k]]
+
+
+def _score_cases(rng):
+    yield rng.uniform(-1, 1, 300).astype(np.float32)
+    yield np.round(rng.uniform(-3, 3, 200)).astype(np.float32)  # many exact ties
+    s = rng.uniform(-1, 1, 50).astype(np.float32)
+    s[[0, 7]] = np.nan
+    yield s
+    s = rng.uniform(-1, 1, 50).astype(np.float32)
+    s[[3, 9, 11]] = np.nan
+    yield s
+    yield np.array([-0.0, 0.0, -0.0, -1.0, np.inf, -np.inf, np.inf], np.float32)
+    yield np.full(5, np.nan, np.float32)
+
+
+def test_topk_definition_brute_force_and_top1_is_greedy():
+    rng = np.random.default_rng(17)
+    for s in _score_cases(rng):
+        n = s.size
+        ids = np.sort(rng.choice(10 * n, n, replace=False)).astype(np.uint32)
+        # an identity "head" whose logits are exactly the scores: row r = e_r * s_r
+        W = np.zeros((n, n), np.float32)
+        W[np.arange(n), np.arange(n)] = s
+        h = np.ones(n, np.float32)
+        sc = orc.logits(W, h)
+        for k in (1, 3, n, n + 4):
+            got, vals = orc.topk(W, h, ids, k)
+            want = _topk_brute(sc, ids, k)
+            assert got[:len(want)].tolist() == want, (k, s)
+            assert all(x == 0xFFFFFFFF for x in got[len(want):])
+            assert got[0] == orc.greedy_step(W, h, ids)[0]
+            for j, gid in enumerate(want):
+                r = int(np.searchsorted(ids, gid))
+                assert bits([vals[j]])[0] == bits([sc[r]])[0]
+
+
+@needs_ref
+def test_topk_top1_matches_reference_greedy():
+    ref = ref_lib()
+    rng = np.random.default_rng(23)
+    for _ in range(40):
+        V, d = int(rng.integers(2, 2000)), int(rng.integers(1, 64))
+        W = orc.head_random(V, d, int(rng.integers(0, 2**62)))
+        plan = np.sort(rng.choice(V, int(rng.integers(1, V + 1)), replace=False)).astype(np.uint32)
+        h = rng.uniform(-1, 1, d).astype(np.float32)
+        sub = orc.gather(W, plan)
+        ids, _ = orc.topk(sub, h, plan, 5)
+        assert ids[0] == ref.greedy_step(sub, h, plan)
