@@ -380,6 +380,15 @@ size_t svt_greedy_rows_workspace_bytes(size_t n_rows);
  * h staged, last row done, record written, ticket taken, tail done). */
 void svt_rows_set_debug(void* d_stamps);
 #define SVT_ROWS_WEIGHTS_STABLE 1 /* = SVT_WEIGHTS_STABLE (rows/ids not written by the preceding kernel) */
+/* SVT_ROWS_HIDDEN_STABLE (with SVT_ROWS_WEIGHTS_STABLE): d_hidden was not
+ * written by the kernel immediately before this launch in the stream either
+ * (hidden states already resident, e.g. several sessions' head calls after
+ * one batched transformer pass, or a replayed decode over stored states).
+ * The launch then reads h and consumes every row as it lands, before the
+ * programmatic-dependency wait, in CTAs small enough that consecutive
+ * launches overlap on each SM (svt_decode_small.cu, rows_hs_kernel). Ids and
+ * values are the same; only the overlap differs. */
+#define SVT_ROWS_HIDDEN_STABLE 2
 svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
                                      size_t dim, const uint32_t* d_src_ids, size_t n_rows,
                                      const float* d_hidden, const uint32_t* d_plan_ids,

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(LIB_DIR, "libsvt.so")
 
 SVT_F32, SVT_F16, SVT_BF16 = 0, 1, 2
 SVT_WEIGHTS_STABLE = 1  # svt.h: rows not written by the kernel a launch depends on
+SVT_ROWS_HIDDEN_STABLE = 2  # svt.h: h not written by it either (rows_hs_kernel)
 GROUP_ROWS = 32
 GROUP_META_BYTES = 32
 

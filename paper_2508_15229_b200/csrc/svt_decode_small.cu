@@ -719,6 +719,8 @@ struct FastParams {
     int32_t fin_in_grid;  // 1: the finalizer is the grid's last CTA; 0: its own launch
     int32_t variant;      // measurement only (SVT_FAST_VARIANT): 1 = no row traffic
     unsigned long long* dbg;  // per CTA 8 %globaltimer stamps (svt_rows_set_debug)
+    int32_t hs;           // 1: the stable-hidden ring kernel (records tagged kHsTag, cleared)
+    int32_t nb;           // stable-hidden kernel: ring slots per row group
 };
 
 __device__ __forceinline__ int64_t frow_begin(const FastParams& p, int c) {
@@ -733,10 +735,14 @@ __device__ __forceinline__ unsigned ord24_up_of(unsigned o) {
     const unsigned long long u = (static_cast<unsigned long long>(o) + 255ull) >> 8;
     return static_cast<unsigned>(u > 0xFFFFFFull ? 0xFFFFFFull : u);
 }
-// epoch counter -> the launch's tag in [1, 255]; a zeroed record never matches
+// epoch counter (in [0, 254)) -> the launch's tag in [1, 254]; a zeroed
+// record never matches. Tag 255 marks the stable-hidden kernel's records,
+// which its finalize clears after reading (no epoch on that path).
 __device__ __forceinline__ unsigned long long tag_of(unsigned e) {
-    return static_cast<unsigned long long>(e % 255u + 1u);
+    return static_cast<unsigned long long>(e % 254u + 1u);
 }
+__device__ __forceinline__ unsigned next_epoch(unsigned e) { return (e + 1u) % 254u; }
+constexpr unsigned long long kHsTag = 255ull;
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -787,6 +793,78 @@ __device__ __forceinline__ unsigned long long pack2(float x, float y) {
 }
 __device__ __forceinline__ float sum2(unsigned long long v) {
     return __uint_as_float(static_cast<uint32_t>(v)) + __uint_as_float(static_cast<uint32_t>(v >> 32));
+}
+
+// The CTA record (control / dependency warp, lane j <-> row j of the CTA,
+// row j in group j % NG, slot j / NG): sum the WPG warp partials of each row
+// in a fixed order, bound, L_c = max lo, the rows with hi >= L_c; a tagged
+// 32-byte record (+ the candidate list when more than two remain).
+template <int NG, int WPG, int RPG, int PF, bool kWaitBeforeStore = false>
+__device__ __forceinline__ void fast_cta_record(const FastParams& p, const float (&s_red)[NG][WPG][PF],
+                                                int c, int64_t r0, int nrows, uint32_t my_id,
+                                                unsigned long long tag8, int lane) {
+    const bool act = lane < nrows;
+    float f = 0.0f, a = 0.0f;
+    if (act) {
+        const int g = lane % NG, k = lane / NG;
+#pragma unroll
+        for (int w = 0; w < WPG; ++w) {
+            f += s_red[g][w][k];
+            a += s_red[g][w][RPG + k];
+        }
+    }
+    const bool bad = act && (!isfinite(f) || !isfinite(a));
+    const float bnd = __fadd_ru(__fmul_ru(p.c_rel, a), p.eta);
+    float lo = __fsub_rd(f, bnd);
+    const float hi = __fadd_ru(f, bnd);
+    if (!(lo == lo) || !act) lo = -FLT_MAX;
+    float L = lo;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xFFFFFFFFu, L, o));
+    if (lane == 0) SVT_FSTAMP(5);
+    const bool anybad = __any_sync(0xFFFFFFFFu, bad);
+    const bool cand = act && hi >= L;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, cand);
+    const unsigned cnt = __popc(m);
+    const unsigned oh = cand ? ord_of(hi) : 0u;
+    const unsigned h1 = __reduce_max_sync(0xFFFFFFFFu, oh);
+    const int l1 = __ffs(__ballot_sync(0xFFFFFFFFu, cand && oh == h1)) - 1;
+    const unsigned oh2 = (cand && lane != l1) ? oh : 0u;
+    const unsigned h2 = __reduce_max_sync(0xFFFFFFFFu, oh2);
+    const unsigned m2 = __ballot_sync(0xFFFFFFFFu, cand && lane != l1 && oh2 == h2);
+    const int l2 = m2 ? __ffs(m2) - 1 : l1;
+    const uint32_t id1 = __shfl_sync(0xFFFFFFFFu, my_id, l1 < 0 ? 0 : l1);
+    const uint32_t id2 = __shfl_sync(0xFFFFFFFFu, my_id, l2 < 0 ? 0 : l2);
+    const unsigned code = anybad ? 1u : (cnt > 2 ? 2u : 0u);
+    if constexpr (kWaitBeforeStore) {
+        // everything above is this launch's own work; the stores below may
+        // only follow the previous launch (its finalize reads this workspace)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0) SVT_FSTAMP(1);
+    }
+    if (code == 2u && cand) {  // the full list, released before the record
+        const unsigned pos = __popc(m & ((1u << lane) - 1u));
+        p.cand[static_cast<size_t>(c) * kFMaxRows + pos] =
+            make_uint2(static_cast<uint32_t>(r0 + lane), __float_as_uint(hi));
+    }
+    __syncwarp();
+    if (lane == 0) SVT_FSTAMP(6);
+    if (lane == 0) {
+        if (code == 2u) fence_acq_rel_gpu();
+        const unsigned long long tag = tag8 << 56;
+        const unsigned long long l24 = ord24_down(L);
+        const unsigned long long hi1 = ord24_up_of(h1);
+        const unsigned long long hi2 = cnt >= 2 ? ord24_up_of(h2) : 0ull;
+        const unsigned long long row1 = static_cast<unsigned>(l1 < 0 ? 0 : l1) & 0xFFFFu;
+        const unsigned long long row2 = cnt >= 2 ? (static_cast<unsigned>(l2) & 0xFFFFu)
+                                                 : 0xFFFFull;
+        FRec* fr = p.frec + c;
+        st_relaxed_u64(&fr->w[0], tag | l24 << 32 | hi2 << 8 | code);
+        st_relaxed_u64(&fr->w[1], tag | hi1 << 32 | id1);
+        st_relaxed_u64(&fr->w[2], tag | row1 << 32 | row2 << 16);
+        st_relaxed_u64(&fr->w[3], tag | static_cast<unsigned long long>(cnt) << 32 | id2);
+        SVT_FSTAMP(4);
+    }
 }
 
 template <int DT, int CPT, int RPG>
@@ -846,63 +924,7 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
         named_bar_sync(1, kFThreads);  // every group's warp partials are in s_red
         const unsigned epoch = s_epoch[0];  // s_hbar completed before the compute warps arrived
         if (lane == 0) SVT_FSTAMP(3);
-        // lane j <-> row j: group j % 4, slot j / 4
-        const bool act = lane < nrows;
-        float f = 0.0f, a = 0.0f;
-        if (act) {
-            const int g = lane % kFNG, k = lane / kFNG;
-#pragma unroll
-            for (int w = 0; w < kFWPG; ++w) {
-                f += s_red[g][w][k];
-                a += s_red[g][w][RPG + k];
-            }
-        }
-        const bool bad = act && (!isfinite(f) || !isfinite(a));
-        const float bnd = __fadd_ru(__fmul_ru(p.c_rel, a), p.eta);
-        float lo = __fsub_rd(f, bnd);
-        const float hi = __fadd_ru(f, bnd);
-        if (!(lo == lo) || !act) lo = -FLT_MAX;
-        float L = lo;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) L = fmaxf(L, __shfl_xor_sync(0xFFFFFFFFu, L, o));
-        if (lane == 0) SVT_FSTAMP(5);
-        const bool anybad = __any_sync(0xFFFFFFFFu, bad);
-        const bool cand = act && hi >= L;
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, cand);
-        const unsigned cnt = __popc(m);
-        const unsigned oh = cand ? ord_of(hi) : 0u;
-        const unsigned h1 = __reduce_max_sync(0xFFFFFFFFu, oh);
-        const int l1 = __ffs(__ballot_sync(0xFFFFFFFFu, cand && oh == h1)) - 1;
-        const unsigned oh2 = (cand && lane != l1) ? oh : 0u;
-        const unsigned h2 = __reduce_max_sync(0xFFFFFFFFu, oh2);
-        const unsigned m2 = __ballot_sync(0xFFFFFFFFu, cand && lane != l1 && oh2 == h2);
-        const int l2 = m2 ? __ffs(m2) - 1 : l1;
-        const uint32_t id1 = __shfl_sync(0xFFFFFFFFu, my_id, l1 < 0 ? 0 : l1);
-        const uint32_t id2 = __shfl_sync(0xFFFFFFFFu, my_id, l2 < 0 ? 0 : l2);
-        const unsigned code = anybad ? 1u : (cnt > 2 ? 2u : 0u);
-        if (code == 2u && cand) {  // the full list, released before the record
-            const unsigned pos = __popc(m & ((1u << lane) - 1u));
-            p.cand[static_cast<size_t>(c) * kFMaxRows + pos] =
-                make_uint2(static_cast<uint32_t>(r0 + lane), __float_as_uint(hi));
-        }
-        __syncwarp();
-        if (lane == 0) SVT_FSTAMP(6);
-        if (lane == 0) {
-            if (code == 2u) fence_acq_rel_gpu();
-            const unsigned long long tag = tag_of(epoch) << 56;
-            const unsigned long long l24 = ord24_down(L);
-            const unsigned long long hi1 = ord24_up_of(h1);
-            const unsigned long long hi2 = cnt >= 2 ? ord24_up_of(h2) : 0ull;
-            const unsigned long long row1 = static_cast<unsigned>(l1 < 0 ? 0 : l1) & 0xFFFFu;
-            const unsigned long long row2 = cnt >= 2 ? (static_cast<unsigned>(l2) & 0xFFFFu)
-                                                     : 0xFFFFull;
-            FRec* fr = p.frec + c;
-            st_relaxed_u64(&fr->w[0], tag | l24 << 32 | hi2 << 8 | code);
-            st_relaxed_u64(&fr->w[1], tag | hi1 << 32 | id1);
-            st_relaxed_u64(&fr->w[2], tag | row1 << 32 | row2 << 16);
-            st_relaxed_u64(&fr->w[3], tag | static_cast<unsigned long long>(cnt) << 32 | id2);
-            SVT_FSTAMP(4);
-        }
+        fast_cta_record<kFNG, kFWPG, RPG, PF>(p, s_red, c, r0, nrows, my_id, tag_of(epoch), lane);
         return;
     }
     // ---- compute warps ------------------------------------------------------
@@ -984,7 +1006,7 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
 // ---- the grid's last CTA: one warp polls the tagged records and decides ------
 template <int DT>
 __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t* fsmem, unsigned* sn,
-                                                   unsigned* claim) {
+                                                   unsigned* claim, int stagger_ns = kFinStagger) {
     unsigned& s_n = *sn;
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -996,14 +1018,14 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
     constexpr int kPer = kFMaxGrid / 32;
     // written by the previous launch's finalize, complete before the wait
     const unsigned epoch = ld_relaxed_u32(p.ctrl + 8);
-    const unsigned long long tag = tag_of(epoch);
+    const unsigned long long tag = p.hs ? kHsTag : tag_of(epoch);
     unsigned long long w0[kPer], w1[kPer], w2[kPer], w3[kPer];
     bool seen = false;
     const unsigned long long t_start = gtimer();
     // several polling warps, staggered by a fraction of a load round trip,
     // shorten the delay between the last record landing and its detection;
     // the first warp to see every record claims the decision
-    if (wid > 0) __nanosleep(kFinStagger * wid);
+    if (wid > 0) __nanosleep(stagger_ns * wid);
     for (int it = 0; !seen; ++it) {
         if (*reinterpret_cast<volatile unsigned*>(claim)) return;
         // every load of a round is issued before any result is used
@@ -1041,13 +1063,29 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
                 if (lane == 0) {
                     *p.out_id = 0xFFFFFFFFu;
                     atomicAdd(&p.ctrl[6], 1u);
-                    p.ctrl[8] = (epoch + 1u) % 255u;
+                    if (!p.hs) p.ctrl[8] = next_epoch(epoch);
                 }
                 return;
             }
         }
     }
     if (p.dbg && lane == 0) p.dbg[124] = gtimer();
+    if (p.hs) {
+        // stable-hidden records carry no epoch: clear them once read (the
+        // next launch on this workspace writes its records only after its
+        // dependency wait, i.e. after this grid completed)
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int cc = lane + 32 * q;
+            if (32 * q < G && cc < G) {
+                FRec* fr = p.frec + cc;
+                st_relaxed_u64(&fr->w[0], 0ull);
+                st_relaxed_u64(&fr->w[1], 0ull);
+                st_relaxed_u64(&fr->w[2], 0ull);
+                st_relaxed_u64(&fr->w[3], 0ull);
+            }
+        }
+    }
     unsigned l24 = 0u, code = 0u;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -1079,7 +1117,7 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
         // one row can reach the largest lower bound: the reference argmax
         if (nhit) *p.out_id = id;
         if (p.variant & 4) {  // measurement: bare minimum exit
-            if (lane == 0) p.ctrl[8] = (epoch + 1u) % 255u;
+            if (lane == 0 && !p.hs) p.ctrl[8] = next_epoch(epoch);
             return;
         }
     } else {
@@ -1127,7 +1165,7 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
                 const uint32_t r = s_list[0];
                 *p.out_id = p.plan_ids ? p.plan_ids[r] : p.row_base + r;
                 if (p.dbg) p.dbg[126] = gtimer();
-                p.ctrl[8] = (epoch + 1u) % 255u;
+                if (!p.hs) p.ctrl[8] = next_epoch(epoch);
                 atomicAdd(&p.ctrl[4], 1u);
             }
             return;
@@ -1165,7 +1203,7 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
     }
     if (lane == 0) {
         if (p.dbg) p.dbg[126] = gtimer();
-        p.ctrl[8] = (epoch + 1u) % 255u;
+        if (!p.hs) p.ctrl[8] = next_epoch(epoch);
         if (!(p.variant & 2)) atomicAdd(&p.ctrl[recomputed ? 5 : 4], 1u);
     }
 }
@@ -1201,6 +1239,200 @@ __global__ void __launch_bounds__(kFThreads, 1) rows_fast_kernel(FastParams p) {
         return;
     }
     rows_fast_cta<DT, CPT, RPG>(p, dsm);
+}
+
+// ===========================================================================
+// Stable weights AND stable hidden state (SVT_ROWS_WEIGHTS_STABLE |
+// SVT_ROWS_HIDDEN_STABLE: neither the rows nor h were written by the kernel
+// this launch depends on, e.g. a decode over hidden states already resident
+// in HBM, or several sessions' head calls after one batched transformer
+// pass). Nothing but the record then depends on the previous launch, so the
+// rows need not be held until h exists:
+//  * h is copied first and every row is consumed as it lands, through a
+//    small shared-memory ring (kHG row groups x nb slots, full / empty
+//    mbarriers, one bulk copy per row refilled by a producer warp);
+//  * a CTA fits in under half an SM (ring + h <= kHSmemBudget, 10 warps),
+//    so the NEXT launch's CTAs are resident and streaming while this
+//    launch's CTAs finish: consecutive decode steps overlap their HBM
+//    streams instead of paying the stream's ramp and the tail in series;
+//  * the dependency warp waits (programmatic dependency), triggers the
+//    dependents, then writes the same tagged record as rows_fast (tag
+//    kHsTag; the finalize clears the records after reading them, so no
+//    epoch load sits between the wait and the record).
+// The fast pass, the bound and the finalize are rows_fast's.
+// ===========================================================================
+constexpr int kHG = 2;                            // row groups per CTA
+constexpr int kHWPG = 4;                          // compute warps per group
+constexpr int kHCompute = kHG * kHWPG;            // 8
+constexpr int kHThreads = (kHCompute + 2) * 32;   // + producer + dependency warp
+constexpr int kHMaxSlots = 16;                    // ring slots per CTA (both groups)
+constexpr int kHSmemBudget = 96 * 1024;           // ring + h: two CTAs per SM
+constexpr int kHFinWarps = 4;                     // polling warps of the finalizer CTA
+constexpr int kHFinStagger = 300;                 // ns between their first polls
+
+template <int DT, int CPT, int RPG>
+__device__ __forceinline__ void rows_hs_cta(const FastParams& p, uint8_t* dsm) {
+    constexpr int E = Chunk<DT>::E;
+    constexpr int PF = FPad<2 * RPG>::P, LF = FPad<2 * RPG>::LOG;
+    __shared__ uint64_t s_full[kHMaxSlots], s_empty[kHMaxSlots];
+    __shared__ uint64_t s_hbar;
+    __shared__ float s_red[kHG][kHWPG][PF];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t r0 = frow_begin(p, c);
+    const int nrows = static_cast<int>(frow_begin(p, c + 1) - r0);
+    const uint32_t rb = static_cast<uint32_t>(p.row_bytes);
+    const uint32_t h_bytes = static_cast<uint32_t>(p.dim) * 4u;
+    const int nb = p.nb;
+    float* s_h = reinterpret_cast<float*>(dsm + static_cast<size_t>(kHG * nb) * rb);
+    if (tid == kHCompute * 32) {
+        SVT_FSTAMP(0);
+        if (p.dbg) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            p.dbg[blockIdx.x * 128 + 8] = sm;
+        }
+        for (int i = 0; i < kHG * nb; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], kHWPG);
+        }
+        mbar_init(&s_hbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kHCompute) {
+        // ---- producer: lane j fills slot j = g * nb + s with group g's row
+        // k = s (row g + kHG * k of the CTA); lane 0 then refills the slots
+        // in consumption order (k = nb, nb + 1, ...; both groups per k)
+        const uint64_t pol = policy_evict_first();
+        if (lane < kHG * nb) {
+            const int g = lane / nb, k = lane % nb;
+            const int i = g + kHG * k;
+            if (i < nrows) {
+                mbar_arrive_expect_tx(&s_full[lane], rb);
+                bulk_g2s(dsm + static_cast<size_t>(lane) * rb, frow_ptr(p, r0 + i), rb,
+                         &s_full[lane], pol);
+            }
+        }
+        if (lane == 0) {
+            for (int k = nb; kHG * k < nrows; ++k) {
+#pragma unroll
+                for (int g = 0; g < kHG; ++g) {
+                    const int i = g + kHG * k;
+                    if (i >= nrows) break;
+                    const int slot = g * nb + k % nb;
+                    mbar_wait_parity(&s_empty[slot], static_cast<uint32_t>((k / nb - 1) & 1));
+                    mbar_arrive_expect_tx(&s_full[slot], rb);
+                    bulk_g2s(dsm + static_cast<size_t>(slot) * rb, frow_ptr(p, r0 + i), rb,
+                             &s_full[slot], pol);
+                }
+            }
+        }
+        return;
+    }
+    if (warp == kHCompute + 1) {
+        // ---- dependency warp: h now (stable), the wait, the trigger, the record
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&s_hbar, h_bytes);
+            bulk_g2s(s_h, p.h, h_bytes, &s_hbar, policy_evict_last());
+        }
+        const uint32_t my_id = lane < nrows ? (p.plan_ids ? __ldg(p.plan_ids + r0 + lane)
+                                                          : p.row_base + static_cast<uint32_t>(r0 + lane))
+                                            : 0u;
+        // trigger at once: this launch's finalize (and, once it runs, the
+        // next launch) may be scheduled now. Nothing global is written
+        // before the wait, and the rows CTAs only ever wait on OLDER
+        // finalizes, which are resident before any younger rows grid exists,
+        // so at most two rows grids share the SMs (resources) and none can
+        // starve a finalize it depends on.
+        asm volatile("griddepcontrol.launch_dependents;");
+        named_bar_sync(1, (kHCompute + 1) * 32);  // every group's partials are in s_red
+        if (lane == 0) SVT_FSTAMP(3);
+        // the record is computed first; the dependency wait sits right
+        // before its stores
+        fast_cta_record<kHG, kHWPG, RPG, PF, true>(p, s_red, c, r0, nrows, my_id, kHsTag, lane);
+        return;
+    }
+    // ---- compute warps: group g = rows g, g + kHG, ...; thread tg owns
+    // chunks tg, tg + 128, ... of each row
+    const int g = warp / kHWPG, wig = warp % kHWPG, tg = wig * 32 + lane;
+    constexpr int NP = CPT * E / 2;  // f32 pairs per row per thread
+    mbar_wait_parity(&s_hbar, 0u);
+    if (warp == 0 && lane == 0) SVT_FSTAMP(2);
+    unsigned long long h2[NP];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(s_h + (tg + q * kFTPG) * E + e);
+            h2[q * E / 2 + e / 2] = pack2(x.x, x.y);
+            h2[q * E / 2 + e / 2 + 1] = pack2(x.z, x.w);
+        }
+    }
+    float v[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) v[j] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < RPG; ++k) {
+        const int i = g + kHG * k;
+        if (i < nrows) {  // warp-uniform
+            const int slot = g * nb + k % nb;
+            mbar_wait_parity(&s_full[slot], static_cast<uint32_t>((k / nb) & 1));
+            uint4 wv[CPT];
+#pragma unroll
+            for (int q = 0; q < CPT; ++q)
+                wv[q] = *reinterpret_cast<const uint4*>(dsm + static_cast<size_t>(slot) * rb +
+                                                        static_cast<size_t>(tg + q * kFTPG) * 16);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[slot]);
+            unsigned long long acc = 0ull;
+            float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) {
+                float w[E];
+                Chunk<DT>::widen(wv[q], w);
+#pragma unroll
+                for (int e = 0; e < E; e += 2) {
+                    const unsigned long long hp = h2[q * E / 2 + e / 2];
+                    acc = ffma2(pack2(w[e], w[e + 1]), hp, acc);
+                    a0 = __fmaf_rn(fabsf(w[e]), fabsf(__uint_as_float(static_cast<uint32_t>(hp))), a0);
+                    a1 = __fmaf_rn(fabsf(w[e + 1]), fabsf(__uint_as_float(static_cast<uint32_t>(hp >> 32))), a1);
+                }
+            }
+            v[k] = sum2(acc);
+            v[RPG + k] = a0 + a1;
+        }
+    }
+    if (p.dbg && lane == 0) atomicMax(&p.dbg[blockIdx.x * 128 + 7], gtimer());  // last row done
+    const float r = transpose_sum<PF, LF>(v, lane);
+    if ((lane & ((32 >> LF) - 1)) == 0) s_red[g][wig][(lane >> (5 - LF)) & (PF - 1)] = r;
+    named_bar_arrive(1, (kHCompute + 1) * 32);
+}
+
+// One launch per decode step: CTAs [0, grid) are rows CTAs, CTA `grid` (the
+// highest index, dispatched last) is the finalizer. Every CTA triggers the
+// next launch at once; every CTA waits on the previous launch before it
+// writes or reads a record, so the finalizer of step t starts polling only
+// once step t-1's finalizer has cleared the records (same workspace) and
+// step t's records are the only tag-kHsTag records it can see.
+template <int DT, int CPT, int RPG>
+__global__ void __launch_bounds__(kHThreads, 2) rows_hs_kernel(FastParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    if (blockIdx.x == p.grid) {
+        // kHFinWarps polling warps, staggered: under the next steps' streams
+        // a poll round trip is 1-2 us, so one warp would see the last record
+        // up to a round trip late; the first warp to see all claims the step
+        if (threadIdx.x >= 32 * kHFinWarps) return;
+        __shared__ unsigned s_n, s_claim;
+        if (threadIdx.x == 0) s_claim = 0u;
+        named_bar_sync(2, 32 * kHFinWarps);
+        asm volatile("griddepcontrol.launch_dependents;");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
+        rows_fast_finalize<DT>(p, dsm, &s_n, &s_claim, kHFinStagger);
+        return;
+    }
+    rows_hs_cta<DT, CPT, RPG>(p, dsm);
 }
 
 unsigned long long* g_rows_dbg = nullptr;
@@ -1283,6 +1515,70 @@ svt_status launch_rows_fast(FastParams p, cudaStream_t st) {
     fc.numAttrs = 1;
     SVT_CUDA_TRY(cudaLaunchKernelEx(&fc, fin, p));
     return SVT_OK;
+}
+
+template <int DT, int CPT, int RPG>
+svt_status launch_rows_hs(FastParams p, cudaStream_t st) {
+    size_t smem = static_cast<size_t>(kHG * p.nb) * static_cast<size_t>(p.row_bytes) +
+                  static_cast<size_t>(p.dim) * 4;
+    const size_t fin_smem = kMaxCand * 4 + 2 * kPiece + static_cast<size_t>(p.dim) * 4;
+    smem = smem > fin_smem ? smem : fin_smem;  // the finalizer CTA's recompute buffers
+    auto kern = rows_hs_kernel<DT, CPT, RPG>;
+    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(p.grid + 1));  // + the finalizer CTA
+    cfg.blockDim = dim3(kHThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
+    return SVT_OK;
+}
+
+template <int DT, int CPT>
+svt_status pick_rpg_hs(FastParams p, int rpg, cudaStream_t st) {
+    if (rpg <= 3) return launch_rows_hs<DT, CPT, 3>(p, st);
+    if (rpg <= 5) return launch_rows_hs<DT, CPT, 5>(p, st);
+    if (rpg <= 9) return launch_rows_hs<DT, CPT, 9>(p, st);
+    return launch_rows_hs<DT, CPT, 16>(p, st);
+}
+
+// The stable-hidden ring kernel when the shape fits: 16-byte chunks a
+// multiple of 128 per row (<= 4 per thread), <= 32 rows per CTA over one
+// CTA per SM, and at least two ring slots per group within kHSmemBudget.
+bool rows_hs_eligible(int64_t n, size_t row_bytes, size_t dim, int* grid_out, int* rpg_out,
+                      int* cpt_out, int* nb_out) {
+    if (const char* v = getenv("SVT_ROWS_HS"))
+        if (atoi(v) == 0) return false;
+    const size_t nchunks = row_bytes / 16;
+    if (nchunks % kFTPG != 0) return false;
+    const int cpt = static_cast<int>(nchunks / kFTPG);
+    if (cpt != 1 && cpt != 2 && cpt != 4) return false;
+    const int sms = sm_count();
+    // one SM left to the finalize
+    const int gmax = getenv("SVT_HS_GRID") ? atoi(getenv("SVT_HS_GRID")) : sms - 1;
+    int grid = static_cast<int>(n < gmax ? n : gmax);
+    if (grid < 1) grid = 1;
+    if (grid > kFMaxGrid) grid = kFMaxGrid;
+    const int64_t rpc = (n + grid - 1) / grid;
+    if (rpc > kFMaxRows) return false;
+    const int rpg = static_cast<int>((rpc + kHG - 1) / kHG);
+    if (dim * 4 >= static_cast<size_t>(kHSmemBudget)) return false;
+    int nb = static_cast<int>((kHSmemBudget - dim * 4) / (kHG * row_bytes));
+    if (const char* v = getenv("SVT_ROWS_HS_NB")) nb = atoi(v);
+    if (nb > rpg) nb = rpg;
+    if (nb > kHMaxSlots / kHG) nb = kHMaxSlots / kHG;
+    if (nb < 1 || (nb < 2 && rpg > 1)) return false;
+    *grid_out = grid;
+    *rpg_out = rpg;
+    *cpt_out = cpt;
+    *nb_out = nb;
+    return true;
 }
 
 template <int DT, int CPT>
@@ -1420,9 +1716,12 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
     p.eta = static_cast<float>((static_cast<double>(dim) + n_fast) * 4.0) * 1.40129846e-45f;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     {
-        int fgrid = 0, rpg = 0, cpt = 0;
-        if (!getenv("SVT_ROWS_GRID") &&
-            rows_fast_eligible(p.n, row_bytes, dim, &fgrid, &rpg, &cpt)) {
+        int fgrid = 0, rpg = 0, cpt = 0, nb = 0;
+        const bool hs_flags = (flags & SVT_ROWS_WEIGHTS_STABLE) && (flags & SVT_ROWS_HIDDEN_STABLE);
+        const bool hs = hs_flags && !getenv("SVT_ROWS_GRID") &&
+                        rows_hs_eligible(p.n, row_bytes, dim, &fgrid, &rpg, &cpt, &nb);
+        if (hs || (!getenv("SVT_ROWS_GRID") &&
+                   rows_fast_eligible(p.n, row_bytes, dim, &fgrid, &rpg, &cpt))) {
             FastParams f = {};
             f.W = p.W;
             f.row_bytes = p.row_bytes;
@@ -1455,6 +1754,24 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
                                (1.0 - gamma_n(nf)) * 1.0001;
             f.c_rel = static_cast<float>(crf) * (1.0f + FLT_EPSILON);
             f.eta = static_cast<float>((static_cast<double>(dim) + nf) * 4.0) * 1.40129846e-45f;
+            if (hs) {
+                f.hs = 1;
+                f.nb = nb;
+                switch (dt) {
+                    case SVT_F32:
+                        return cpt == 1   ? pick_rpg_hs<SVT_F32, 1>(f, rpg, st)
+                               : cpt == 2 ? pick_rpg_hs<SVT_F32, 2>(f, rpg, st)
+                                          : pick_rpg_hs<SVT_F32, 4>(f, rpg, st);
+                    case SVT_F16:
+                        return cpt == 1   ? pick_rpg_hs<SVT_F16, 1>(f, rpg, st)
+                               : cpt == 2 ? pick_rpg_hs<SVT_F16, 2>(f, rpg, st)
+                                          : pick_rpg_hs<SVT_F16, 4>(f, rpg, st);
+                    default:
+                        return cpt == 1   ? pick_rpg_hs<SVT_BF16, 1>(f, rpg, st)
+                               : cpt == 2 ? pick_rpg_hs<SVT_BF16, 2>(f, rpg, st)
+                                          : pick_rpg_hs<SVT_BF16, 4>(f, rpg, st);
+                }
+            }
             switch (dt) {
                 case SVT_F32:
                     return cpt == 1   ? pick_rpg<SVT_F32, 1>(f, rpg, st)

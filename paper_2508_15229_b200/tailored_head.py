@@ -24,7 +24,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (SVT_BF16, SVT_F16, SVT_F32, SVT_WEIGHTS_STABLE, ConfigError, Error,
+from ._lib import (SVT_BF16, SVT_F16, SVT_F32, SVT_ROWS_HIDDEN_STABLE, SVT_WEIGHTS_STABLE,
+                   ConfigError, Error,
                    IntegrityError, ParseError, call)
 
 __all__ = [
@@ -514,12 +515,16 @@ class RowDecoder:
 
     def greedy(self, hidden: torch.Tensor, out_id: torch.Tensor,
                out_max: Optional[torch.Tensor] = None,
-               out_record: Optional[torch.Tensor] = None) -> torch.Tensor:
+               out_record: Optional[torch.Tensor] = None,
+               hidden_stable: bool = False) -> torch.Tensor:
         """hidden: f32 [dim] on the device (16-byte aligned); out_id: one
         int32; out_max (optional): the exact reference logit of the winner;
         out_record (optional, 4 int32): the vocab-shard record for
-        svt_shard_combine."""
-        st = self._fn(*self._pre, hidden.data_ptr(), *self._post, self._stable,
+        svt_shard_combine. hidden_stable: ``hidden`` was not written by the
+        kernel queued right before this call (SVT_ROWS_HIDDEN_STABLE: the
+        step then overlaps the previous one on every SM)."""
+        flags = self._stable | (SVT_ROWS_HIDDEN_STABLE if hidden_stable else 0)
+        st = self._fn(*self._pre, hidden.data_ptr(), *self._post, flags,
                       out_id.data_ptr(), _ptr(out_max), _ptr(out_record), self.ws.data_ptr(),
                       _stream(self.stream))
         _lib.check(st, "svt_greedy_certified_rows")

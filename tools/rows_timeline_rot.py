@@ -32,7 +32,7 @@ def decode(stamp):
                 th._lib.lib.svt_rows_set_debug(dbg[k].data_ptr())
             elif stamp:
                 th._lib.lib.svt_rows_set_debug(None)
-            rd.greedy(hid[t, j], out[t, j])
+            rd.greedy(hid[t, j], out[t, j], hidden_stable=rot.HS)
             k += 1
     th._lib.lib.svt_rows_set_debug(None)
 
@@ -52,11 +52,13 @@ with torch.cuda.stream(s):
     g.replay()
 torch.cuda.synchronize()
 d = dbg.view(K, 256, 128).cpu().numpy().astype(np.int64)
-G = 147 if os.environ.get("SVT_ROWS_FAST", "1") != "0" else 148
+G = 148 if os.environ.get("SVT_ROWS_FAST", "1") == "0" else 147
 t0 = d[0, :G, 0][d[0, :G, 0] > 0].min()
 for k in range(K):
     x = d[k, :G, :8] - t0
-    print(json.dumps({"k": k, "start_med": int(np.median(x[:, 0])), "start_max": int(x[:, 0].max()),
+    sm = d[k, :G, 8]
+    print(json.dumps({"k": k, "start_min": int(x[:, 0].min()), "start_med": int(np.median(x[:, 0])), "start_max": int(x[:, 0].max()),
+                      "distinct_sms": int(len(set(sm.tolist()))),
                       "depwait_med": int(np.median(x[:, 1])), "rows_in_med": int(np.median(x[:, 7])),
                       "rows_in_max": int(x[:, 7].max()), "h_med": int(np.median(x[:, 2])),
                       "reduced_med": int(np.median(x[:, 3])), "ctl_L_med": int(np.median(x[:, 5])),

@@ -16,6 +16,7 @@ from paper_2508_15229_b200 import synth  # noqa: E402
 from paper_2508_15229_b200 import tailored_head as th  # noqa: E402
 
 V, d, STEPS = 128256, 2048, 64
+HS = os.environ.get("SVT_HS", "0") == "1"  # SVT_ROWS_HIDDEN_STABLE
 head = th.HeadMatrix.random(V, d, synth.SEED_W, storage=th.SVT_F32)
 t_ids = synth.static_ids(V, 2048)
 words = torch.from_numpy(synth.words_of(t_ids, V).view(np.int64)).cuda()
@@ -47,7 +48,7 @@ def run(R, reps=10):
     def decode():
         for t in range(STEPS):
             for j, (_, rd, _) in enumerate(jobs):
-                rd.greedy(hid[t, j], out[t, j])
+                rd.greedy(hid[t, j], out[t, j], hidden_stable=HS)
 
     with torch.cuda.stream(s):
         decode()
@@ -71,7 +72,7 @@ def run(R, reps=10):
     nbytes = sum(n for _, _, n in jobs) / R * d * 4
     med = float(np.median(ts))
     stats = [rd.stats() for _, rd, _ in jobs]
-    return {"R": R, "us_per_token": med, "min": min(ts), "gbs": nbytes / med / 1e3,
+    return {"R": R, "hs": HS, "nb": os.environ.get("SVT_ROWS_HS_NB"), "us_per_token": med, "min": min(ts), "gbs": nbytes / med / 1e3,
             "frac": nbytes / med / 1e3 / 6551.7, "rows": nbytes / d / 4,
             "recomputed": sum(s[1] for s in stats), "certified": sum(s[0] for s in stats)}
 
