@@ -575,11 +575,17 @@ class Cfg1Jobs:
             tb.run_select(layout=False)
             rd.gather()
 
-    def decode(self, jobs=None):
+    def decode(self, jobs=None, hidden_stable=True):
+        """Every step's hidden state is resident before the decode starts,
+        so no launch's h is written by the kernel before it
+        (SVT_ROWS_HIDDEN_STABLE: consecutive tokens overlap on the SMs);
+        hidden_stable=False is the general contract (h may come from the
+        kernel right before each call)."""
         jobs = range(self.R) if jobs is None else jobs
         for t in range(self.steps):
             for j in jobs:
-                self.decs[j].greedy(self.hidden[t, j], self.out[t, j])
+                self.decs[j].greedy(self.hidden[t, j], self.out[t, j],
+                                    hidden_stable=hidden_stable)
 
     def token_bytes(self):
         """Algorithmic bytes of one decode launch: the plan's
@@ -588,10 +594,11 @@ class Cfg1Jobs:
         d = CFG1["d"]
         return sum(n * d * 4 + d * 4 + n * 4 + 8 for n in self.n) / self.R
 
-    # launches per step: per job select + gather, per token the rows grid +
-    # its finalize
+    # launches per step: per job select + gather; per job the first token
+    # after the gather is the rows grid + its finalize (weights not yet
+    # stable), every later token ONE launch (rows CTAs + finalizer CTA)
     def launches_per_step(self):
-        return self.R * 2 + self.steps * self.R * 2
+        return self.R * 2 + self.R * 2 + (self.steps - 1) * self.R
 
     def stats(self):
         fast = slow = 0
@@ -660,8 +667,26 @@ def time_cfg1(jobs, K, W, torch, dist, world):
         y.record(s)
     torch.cuda.synchronize()
     warm_us = x.elapsed_time(y) / 10 / jobs.steps * 1e3
+    # the general contract (h possibly written by the kernel right before
+    # each call): the same R jobs, cold, without SVT_ROWS_HIDDEN_STABLE
+    gen_g = _capture(torch, lambda: jobs.decode(hidden_stable=False), s)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            prep.replay()
+            gen_g.replay()
+        x, y = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gen = []
+        for _ in range(5):
+            prep.replay()
+            x.record(s)
+            gen_g.replay()
+            y.record(s)
+            y.synchronize()
+            gen.append(x.elapsed_time(y) / (jobs.steps * jobs.R) * 1e3)
+    torch.cuda.synchronize()
+    general_us = float(np.median(gen))
     jobs.set_stream(None)
-    return ms, dec_ms, warm_us, clk.summary()
+    return ms, dec_ms, warm_us, general_us, clk.summary()
 
 
 def cfg1_e2e(jobs, K, W, torch, th, session_mod):
@@ -833,7 +858,8 @@ def run_cfg1(args, torch, dist, world, rank):
 
     R, steps = args.jobs, args.decode_steps
     jobs = Cfg1Jobs(R, steps, rank, torch, th, synth)
-    ms, dec_ms, warm_us, clocks = time_cfg1(jobs, args.steps, args.warmup, torch, dist, world)
+    ms, dec_ms, warm_us, general_us, clocks = time_cfg1(jobs, args.steps, args.warmup, torch, dist,
+                                                         world)
     tokens = R * steps * args.steps * world
     value = tokens / (ms / 1000.0)
     tok_us = sum(dec_ms) / len(dec_ms) / (R * steps) * 1e3
@@ -845,8 +871,10 @@ def run_cfg1(args, torch, dist, world, rank):
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": load_traffic("rows_fast_cfg1"),
-        "kernel": "rows_fast_kernel<f32,4,5> + rows_fast_fin_kernel<f32> "
-                  "(svt_greedy_certified_rows, one decode token)",
+        "kernel": "rows_hs_kernel<f32,4,9> (svt_greedy_certified_rows with "
+                  "SVT_ROWS_HIDDEN_STABLE: 147 rows CTAs + 1 finalizer CTA, one launch per "
+                  "decode token; the first token after each gather: rows_fast_kernel + "
+                  "rows_fast_fin_kernel)",
         "bytes_per_launch": bpt, "avg_launch_us": tok_us,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "l2": "cold: consecutive launches read different sub-heads (8 x 20.9 MB > 126 MB L2)",
@@ -855,6 +883,11 @@ def run_cfg1(args, torch, dist, world, rank):
         "decode_share_of_step": sum(dec_ms) / ms if world == 1 else None,
         "warm": {"us_per_token": warm_us, "gbs": warm_gbs, "frac": warm_gbs / peak,
                  "what": "job 0 alone: its 20.9 MB sub-head stays in L2 across its 64 tokens"},
+        "general_contract": {
+            "us_per_token": general_us, "frac": bpt / (general_us / 1e6) / 1e9 / peak,
+            "what": "the same cold decode without SVT_ROWS_HIDDEN_STABLE (h may be written by "
+                    "the kernel right before each call): rows_fast_kernel + its finalize, "
+                    "rows held on chip until h exists, one step resident per SM"},
         "certified": {"direct": fast, "exact_recompute": slow},
     }
     result = {

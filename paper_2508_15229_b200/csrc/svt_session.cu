@@ -534,8 +534,14 @@ svt_status svt_session_plans_host(svt_session* s, int64_t* h_n_active, int64_t* 
     return SVT_OK;
 }
 
-svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size_t hidden_ld,
-                                     uint32_t* d_out_ids, float* d_out_max) {
+}  // extern "C"
+
+namespace {
+// extra_flags: SVT_ROWS_HIDDEN_STABLE when the caller knows d_hidden was not
+// written by the kernel queued right before this step (decode_host uploads
+// every step's hidden states before the first launch)
+svt_status session_greedy_device(svt_session* s, const float* d_hidden, size_t hidden_ld,
+                                 uint32_t* d_out_ids, float* d_out_max, int32_t extra_flags) {
     if (!s) {
         set_error("null session");
         return SVT_ERR_CONFIG;
@@ -552,8 +558,8 @@ svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size
     if (s->rows_mode) {
         const size_t n = static_cast<size_t>(s->n_active[0]);
         return svt_greedy_certified_rows(s->d_rows, s->dt, n, s->dim, nullptr, n, d_hidden,
-                                         s->d_active, 0u, 1, flags, d_out_ids, d_out_max,
-                                         nullptr, s->d_rows_ws, s->stream);
+                                         s->d_active, 0u, 1, flags | extra_flags, d_out_ids,
+                                         d_out_max, nullptr, s->d_rows_ws, s->stream);
     }
     if (s->split)
         return svt_greedy_split(s->d_st_sub, s->dt, s->n_st, s->dim, s->d_st_ids, s->st_valid_d(),
@@ -564,6 +570,14 @@ svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size
     return svt_greedy_interleaved(s->d_sub, s->dt, s->dim, s->group_begin_d(), s->d_group_req,
                                   s->d_active, s->batch, s->max_groups, d_hidden, hidden_ld, 0, 1,
                                   flags, d_out_ids, d_out_max, nullptr, s->d_ws, s->stream);
+}
+}  // namespace
+
+extern "C" {
+
+svt_status svt_session_greedy_device(svt_session* s, const float* d_hidden, size_t hidden_ld,
+                                     uint32_t* d_out_ids, float* d_out_max) {
+    return session_greedy_device(s, d_hidden, hidden_ld, d_out_ids, d_out_max, 0);
 }
 
 svt_status svt_session_greedy_host(svt_session* s, const float* h_hidden, size_t host_ld,
@@ -729,8 +743,8 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
         for (int32_t i = 0; i < n_sessions; ++i) {
             svt_session* si = sessions[i];
             if (si->batch == 0) continue;
-            st = svt_session_greedy_device(si, s0->d_multi + off * dim, dim,
-                                           s0->d_multi_ids + off, nullptr);
+            st = session_greedy_device(si, s0->d_multi + off * dim, dim, s0->d_multi_ids + off,
+                                       nullptr, SVT_ROWS_HIDDEN_STABLE);
             if (st) return st;
             off += static_cast<size_t>(si->batch);
         }

@@ -7,7 +7,7 @@ R, steps = int(sys.argv[1]), int(sys.argv[2])
 jobs = bench.Cfg1Jobs(R, steps, 0, torch, th, synth)
 jobs.prep(); jobs.decode(); torch.cuda.synchronize()
 eager = jobs.out.cpu().numpy().copy()
-ms, dec_ms, warm, clk = bench.time_cfg1(jobs, 5, 3, torch, None, 1)
+ms, dec_ms, warm, gen, clk = bench.time_cfg1(jobs, 5, 3, torch, None, 1)
 graph = jobs.out.cpu().numpy().copy()
 v, h2d, d2h, ok, sec = bench.cfg1_e2e(jobs, 2, 1, torch, th, session_mod)
 orc = O.c_oracle()
