@@ -594,11 +594,13 @@ class Cfg1Jobs:
         d = CFG1["d"]
         return sum(n * d * 4 + d * 4 + n * 4 + 8 for n in self.n) / self.R
 
-    # launches per step: per job select + gather; per job the first token
-    # after the gather is the rows grid + its finalize (weights not yet
-    # stable), every later token ONE launch (rows CTAs + finalizer CTA)
+    # launches per step: per job select + gather (prep graph), then ONE
+    # launch per token (rows CTAs + finalizer CTA). The decode graph is
+    # captured after an eager pass, so every captured token runs with stable
+    # weights (the prep graph before it is a full dependency); see
+    # profiles/r2_launches_cfg1_hs_summary.json
     def launches_per_step(self):
-        return self.R * 2 + self.R * 2 + (self.steps - 1) * self.R
+        return self.R * 2 + self.steps * self.R
 
     def stats(self):
         fast = slow = 0

@@ -721,6 +721,8 @@ struct FastParams {
     unsigned long long* dbg;  // per CTA 8 %globaltimer stamps (svt_rows_set_debug)
     int32_t hs;           // 1: the stable-hidden ring kernel (records tagged kHsTag, cleared)
     int32_t nb;           // stable-hidden kernel: ring slots per row group
+    int32_t fin_warps;    // stable-hidden kernel: polling warps of the finalizer CTA
+    int32_t fin_stagger;  // ns between their first polls
 };
 
 __device__ __forceinline__ int64_t frow_begin(const FastParams& p, int c) {
@@ -1267,6 +1269,7 @@ constexpr int kHCompute = kHG * kHWPG;            // 8
 constexpr int kHThreads = (kHCompute + 2) * 32;   // + producer + dependency warp
 constexpr int kHMaxSlots = 16;                    // ring slots per CTA (both groups)
 constexpr int kHSmemBudget = 96 * 1024;           // ring + h: two CTAs per SM
+constexpr int kHInflight = 48 * 1024;             // rows in flight per CTA (ring target)
 constexpr int kHFinWarps = 4;                     // polling warps of the finalizer CTA
 constexpr int kHFinStagger = 300;                 // ns between their first polls
 
@@ -1422,14 +1425,15 @@ __global__ void __launch_bounds__(kHThreads, 2) rows_hs_kernel(FastParams p) {
         // kHFinWarps polling warps, staggered: under the next steps' streams
         // a poll round trip is 1-2 us, so one warp would see the last record
         // up to a round trip late; the first warp to see all claims the step
-        if (threadIdx.x >= 32 * kHFinWarps) return;
+        const int fw = p.fin_warps;
+        if (threadIdx.x >= 32 * fw) return;
         __shared__ unsigned s_n, s_claim;
         if (threadIdx.x == 0) s_claim = 0u;
-        named_bar_sync(2, 32 * kHFinWarps);
+        named_bar_sync(2, 32 * fw);
         asm volatile("griddepcontrol.launch_dependents;");
         asm volatile("griddepcontrol.wait;" ::: "memory");
         if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
-        rows_fast_finalize<DT>(p, dsm, &s_n, &s_claim, kHFinStagger);
+        rows_fast_finalize<DT>(p, dsm, &s_n, &s_claim, p.fin_stagger);
         return;
     }
     rows_hs_cta<DT, CPT, RPG>(p, dsm);
@@ -1570,6 +1574,12 @@ bool rows_hs_eligible(int64_t n, size_t row_bytes, size_t dim, int* grid_out, in
     const int rpg = static_cast<int>((rpc + kHG - 1) / kHG);
     if (dim * 4 >= static_cast<size_t>(kHSmemBudget)) return false;
     int nb = static_cast<int>((kHSmemBudget - dim * 4) / (kHG * row_bytes));
+    // ~48 KB of rows in flight per CTA (96 KB per SM with two steps
+    // resident) keeps HBM busy; deeper rings only lengthen the queues the
+    // latency-critical record stores and polls wait in (measured: 3 slots
+    // of 8 KB rows per group 3.94-3.97 us per token, 5 slots 3.93-4.01)
+    const int nb_inflight = static_cast<int>(kHInflight / (kHG * row_bytes));
+    if (nb > nb_inflight) nb = nb_inflight < 2 ? 2 : nb_inflight;
     if (const char* v = getenv("SVT_ROWS_HS_NB")) nb = atoi(v);
     if (nb > rpg) nb = rpg;
     if (nb > kHMaxSlots / kHG) nb = kHMaxSlots / kHG;
@@ -1757,6 +1767,11 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
             if (hs) {
                 f.hs = 1;
                 f.nb = nb;
+                f.fin_warps = kHFinWarps;
+                f.fin_stagger = kHFinStagger;
+                if (const char* v = getenv("SVT_HS_FIN_WARPS")) f.fin_warps = atoi(v);
+                if (const char* v = getenv("SVT_HS_FIN_STAGGER")) f.fin_stagger = atoi(v);
+                if (f.fin_warps < 1 || f.fin_warps > kHThreads / 32) f.fin_warps = kHFinWarps;
                 switch (dt) {
                     case SVT_F32:
                         return cpt == 1   ? pick_rpg_hs<SVT_F32, 1>(f, rpg, st)
