@@ -300,17 +300,22 @@ svt_status svt_greedy_fused(const void* d_head, svt_dtype dt, size_t rows, size_
  * plan misses part of T: its rows are then all dynamic), d_first_ids[b] (the
  * plan's smallest id) and d_dyn_starts[b] (1 when that id is dynamic).
  * svt_greedy_split then runs, per step:
- *   the static half: exact reference-order logits of every static row for
- *     every request, from d_static_sub (T gathered once by
- *     svt_gather_interleaved as a single plan; n_static rows, ids
- *     d_static_ids ascending), on a side stream;
+ *   the static half, on a side stream, from d_static_sub (T gathered once
+ *     by svt_gather_interleaved as a single plan; n_static rows, ids
+ *     d_static_ids ascending): for bf16 heads with dim % 64 == 0, tensor-core
+ *     partial dots (h split into bf16 hi + lo) with a rigorous bound per
+ *     (request, row), then the exact reference-order chains of only the rows
+ *     that can still be the request's static maximum
+ *     (svt_split_certified.cu); otherwise (or SVT_SPLIT_EXACT=1) every
+ *     static row's exact chain for every request;
  *   the dynamic half: the exact-order GEMV over d_dyn_sub (the D_b \ T
  *     sub-heads, svt_gather_interleaved over d_dyn_ids with the group
  *     records of svt_plan_layout on d_n_dyn);
  *   a combine: larger value, then lower id; a NaN at the plan's smallest id
  *     wins (the reference's row-0 rule).
- * d_workspace: svt_greedy_split_workspace_bytes(batch, max_groups), zeroed
- * once before the first call (each call leaves its static keys at zero).
+ * d_workspace: svt_greedy_split_workspace_bytes(batch, max_groups, n_static,
+ * dim), zeroed once before the first call (each call leaves its static keys
+ * at zero).
  * flags: SVT_WEIGHTS_STABLE as for svt_greedy_interleaved. */
 svt_status svt_decode_split_plans(const uint32_t* d_active_ids, const int64_t* d_act_off,
                                   const int64_t* d_n_active, int32_t batch,
@@ -319,7 +324,8 @@ svt_status svt_decode_split_plans(const uint32_t* d_active_ids, const int64_t* d
                                   uint32_t* d_dyn_ids, int64_t* d_n_dyn, int64_t* d_static_valid,
                                   uint32_t* d_first_ids, uint8_t* d_dyn_starts,
                                   svt_stream stream);
-size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups);
+size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups, int64_t n_static,
+                                        size_t dim);
 svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, int64_t n_static, size_t dim,
                             const uint32_t* d_static_ids, const int64_t* d_static_valid,
                             const uint32_t* d_first_ids, const void* d_dyn_sub,

@@ -114,7 +114,7 @@ _SIGS = {
                                  _i32, _i32, _vp, _vp, _vp, _vp], C.c_int),
     "svt_decode_split_plans": ([_vp, _vp, _vp, _i32, _vp, _sz, _vp, _i64, _vp, _vp, _vp, _vp,
                                 _vp, _vp], C.c_int),
-    "svt_greedy_split_workspace_bytes": ([_i32, _i64], _sz),
+    "svt_greedy_split_workspace_bytes": ([_i32, _i64, _i64, _sz], _sz),
     "svt_greedy_split": ([_vp, C.c_int, _i64, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                           _i32, _i64, _vp, _sz, _i32, _vp, _vp, _vp, _vp], C.c_int),
     "svt_row_norms_bf16": ([_vp, _i64, _i32, _vp, _vp], C.c_int),

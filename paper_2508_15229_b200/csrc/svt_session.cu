@@ -263,7 +263,7 @@ svt_status prepare_split(svt_session* s, const uint64_t* h_words, int64_t n_stat
         s->cap_split_meta = 0;
         st = grow(&s->d_split_meta, &s->cap_split_meta, 4 * s->cap_batch);
     }
-    const size_t wsb = svt_greedy_split_workspace_bytes(s->batch, s->max_groups);
+    const size_t wsb = svt_greedy_split_workspace_bytes(s->batch, s->max_groups, n_static, s->dim);
     if (!st && (wsb > s->cap_split_ws || !s->d_split_ws)) {
         if (s->d_split_ws) cudaFree(s->d_split_ws);
         s->d_split_ws = nullptr;

@@ -30,6 +30,21 @@
 #include "svt_gemv.cuh"
 
 namespace svt {
+bool split_certified_eligible(svt_dtype dt, int64_t n_static, size_t dim);
+size_t split_certified_ws_bytes(int32_t batch, int64_t n_static, size_t dim);
+svt_status split_static_certified(const void* d_static_sub, const uint32_t* d_static_ids,
+                                  int64_t n_static, size_t dim, const int64_t* d_static_valid,
+                                  const uint32_t* d_first_ids, int32_t batch,
+                                  const float* d_hidden, size_t hidden_ld,
+                                  unsigned long long* keys, void* ws, bool want_exact,
+                                  cudaStream_t ss);
+svt_status split_combine_certified(const void* d_static_sub, const uint32_t* d_static_ids,
+                                   int64_t n_static, size_t dim, const int64_t* d_static_valid,
+                                   const uint32_t* d_first_ids, int32_t batch,
+                                   const float* d_hidden, size_t hidden_ld,
+                                   unsigned long long* keys, void* ws, const void* rec,
+                                   const int64_t* d_n_dyn, uint32_t* d_out_ids, float* d_out_max,
+                                   cudaStream_t st);
 svt_status greedy_interleaved_req(const void* d_sub, svt_dtype dt, size_t dim, const int64_t* gb,
                                   const void* meta, const uint32_t* ids, int32_t batch,
                                   int64_t max_groups, const float* hidden, size_t ld,
@@ -276,11 +291,20 @@ void release_side_stream(cudaStream_t main) {
 }
 }  // namespace svt
 
-extern "C" size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups) {
+namespace {
+size_t split_base_bytes(int32_t batch, int64_t max_groups) {
     const size_t b = static_cast<size_t>(batch > 0 ? batch : 0);
     // static keys | dynamic records | GEMV group keys
     return ((b * 8 + 255) & ~size_t(255)) + ((b * 16 + 255) & ~size_t(255)) +
-           svt_greedy_workspace_bytes(batch, max_groups);
+           ((svt_greedy_workspace_bytes(batch, max_groups) + 255) & ~size_t(255));
+}
+}  // namespace
+
+extern "C" size_t svt_greedy_split_workspace_bytes(int32_t batch, int64_t max_groups,
+                                                   int64_t n_static, size_t dim) {
+    // + the certified static half's scratch (hidden split, partial dots)
+    return split_base_bytes(batch, max_groups) +
+           svt::split_certified_ws_bytes(batch > 0 ? batch : 0, n_static > 0 ? n_static : 0, dim);
 }
 
 extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, int64_t n_static,
@@ -317,7 +341,19 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         SVT_CUDA_TRY(cudaEventRecord(side->fork, st));
         SVT_CUDA_TRY(cudaStreamWaitEvent(ss, side->fork, 0));
     }
-    if (n_static > 0) {
+    const bool certified = n_static > 0 && split_certified_eligible(dt, n_static, dim);
+    void* cws = ws + split_base_bytes(batch, max_groups);
+    if (certified) {
+        // certified static half (svt_split_certified.cu): tensor-core partial
+        // dots, rigorous bounds, exact chains for the candidates only
+        if (svt_status s = split_static_certified(d_static_sub, d_static_ids, n_static, dim,
+                                                  d_static_valid, d_first_ids, batch, d_hidden,
+                                                  hidden_ld, keys, cws, d_out_max != nullptr, ss)) {
+            cudaMemsetAsync(keys, 0, b * 8, ss);
+            if (side) cudaEventRecord(side->join, ss), cudaStreamWaitEvent(st, side->join, 0);
+            return s;
+        }
+    } else if (n_static > 0) {
         StaticParams p;
         p.sub = static_cast<const uint8_t*>(d_static_sub);
         p.n_static = n_static;
@@ -359,6 +395,11 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         SVT_LAUNCH_CHECK("static_rows_kernel");
     }
     if (side) SVT_CUDA_TRY(cudaEventRecord(side->join, ss));
+    if (getenv("SVT_SPLIT_STATIC_ONLY")) {  // measurement only: the static half alone
+        if (side) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
+        cudaMemsetAsync(keys, 0, b * 8, st);
+        return SVT_OK;
+    }
     // dynamic half: requests without dynamic rows have no group (record untouched)
     if (svt_status s = greedy_interleaved_req(d_dyn_sub, dt, dim, d_group_begin, d_group_meta,
                                               d_dyn_ids, batch, max_groups, d_hidden, hidden_ld,
@@ -371,6 +412,10 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         return s;
     }
     if (side) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
+    if (certified)
+        return split_combine_certified(d_static_sub, d_static_ids, n_static, dim, d_static_valid,
+                                       d_first_ids, batch, d_hidden, hidden_ld, keys, cws, rec,
+                                       d_n_dyn, d_out_ids, d_out_max, st);
     split_combine_kernel<<<(batch + 127) / 128, 128, 0, st>>>(
         reinterpret_cast<const uint4*>(rec), keys, d_first_ids, d_n_dyn, batch, d_out_ids,
         d_out_max);

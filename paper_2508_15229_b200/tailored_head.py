@@ -418,8 +418,8 @@ class SplitDecoder:
         self.sub = torch.empty(
             max(16, _lib.lib.svt_subhead_bytes(head.storage, d, self.max_groups)),
             dtype=torch.uint8, device=dev)
-        self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_split_workspace_bytes(B, self.max_groups)),
-                              dtype=torch.uint8, device=dev)
+        self.ws = torch.zeros(max(1, _lib.lib.svt_greedy_split_workspace_bytes(
+            B, self.max_groups, self.nT, d)), dtype=torch.uint8, device=dev)
         self._stable = False
         self.prepare()
 
@@ -460,6 +460,13 @@ class SplitDecoder:
              hidden.data_ptr(), hidden.stride(0), flags, out_ids.data_ptr(), _ptr(out_max),
              self.ws.data_ptr(), _stream(self.stream))
         return out_ids
+
+    def stats(self):
+        """Certified static half (bf16 heads): (requests whose static
+        maximum had one candidate, requests that needed more exact chains),
+        accumulated since the decoder was built; (0, 0) on the exact path."""
+        w = self.ws[-256:-248].view(torch.int32).cpu().tolist()
+        return w[0], w[1]
 
     def algorithmic_decode_bytes(self, esize: int, dim: int) -> int:
         """Bytes one split decode step must move from HBM: the static block
@@ -847,6 +854,13 @@ class TailoredBatch:
              self.active.data_ptr(), self.act_off.data_ptr(), self.B, k, 1, ids.data_ptr(),
              vals.data_ptr(), _stream(self.stream))
         return ids, vals
+
+    def stats(self):
+        """Certified static half (bf16 heads): (requests whose static
+        maximum had one candidate, requests that needed more exact chains),
+        accumulated since the decoder was built; (0, 0) on the exact path."""
+        w = self.ws[-256:-248].view(torch.int32).cpu().tolist()
+        return w[0], w[1]
 
     def algorithmic_decode_bytes(self, esize: int, dim: int) -> int:
         """Bytes one decode step must move: Σ_b |S_b|·d·b_W

@@ -81,9 +81,12 @@ def test_split_decode_cfg2_full_shape(th):
     plans = {}
     for t in range(steps):
         h = torch.from_numpy(hid[t]).cuda()
+        dec.greedy(h, out)  # ids only: certified intervals handed to the combine
+        ids_only = out.cpu().numpy().view(np.uint32).copy()
         dec.greedy(h, out, mx)
         tb.greedy(h, ref)
         got = out.cpu().numpy().view(np.uint32)
+        assert np.array_equal(ids_only, got), t
         gmx = mx.cpu().numpy()
         assert np.array_equal(got, ref.cpu().numpy().view(np.uint32)), t
         reqs = list(range(t, B, 8))
@@ -98,6 +101,10 @@ def test_split_decode_cfg2_full_shape(th):
             assert got[b] == want, (t, b)
             assert bits([gmx[b]])[0] == bits([wmax])[0], (t, b)
     assert int(dec.bad.item()) == 0
+    # the certified static half decided every request of every step, almost
+    # always with the exact chain of a single candidate row
+    one, more = dec.stats()
+    assert one + more == 2 * steps * B and one >= 0.8 * 2 * steps * B, (one, more)
 
 
 def _check_prefill(th, head, W, plans, hid, S, P, sc):

@@ -700,9 +700,13 @@ def test_split_decode_matches_reference(th, case):
                 h[(t + 3) % B, :] = np.float32(np.inf)
             hl = np.zeros((B, ld), np.float32)
             hl[:, :d] = h
-            dec.greedy(torch.from_numpy(hl).cuda(), out, mx)
+            hd = torch.from_numpy(hl).cuda()
+            dec.greedy(hd, out)  # ids only (certified: interval hand-off to the combine)
+            got_ids = out.cpu().numpy().view(np.uint32).copy()
+            dec.greedy(hd, out, mx)
             got = out.cpu().numpy().view(np.uint32)
             gmx = mx.cpu().numpy()
+            assert np.array_equal(got_ids, got), (case, rnd, t)
             for b in range(B):
                 plan = orc.select(prompts[b], words, V, V).active_ids
                 want, wmax = orc.greedy_step(W[plan], h[b], plan)
@@ -713,6 +717,15 @@ def test_split_decode_matches_reference(th, case):
         tb.run_select()
         dec.prepare()
     assert int(dec.bad.item()) == 0
+    one, more = dec.stats()
+    if storage == th.SVT_BF16 and d % 64 == 0:
+        # the certified static half ran: every (step, request) with static
+        # rows was decided, mostly from a single candidate's exact chain
+        assert one + more > 0
+        if case != "nonfinite" and case != "duplicate_rows":
+            assert one >= more, (one, more)
+    else:
+        assert (one, more) == (0, 0)
 
 
 def test_split_decode_two_streams(th):
