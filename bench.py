@@ -704,15 +704,23 @@ def cfg1_e2e(jobs, K, W, torch, th, session_mod):
     sess = [session_mod.Session(jobs.head, max_batch=1, stream=st) for _ in range(R)]
     offs = [np.array([0, len(p)], np.int64) for p in jobs.prompts_h]
 
+    split = [0.0, 0.0]  # host seconds in the prepares / in decode_host
+
     def one():
+        t0 = time.perf_counter()
         for j in range(R):
             sess[j].prepare(jobs.words_h, V, jobs.prompts_h[j], offs[j])
+        t1 = time.perf_counter()
         session_mod.decode_host(sess, hid_h, steps, ids_h)
+        t2 = time.perf_counter()
+        split[0] += t1 - t0
+        split[1] += t2 - t1
 
     try:
         for _ in range(W):
             one()
         torch.cuda.synchronize()
+        split[0] = split[1] = 0.0
         t0 = time.perf_counter()
         for _ in range(K):
             one()
@@ -721,6 +729,12 @@ def cfg1_e2e(jobs, K, W, torch, th, session_mod):
     finally:
         for x in sess:
             x.close()
+    one.breakdown = {"prepare_ms_per_step": split[0] / K * 1e3,
+                     "decode_host_ms_per_step": split[1] / K * 1e3,
+                     "what": "host clock: R x svt_session_prepare_host (static bitmap + prompt H2D, "
+                             "select, row gather, one sync each) vs one svt_session_decode_host "
+                             "(hidden states H2D, the 64 x R certified tokens, ids D2H)"}
+    cfg1_e2e.breakdown = one.breakdown
     h2d = R * (jobs.words_h.nbytes + jobs.prompts_h[0].nbytes + 16) + steps * R * d * 4
     d2h = steps * R * 4 + R * 4 * 8  # ids + per-job plan counters / status words
     ok = bool(np.array_equal(ids_h.numpy(), jobs.out.cpu().numpy()))
@@ -910,7 +924,8 @@ def run_cfg1(args, torch, dist, world, rank):
         result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
                          "api": "svt_session_prepare_host x R + svt_session_decode_host "
-                                "(host buffers)", "ids_match_device_path": ok}
+                                "(host buffers)", "ids_match_device_path": ok,
+                         "breakdown": getattr(cfg1_e2e, "breakdown", None)}
     ids_dev = jobs.out.cpu().numpy().view(np.uint32).copy()
     head = jobs.head
     del jobs
