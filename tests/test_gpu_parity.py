@@ -728,6 +728,42 @@ def test_split_decode_matches_reference(th, case):
         assert (one, more) == (0, 0)
 
 
+def test_split_decode_certified_many_requests(th):
+    """The certified static half with more than one 64-request block (B =
+    150: three blocks, the last partial), |T| not a multiple of the 128-row
+    tile and d = 384 (three 128-wide K slices): ids-only calls and calls
+    with the exact logit equal the reference greedy_step."""
+    V, B, d, nT = 30000, 150, 384, 700
+    rng = np.random.default_rng(150)
+    head = th.HeadMatrix.random(V, d, 0xB150, storage=th.SVT_BF16)
+    W = head.to_host()
+    t_ids = rng.choice(V, nT, replace=False)
+    words = words_from_ids(t_ids, V)
+    prompts = [rng.integers(0, V, int(rng.integers(0, 90))).astype(np.uint32) for _ in range(B)]
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(q) for q in prompts])
+    tb = th.TailoredBatch.build(torch.from_numpy(words.view(np.int64)).cuda(), nT, V,
+                                torch.from_numpy(np.concatenate(prompts).view(np.int32)).cuda(), off)
+    dec = th.SplitDecoder(tb, head)
+    out = torch.empty(B, dtype=torch.int32, device="cuda")
+    mx = torch.empty(B, dtype=torch.float32, device="cuda")
+    plans = [orc.select(prompts[b], words, V, V).active_ids for b in range(B)]
+    for t in range(2):
+        h = bf16_np(rng.uniform(-1, 1, (B, d)).astype(np.float32))
+        hd = torch.from_numpy(h).cuda()
+        dec.greedy(hd, out)
+        ids_only = out.cpu().numpy().view(np.uint32).copy()
+        dec.greedy(hd, out, mx)
+        got = out.cpu().numpy().view(np.uint32)
+        gmx = mx.cpu().numpy()
+        assert np.array_equal(ids_only, got), t
+        for b in range(B):
+            want, wmax = orc.greedy_step(W[plans[b]], h[b], plans[b])
+            assert got[b] == want and bits([gmx[b]])[0] == bits([wmax])[0], (t, b)
+    one, more = dec.stats()
+    assert one + more == 4 * B and one >= more, (one, more)
+
+
 def test_split_decode_two_streams(th):
     """Two split decoders on two streams, launched back to back without a
     host sync between them: each stream's static half runs on its own side
