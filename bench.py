@@ -1008,9 +1008,9 @@ def run_cfg2(args, torch, dist, world, rank):
     peak, peak_kind = load_peaks()
     achieved = dec_bytes / (dec_avg_ms / 1000.0) / 1e9
     if args.mode == "split":
-        kernel = ("decode step: static_rows_kernel<bf16> (side stream) || "
-                  "gemv_ring_kernel<bf16,INTERLEAVED,argmax> + argmax_finalize_kernel, "
-                  "then split_combine_kernel (svt_greedy_split)")
+        kernel = ("decode step: static_gemm_kernel (tcgen05) + static_select_kernel (side "
+                  "stream) || gemv_ring_kernel<bf16,INTERLEAVED,argmax> + "
+                  "argmax_finalize_kernel, then split_combine_cert_kernel (svt_greedy_split)")
     else:
         kernel = "gemv_ring_kernel<bf16,%s,argmax>" % (
             "INTERLEAVED" if args.mode == "interleaved" else "ROWS")
@@ -1043,9 +1043,10 @@ def run_cfg2(args, torch, dist, world, rank):
                           "+ each request's D_b \\ T rows + hidden states + outputs",
             "unsplit_bytes_per_launch": unsplit,
             "unsplit_equivalent_gbs": unsplit / (dec_avg_ms / 1000.0) / 1e9,
-            "bound_note": "the split step is not HBM-bound: its static half computes "
-                          "64 x 2,048 exact reference-order chains of 896 MUL+ADD per step "
-                          "(FP32 issue) beside the HBM-bound GEMV over the dynamic rows; "
+            "bound_note": "the split step is not HBM-bound: its static half (bf16: "
+                          "tcgen05 partial dots + certification + the candidates' exact "
+                          "chains, DESIGN 5e') and the exact-order GEMV over the dynamic "
+                          "rows (chain- and launch-latency bound at 58 MB) share the SMs; "
                           "frac is the HBM view of the whole step"})
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
