@@ -51,9 +51,8 @@ constexpr int kGemmThreads = 256;
 constexpr int kSelThreads = 512;
 constexpr int kSelRows = 4;      // static rows per select thread kept in registers
 constexpr int kChainWarps = 8;   // warps running exact chains
-constexpr int kSelSplit = 8;     // K slices loaded in one batch by the select
 constexpr int kSelCand = 256;  // candidate list per request (more: every row)
-constexpr int kProdChunk = 1024;  // exact recompute: products staged per pass (per warp)
+constexpr int kProdChunk = 512;   // exact recompute: products staged per pass (per warp)
 
 // measurement only (SVT_CERT_STAMPS=1): per GEMM CTA 8 %globaltimer stamps
 __device__ unsigned long long g_cert_stamps[512 * 8];
@@ -79,8 +78,10 @@ struct SplitCertParams {
     int64_t ld;
     const int64_t* st_valid;   // [B]
     const uint32_t* first_ids; // [B]
-    float* part;               // [ksplit][B][nst_pad] partial dots
-    float* pnorm;              // [ksplit][nst_pad] partial sums of squares (rounded up)
+    float* part;               // [B][nst_pad] dots: the K slices' partials added atomically
+                               // (any order: the bound covers it); zeroed by the select
+    float* pnorm;              // [nst_pad] ||w_r||^2: the slices' rounded-up partial sums
+                               // added atomically; zeroed by the combine
     unsigned long long* keys;  // [B] static keys (the split combine reads and resets them)
     uint4* srec;               // [B] {lo, hi, id, row | 1<<31}: the static maximum as an
                                // interval (one candidate, ids-only call); .w = 0 otherwise
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) static_gemm_kernel(const Spli
                 ss = __fmaf_ru(y, y, ss);
             }
         }
-        if (r < p.n_static) p.pnorm[static_cast<int64_t>(sl) * p.nst_pad + r] = ss;
+        if (r < p.n_static) atomicAdd(&p.pnorm[r], ss);
     }
     mbar_wait_parity(&s_done, 0u);
     CERT_STAMP(5);
@@ -301,8 +302,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) static_gemm_kernel(const Spli
             for (int j = 0; j < 32; ++j) {
                 const int n = c0 + j;
                 if (n < nlive)
-                    p.part[(static_cast<int64_t>(sl) * p.B + blk * kSN + n) * p.nst_pad + r] =
-                        __uint_as_float(vh[j]) + __uint_as_float(vl[j]);
+                    atomicAdd(&p.part[static_cast<int64_t>(blk * kSN + n) * p.nst_pad + r],
+                              __uint_as_float(vh[j]) + __uint_as_float(vl[j]));
             }
         }
     }
@@ -362,27 +363,27 @@ __device__ float exact_static_row(const SplitCertParams& p, int64_t r, const flo
         }
         __syncwarp();
         if (lane == 0) {
-            // the next 32 products are loaded while the current 32 are added
+            // the next 16 products are loaded while the current 16 are added
             // (software pipeline: the add chain never waits on shared memory)
             int k = 0;
-            if (kn >= 32) {
-                float4 q[8], nq[8];
+            if (kn >= 16) {
+                float4 q[4], nq[4];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) q[j] = *reinterpret_cast<const float4*>(prod + 4 * j);
-                for (; k + 32 <= kn; k += 32) {
-                    const bool more = k + 64 <= kn;
+                for (int j = 0; j < 4; ++j) q[j] = *reinterpret_cast<const float4*>(prod + 4 * j);
+                for (; k + 16 <= kn; k += 16) {
+                    const bool more = k + 32 <= kn;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        nq[j] = more ? *reinterpret_cast<const float4*>(prod + k + 32 + 4 * j) : q[j];
+                    for (int j = 0; j < 4; ++j)
+                        nq[j] = more ? *reinterpret_cast<const float4*>(prod + k + 16 + 4 * j) : q[j];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < 4; ++j) {
                         acc = __fadd_rn(acc, q[j].x);
                         acc = __fadd_rn(acc, q[j].y);
                         acc = __fadd_rn(acc, q[j].z);
                         acc = __fadd_rn(acc, q[j].w);
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) q[j] = nq[j];
+                    for (int j = 0; j < 4; ++j) q[j] = nq[j];
                 }
             }
             for (; k < kn; k += 4) {
@@ -398,7 +399,7 @@ __device__ float exact_static_row(const SplitCertParams& p, int64_t r, const flo
     return __shfl_sync(0xFFFFFFFFu, acc, 0);
 }
 
-__global__ void __launch_bounds__(kSelThreads) static_select_kernel(const SplitCertParams p) {
+__global__ void __launch_bounds__(kSelThreads, 2) static_select_kernel(const SplitCertParams p) {
     __shared__ float s_red[kSelThreads / 32];
     __shared__ float s_hn;
     __shared__ int s_bad;
@@ -410,6 +411,10 @@ __global__ void __launch_bounds__(kSelThreads) static_select_kernel(const SplitC
     const int b = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (p.st_valid[b] <= 0) {
+        // no static rows in this plan: only the zero invariant of its dots
+        // (the GEMM accumulated them regardless) and an empty static key
+        float* fz = p.part + static_cast<int64_t>(b) * p.nst_pad;
+        for (int64_t r = tid; r < p.n_static; r += kSelThreads) fz[r] = 0.0f;
         if (tid == 0) {
             p.keys[b] = 0ull;
             p.srec[b].w = 0u;
@@ -454,49 +459,17 @@ __global__ void __launch_bounds__(kSelThreads) static_select_kernel(const SplitC
     // above overlapped its tail)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     SEL_STAMP(1);
-    // f (the slices' partials summed in order) and ||w||^2 (rounded up) of
-    // this thread's rows, all loads in flight at once
-    const int64_t pstride = static_cast<int64_t>(p.B) * p.nst_pad;
-    const float* fb = p.part + static_cast<int64_t>(b) * p.nst_pad;
+    // f (the K slices' partials, added atomically by the GEMM) and ||w||^2
+    // (the slices' rounded-up sums, added atomically: inflated by 16u for
+    // the round-to-nearest adds) of this thread's rows, all loads in flight
+    float* fb = p.part + static_cast<int64_t>(b) * p.nst_pad;
     const bool regs = p.n_static <= static_cast<int64_t>(kSelThreads) * kSelRows;
     auto load = [&](int64_t r, float& f, float& w2) {
-        float s = 0.0f, q = 0.0f;
-#pragma unroll 4
-        for (int k = 0; k < p.ksplit; ++k) {
-            s += fb[k * pstride + r];
-            q = __fadd_ru(q, p.pnorm[static_cast<int64_t>(k) * p.nst_pad + r]);
-        }
-        f = s;
-        w2 = q;
+        f = fb[r];
+        w2 = __fmul_ru(p.pnorm[r], 1.0f + 16.0f * 5.9604645e-08f);
     };
     float fr[kSelRows], wr[kSelRows];
-    if (regs && p.ksplit <= kSelSplit) {
-        // every load of the thread's rows issued before any is summed
-        float pf[kSelRows][kSelSplit], pw[kSelRows][kSelSplit];
-#pragma unroll
-        for (int i = 0; i < kSelRows; ++i) {
-            const int64_t r = tid + static_cast<int64_t>(i) * kSelThreads;
-#pragma unroll
-            for (int k = 0; k < kSelSplit; ++k) {
-                const bool on = r < p.n_static && k < p.ksplit;
-                pf[i][k] = on ? fb[k * pstride + r] : 0.0f;
-                pw[i][k] = on ? p.pnorm[static_cast<int64_t>(k) * p.nst_pad + r] : 0.0f;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kSelRows; ++i) {
-            float s = 0.0f, q = 0.0f;
-#pragma unroll
-            for (int k = 0; k < kSelSplit; ++k) {
-                if (k < p.ksplit) {
-                    s += pf[i][k];
-                    q = __fadd_ru(q, pw[i][k]);
-                }
-            }
-            fr[i] = s;
-            wr[i] = q;
-        }
-    } else if (regs) {
+    if (regs) {
 #pragma unroll
         for (int i = 0; i < kSelRows; ++i) {
             const int64_t r = tid + static_cast<int64_t>(i) * kSelThreads;
@@ -569,6 +542,8 @@ __global__ void __launch_bounds__(kSelThreads) static_select_kernel(const SplitC
     }
     __syncthreads();
     SEL_STAMP(4);
+    // this request's dots are consumed: leave them zeroed for the next step
+    for (int64_t r = tid; r < p.n_static; r += kSelThreads) fb[r] = 0.0f;
     const unsigned nc = s_nc;
     const bool every = all || nc > static_cast<unsigned>(kSelCand);
     if (!every && nc == 1u && !p.want_exact) {
@@ -618,6 +593,10 @@ __global__ void __launch_bounds__(kCombWarps * 32) split_combine_cert_kernel(
     __shared__ __align__(16) float s_prod[kCombWarps][kProdChunk];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * kCombWarps + warp;
+    // every select has read ||w||^2: leave it zeroed for the next step
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < p.n_static;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p.pnorm[r] = 0.0f;
     if (b >= p.B) return;
     unsigned long long ks = p.keys[b];
     const uint4 sr = p.srec[b];
@@ -689,14 +668,15 @@ bool split_certified_eligible(svt_dtype dt, int64_t n_static, size_t dim) {
     if (const char* v = getenv("SVT_SPLIT_EXACT"))
         if (atoi(v) != 0) return false;
     return dt == SVT_BF16 && n_static > 0 && dim >= 64 && dim <= 8192 && pick_ks(dim) > 0 &&
-           dim / pick_ks(dim) <= kSelSplit;
+           dim / pick_ks(dim) <= 64;
 }
 
 size_t split_certified_ws_bytes(int32_t batch, int64_t n_static, size_t dim) {
     const size_t ksplit = pick_ks(dim) > 0 ? dim / static_cast<size_t>(pick_ks(dim)) : 1;
     const size_t nst_pad = static_cast<size_t>((n_static + kSM - 1) / kSM * kSM);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    return al(ksplit * static_cast<size_t>(batch) * nst_pad * 4) + al(ksplit * nst_pad * 4) +
+    (void)ksplit;
+    return al(static_cast<size_t>(batch) * nst_pad * 4) + al(nst_pad * 4) +
            al(static_cast<size_t>(batch) * 16) + 256;
 }
 
@@ -725,9 +705,9 @@ SplitCertParams make_params(const void* d_static_sub, const uint32_t* d_static_i
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     uint8_t* w = static_cast<uint8_t*>(ws);
     p.part = reinterpret_cast<float*>(w);
-    w += al(static_cast<size_t>(p.ksplit) * batch * p.nst_pad * 4);
+    w += al(static_cast<size_t>(batch) * p.nst_pad * 4);
     p.pnorm = reinterpret_cast<float*>(w);
-    w += al(static_cast<size_t>(p.ksplit) * p.nst_pad * 4);
+    w += al(static_cast<size_t>(p.nst_pad) * 4);
     p.srec = reinterpret_cast<uint4*>(w);
     w += al(static_cast<size_t>(batch) * 16);
     p.stats = reinterpret_cast<unsigned*>(w);
@@ -735,7 +715,8 @@ SplitCertParams make_params(const void* d_static_sub, const uint32_t* d_static_i
     // bound constant (see the header); Cauchy-Schwarz makes it a multiple of
     // ||w|| ||h||, eta covers products that underflow
     // (tensor-core sums of ks products per half, modelled as 8·ks steps of
-    // relative error u; the hi + lo add and the slices' sum: ksplit + 2)
+    // relative error u; the hi + lo add and the slices' atomic sum in any
+    // order: ksplit + 2)
     const double c = (gamma_n(static_cast<double>(dim)) + gamma_n(8.0 * p.ks) +
                       gamma_n(static_cast<double>(p.ksplit) + 2.0) + 1.52587890625e-05) * 1.01;
     p.c_rel = static_cast<float>(c) * (1.0f + FLT_EPSILON);
@@ -764,7 +745,7 @@ svt_status split_static_certified(const void* d_static_sub, const uint32_t* d_st
         static_gemm_kernel<<<grid, kGemmThreads, smem, ss>>>(p);
         SVT_LAUNCH_CHECK("static_gemm_kernel");
     }
-    if (skip & 2) return SVT_OK;
+    if (skip & 2) return SVT_OK;  // (measurement) the caller resets the scratch
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -776,6 +757,16 @@ svt_status split_static_certified(const void* d_static_sub, const uint32_t* d_st
     cfg.numAttrs = 1;
     SVT_CUDA_TRY(cudaLaunchKernelEx(&cfg, static_select_kernel, p));
     return SVT_OK;
+}
+
+// restore the zero invariants of the certified scratch (the dots and
+// ||w||^2 accumulate atomically; the select / combine zero them) on paths
+// that skip the select or the combine
+void split_certified_reset(int32_t batch, int64_t n_static, size_t dim, void* ws, cudaStream_t st) {
+    (void)dim;
+    const size_t nst_pad = static_cast<size_t>((n_static + kSM - 1) / kSM * kSM);
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    cudaMemsetAsync(ws, 0, al(static_cast<size_t>(batch) * nst_pad * 4) + al(nst_pad * 4), st);
 }
 
 svt_status split_combine_certified(const void* d_static_sub, const uint32_t* d_static_ids,

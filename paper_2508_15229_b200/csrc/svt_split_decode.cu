@@ -45,6 +45,7 @@ svt_status split_combine_certified(const void* d_static_sub, const uint32_t* d_s
                                    unsigned long long* keys, void* ws, const void* rec,
                                    const int64_t* d_n_dyn, uint32_t* d_out_ids, float* d_out_max,
                                    cudaStream_t st);
+void split_certified_reset(int32_t batch, int64_t n_static, size_t dim, void* ws, cudaStream_t st);
 svt_status greedy_interleaved_req(const void* d_sub, svt_dtype dt, size_t dim, const int64_t* gb,
                                   const void* meta, const uint32_t* ids, int32_t batch,
                                   int64_t max_groups, const float* hidden, size_t ld,
@@ -350,6 +351,7 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
                                                   d_static_valid, d_first_ids, batch, d_hidden,
                                                   hidden_ld, keys, cws, d_out_max != nullptr, ss)) {
             cudaMemsetAsync(keys, 0, b * 8, ss);
+            split_certified_reset(batch, n_static, dim, cws, ss);
             if (side) cudaEventRecord(side->join, ss), cudaStreamWaitEvent(st, side->join, 0);
             return s;
         }
@@ -398,6 +400,7 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
     if (getenv("SVT_SPLIT_STATIC_ONLY")) {  // measurement only: the static half alone
         if (side) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
         cudaMemsetAsync(keys, 0, b * 8, st);
+        if (certified) split_certified_reset(batch, n_static, dim, cws, st);
         return SVT_OK;
     }
     // dynamic half: requests without dynamic rows have no group (record untouched)
@@ -409,6 +412,7 @@ extern "C" svt_status svt_greedy_split(const void* d_static_sub, svt_dtype dt, i
         // does not fold into stale keys
         if (side) cudaStreamWaitEvent(st, side->join, 0);
         cudaMemsetAsync(keys, 0, b * 8, st);
+        if (certified) split_certified_reset(batch, n_static, dim, cws, st);
         return s;
     }
     if (side) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
