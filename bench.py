@@ -329,25 +329,38 @@ def e2e_session(job, K, W, th, torch, session_mod):
     the static bitmap + prompts (select+gather inside), then per decode step
     H2D of the hidden states from pinned memory and D2H of the ids."""
     B, steps, d = job.B, job.steps, job.cfg["d"]
-    hid_h = job.hidden[:, :, :d].cpu().pin_memory()
+    hid_h = job.hidden[:, :, :d].contiguous().cpu().pin_memory()
     ids_h = torch.empty((steps, B), dtype=torch.int32).pin_memory()
+    ids_h2 = torch.empty((steps, B), dtype=torch.int32).pin_memory()
+    res = {}
     with session_mod.Session(job.head, max_batch=B) as s:
-        def one():
+        # (a) the job's hidden states uploaded once, every decode step on
+        # the device, one D2H (svt_session_decode_host); (b) one host call
+        # and one synchronisation per decode step (svt_session_greedy_host)
+        def batched():
+            s.prepare(job.words_h, job.cfg["V"], job.flat_h, job.off_h)
+            session_mod.decode_host([s], hid_h, steps, ids_h)
+
+        def per_step():
             s.prepare(job.words_h, job.cfg["V"], job.flat_h, job.off_h)
             for t in range(steps):
-                s.greedy(hid_h[t], ids_h[t])
-        for _ in range(W):
-            one()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(K):
-            one()
-        torch.cuda.synchronize()
-        sec = time.perf_counter() - t0
+                s.greedy(hid_h[t], ids_h2[t])
+
+        for name, fn in (("batched", batched), ("per_step", per_step)):
+            for _ in range(W):
+                fn()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(K):
+                fn()
+            torch.cuda.synchronize()
+            res[name] = B * steps * K / (time.perf_counter() - t0)
     h2d = job.words_h.nbytes + job.flat_h.nbytes + job.off_h.nbytes + steps * B * d * 4
     d2h = steps * B * 4 + 3 * B * 8 + B * 8  # ids + plan counters + status words
-    ok = np.array_equal(ids_h.numpy(), job.out.cpu().numpy())
-    return B * steps * K / sec, h2d, d2h, ok
+    want = job.out.cpu().numpy()
+    ok = np.array_equal(ids_h.numpy(), want) and np.array_equal(ids_h2.numpy(), want)
+    e2e_session.per_step = res["per_step"]
+    return res["batched"], h2d, d2h, ok
 
 
 # --------------------------------------------------------------------------
@@ -1072,7 +1085,10 @@ def run_cfg2(args, torch, dist, world, rank):
         # host timing: more steps and a warm-up step damp host-side noise
         e2e_v, h2d, d2h, ok = e2e_session(job, max(4, args.steps // 2), 2, th, torch, session_mod)
         result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                         "d2h_bytes_per_step": d2h, "api": "svt_session_* (host buffers)",
+                         "d2h_bytes_per_step": d2h,
+                         "api": "svt_session_prepare_host + svt_session_decode_host (host "
+                                "buffers: the job's hidden states in, its ids out)",
+                         "per_step_host_calls_tokens_per_s": getattr(e2e_session, "per_step", None),
                          "ids_match_device_path": ok}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_reference(CFG2, B, 2, os.cpu_count() or 1)
