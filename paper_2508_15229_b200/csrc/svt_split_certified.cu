@@ -9,36 +9,38 @@
 // step at cfg2). This file proves which static row wins per request instead
 // and runs only the candidates' chains:
 //
-//  1. static_gemm_kernel (tcgen05.mma kind::f16, M = 128 static rows,
-//     N = 16 requests, f32 accumulators in TMEM): one CTA per (128-row tile,
-//     16-request block, K slice); the A tile comes straight from the
-//     lane-interleaved static block (bulk copies of 512 B reorder it into
-//     the UMMA no-swizzle K-major core-matrix layout, in four K stages so
-//     the MMAs start on the first), and the CTA's threads split its requests'
-//     h = hi + lo + r into that layout (hi = bf16(h), lo = bf16(h - hi),
-//     |r| <= 2^-16 |h|; bf16 x bf16 products are exact in f32): two MMAs per
-//     K step into one accumulator. The epilogue (tcgen05.ld, one thread per
-//     row) stores the slice's partial dots and, from the staged A tile, the
-//     rows' partial sums of squares (rounded up).
-//  2. static_select_kernel (one CTA per request): ||h_b|| rounded up (+inf
-//     when h is not finite); f_br = the K slices'
-//     partials summed in order; with ||w_r|| and ||h_b|| rounded up,
+//  1. static_gemm_kernel (tcgen05.mma kind::f16, f32 accumulators in TMEM):
+//     one CTA per (128 static rows, 128-wide K slice, 64 requests). The
+//     threads copy the rows' 16-byte chunks from the lane-interleaved static
+//     block into 128B-swizzled K-major tiles (cp.async) and split the
+//     requests' h = hi + lo + r (hi = bf16(h), lo = bf16(h - hi),
+//     |r| <= 2^-16 |h|; bf16 x bf16 products are exact in f32) into a B tile
+//     whose N = 128 rows are hi then lo: one MMA (M = 128, N = 128, K = 16)
+//     per K step reads the A tile once for both halves. The epilogue
+//     (tcgen05.ld, one thread per row) adds f = D[hi] + D[lo] into the
+//     request's dot (red.add.f32, any order) and the row's rounded-up
+//     partial sum of squares into ||w_r||^2.
+//  2. static_select_kernel (one CTA per request, a programmatic dependent
+//     of the GEMM: ||h_b|| is computed before the wait), with ||w_r|| and
+//     ||h_b|| rounded up,
 //       |f_br - ref_br| <= B_br = c ||w_r|| ||h_b|| + eta,
-//       c = (γ_d [reference] + γ_{8·2·Ks} [tensor-core accumulation, a
-//            deliberately loose 4u-per-step model] + γ_{ksplit+1} [slice
-//            sum] + 2^-16 [split residual]) * 1.01,
+//       c = (γ_d [reference] + γ_{8·Ks} [tensor-core accumulation, a
+//            deliberately loose model] + γ_{ksplit+2} [hi + lo, slices in
+//            any order] + 2^-16 [split residual]) * 1.01,
 //     by Cauchy-Schwarz (Σ|w h| <= ||w|| ||h||). L = max_r (f - B); the
 //     static argmax (first max, the reference's scan restricted to T) is
-//     among {r : f + B >= L}; those rows (typically one or two) are
-//     recomputed in the exact reference order and the request's static key
-//     (value, ~id; NaN at the plan's smallest id wins) is written for the
-//     split combine. Non-finite values or too many candidates: every static
-//     row is recomputed.
-// The whole static half stays on the split decode's side stream, beside the
-// HBM-bound dynamic GEMV.
+//     among {r : f + B >= L}. One candidate in an ids-only call: its
+//     interval and id go to the combine. Otherwise (more candidates, a
+//     requested logit, non-finite values: every static row) the candidates
+//     are recomputed in the exact reference order and the request's static
+//     key (value, ~id; NaN at the plan's smallest id wins) is written.
+//  3. split_combine_cert_kernel (a warp per request): the exact dynamic
+//     maximum against the static key or interval; where an interval and the
+//     dynamic value meet, the static row's exact chain decides.
+// The static half stays on the split decode's side stream, beside the
+// dynamic GEMV; the select fits in 64 registers so it co-resides with it.
 #include <cfloat>
 #include <cstdlib>
-#include <cuda.h>
 
 #include "svt_common.cuh"
 
@@ -89,7 +91,8 @@ struct SplitCertParams {
     float c_rel;
     float eta;
     unsigned* stats;           // [0] requests decided by one candidate, [1] by more
-    int32_t dbg_mode;          // measurement only (SVT_CERT_SKIP bits 4, 8; 16 = stamps)
+    int32_t dbg_mode;          // measurement only (SVT_CERT_SKIP: 1 no GEMM, 2 no select,
+                               // 8 no h loads, 16 %globaltimer stamps)
 };
 #define SEL_STAMP(k)                                                                           \
     if ((p.dbg_mode & 16) && threadIdx.x == 0 && blockIdx.x < 256) g_sel_stamps[blockIdx.x * 8 + (k)] = gtime();
