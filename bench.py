@@ -899,7 +899,7 @@ def run_cfg1(args, torch, dist, world, rank):
     fast, slow = jobs.stats()
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": load_traffic("rows_fast_cfg1"),
+        "frac": achieved / peak, "traffic": load_traffic("rows_hs_cfg1"),
         "kernel": "rows_hs_kernel<f32,4,9> (svt_greedy_certified_rows with "
                   "SVT_ROWS_HIDDEN_STABLE: 147 rows CTAs + 1 finalizer CTA, one launch per "
                   "decode token; the first token after each gather: rows_fast_kernel + "
