@@ -721,8 +721,7 @@ def cfg1_e2e(jobs, K, W, torch, th, session_mod):
 
     def one():
         t0 = time.perf_counter()
-        for j in range(R):
-            sess[j].prepare(jobs.words_h, V, jobs.prompts_h[j], offs[j])
+        session_mod.prepare_many(sess, jobs.words_h, V, jobs.prompts_h, offs)
         t1 = time.perf_counter()
         session_mod.decode_host(sess, hid_h, steps, ids_h)
         t2 = time.perf_counter()
@@ -744,9 +743,10 @@ def cfg1_e2e(jobs, K, W, torch, th, session_mod):
             x.close()
     one.breakdown = {"prepare_ms_per_step": split[0] / K * 1e3,
                      "decode_host_ms_per_step": split[1] / K * 1e3,
-                     "what": "host clock: R x svt_session_prepare_host (static bitmap + prompt H2D, "
-                             "select, row gather, one sync each) vs one svt_session_decode_host "
-                             "(hidden states H2D, the 64 x R certified tokens, ids D2H)"}
+                     "what": "host clock: svt_session_prepare_host_many over the R sessions "
+                             "(static bitmap + prompt H2D, select, row gather; one sync) vs one "
+                             "svt_session_decode_host (hidden states H2D, the 64 x R certified "
+                             "tokens, ids D2H)"}
     cfg1_e2e.breakdown = one.breakdown
     h2d = R * (jobs.words_h.nbytes + jobs.prompts_h[0].nbytes + 16) + steps * R * d * 4
     d2h = steps * R * 4 + R * 4 * 8  # ids + per-job plan counters / status words
@@ -936,8 +936,8 @@ def run_cfg1(args, torch, dist, world, rank):
                                             session_mod)
         result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
-                         "api": "svt_session_prepare_host x R + svt_session_decode_host "
-                                "(host buffers)", "ids_match_device_path": ok,
+                         "api": "svt_session_prepare_host_many (R sessions) + "
+                                "svt_session_decode_host (host buffers)", "ids_match_device_path": ok,
                          "breakdown": getattr(cfg1_e2e, "breakdown", None)}
     ids_dev = jobs.out.cpu().numpy().view(np.uint32).copy()
     head = jobs.head

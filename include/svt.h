@@ -674,6 +674,17 @@ svt_status svt_session_destroy(svt_session* s);
 svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_words,
                                     size_t static_universe, const uint32_t* h_input_ids,
                                     const int64_t* h_input_offsets, int32_t batch);
+/* svt_session_prepare_host for n sessions with one synchronisation per
+ * distinct stream instead of one per session: every session's H2D, select,
+ * layout and gather are enqueued first, then the plan counts are read back
+ * and checked (the first failing session's error is returned, in session
+ * order), then batch-1 sessions gather their rows. Session i uses
+ * h_input_ids[i], h_input_offsets[i] (batches[i] + 1 entries), batches[i]. */
+svt_status svt_session_prepare_host_many(svt_session* const* sessions, int32_t n_sessions,
+                                         const uint64_t* h_static_words, size_t static_universe,
+                                         const uint32_t* const* h_input_ids,
+                                         const int64_t* const* h_input_offsets,
+                                         const int32_t* batches);
 /* Copy the prepared plans back: per request n_active/n_static/n_dynamic
  * (each batch-long, optional) and ids in CSR order (optional). */
 svt_status svt_session_plans_host(svt_session* s, int64_t* h_n_active, int64_t* h_n_static,

@@ -136,6 +136,7 @@ _SIGS = {
     "svt_session_create": ([C.POINTER(_vp), _vp, C.c_int, _sz, _sz, _i32, _i64, _vp], C.c_int),
     "svt_session_destroy": ([_vp], C.c_int),
     "svt_session_prepare_host": ([_vp, _vp, _sz, _vp, _vp, _i32], C.c_int),
+    "svt_session_prepare_host_many": ([_vp, C.c_int32, _vp, _sz, _vp, _vp, _vp], C.c_int),
     "svt_session_plans_host": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "svt_session_greedy_host": ([_vp, _vp, _sz, _vp, _vp], C.c_int),
     "svt_session_greedy_device": ([_vp, _vp, _sz, _vp, _vp], C.c_int),

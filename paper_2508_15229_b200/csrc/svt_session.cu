@@ -27,6 +27,9 @@ struct svt_session {
     int32_t batch = 0;
     int64_t max_groups = 0;
     std::vector<int64_t> n_active, n_static, n_dynamic, act_off;
+    std::vector<int64_t> meta_h;  // prepare: n_active | n_static | n_dynamic | first_bad (D2H)
+    const uint32_t* prep_ids = nullptr;   // prepare: the caller's ids / offsets (error text)
+    const int64_t* prep_offs = nullptr;
 
     // device buffers (capacity in elements)
     uint64_t* d_words = nullptr;
@@ -372,9 +375,15 @@ svt_status svt_session_destroy(svt_session* s) {
 
 svt_stream svt_session_stream(svt_session* s) { return s ? s->stream : nullptr; }
 
-svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_words,
-                                    size_t static_universe, const uint32_t* h_input_ids,
-                                    const int64_t* h_input_offsets, int32_t batch) {
+}  // extern "C"
+
+namespace {
+// prepare, phase 1: everything up to the plan-count read-back, enqueued on
+// the session's stream (no synchronisation); *done = the batch was empty
+svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_t static_universe,
+                           const uint32_t* h_input_ids, const int64_t* h_input_offsets,
+                           int32_t batch, bool* done) {
+    *done = true;
     if (!s) {
         set_error("null session");
         return SVT_ERR_CONFIG;
@@ -455,16 +464,31 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
                                     s->split ? s->d_dyn_ids : s->d_active, s->group_begin_d(),
                                     s->d_group_req, batch, s->max_groups, s->d_sub, s->d_bad, q);
     if (st) return st;
-    std::vector<int64_t> meta(4 * B);
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data(), s->n_active_d(), B * sizeof(int64_t),
+    s->meta_h.assign(4 * B, 0);
+    int64_t* meta = s->meta_h.data();
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta, s->n_active_d(), B * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data() + B, s->n_static_d(), B * sizeof(int64_t),
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta + B, s->n_static_d(), B * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data() + 2 * B, s->n_dynamic_d(), B * sizeof(int64_t),
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta + 2 * B, s->n_dynamic_d(), B * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta.data() + 3 * B, s->first_bad_d(), B * sizeof(int64_t),
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta + 3 * B, s->first_bad_d(), B * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaStreamSynchronize(q));
+    s->prep_ids = h_input_ids;
+    s->prep_offs = h_input_offsets;
+    *done = false;
+    return SVT_OK;
+}
+
+// prepare, phase 2 (after the session's stream was synchronised): the plan
+// counts, the reference's error order, and the batch-1 row gather
+svt_status prepare_finish(svt_session* s) {
+    const size_t B = static_cast<size_t>(s->batch);
+    cudaStream_t q = s->stream;
+    svt_status st = SVT_OK;
+    const std::vector<int64_t>& meta = s->meta_h;
+    const uint32_t* h_input_ids = s->prep_ids;
+    const int64_t* h_input_offsets = s->prep_offs;
     s->n_active.assign(meta.begin(), meta.begin() + B);
     s->n_static.assign(meta.begin() + B, meta.begin() + 2 * B);
     s->n_dynamic.assign(meta.begin() + 2 * B, meta.begin() + 3 * B);
@@ -507,6 +531,59 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
             return st;
         }
     }
+    return SVT_OK;
+}
+}  // namespace
+
+extern "C" {
+
+svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_words,
+                                    size_t static_universe, const uint32_t* h_input_ids,
+                                    const int64_t* h_input_offsets, int32_t batch) {
+    bool done = false;
+    if (svt_status st = prepare_enqueue(s, h_static_words, static_universe, h_input_ids,
+                                        h_input_offsets, batch, &done))
+        return st;
+    if (done) return SVT_OK;
+    SVT_CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return prepare_finish(s);
+}
+
+svt_status svt_session_prepare_host_many(svt_session* const* sessions, int32_t n_sessions,
+                                         const uint64_t* h_static_words, size_t static_universe,
+                                         const uint32_t* const* h_input_ids,
+                                         const int64_t* const* h_input_offsets,
+                                         const int32_t* batches) {
+    if (!sessions || n_sessions < 0 || (n_sessions > 0 && (!h_input_ids || !h_input_offsets ||
+                                                           !batches))) {
+        set_error("prepare_host_many: null argument");
+        return SVT_ERR_CONFIG;
+    }
+    std::vector<char> pending(static_cast<size_t>(n_sessions), 0);
+    svt_status first = SVT_OK;
+    for (int32_t i = 0; i < n_sessions; ++i) {
+        bool done = false;
+        const svt_status st = prepare_enqueue(sessions[i], h_static_words, static_universe,
+                                              h_input_ids[i], h_input_offsets[i], batches[i],
+                                              &done);
+        if (st) {
+            first = st;
+            break;
+        }
+        pending[static_cast<size_t>(i)] = done ? 0 : 1;
+    }
+    // one synchronisation per distinct stream, then every session's finish
+    for (int32_t i = 0; i < n_sessions; ++i) {
+        if (!pending[static_cast<size_t>(i)]) continue;
+        bool seen = false;
+        for (int32_t j = 0; j < i; ++j)
+            seen = seen || (pending[static_cast<size_t>(j)] && sessions[j]->stream == sessions[i]->stream);
+        if (!seen) SVT_CUDA_TRY(cudaStreamSynchronize(sessions[i]->stream));
+    }
+    if (first) return first;
+    for (int32_t i = 0; i < n_sessions; ++i)
+        if (pending[static_cast<size_t>(i)])
+            if (svt_status st = prepare_finish(sessions[i])) return st;
     return SVT_OK;
 }
 

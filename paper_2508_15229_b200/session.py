@@ -68,6 +68,22 @@ class Session:
         return out_ids
 
 
+def prepare_many(sessions, static_words: np.ndarray, V: int, prompts, offsets):
+    """svt_session_prepare_host_many: prepare every session (session i over
+    prompts[i] / offsets[i]) with one synchronisation per stream."""
+    w = np.ascontiguousarray(static_words, np.uint64)
+    ps = [np.ascontiguousarray(p, np.uint32) for p in prompts]
+    os_ = [np.ascontiguousarray(o, np.int64) for o in offsets]
+    n = len(sessions)
+    arr = (C.c_void_p * n)(*[s.h.value for s in sessions])
+    pid = (C.c_void_p * n)(*[p.ctypes.data if p.size else None for p in ps])
+    poff = (C.c_void_p * n)(*[o.ctypes.data for o in os_])
+    bs = (C.c_int32 * n)(*[len(o) - 1 for o in os_])
+    call("svt_session_prepare_host_many", arr, n, w.ctypes.data, V, pid, poff, bs)
+    for s_, o in zip(sessions, os_):
+        s_.B = len(o) - 1
+
+
 def decode_host(sessions, hidden, steps: int, out_ids=None):
     """svt_session_decode_host: `steps` token-interleaved decode steps over
     prepared sessions sharing one stream. hidden: host [steps][sum B][dim]

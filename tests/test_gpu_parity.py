@@ -889,6 +889,36 @@ def test_rows_cfg1_all_64_steps_graph_and_exact_logits(th):
             assert gid == want[t, j] and bits([gmax])[0] == bits([wmax[t, j]])[0], (t, j)
 
 
+def test_session_prepare_many(th):
+    """svt_session_prepare_host_many (one sync for every session) prepares
+    the same plans as per-session prepares: five batch-1 sessions on one
+    stream then decode_host equals the reference; an out-of-range prompt id
+    in the third session raises the reference's IntegrityError."""
+    from paper_2508_15229_b200 import session
+
+    V, d, steps, R = 128256, 2048, 4, 5
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_F32, R, 512, 2048, steps)
+    W = head.to_host()
+    plans = [orc.select(prompts[j], words, V, V).active_ids for j in range(R)]
+    want = np.array([[orc.greedy_step(W[plans[j]], hid[t][j], plans[j])[0] for j in range(R)]
+                     for t in range(steps)], np.uint32)
+    st = torch.cuda.Stream()
+    sess = [session.Session(head, max_batch=1, stream=st) for _ in range(R)]
+    offs = [np.array([0, len(p)], np.int64) for p in prompts]
+    try:
+        for rnd in range(2):
+            session.prepare_many(sess, words, V, prompts, offs)
+            ids = session.decode_host(sess, np.ascontiguousarray(hid, np.float32), steps)
+            assert np.array_equal(ids, want), rnd
+        bad = [p.copy() for p in prompts]
+        bad[2][7] = V + 3
+        with pytest.raises(th.IntegrityError, match=f"input token id {V + 3} out of range"):
+            session.prepare_many(sess, words, V, bad, offs)
+    finally:
+        for s_ in sess:
+            s_.close()
+
+
 def test_session_batch1_rows_and_decode_host(th):
     """Batch-1 sessions run the certified rows kernel (row-major gather per
     prepare); svt_session_decode_host over three sessions sharing a stream
