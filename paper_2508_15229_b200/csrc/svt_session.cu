@@ -27,7 +27,7 @@ struct svt_session {
     int32_t batch = 0;
     int64_t max_groups = 0;
     std::vector<int64_t> n_active, n_static, n_dynamic, act_off;
-    std::vector<int64_t> meta_h;  // prepare: n_active | n_static | n_dynamic | first_bad (D2H)
+    size_t meta_off = 0;  // prepare: n_active | n_static | n_dynamic | first_bad in h_stage
     const uint32_t* prep_ids = nullptr;   // prepare: the caller's ids / offsets (error text)
     const int64_t* prep_offs = nullptr;
 
@@ -52,6 +52,8 @@ struct svt_session {
     size_t cap_ws = 0;
     int32_t* d_bad = nullptr;
     // pinned host mirrors
+    uint8_t* h_stage = nullptr;  // prepare: static words | prompt ids | offsets (async H2D)
+    size_t cap_stage = 0;
     float* h_hidden = nullptr;
     uint32_t* h_ids = nullptr;
     float* h_max = nullptr;
@@ -131,7 +133,7 @@ void free_all(svt_session* s) {
                    s->d_multi, s->d_multi_ids};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* host[] = {s->h_hidden, s->h_ids, s->h_max};
+    void* host[] = {s->h_hidden, s->h_ids, s->h_max, s->h_stage};
     for (void* p : host)
         if (p) cudaFreeHost(p);
 }
@@ -434,16 +436,35 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
     if (B == 0) return SVT_OK;
 
     cudaStream_t q = s->stream;
-    std::vector<int64_t> in_off(B + 1);
+    // the host inputs are staged in pinned memory so the copies are truly
+    // asynchronous (the previous prepare of this session has synchronised,
+    // so the staging area is free)
+    const size_t o_words = 0, o_in = nw * sizeof(uint64_t);
+    const size_t o_inoff = (o_in + n_inputs * sizeof(uint32_t) + 15) & ~size_t(15);
+    const size_t o_actoff = o_inoff + (B + 1) * sizeof(int64_t);
+    const size_t o_meta = o_actoff + (B + 1) * sizeof(int64_t);  // D2H: the plan counts
+    const size_t stage = o_meta + 4 * B * sizeof(int64_t);
+    if (stage > s->cap_stage) {
+        if (s->h_stage) cudaFreeHost(s->h_stage);
+        s->h_stage = nullptr;
+        s->cap_stage = 0;
+        SVT_CUDA_TRY(cudaMallocHost(&s->h_stage, stage + stage / 2));
+        s->cap_stage = stage + stage / 2;
+    }
+    std::memcpy(s->h_stage + o_words, h_static_words, nw * sizeof(uint64_t));
+    if (n_inputs)
+        std::memcpy(s->h_stage + o_in, h_input_ids + h_input_offsets[0], n_inputs * sizeof(uint32_t));
+    int64_t* in_off = reinterpret_cast<int64_t*>(s->h_stage + o_inoff);
     for (size_t b = 0; b <= B; ++b) in_off[b] = h_input_offsets[b] - h_input_offsets[0];
-    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_words, h_static_words, nw * sizeof(uint64_t),
+    std::memcpy(s->h_stage + o_actoff, s->act_off.data(), (B + 1) * sizeof(int64_t));
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_words, s->h_stage + o_words, nw * sizeof(uint64_t),
                                  cudaMemcpyHostToDevice, q));
     if (n_inputs)
-        SVT_CUDA_TRY(cudaMemcpyAsync(s->d_inputs, h_input_ids + h_input_offsets[0],
-                                     n_inputs * sizeof(uint32_t), cudaMemcpyHostToDevice, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_in_off, in_off.data(), (B + 1) * sizeof(int64_t),
+        SVT_CUDA_TRY(cudaMemcpyAsync(s->d_inputs, s->h_stage + o_in, n_inputs * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_in_off, in_off, (B + 1) * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_act_off, s->act_off.data(), (B + 1) * sizeof(int64_t),
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_act_off, s->h_stage + o_actoff, (B + 1) * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, q));
     SVT_CUDA_TRY(cudaMemsetAsync(s->d_bad, 0, sizeof(int32_t), q));
     st = svt_select_batched(s->d_words, static_universe, s->rows, s->d_inputs, s->d_in_off, batch,
@@ -464,8 +485,9 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
                                     s->split ? s->d_dyn_ids : s->d_active, s->group_begin_d(),
                                     s->d_group_req, batch, s->max_groups, s->d_sub, s->d_bad, q);
     if (st) return st;
-    s->meta_h.assign(4 * B, 0);
-    int64_t* meta = s->meta_h.data();
+    // (into pinned memory: the read-back stays asynchronous)
+    int64_t* meta = reinterpret_cast<int64_t*>(s->h_stage + o_meta);
+    s->meta_off = o_meta;
     SVT_CUDA_TRY(cudaMemcpyAsync(meta, s->n_active_d(), B * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, q));
     SVT_CUDA_TRY(cudaMemcpyAsync(meta + B, s->n_static_d(), B * sizeof(int64_t),
@@ -486,12 +508,12 @@ svt_status prepare_finish(svt_session* s) {
     const size_t B = static_cast<size_t>(s->batch);
     cudaStream_t q = s->stream;
     svt_status st = SVT_OK;
-    const std::vector<int64_t>& meta = s->meta_h;
+    const int64_t* meta = reinterpret_cast<const int64_t*>(s->h_stage + s->meta_off);
     const uint32_t* h_input_ids = s->prep_ids;
     const int64_t* h_input_offsets = s->prep_offs;
-    s->n_active.assign(meta.begin(), meta.begin() + B);
-    s->n_static.assign(meta.begin() + B, meta.begin() + 2 * B);
-    s->n_dynamic.assign(meta.begin() + 2 * B, meta.begin() + 3 * B);
+    s->n_active.assign(meta, meta + B);
+    s->n_static.assign(meta + B, meta + 2 * B);
+    s->n_dynamic.assign(meta + 2 * B, meta + 3 * B);
     for (size_t b = 0; b < B; ++b) {
         const int64_t bad = meta[3 * B + b];
         if (bad >= 0) {
