@@ -53,8 +53,9 @@ constexpr int kGemmThreads = 256;
 constexpr int kSelThreads = 512;
 constexpr int kSelRows = 4;      // static rows per select thread kept in registers
 constexpr int kChainWarps = 8;   // warps running exact chains
+constexpr int kSelH = 1024;      // hidden values staged in shared memory by the select
 constexpr int kSelCand = 256;  // candidate list per request (more: every row)
-constexpr int kProdChunk = 512;   // exact recompute: products staged per pass (per warp)
+constexpr int kProdChunk = 1024;  // exact recompute: products staged per pass (per warp)
 
 // measurement only (SVT_CERT_STAMPS=1): per GEMM CTA 8 %globaltimer stamps
 __device__ unsigned long long g_cert_stamps[512 * 8];
@@ -332,24 +333,22 @@ __device__ float exact_static_row(const SplitCertParams& p, int64_t r, const flo
     float acc = 0.0f;
     for (int k0 = 0; k0 < p.dim; k0 += kProdChunk) {
         const int kn = p.dim - k0 < kProdChunk ? p.dim - k0 : kProdChunk;
-        // kProdChunk / 8 / 32 = 4 chunks per lane: every load first
+        // kProdChunk / 8 / 32 chunks per lane: every weight load first (h is
+        // read from shared memory when the caller staged it there)
         constexpr int kPer = kProdChunk / 8 / 32;
         uint4 wv[kPer];
-        float4 ha[kPer], hb[kPer];
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             const int c = lane + 32 * j;
-            if (c < kn / 8) {
-                wv[j] = rowp[static_cast<int64_t>(k0 / 8 + c) * 32];
-                ha[j] = __ldg(reinterpret_cast<const float4*>(h + k0 + c * 8));
-                hb[j] = __ldg(reinterpret_cast<const float4*>(h + k0 + c * 8 + 4));
-            }
+            if (c < kn / 8) wv[j] = rowp[static_cast<int64_t>(k0 / 8 + c) * 32];
         }
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
             const int c = lane + 32 * j;
             if (c < kn / 8) {
-                const float hv[8] = {ha[j].x, ha[j].y, ha[j].z, ha[j].w, hb[j].x, hb[j].y, hb[j].z, hb[j].w};
+                const float4 ha = *reinterpret_cast<const float4*>(h + k0 + c * 8);
+                const float4 hb = *reinterpret_cast<const float4*>(h + k0 + c * 8 + 4);
+                const float hv[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
                 const uint32_t u[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
                 float4 q0, q1;
                 q0.x = __fmul_rn(__uint_as_float(u[0] << 16), hv[0]);
@@ -411,6 +410,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) static_select_kernel(const Spl
     __shared__ uint32_t s_one[2];
     __shared__ unsigned long long s_key;
     __shared__ __align__(16) float s_prod[kChainWarps][kProdChunk];
+    __shared__ __align__(16) float s_hid[kSelH];  // h_b (d <= kSelH): the chains' operand
     const int b = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (p.st_valid[b] <= 0) {
@@ -457,6 +457,10 @@ __global__ void __launch_bounds__(kSelThreads, 2) static_select_kernel(const Spl
         for (int o = 16; o > 0; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xFFFFFFFFu, ss, o));
         bad = __any_sync(0xFFFFFFFFu, bad);
         if (lane == 0) s_hn = bad ? __int_as_float(0x7F800000) : __fsqrt_ru(ss);
+    } else if (p.dim <= kSelH) {
+        // the other warps stage h for the exact chains
+        for (int k = (tid - 32) * 4; k < p.dim; k += (kSelThreads - 32) * 4)
+            *reinterpret_cast<float4*>(s_hid + k) = __ldg(reinterpret_cast<const float4*>(h + k));
     }
     // the partials are the GEMM's (a programmatic dependency: everything
     // above overlapped its tail)
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) static_select_kernel(const Spl
         unsigned long long best = 0ull;
         for (int64_t i = warp; i < nwork; i += kChainWarps) {
             const int64_t r = every ? i : static_cast<int64_t>(s_cand[i]);
-            const float v = exact_static_row(p, r, h, s_prod[warp], lane);
+            const float v = exact_static_row(p, r, p.dim <= kSelH ? s_hid : h, s_prod[warp], lane);
             const uint32_t id = p.st_ids[r];
             const unsigned long long key = make_key(v, id, true, v != v && id == first);
             best = key > best ? key : best;

@@ -19,8 +19,19 @@ from paper_2508_15229_b200 import tailored_head as th  # noqa: E402
 job = bench.Job(bench.CFG2, 64, 4, 0, torch, th, synth)
 job.run("split")
 torch.cuda.synchronize()
-for _ in range(3):
+# warm: back-to-back steps in a CUDA graph (stamps of the last one kept)
+st = torch.cuda.Stream()
+job.sdec.stream = st
+with torch.cuda.stream(st):
     job.sdec.greedy(job.hidden[0], job.out[0])
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for t in range(16):
+        job.sdec.greedy(job.hidden[t % job.steps], job.out[0])
+with torch.cuda.stream(st):
+    for _ in range(4):
+        g.replay()
 torch.cuda.synchronize()
 buf = np.zeros(512 * 8 + 256 * 8, np.uint64)
 th._lib.lib.svt_cert_stamps_read.argtypes = [ctypes.c_void_p]
