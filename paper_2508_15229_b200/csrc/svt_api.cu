@@ -239,7 +239,7 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
                                 size_t ld, uint32_t row_base, int32_t plan_start, int32_t flags,
                                 uint32_t* out_ids, float* out_max, uint64_t* out_keys, void* ws,
                                 svt_stream stream, const uint8_t* plan_start_req = nullptr,
-                                int32_t smem_budget = 0) {
+                                int32_t smem_budget = 0, int32_t warps_cap = 0) {
     if (svt_status s = check_dtype(dt)) return s;
     if (svt_status s = need_device()) return s;
     if (batch <= 0) return SVT_OK;
@@ -265,6 +265,7 @@ static svt_status greedy_common(int src, const void* W, svt_dtype dt, size_t row
     p.plan_start_req = plan_start_req;
     p.smem_budget = smem_budget;
     p.weights_stable = (flags & SVT_WEIGHTS_STABLE) ? 1 : 0;
+    p.warps_cap = warps_cap;
     return gemv_run(src, MODE_ARGMAX, dt, p, static_cast<cudaStream_t>(stream));
 }
 
@@ -338,7 +339,7 @@ svt_status greedy_interleaved_req(const void* d_sub, svt_dtype dt, size_t dim,
     const int32_t budget = env ? atoi(env) : 112 * 1024;
     return greedy_common(SRC_INTERLEAVED, d_sub, dt, 0, dim, gb, meta, ids, batch, max_groups,
                          hidden, ld, 0, 0, flags, out_ids, nullptr, out_keys, ws, st,
-                         plan_start_req, budget);
+                         plan_start_req, budget, 4);
 }
 }  // namespace svt
 

@@ -509,7 +509,11 @@ svt_status launch_ring(GemvParams p, cudaStream_t st) {
     // measured on B200 (tools/sweep_decode.py, cfg2 bf16): the interleaved
     // stream is consumer-bound up to 6 pairs and best at 6 x 3 stages; the
     // fused row gather is producer-bound and best at 8 pairs
-    const int wmax = g_tuning.warps > 0 ? g_tuning.warps : (SRC == SRC_INTERLEAVED ? 6 : 8);
+    // (the split decode's dynamic half shares the SMs with the static half:
+    // 4 pairs, measured 21.3 against 21.9 us per cfg2 step with 6)
+    const int wmax = g_tuning.warps > 0 ? g_tuning.warps
+                                        : (p.warps_cap > 0 ? p.warps_cap
+                                                           : (SRC == SRC_INTERLEAVED ? 6 : 8));
     nwa = nwa < 1 ? 1 : (nwa > wmax ? wmax : nwa);
     // one pair per SM (small batches): deep 32 KB stages
     if (nwa == 1 && p.nchunks >= 64) return launch_ring_cr<DT, SRC, MODE, 64>(p, st, nwa, grid);

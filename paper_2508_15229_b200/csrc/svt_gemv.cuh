@@ -53,6 +53,7 @@ struct GemvParams {
     int32_t smem_budget;
     int32_t stages;
     int32_t weights_stable;  // sub-head / rows not written by the kernel this launch depends on
+    int32_t warps_cap;       // > 0: at most this many warp pairs per CTA (split decode: 4)
     int64_t single_rows;
     // optional instrumentation (svt_set_debug): per (block, pair) cycle
     // counters {producer total, producer empty-wait, consumer total,
