@@ -45,6 +45,10 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "svt_common.cuh"
 
 namespace svt {
@@ -1446,13 +1450,60 @@ double gamma_n(double n) {
     return n * u / (1.0 - n * u);
 }
 
+// Measurement / A-B knobs of this path, read once per process: the batch-1
+// decode is host-launch bound at a few microseconds per token, and getenv
+// scans the whole environment on every call.
+struct Knob {
+    bool set = false;
+    int value = 0;
+};
+Knob read_knob(const char* name) {
+    Knob k;
+    if (const char* v = getenv(name)) {
+        k.set = true;
+        k.value = atoi(v);
+    }
+    return k;
+}
+struct RowsKnobs {
+    Knob rows_hs = read_knob("SVT_ROWS_HS"), hs_grid = read_knob("SVT_HS_GRID"),
+         rows_hs_nb = read_knob("SVT_ROWS_HS_NB"), rows_fast = read_knob("SVT_ROWS_FAST"),
+         rows_grid = read_knob("SVT_ROWS_GRID"), rows_fin = read_knob("SVT_ROWS_FIN"),
+         fast_variant = read_knob("SVT_FAST_VARIANT"), fin_warps = read_knob("SVT_HS_FIN_WARPS"),
+         fin_stagger = read_knob("SVT_HS_FIN_STAGGER"), rows_variant = read_knob("SVT_ROWS_VARIANT");
+    bool l2_keep = false;
+    RowsKnobs() {
+        if (const char* v = getenv("SVT_ROWS_L2")) l2_keep = v[0] == 'k' || v[0] == 'l';
+    }
+};
+const RowsKnobs& knobs() {
+    static const RowsKnobs k;
+    return k;
+}
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device
+// and size (a per-launch call costs host time on the token path)
+std::mutex g_smem_mu;
+std::map<std::pair<const void*, int>, int> g_smem_set;  // (kernel, device) -> bytes set
+template <typename K>
+cudaError_t ensure_dyn_smem(K kern, size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::pair<const void*, int> key(reinterpret_cast<const void*>(kern), dev);
+    std::lock_guard<std::mutex> lock(g_smem_mu);
+    auto it = g_smem_set.find(key);
+    if (it != g_smem_set.end() && it->second >= static_cast<int>(bytes)) return cudaSuccess;
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e == cudaSuccess) g_smem_set[key] = static_cast<int>(bytes);
+    return e;
+}
+
 template <int DT, int CPL>
 svt_status launch_rows(SmallParams p, int grid, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(p.slots) * static_cast<size_t>(p.row_bytes) +
                         static_cast<size_t>(p.dim) * 4;
     auto kern = greedy_rows_kernel<DT, CPL>;
-    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+    SVT_CUDA_TRY(ensure_dyn_smem(kern, smem));
     p.grid = grid;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1468,8 +1519,7 @@ svt_status launch_rows(SmallParams p, int grid, cudaStream_t st) {
     // the one-warp finalize, a programmatic dependent of the rows grid
     const size_t fsmem = kMaxCand * 4 + 2 * kPiece + static_cast<size_t>(p.dim) * 4;
     auto fin = greedy_rows_finalize_kernel<DT>;
-    SVT_CUDA_TRY(cudaFuncSetAttribute(fin, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(fsmem)));
+    SVT_CUDA_TRY(ensure_dyn_smem(fin, fsmem));
     cudaLaunchConfig_t fc = {};
     fc.gridDim = dim3(1);
     fc.blockDim = dim3(32);
@@ -1488,8 +1538,7 @@ svt_status launch_rows_fast(FastParams p, cudaStream_t st) {
     const size_t fin_smem = kMaxCand * 4 + 2 * kPiece + static_cast<size_t>(p.dim) * 4;
     smem = smem > fin_smem ? smem : fin_smem;  // the finalizer's recompute buffers
     auto kern = rows_fast_kernel<DT, CPT, RPG>;
-    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+    SVT_CUDA_TRY(ensure_dyn_smem(kern, smem));
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1508,8 +1557,7 @@ svt_status launch_rows_fast(FastParams p, cudaStream_t st) {
     if (smem < sm_smem && sm_smem - smem > fsmem) fsmem = sm_smem - smem;
     if (fsmem > 200 * 1024) fsmem = 200 * 1024;
     auto fin = rows_fast_fin_kernel<DT>;
-    SVT_CUDA_TRY(cudaFuncSetAttribute(fin, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(fsmem)));
+    SVT_CUDA_TRY(ensure_dyn_smem(fin, fsmem));
     cudaLaunchConfig_t fc = {};
     fc.gridDim = dim3(1);
     fc.blockDim = dim3(32 * kFinWarps);
@@ -1528,8 +1576,7 @@ svt_status launch_rows_hs(FastParams p, cudaStream_t st) {
     const size_t fin_smem = kMaxCand * 4 + 2 * kPiece + static_cast<size_t>(p.dim) * 4;
     smem = smem > fin_smem ? smem : fin_smem;  // the finalizer CTA's recompute buffers
     auto kern = rows_hs_kernel<DT, CPT, RPG>;
-    SVT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+    SVT_CUDA_TRY(ensure_dyn_smem(kern, smem));
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1557,15 +1604,14 @@ svt_status pick_rpg_hs(FastParams p, int rpg, cudaStream_t st) {
 // CTA per SM, and at least two ring slots per group within kHSmemBudget.
 bool rows_hs_eligible(int64_t n, size_t row_bytes, size_t dim, int* grid_out, int* rpg_out,
                       int* cpt_out, int* nb_out) {
-    if (const char* v = getenv("SVT_ROWS_HS"))
-        if (atoi(v) == 0) return false;
+    if (knobs().rows_hs.set && knobs().rows_hs.value == 0) return false;
     const size_t nchunks = row_bytes / 16;
     if (nchunks % kFTPG != 0) return false;
     const int cpt = static_cast<int>(nchunks / kFTPG);
     if (cpt != 1 && cpt != 2 && cpt != 4) return false;
     const int sms = sm_count();
     // one SM left to the finalize
-    const int gmax = getenv("SVT_HS_GRID") ? atoi(getenv("SVT_HS_GRID")) : sms - 1;
+    const int gmax = knobs().hs_grid.set ? knobs().hs_grid.value : sms - 1;
     int grid = static_cast<int>(n < gmax ? n : gmax);
     if (grid < 1) grid = 1;
     if (grid > kFMaxGrid) grid = kFMaxGrid;
@@ -1580,7 +1626,7 @@ bool rows_hs_eligible(int64_t n, size_t row_bytes, size_t dim, int* grid_out, in
     // of 8 KB rows per group 3.94-3.97 us per token, 5 slots 3.93-4.01)
     const int nb_inflight = static_cast<int>(kHInflight / (kHG * row_bytes));
     if (nb > nb_inflight) nb = nb_inflight < 2 ? 2 : nb_inflight;
-    if (const char* v = getenv("SVT_ROWS_HS_NB")) nb = atoi(v);
+    if (knobs().rows_hs_nb.set) nb = knobs().rows_hs_nb.value;
     if (nb > rpg) nb = rpg;
     if (nb > kHMaxSlots / kHG) nb = kHMaxSlots / kHG;
     if (nb < 1 || (nb < 2 && rpg > 1)) return false;
@@ -1610,8 +1656,7 @@ svt_status pick_rpg(FastParams p, int rpg, cudaStream_t st) {
 // registers); returns false to fall back to the streaming kernel.
 bool rows_fast_eligible(int64_t n, size_t row_bytes, size_t dim, int* grid_out, int* rpg_out,
                         int* cpt_out) {
-    if (const char* v = getenv("SVT_ROWS_FAST"))
-        if (atoi(v) == 0) return false;
+    if (knobs().rows_fast.set && knobs().rows_fast.value == 0) return false;
     const size_t nchunks = row_bytes / 16;
     if (nchunks % kFTPG != 0) return false;
     const int cpt = static_cast<int>(nchunks / kFTPG);
@@ -1689,11 +1734,15 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
                   "dim*esize %% 16 == 0 and dim <= 8192");
         return SVT_ERR_CONFIG;
     }
-    int dev_count = 0;
-    if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
-        cudaGetLastError();
-        set_error("no CUDA device available (the tailored-head kernels have no CPU fallback)");
-        return SVT_ERR_RUNTIME;
+    static bool have_device = false;  // (once found, a device does not go away)
+    if (!have_device) {
+        int dev_count = 0;
+        if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+            cudaGetLastError();
+            set_error("no CUDA device available (the tailored-head kernels have no CPU fallback)");
+            return SVT_ERR_RUNTIME;
+        }
+        have_device = true;
     }
     SmallParams p = {};
     p.W = static_cast<const uint8_t*>(d_head);
@@ -1728,9 +1777,9 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
     {
         int fgrid = 0, rpg = 0, cpt = 0, nb = 0;
         const bool hs_flags = (flags & SVT_ROWS_WEIGHTS_STABLE) && (flags & SVT_ROWS_HIDDEN_STABLE);
-        const bool hs = hs_flags && !getenv("SVT_ROWS_GRID") &&
+        const bool hs = hs_flags && !knobs().rows_grid.set &&
                         rows_hs_eligible(p.n, row_bytes, dim, &fgrid, &rpg, &cpt, &nb);
-        if (hs || (!getenv("SVT_ROWS_GRID") &&
+        if (hs || (!knobs().rows_grid.set &&
                    rows_fast_eligible(p.n, row_bytes, dim, &fgrid, &rpg, &cpt))) {
             FastParams f = {};
             f.W = p.W;
@@ -1754,8 +1803,8 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
             f.per_cta = p.n / fgrid;
             f.extra = static_cast<int32_t>(p.n % fgrid);
             f.dbg = g_rows_dbg;
-            if (const char* v = getenv("SVT_ROWS_FIN")) f.fin_in_grid = atoi(v) != 0;
-            if (const char* v = getenv("SVT_FAST_VARIANT")) f.variant = atoi(v);
+            if (knobs().rows_fin.set) f.fin_in_grid = knobs().rows_fin.value != 0;
+            if (knobs().fast_variant.set) f.variant = knobs().fast_variant.value;
             // fast-pass depth: CPT*E/2 FFMAs per accumulator (+1 combine), 5
             // shuffle levels, 4 warp partials summed in order (+ slack)
             const int Ef = dt == SVT_F32 ? 4 : 8;
@@ -1769,8 +1818,8 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
                 f.nb = nb;
                 f.fin_warps = kHFinWarps;
                 f.fin_stagger = kHFinStagger;
-                if (const char* v = getenv("SVT_HS_FIN_WARPS")) f.fin_warps = atoi(v);
-                if (const char* v = getenv("SVT_HS_FIN_STAGGER")) f.fin_stagger = atoi(v);
+                if (knobs().fin_warps.set) f.fin_warps = knobs().fin_warps.value;
+                if (knobs().fin_stagger.set) f.fin_stagger = knobs().fin_stagger.value;
                 if (f.fin_warps < 1 || f.fin_warps > kHThreads / 32) f.fin_warps = kHFinWarps;
                 switch (dt) {
                     case SVT_F32:
@@ -1804,9 +1853,9 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
         }
     }
     int grid = sm_count();
-    if (const char* v = getenv("SVT_ROWS_GRID")) grid = atoi(v);
-    if (const char* v = getenv("SVT_ROWS_VARIANT")) p.variant = atoi(v);
-    if (const char* v = getenv("SVT_ROWS_L2")) p.l2_keep = v[0] == 'k' || v[0] == 'l';
+    if (knobs().rows_grid.set) grid = knobs().rows_grid.value;
+    if (knobs().rows_variant.set) p.variant = knobs().rows_variant.value;
+    p.l2_keep = knobs().l2_keep;
     grid = grid > kMaxGrid ? kMaxGrid : grid;
     if (static_cast<int64_t>(grid) > p.n) grid = static_cast<int>(p.n);
     if (grid < 1) grid = 1;
