@@ -47,6 +47,7 @@
 
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "svt_common.cuh"
@@ -723,11 +724,18 @@ struct FastParams {
     int32_t fin_in_grid;  // 1: the finalizer is the grid's last CTA; 0: its own launch
     int32_t variant;      // measurement only (SVT_FAST_VARIANT): 1 = no row traffic
     unsigned long long* dbg;  // per CTA 8 %globaltimer stamps (svt_rows_set_debug)
-    int32_t hs;           // 1: the stable-hidden ring kernel (records tagged kHsTag, cleared)
+    int32_t hs;           // 1: the stable-hidden ring kernel (slot / sequence-tag record protocol)
     int32_t nb;           // stable-hidden kernel: ring slots per row group
     int32_t fin_warps;    // stable-hidden kernel: polling warps of the finalizer CTA
     int32_t fin_stagger;  // ns between their first polls
+    uint32_t hs_tags;     // stable-hidden kernel: the launch's four record-word tags (bytes,
+                          // each in [1, 255]: a 32-bit call sequence number per workspace)
 };
+// tag of record word k (0..3): byte k of the launch's tags (stable-hidden) or
+// the epoch tag for every word (epoch protocol)
+__device__ __forceinline__ unsigned long long word_tag(uint32_t tags, int k) {
+    return static_cast<unsigned long long>((tags >> (8 * k)) & 0xFFu);
+}
 
 __device__ __forceinline__ int64_t frow_begin(const FastParams& p, int c) {
     return p.per_cta * c + (c < p.extra ? c : p.extra);
@@ -742,13 +750,13 @@ __device__ __forceinline__ unsigned ord24_up_of(unsigned o) {
     return static_cast<unsigned>(u > 0xFFFFFFull ? 0xFFFFFFull : u);
 }
 // epoch counter (in [0, 254)) -> the launch's tag in [1, 254]; a zeroed
-// record never matches. Tag 255 marks the stable-hidden kernel's records,
-// which its finalize clears after reading (no epoch on that path).
+// record never matches. (The stable-hidden kernel tags each record word with
+// a byte of its call sequence number and keeps its records in its own
+// slots, cleared by the finalizer after reading.)
 __device__ __forceinline__ unsigned long long tag_of(unsigned e) {
     return static_cast<unsigned long long>(e % 254u + 1u);
 }
 __device__ __forceinline__ unsigned next_epoch(unsigned e) { return (e + 1u) % 254u; }
-constexpr unsigned long long kHsTag = 255ull;
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -805,10 +813,14 @@ __device__ __forceinline__ float sum2(unsigned long long v) {
 // row j in group j % NG, slot j / NG): sum the WPG warp partials of each row
 // in a fixed order, bound, L_c = max lo, the rows with hi >= L_c; a tagged
 // 32-byte record (+ the candidate list when more than two remain).
-template <int NG, int WPG, int RPG, int PF, bool kWaitBeforeStore = false>
+// kStoreMode 0: store at once; 1: griddepcontrol.wait first; 2: first wait
+// until this CTA's record slot reads zero in all four words (cleared by the
+// finalizer of the previous launch that used the slot) — stable-hidden
+// kernel. tags: one byte per record word (all four equal for the epoch tag).
+template <int NG, int WPG, int RPG, int PF, int kStoreMode = 0>
 __device__ __forceinline__ void fast_cta_record(const FastParams& p, const float (&s_red)[NG][WPG][PF],
                                                 int c, int64_t r0, int nrows, uint32_t my_id,
-                                                unsigned long long tag8, int lane) {
+                                                uint32_t tags, int lane) {
     const bool act = lane < nrows;
     float f = 0.0f, a = 0.0f;
     if (act) {
@@ -842,10 +854,23 @@ __device__ __forceinline__ void fast_cta_record(const FastParams& p, const float
     const uint32_t id1 = __shfl_sync(0xFFFFFFFFu, my_id, l1 < 0 ? 0 : l1);
     const uint32_t id2 = __shfl_sync(0xFFFFFFFFu, my_id, l2 < 0 ? 0 : l2);
     const unsigned code = anybad ? 1u : (cnt > 2 ? 2u : 0u);
-    if constexpr (kWaitBeforeStore) {
+    if constexpr (kStoreMode == 1) {
         // everything above is this launch's own work; the stores below may
         // only follow the previous launch (its finalize reads this workspace)
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0) SVT_FSTAMP(1);
+    } else if constexpr (kStoreMode == 2) {
+        // the slot's previous user has been decided and cleared: every word
+        // reads zero (observed, so this launch's stores follow the clears in
+        // each word's coherence order). Bounded: after 2 s the stores go
+        // ahead (that step's id is then unreliable, but nothing hangs).
+        if (lane < 4) {
+            FRec* fr = p.frec + c;
+            const unsigned long long t0 = gtimer();
+            while (ld_relaxed_u64(&fr->w[lane]) != 0ull && gtimer() - t0 < 2000000000ull)
+                __nanosleep(64);
+        }
+        __syncwarp();
         if (lane == 0) SVT_FSTAMP(1);
     }
     if (code == 2u && cand) {  // the full list, released before the record
@@ -857,7 +882,6 @@ __device__ __forceinline__ void fast_cta_record(const FastParams& p, const float
     if (lane == 0) SVT_FSTAMP(6);
     if (lane == 0) {
         if (code == 2u) fence_acq_rel_gpu();
-        const unsigned long long tag = tag8 << 56;
         const unsigned long long l24 = ord24_down(L);
         const unsigned long long hi1 = ord24_up_of(h1);
         const unsigned long long hi2 = cnt >= 2 ? ord24_up_of(h2) : 0ull;
@@ -865,10 +889,10 @@ __device__ __forceinline__ void fast_cta_record(const FastParams& p, const float
         const unsigned long long row2 = cnt >= 2 ? (static_cast<unsigned>(l2) & 0xFFFFu)
                                                  : 0xFFFFull;
         FRec* fr = p.frec + c;
-        st_relaxed_u64(&fr->w[0], tag | l24 << 32 | hi2 << 8 | code);
-        st_relaxed_u64(&fr->w[1], tag | hi1 << 32 | id1);
-        st_relaxed_u64(&fr->w[2], tag | row1 << 32 | row2 << 16);
-        st_relaxed_u64(&fr->w[3], tag | static_cast<unsigned long long>(cnt) << 32 | id2);
+        st_relaxed_u64(&fr->w[0], word_tag(tags, 0) << 56 | l24 << 32 | hi2 << 8 | code);
+        st_relaxed_u64(&fr->w[1], word_tag(tags, 1) << 56 | hi1 << 32 | id1);
+        st_relaxed_u64(&fr->w[2], word_tag(tags, 2) << 56 | row1 << 32 | row2 << 16);
+        st_relaxed_u64(&fr->w[3], word_tag(tags, 3) << 56 | static_cast<unsigned long long>(cnt) << 32 | id2);
         SVT_FSTAMP(4);
     }
 }
@@ -930,7 +954,8 @@ __device__ __forceinline__ void rows_fast_cta(const FastParams& p, uint8_t* dsm)
         named_bar_sync(1, kFThreads);  // every group's warp partials are in s_red
         const unsigned epoch = s_epoch[0];  // s_hbar completed before the compute warps arrived
         if (lane == 0) SVT_FSTAMP(3);
-        fast_cta_record<kFNG, kFWPG, RPG, PF>(p, s_red, c, r0, nrows, my_id, tag_of(epoch), lane);
+        const uint32_t t8 = static_cast<uint32_t>(tag_of(epoch));
+        fast_cta_record<kFNG, kFWPG, RPG, PF>(p, s_red, c, r0, nrows, my_id, t8 * 0x01010101u, lane);
         return;
     }
     // ---- compute warps ------------------------------------------------------
@@ -1024,7 +1049,7 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
     constexpr int kPer = kFMaxGrid / 32;
     // written by the previous launch's finalize, complete before the wait
     const unsigned epoch = ld_relaxed_u32(p.ctrl + 8);
-    const unsigned long long tag = p.hs ? kHsTag : tag_of(epoch);
+    const uint32_t tags = p.hs ? p.hs_tags : static_cast<uint32_t>(tag_of(epoch)) * 0x01010101u;
     unsigned long long w0[kPer], w1[kPer], w2[kPer], w3[kPer];
     bool seen = false;
     const unsigned long long t_start = gtimer();
@@ -1049,8 +1074,8 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
 #pragma unroll
         for (int q = 0; q < kPer; ++q)
             if (32 * q < G)
-                mine = mine && (w0[q] >> 56) == tag && (w1[q] >> 56) == tag &&
-                       (w2[q] >> 56) == tag && (w3[q] >> 56) == tag;
+                mine = mine && (w0[q] >> 56) == word_tag(tags, 0) && (w1[q] >> 56) == word_tag(tags, 1) &&
+                       (w2[q] >> 56) == word_tag(tags, 2) && (w3[q] >> 56) == word_tag(tags, 3);
         seen = __all_sync(0xFFFFFFFFu, mine);
         if (seen) {
             unsigned won = 0u;
@@ -1076,22 +1101,6 @@ __device__ __forceinline__ void rows_fast_finalize(const FastParams& p, uint8_t*
         }
     }
     if (p.dbg && lane == 0) p.dbg[124] = gtimer();
-    if (p.hs) {
-        // stable-hidden records carry no epoch: clear them once read (the
-        // next launch on this workspace writes its records only after its
-        // dependency wait, i.e. after this grid completed)
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int cc = lane + 32 * q;
-            if (32 * q < G && cc < G) {
-                FRec* fr = p.frec + cc;
-                st_relaxed_u64(&fr->w[0], 0ull);
-                st_relaxed_u64(&fr->w[1], 0ull);
-                st_relaxed_u64(&fr->w[2], 0ull);
-                st_relaxed_u64(&fr->w[3], 0ull);
-            }
-        }
-    }
     unsigned l24 = 0u, code = 0u;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -1261,10 +1270,13 @@ __global__ void __launch_bounds__(kFThreads, 1) rows_fast_kernel(FastParams p) {
 //    so the NEXT launch's CTAs are resident and streaming while this
 //    launch's CTAs finish: consecutive decode steps overlap their HBM
 //    streams instead of paying the stream's ramp and the tail in series;
-//  * the dependency warp waits (programmatic dependency), triggers the
-//    dependents, then writes the same tagged record as rows_fast (tag
-//    kHsTag; the finalize clears the records after reading them, so no
-//    epoch load sits between the wait and the record).
+//  * no grid-level dependency wait before the record: records live in one
+//    of several slots of the workspace (the host rotates them per call, one
+//    more slot than grids of this kernel can be resident at once) and every
+//    word carries a byte of the call's sequence number; a rows CTA stores
+//    its record once its slot reads zero, the finalizer CTA (same grid)
+//    accepts only its own tags, decides, clears the slot and only then
+//    waits for the previous launch, so grids still complete in stream order.
 // The fast pass, the bound and the finalize are rows_fast's.
 // ===========================================================================
 constexpr int kHG = 2;                            // row groups per CTA
@@ -1274,6 +1286,7 @@ constexpr int kHThreads = (kHCompute + 2) * 32;   // + producer + dependency war
 constexpr int kHMaxSlots = 16;                    // ring slots per CTA (both groups)
 constexpr int kHSmemBudget = 96 * 1024;           // ring + h: two CTAs per SM
 constexpr int kHInflight = 48 * 1024;             // rows in flight per CTA (ring target)
+constexpr int kHRecSlots = 8;                     // record slots per workspace (max)
 constexpr int kHFinWarps = 4;                     // polling warps of the finalizer CTA
 constexpr int kHFinStagger = 300;                 // ns between their first polls
 
@@ -1355,9 +1368,9 @@ __device__ __forceinline__ void rows_hs_cta(const FastParams& p, uint8_t* dsm) {
         asm volatile("griddepcontrol.launch_dependents;");
         named_bar_sync(1, (kHCompute + 1) * 32);  // every group's partials are in s_red
         if (lane == 0) SVT_FSTAMP(3);
-        // the record is computed first; the dependency wait sits right
-        // before its stores
-        fast_cta_record<kHG, kHWPG, RPG, PF, true>(p, s_red, c, r0, nrows, my_id, kHsTag, lane);
+        // the record is computed first; its stores wait only for this
+        // CTA's slot to be cleared (no grid-level dependency wait)
+        fast_cta_record<kHG, kHWPG, RPG, PF, 2>(p, s_red, c, r0, nrows, my_id, p.hs_tags, lane);
         return;
     }
     // ---- compute warps: group g = rows g, g + kHG, ...; thread tg owns
@@ -1418,10 +1431,14 @@ __device__ __forceinline__ void rows_hs_cta(const FastParams& p, uint8_t* dsm) {
 
 // One launch per decode step: CTAs [0, grid) are rows CTAs, CTA `grid` (the
 // highest index, dispatched last) is the finalizer. Every CTA triggers the
-// next launch at once; every CTA waits on the previous launch before it
-// writes or reads a record, so the finalizer of step t starts polling only
-// once step t-1's finalizer has cleared the records (same workspace) and
-// step t's records are the only tag-kHsTag records it can see.
+// next launch at once. Records live in one of two slots of the workspace
+// (the host alternates them per call) and carry the call's 32-bit sequence
+// number, one nonzero byte per word: a rows CTA stores its record once its
+// slot reads zero (the previous user of the slot has been decided and
+// cleared), the finalizer accepts only words with its own tags, decides,
+// clears the slot, and only then waits for the previous launch — so grids
+// still complete in stream order, but no dependency release sits between
+// one step's decision and the next step's records.
 template <int DT, int CPT, int RPG>
 __global__ void __launch_bounds__(kHThreads, 2) rows_hs_kernel(FastParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
@@ -1435,9 +1452,20 @@ __global__ void __launch_bounds__(kHThreads, 2) rows_hs_kernel(FastParams p) {
         if (threadIdx.x == 0) s_claim = 0u;
         named_bar_sync(2, 32 * fw);
         asm volatile("griddepcontrol.launch_dependents;");
-        asm volatile("griddepcontrol.wait;" ::: "memory");
         if (p.dbg && threadIdx.x == 0) p.dbg[123] = gtimer();
         rows_fast_finalize<DT>(p, dsm, &s_n, &s_claim, p.fin_stagger);
+        // every polling warp is done with the records (and candidate lists):
+        // clear the slot for its next user, then order this grid's
+        // completion after the previous launch's
+        named_bar_sync(2, 32 * fw);
+        for (int cc = threadIdx.x; cc < p.grid; cc += 32 * fw) {
+            FRec* fr = p.frec + cc;
+            st_relaxed_u64(&fr->w[0], 0ull);
+            st_relaxed_u64(&fr->w[1], 0ull);
+            st_relaxed_u64(&fr->w[2], 0ull);
+            st_relaxed_u64(&fr->w[3], 0ull);
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         return;
     }
     rows_hs_cta<DT, CPT, RPG>(p, dsm);
@@ -1698,9 +1726,86 @@ extern "C" size_t svt_greedy_rows_workspace_bytes(size_t rows) {
     using namespace svt;
     // streaming-kernel area, then the small-plan kernel's tagged records and
     // candidate lists (disjoint: a workspace may serve both kernels)
-    return rows_stream_ws_bytes(rows) + static_cast<size_t>(kFMaxGrid) * sizeof(FRec) +
-           static_cast<size_t>(kFMaxGrid) * kFMaxRows * sizeof(uint2);
+    // (+ the stable-hidden kernel's record slots with their lists)
+    return rows_stream_ws_bytes(rows) +
+           (1 + kHRecSlots) * (static_cast<size_t>(kFMaxGrid) * sizeof(FRec) +
+                               static_cast<size_t>(kFMaxGrid) * kFMaxRows * sizeof(uint2));
 }
+
+namespace {
+using namespace svt;
+// per-workspace call sequence of the stable-hidden kernel (host side): slot =
+// seq % slots (hs_record_slots), word tags = the four base-255 digits of
+// seq, each + 1 (nonzero)
+std::mutex g_hs_mu;
+std::map<const void*, uint32_t> g_hs_seq;
+uint32_t next_hs_seq(const void* ws) {
+    std::lock_guard<std::mutex> lock(g_hs_mu);
+    if (g_hs_seq.size() > 65536) g_hs_seq.clear();
+    return g_hs_seq[ws]++;
+}
+// Record slots of the stable-hidden kernel: one more than the number of its
+// grids that can be resident at once. A rows CTA waits for its slot to be
+// cleared by the finalizer of the launch that used it `nslots` calls before;
+// a launch `nslots` calls later can only have CTAs resident once every CTA of
+// that earlier launch has left (SM slots), so a slot never has two waiting
+// writers. Computed from the kernel's occupancy, capped at kHRecSlots.
+template <int DT, int CPT, int RPG>
+int hs_slots_for(size_t smem, int grid) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rows_hs_kernel<DT, CPT, RPG>, kHThreads,
+                                                      smem) != cudaSuccess || occ <= 0) {
+        cudaGetLastError();
+        return kHRecSlots;
+    }
+    const int resident = (occ * sm_count() + grid) / (grid + 1) + 1;  // grids (+1: partial)
+    return resident + 1 > kHRecSlots ? kHRecSlots : (resident + 1 < 2 ? 2 : resident + 1);
+}
+template <int DT, int CPT>
+int hs_slots_rpg(int rpg, size_t smem, int grid) {
+    if (rpg <= 3) return hs_slots_for<DT, CPT, 3>(smem, grid);
+    if (rpg <= 5) return hs_slots_for<DT, CPT, 5>(smem, grid);
+    if (rpg <= 9) return hs_slots_for<DT, CPT, 9>(smem, grid);
+    return hs_slots_for<DT, CPT, 16>(smem, grid);
+}
+int hs_record_slots(svt_dtype dt, int cpt, int rpg, int nb, size_t row_bytes, size_t dim, int grid) {
+    size_t smem = static_cast<size_t>(kHG * nb) * row_bytes + dim * 4;
+    const size_t fin_smem = kMaxCand * 4 + 2 * kPiece + dim * 4;
+    smem = smem > fin_smem ? smem : fin_smem;
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, size_t, int, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(static_cast<int>(dt), cpt, rpg, smem, grid, dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int n = kHRecSlots;
+    if (dt == SVT_F32)
+        n = cpt == 1 ? hs_slots_rpg<SVT_F32, 1>(rpg, smem, grid)
+            : cpt == 2 ? hs_slots_rpg<SVT_F32, 2>(rpg, smem, grid)
+                       : hs_slots_rpg<SVT_F32, 4>(rpg, smem, grid);
+    else if (dt == SVT_F16)
+        n = cpt == 1 ? hs_slots_rpg<SVT_F16, 1>(rpg, smem, grid)
+            : cpt == 2 ? hs_slots_rpg<SVT_F16, 2>(rpg, smem, grid)
+                       : hs_slots_rpg<SVT_F16, 4>(rpg, smem, grid);
+    else
+        n = cpt == 1 ? hs_slots_rpg<SVT_BF16, 1>(rpg, smem, grid)
+            : cpt == 2 ? hs_slots_rpg<SVT_BF16, 2>(rpg, smem, grid)
+                       : hs_slots_rpg<SVT_BF16, 4>(rpg, smem, grid);
+    cache[key] = n;
+    return n;
+}
+
+uint32_t hs_tags_of(uint32_t seq) {
+    uint32_t t = 0, v = seq;
+    for (int k = 0; k < 4; ++k) {
+        t |= ((v % 255u) + 1u) << (8 * k);
+        v /= 255u;
+    }
+    return t;
+}
+}  // namespace
 
 extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt, size_t head_rows,
                                                 size_t dim, const uint32_t* d_src_ids,
@@ -1816,6 +1921,14 @@ extern "C" svt_status svt_greedy_certified_rows(const void* d_head, svt_dtype dt
             if (hs) {
                 f.hs = 1;
                 f.nb = nb;
+                const uint32_t seq = next_hs_seq(d_workspace);
+                f.hs_tags = hs_tags_of(seq);
+                const size_t slot_bytes = static_cast<size_t>(kFMaxGrid) * sizeof(FRec) +
+                                          static_cast<size_t>(kFMaxGrid) * kFMaxRows * sizeof(uint2);
+                const int nslots = hs_record_slots(dt, cpt, rpg, nb, row_bytes, dim, fgrid);
+                uint8_t* sb = fb + slot_bytes * (1 + seq % static_cast<uint32_t>(nslots));
+                f.frec = reinterpret_cast<FRec*>(sb);
+                f.cand = reinterpret_cast<uint2*>(sb + kFMaxGrid * sizeof(FRec));
                 f.fin_warps = kHFinWarps;
                 f.fin_stagger = kHFinStagger;
                 if (knobs().fin_warps.set) f.fin_warps = knobs().fin_warps.value;
