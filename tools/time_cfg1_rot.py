@@ -29,7 +29,8 @@ def make(R):
         off = np.array([0, len(p)], np.int64)
         tb = th.TailoredBatch.build(words, 2048, V, torch.from_numpy(p.view(np.int32)).cuda(), off)
         n = int(tb.n_active[0].item())
-        jobs.append((tb, th.RowDecoder(head, tb.active[:n], n), n))
+        jobs.append((tb, th.RowDecoder(head, tb.active[:n], n,
+                                        materialize=os.environ.get("SVT_FUSED", "0") != "1"), n))
     n = STEPS * R * d
     hid = torch.empty(n, dtype=torch.float32, device="cuda")
     th._lib.call("svt_head_random", hid.data_ptr(), th.SVT_F32, th.SVT_F32, 0, n, synth.SEED_H,
