@@ -170,3 +170,53 @@ def test_hs_special_values(th):
     got, gmax = _greedy_hs(dt, pos, want_max=True)
     assert got == want and bits([gmax])[0] == bits([wmax])[0]
     assert _greedy_hs(dt, pos) == want
+
+
+def test_hs_two_streams_mixed_eager_and_graphs(th):
+    """Four cfg1-shaped decoders on two streams (two per stream, token-
+    interleaved), resident-hidden calls: stream A replays a CUDA graph while
+    stream B runs eagerly, then the roles swap, with no host sync in
+    between; every id equals the reference (record slots per workspace,
+    grids of both streams competing for the SMs)."""
+    V, d, steps, R = 128256, 2048, 24, 4
+    head, words, prompts, tb, hid = _build_workload(th, V, d, th.SVT_F32, R, 512, 2048, steps)
+    W = head.to_host()
+    plans = [orc.select(prompts[j], words, V, V).active_ids for j in range(R)]
+    want = np.array([[orc.greedy_step(W[plans[j]], hid[t][j], plans[j])[0] for j in range(R)]
+                     for t in range(steps)], np.uint32)
+    decs = [_rows_decoder(th, head, plans[j]) for j in range(R)]
+    hd = torch.from_numpy(np.ascontiguousarray(hid, np.float32)).cuda()
+    out = torch.full((steps, R), -1, dtype=torch.int32, device="cuda")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    groups = {0: ([0, 1], sa), 1: ([2, 3], sb)}
+    for jobs, st in groups.values():
+        for j in jobs:
+            decs[j].stream = st
+
+    def run(jobs):
+        for t in range(steps):
+            for j in jobs:
+                decs[j].greedy(hd[t, j], out[t, j], hidden_stable=True)
+
+    for jobs, st in groups.values():  # first calls (epoch kernel), then capture
+        with torch.cuda.stream(st):
+            run(jobs)
+    torch.cuda.synchronize()
+    graphs = {}
+    for k, (jobs, st) in groups.items():
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            run(jobs)
+        graphs[k] = g
+    for rnd in range(3):
+        out.fill_(-1)
+        torch.cuda.synchronize()
+        ka, kb = (0, 1) if rnd % 2 == 0 else (1, 0)
+        with torch.cuda.stream(groups[ka][1]):
+            graphs[ka].replay()
+        with torch.cuda.stream(groups[kb][1]):
+            run(groups[kb][0])
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want), rnd
+    for dcd in decs:
+        dcd.stream = None
