@@ -32,6 +32,7 @@ for mode in ("interleaved", "split"):
     torch.cuda.synchronize()
     res[mode + "_us_per_decode_step"] = a.elapsed_time(b) / 5 / 64 * 1e3
     outs[mode] = job.out.clone()
+res["split_stats"] = list(job.sdec.stats())
 res["ids_equal"] = bool(torch.equal(outs["interleaved"], outs["split"]))
 res["split_bytes_per_step"] = job.decode_bytes("split")
 res["interleaved_bytes_per_step"] = job.decode_bytes("interleaved")
