@@ -668,18 +668,23 @@ svt_status svt_session_create(svt_session** out, const void* d_head, svt_dtype d
                               size_t rows, size_t dim, int32_t max_batch,
                               int64_t max_plan_rows, svt_stream stream);
 svt_status svt_session_destroy(svt_session* s);
-/* H2D of the static bitmap + prompts, then select + layout + gather on the
- * session stream; synchronises and reports the first per-request error
- * (IntegrityError with the reference's message). */
+/* H2D of the static bitmap + prompts (one copy from pinned staging), then
+ * select + layout + gather on the session stream; reports the first
+ * per-request error (IntegrityError with the reference's message). Batch
+ * 1 (the row-major path): the plan's counts follow from the bitmap and the
+ * prompt, so they and the out-of-range check are computed on the host and
+ * the call returns without synchronising (the select and the row gather
+ * are stream-ordered before every later step). Larger batches read the
+ * counts back and synchronise. */
 svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_words,
                                     size_t static_universe, const uint32_t* h_input_ids,
                                     const int64_t* h_input_offsets, int32_t batch);
-/* svt_session_prepare_host for n sessions with one synchronisation per
- * distinct stream instead of one per session: every session's H2D, select,
- * layout and gather are enqueued first, then the plan counts are read back
- * and checked (the first failing session's error is returned, in session
- * order), then batch-1 sessions gather their rows. Session i uses
- * h_input_ids[i], h_input_offsets[i] (batches[i] + 1 entries), batches[i]. */
+/* svt_session_prepare_host for n sessions: every session's work is
+ * enqueued first, then one synchronisation per distinct stream for the
+ * sessions whose counts are read back (batch > 1; batch-1 sessions need
+ * none); the first failing session's error is returned, in session order.
+ * Session i uses h_input_ids[i], h_input_offsets[i] (batches[i] + 1
+ * entries), batches[i]. */
 svt_status svt_session_prepare_host_many(svt_session* const* sessions, int32_t n_sessions,
                                          const uint64_t* h_static_words, size_t static_universe,
                                          const uint32_t* const* h_input_ids,

@@ -32,12 +32,20 @@ struct svt_session {
     const int64_t* prep_offs = nullptr;
 
     // device buffers (capacity in elements)
+    // prepare inputs, one device block mirroring the pinned staging area
+    // (static words | prompt ids | prompt offsets | plan offsets): a single
+    // H2D per prepare; the four pointers below point into it
+    uint8_t* d_stage = nullptr;
+    size_t cap_dstage = 0;
     uint64_t* d_words = nullptr;
-    size_t cap_words = 0;
     uint32_t* d_inputs = nullptr;
-    size_t cap_inputs = 0;
     int64_t* d_in_off = nullptr;
     int64_t* d_act_off = nullptr;
+    size_t meta_stride = 0;  // cap_batch at the prepare (D2H of the four count arrays)
+    cudaEvent_t ev_stage = nullptr;  // after the prepare's H2D out of h_stage
+    bool stage_busy = false;         // that H2D may still be pending (no sync since)
+    std::vector<uint64_t> seen;      // prepare scratch: prompt-id bitmap (kept all-zero)
+    std::vector<uint32_t> host_ids;  // ... and the ids it set
     int64_t* d_meta = nullptr;  // n_active | n_static | n_dynamic | first_bad | group_begin
     size_t cap_batch = 0;
     uint32_t* d_active = nullptr;
@@ -126,7 +134,7 @@ svt_status grow(T** p, size_t* cap, size_t need) {
 }
 
 void free_all(svt_session* s) {
-    void* dev[] = {s->d_words, s->d_inputs, s->d_in_off, s->d_act_off, s->d_meta, s->d_active,
+    void* dev[] = {s->d_stage, s->d_meta, s->d_active,
                    s->d_group_req, s->d_sub, s->d_hidden, s->d_out_ids, s->d_out_max, s->d_ws,
                    s->d_bad, s->d_st_ids, s->d_st_meta, s->d_st_sub, s->d_st_small,
                    s->d_dyn_ids, s->d_split_meta, s->d_split_ws, s->d_rows, s->d_rows_ws,
@@ -136,6 +144,7 @@ void free_all(svt_session* s) {
     void* host[] = {s->h_hidden, s->h_ids, s->h_max, s->h_stage};
     for (void* p : host)
         if (p) cudaFreeHost(p);
+    if (s->ev_stage) cudaEventDestroy(s->ev_stage);
 }
 
 bool is_pinned(const void* p) {
@@ -218,15 +227,12 @@ void drop_graph(svt_session* s) {
 svt_status ensure_batch(svt_session* s, size_t B) {
     if (B <= s->cap_batch && s->d_meta) return SVT_OK;
     const size_t nb = B + B / 4 + 1;
-    void* old[] = {s->d_in_off, s->d_act_off, s->d_meta, s->d_hidden, s->d_out_ids,
-                   s->d_out_max};
+    void* old[] = {s->d_meta, s->d_hidden, s->d_out_ids, s->d_out_max};
     for (void* p : old)
         if (p) cudaFree(p);
     if (s->h_hidden) cudaFreeHost(s->h_hidden);
     if (s->h_ids) cudaFreeHost(s->h_ids);
     if (s->h_max) cudaFreeHost(s->h_max);
-    SVT_CUDA_TRY(cudaMalloc(&s->d_in_off, (nb + 1) * sizeof(int64_t)));
-    SVT_CUDA_TRY(cudaMalloc(&s->d_act_off, (nb + 1) * sizeof(int64_t)));
     SVT_CUDA_TRY(cudaMalloc(&s->d_meta, (5 * nb + 1) * sizeof(int64_t)));
     SVT_CUDA_TRY(cudaMalloc(&s->d_hidden, nb * s->ld * sizeof(float)));
     SVT_CUDA_TRY(cudaMemset(s->d_hidden, 0, nb * s->ld * sizeof(float)));
@@ -382,9 +388,48 @@ svt_stream svt_session_stream(svt_session* s) { return s ? s->stream : nullptr; 
 namespace {
 // prepare, phase 1: everything up to the plan-count read-back, enqueued on
 // the session's stream (no synchronisation); *done = the batch was empty
+svt_status ensure_events(svt_session* s) {
+    if (!s->ev_stage) SVT_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_stage, cudaEventDisableTiming));
+    return SVT_OK;
+}
+
+// |T|: the static bitmap's population (hardware popcount)
+__attribute__((target("popcnt"))) int64_t popcount_words(const uint64_t* w, size_t nw) {
+    int64_t n = 0;
+    for (size_t i = 0; i < nw; ++i) n += __builtin_popcountll(w[i]);
+    return n;
+}
+
+// batch-1 sessions: the plan's rows gathered row-major (stream-ordered
+// before every later step); the rows workspace zeroed once when it grows
+svt_status rows_gather(svt_session* s, cudaStream_t q) {
+    if (s->n_active.empty() || s->n_active[0] <= 0) return SVT_OK;
+    const size_t n = static_cast<size_t>(s->n_active[0]);
+    const size_t bytes = n * s->dim * svt_dtype_size(s->dt) + 16;
+    svt_status st = grow(&s->d_rows, &s->cap_rows, bytes);
+    const size_t wsb = svt_greedy_rows_workspace_bytes(n);
+    if (!st && (wsb > s->cap_rows_ws || !s->d_rows_ws)) {
+        if (s->d_rows_ws) {
+            cudaStreamSynchronize(s->stream);  // (earlier steps may still use it)
+            cudaFree(s->d_rows_ws);
+        }
+        s->d_rows_ws = nullptr;
+        s->cap_rows_ws = 0;
+        st = grow(&s->d_rows_ws, &s->cap_rows_ws, wsb);
+        if (!st) {
+            const cudaError_t e = cudaMemset(s->d_rows_ws, 0, s->cap_rows_ws);
+            if (e != cudaSuccess) st = svt::cuda_status(e, "rows workspace memset");
+        }
+    }
+    if (!st)
+        st = svt_gather_rows(s->head, s->dt, s->rows, s->dim, s->d_active, n, s->d_rows,
+                             s->d_bad, q);
+    return st;
+}
+
 svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_t static_universe,
                            const uint32_t* h_input_ids, const int64_t* h_input_offsets,
-                           int32_t batch, bool* done) {
+                           int32_t batch, bool* done, cudaStream_t q) {
     *done = true;
     if (!s) {
         set_error("null session");
@@ -403,8 +448,7 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
     }
     const size_t B = static_cast<size_t>(batch);
     const size_t nw = (s->rows + 63) / 64;
-    int64_t n_static = 0;
-    for (size_t i = 0; i < nw; ++i) n_static += __builtin_popcountll(h_static_words[i]);
+    const int64_t n_static = popcount_words(h_static_words, nw);
     // capacities: |S_b| <= |T| + len_b
     s->act_off.assign(B + 1, 0);
     int64_t groups = 0;
@@ -415,8 +459,6 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
     }
     const size_t n_inputs = static_cast<size_t>(B ? h_input_offsets[B] - h_input_offsets[0] : 0);
     svt_status st = ensure_batch(s, B ? B : 1);
-    if (!st) st = grow(&s->d_words, &s->cap_words, nw);
-    if (!st) st = grow(&s->d_inputs, &s->cap_inputs, n_inputs);
     if (!st) st = grow(&s->d_active, &s->cap_active, static_cast<size_t>(s->act_off[B]));
     if (!st && static_cast<size_t>(groups) > s->cap_groups) {
         size_t cap = 0;
@@ -434,16 +476,63 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
     s->batch = batch;
     s->max_groups = groups;
     if (B == 0) return SVT_OK;
+    if (svt_status e = ensure_events(s)) return e;
+    // the previous prepare's H2D may still read the staging area (no wait
+    // when a synchronisation of the session's stream came in between)
+    if (s->stage_busy) SVT_CUDA_TRY(cudaEventSynchronize(s->ev_stage));
+    s->stage_busy = false;
+    const char* rows_env = getenv("SVT_SESSION_ROWS");
+    const bool rows_mode = batch == 1 && (rows_env == nullptr || atoi(rows_env) != 0);
+    if (rows_mode) {
+        // batch 1: the plan's counts follow from the bitmap and the prompt
+        // alone (select, selector.cpp:16-43): n_dynamic = the distinct
+        // prompt ids outside T, and the first id >= V fails the call in
+        // input order as the reference throws. Nothing is read back and the
+        // prepare does not synchronise.
+        const uint32_t* in = h_input_ids + h_input_offsets[0];
+        const int64_t len = h_input_offsets[1] - h_input_offsets[0];
+        if (s->seen.size() != nw) s->seen.assign(nw, 0ull);
+        std::vector<uint32_t>& dyn = s->host_ids;
+        dyn.clear();
+        svt_status bad = SVT_OK;
+        for (int64_t i = 0; i < len; ++i) {
+            const uint32_t id = in[i];
+            if (static_cast<size_t>(id) >= s->rows) {
+                set_error("input token id %u out of range for vocabulary of size %zu", id, s->rows);
+                bad = SVT_ERR_INTEGRITY;
+                break;
+            }
+            const uint64_t bit = 1ull << (id & 63u);
+            if (!(h_static_words[id >> 6] & bit) && !(s->seen[id >> 6] & bit)) {
+                s->seen[id >> 6] |= bit;  // a new dynamic id
+                dyn.push_back(id);
+            }
+        }
+        for (const uint32_t id : dyn) s->seen[id >> 6] = 0ull;  // back to all-zero
+        if (bad) {
+            s->batch = 0;
+            return bad;
+        }
+        const int64_t nd = static_cast<int64_t>(dyn.size());
+        s->n_active.assign(1, n_static + nd);
+        s->n_static.assign(1, n_static);
+        s->n_dynamic.assign(1, nd);
+    }
 
-    cudaStream_t q = s->stream;
     // the host inputs are staged in pinned memory so the copies are truly
     // asynchronous (the previous prepare of this session has synchronised,
-    // so the staging area is free)
+    // so the staging area is free); the device block mirrors the layout
     const size_t o_words = 0, o_in = nw * sizeof(uint64_t);
     const size_t o_inoff = (o_in + n_inputs * sizeof(uint32_t) + 15) & ~size_t(15);
     const size_t o_actoff = o_inoff + (B + 1) * sizeof(int64_t);
     const size_t o_meta = o_actoff + (B + 1) * sizeof(int64_t);  // D2H: the plan counts
-    const size_t stage = o_meta + 4 * B * sizeof(int64_t);
+    s->meta_stride = s->cap_batch;
+    const size_t stage = o_meta + 4 * s->meta_stride * sizeof(int64_t);
+    if (svt_status e = grow(&s->d_stage, &s->cap_dstage, o_meta)) return e;
+    s->d_words = reinterpret_cast<uint64_t*>(s->d_stage + o_words);
+    s->d_inputs = reinterpret_cast<uint32_t*>(s->d_stage + o_in);
+    s->d_in_off = reinterpret_cast<int64_t*>(s->d_stage + o_inoff);
+    s->d_act_off = reinterpret_cast<int64_t*>(s->d_stage + o_actoff);
     if (stage > s->cap_stage) {
         if (s->h_stage) cudaFreeHost(s->h_stage);
         s->h_stage = nullptr;
@@ -457,15 +546,9 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
     int64_t* in_off = reinterpret_cast<int64_t*>(s->h_stage + o_inoff);
     for (size_t b = 0; b <= B; ++b) in_off[b] = h_input_offsets[b] - h_input_offsets[0];
     std::memcpy(s->h_stage + o_actoff, s->act_off.data(), (B + 1) * sizeof(int64_t));
-    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_words, s->h_stage + o_words, nw * sizeof(uint64_t),
-                                 cudaMemcpyHostToDevice, q));
-    if (n_inputs)
-        SVT_CUDA_TRY(cudaMemcpyAsync(s->d_inputs, s->h_stage + o_in, n_inputs * sizeof(uint32_t),
-                                     cudaMemcpyHostToDevice, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_in_off, in_off, (B + 1) * sizeof(int64_t),
-                                 cudaMemcpyHostToDevice, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_act_off, s->h_stage + o_actoff, (B + 1) * sizeof(int64_t),
-                                 cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaMemcpyAsync(s->d_stage, s->h_stage, o_meta, cudaMemcpyHostToDevice, q));
+    SVT_CUDA_TRY(cudaEventRecord(s->ev_stage, q));
+    s->stage_busy = true;
     SVT_CUDA_TRY(cudaMemsetAsync(s->d_bad, 0, sizeof(int32_t), q));
     st = svt_select_batched(s->d_words, static_universe, s->rows, s->d_inputs, s->d_in_off, batch,
                             s->d_active, s->d_act_off, s->n_active_d(), s->n_static_d(),
@@ -474,8 +557,7 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
     const char* split_env = getenv("SVT_SESSION_SPLIT");
     s->split = n_static > 0 && batch >= 2 && (split_env == nullptr || atoi(split_env) != 0);
     // batch 1: row-major gather + the certified rows kernel (SVT_SESSION_ROWS=0: off)
-    const char* rows_env = getenv("SVT_SESSION_ROWS");
-    s->rows_mode = batch == 1 && (rows_env == nullptr || atoi(rows_env) != 0);
+    s->rows_mode = rows_mode;
     if (!st && s->split) st = prepare_split(s, h_static_words, n_static, q);
     if (!st && !s->rows_mode)
         st = svt_plan_layout(s->split ? s->n_dyn_d() : s->n_active_d(), s->d_act_off, batch,
@@ -485,16 +567,18 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
                                     s->split ? s->d_dyn_ids : s->d_active, s->group_begin_d(),
                                     s->d_group_req, batch, s->max_groups, s->d_sub, s->d_bad, q);
     if (st) return st;
+    if (rows_mode) {
+        // the plan size is known: gather its rows now (stream-ordered after
+        // the select, before every later step); nothing left for a finish
+        st = rows_gather(s, q);
+        if (st) s->batch = 0;
+        return st;
+    }
     // (into pinned memory: the read-back stays asynchronous)
     int64_t* meta = reinterpret_cast<int64_t*>(s->h_stage + o_meta);
     s->meta_off = o_meta;
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta, s->n_active_d(), B * sizeof(int64_t),
-                                 cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta + B, s->n_static_d(), B * sizeof(int64_t),
-                                 cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta + 2 * B, s->n_dynamic_d(), B * sizeof(int64_t),
-                                 cudaMemcpyDeviceToHost, q));
-    SVT_CUDA_TRY(cudaMemcpyAsync(meta + 3 * B, s->first_bad_d(), B * sizeof(int64_t),
+    // n_active | n_static | n_dynamic | first_bad: contiguous at stride cap_batch
+    SVT_CUDA_TRY(cudaMemcpyAsync(meta, s->d_meta, 4 * s->meta_stride * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, q));
     s->prep_ids = h_input_ids;
     s->prep_offs = h_input_offsets;
@@ -506,16 +590,15 @@ svt_status prepare_enqueue(svt_session* s, const uint64_t* h_static_words, size_
 // counts, the reference's error order, and the batch-1 row gather
 svt_status prepare_finish(svt_session* s) {
     const size_t B = static_cast<size_t>(s->batch);
-    cudaStream_t q = s->stream;
-    svt_status st = SVT_OK;
     const int64_t* meta = reinterpret_cast<const int64_t*>(s->h_stage + s->meta_off);
     const uint32_t* h_input_ids = s->prep_ids;
     const int64_t* h_input_offsets = s->prep_offs;
+    const size_t ms = s->meta_stride;
     s->n_active.assign(meta, meta + B);
-    s->n_static.assign(meta + B, meta + 2 * B);
-    s->n_dynamic.assign(meta + 2 * B, meta + 3 * B);
+    s->n_static.assign(meta + ms, meta + ms + B);
+    s->n_dynamic.assign(meta + 2 * ms, meta + 2 * ms + B);
     for (size_t b = 0; b < B; ++b) {
-        const int64_t bad = meta[3 * B + b];
+        const int64_t bad = meta[3 * ms + b];
         if (bad >= 0) {
             const uint32_t id = h_input_ids[h_input_offsets[b] + bad];
             set_error("input token id %u out of range for vocabulary of size %zu", id, s->rows);
@@ -526,31 +609,6 @@ svt_status prepare_finish(svt_session* s) {
             set_error("internal: plan capacity exceeded for request %zu", b);
             s->batch = 0;
             return SVT_ERR_RUNTIME;
-        }
-    }
-    if (s->rows_mode && s->n_active[0] > 0) {
-        // the plan size is known now: gather its rows row-major (stream-
-        // ordered before every later step), workspace zeroed once
-        const size_t n = static_cast<size_t>(s->n_active[0]);
-        const size_t bytes = n * s->dim * svt_dtype_size(s->dt) + 16;
-        st = grow(&s->d_rows, &s->cap_rows, bytes);
-        const size_t wsb = svt_greedy_rows_workspace_bytes(n);
-        if (!st && (wsb > s->cap_rows_ws || !s->d_rows_ws)) {
-            if (s->d_rows_ws) cudaFree(s->d_rows_ws);
-            s->d_rows_ws = nullptr;
-            s->cap_rows_ws = 0;
-            st = grow(&s->d_rows_ws, &s->cap_rows_ws, wsb);
-            if (!st) {
-                const cudaError_t e = cudaMemset(s->d_rows_ws, 0, s->cap_rows_ws);
-                if (e != cudaSuccess) st = svt::cuda_status(e, "rows workspace memset");
-            }
-        }
-        if (!st)
-            st = svt_gather_rows(s->head, s->dt, s->rows, s->dim, s->d_active, n, s->d_rows,
-                                 s->d_bad, q);
-        if (st) {
-            s->batch = 0;
-            return st;
         }
     }
     return SVT_OK;
@@ -564,7 +622,7 @@ svt_status svt_session_prepare_host(svt_session* s, const uint64_t* h_static_wor
                                     const int64_t* h_input_offsets, int32_t batch) {
     bool done = false;
     if (svt_status st = prepare_enqueue(s, h_static_words, static_universe, h_input_ids,
-                                        h_input_offsets, batch, &done))
+                                        h_input_offsets, batch, &done, s ? s->stream : nullptr))
         return st;
     if (done) return SVT_OK;
     SVT_CUDA_TRY(cudaStreamSynchronize(s->stream));
@@ -584,10 +642,11 @@ svt_status svt_session_prepare_host_many(svt_session* const* sessions, int32_t n
     std::vector<char> pending(static_cast<size_t>(n_sessions), 0);
     svt_status first = SVT_OK;
     for (int32_t i = 0; i < n_sessions; ++i) {
+        svt_session* si = sessions[i];
         bool done = false;
-        const svt_status st = prepare_enqueue(sessions[i], h_static_words, static_universe,
+        const svt_status st = prepare_enqueue(si, h_static_words, static_universe,
                                               h_input_ids[i], h_input_offsets[i], batches[i],
-                                              &done);
+                                              &done, si ? si->stream : nullptr);
         if (st) {
             first = st;
             break;
@@ -851,6 +910,7 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
     SVT_CUDA_TRY(cudaMemcpyAsync(h_out_ids, s0->d_multi_ids, total * sizeof(uint32_t),
                                  cudaMemcpyDeviceToHost, q));
     SVT_CUDA_TRY(cudaStreamSynchronize(q));
+    for (int32_t i = 0; i < n_sessions; ++i) sessions[i]->stage_busy = false;
     return SVT_OK;
 }
 

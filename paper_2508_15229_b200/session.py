@@ -70,7 +70,8 @@ class Session:
 
 def prepare_many(sessions, static_words: np.ndarray, V: int, prompts, offsets):
     """svt_session_prepare_host_many: prepare every session (session i over
-    prompts[i] / offsets[i]) with one synchronisation per stream."""
+    prompts[i] / offsets[i]); batch-1 sessions do not synchronise (their
+    plan counts are computed on the host)."""
     w = np.ascontiguousarray(static_words, np.uint64)
     ps = [np.ascontiguousarray(p, np.uint32) for p in prompts]
     os_ = [np.ascontiguousarray(o, np.int64) for o in offsets]

@@ -910,6 +910,13 @@ def test_session_prepare_many(th):
             session.prepare_many(sess, words, V, prompts, offs)
             ids = session.decode_host(sess, np.ascontiguousarray(hid, np.float32), steps)
             assert np.array_equal(ids, want), rnd
+            # batch-1 plans: counts computed on the host, ids by the select
+            for j in range(R):
+                op = orc.select(prompts[j], words, V, V)
+                n_act, n_st, n_dyn, pids, _ = sess[j].plans()
+                assert (int(n_act[0]), int(n_st[0]), int(n_dyn[0])) == (
+                    len(op.active_ids), op.n_static, op.n_dynamic), (rnd, j)
+                assert np.array_equal(pids, op.active_ids), (rnd, j)
         bad = [p.copy() for p in prompts]
         bad[2][7] = V + 3
         with pytest.raises(th.IntegrityError, match=f"input token id {V + 3} out of range"):
