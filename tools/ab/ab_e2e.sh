@@ -1,3 +1,5 @@
+# A/B of the cfg1 e2e line: lib_ab/libsvt_old.so vs lib_ab/libsvt_new.so (two
+# builds made here from two source trees; not tracked) swapped into lib/ on the box
 L=paper_2508_15229_b200/lib
 for i in 1 2; do
  for v in old new; do
