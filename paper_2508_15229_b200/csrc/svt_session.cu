@@ -43,10 +43,6 @@ struct svt_session {
     int64_t* d_act_off = nullptr;
     size_t meta_stride = 0;  // cap_batch at the prepare (D2H of the four count arrays)
     cudaEvent_t ev_stage = nullptr;  // after the prepare's H2D out of h_stage
-    // svt_session_decode_host: the hidden states' H2D in chunks on a copy
-    // stream, each step waiting only for its own chunk
-    cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_chunk[8] = {};
     bool stage_busy = false;         // that H2D may still be pending (no sync since)
     std::vector<uint64_t> seen;      // prepare scratch: prompt-id bitmap (kept all-zero)
     std::vector<uint32_t> host_ids;  // ... and the ids it set
@@ -149,9 +145,6 @@ void free_all(svt_session* s) {
     for (void* p : host)
         if (p) cudaFreeHost(p);
     if (s->ev_stage) cudaEventDestroy(s->ev_stage);
-    for (cudaEvent_t e : s->ev_chunk)
-        if (e) cudaEventDestroy(e);
-    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
 }
 
 bool is_pinned(const void* p) {
@@ -901,28 +894,9 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
     if (!st) st = grow(&s0->d_multi_ids, &s0->cap_multi_ids, total);
     if (st) return st;
     cudaStream_t q = s0->stream;
-    // the hidden states go up in (at most 8) chunks of steps on a copy
-    // stream: the first steps start after the first chunk, and the copies
-    // overlap the row gathers queued by the prepare
-    if (!s0->copy_stream)
-        SVT_CUDA_TRY(cudaStreamCreateWithFlags(&s0->copy_stream, cudaStreamNonBlocking));
-    constexpr int32_t kMaxChunks = 8;
-    const int32_t nch = steps < kMaxChunks ? steps : kMaxChunks;
-    for (int32_t c = 0; c < nch; ++c) {
-        if (!s0->ev_chunk[c])
-            SVT_CUDA_TRY(cudaEventCreateWithFlags(&s0->ev_chunk[c], cudaEventDisableTiming));
-        const size_t t0 = static_cast<size_t>(steps) * c / nch;
-        const size_t t1 = static_cast<size_t>(steps) * (c + 1) / nch;
-        SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi + t0 * rows * dim, h_hidden + t0 * rows * dim,
-                                     (t1 - t0) * rows * dim * sizeof(float),
-                                     cudaMemcpyHostToDevice, s0->copy_stream));
-        SVT_CUDA_TRY(cudaEventRecord(s0->ev_chunk[c], s0->copy_stream));
-    }
-    int32_t next_chunk = 0;
+    SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi, h_hidden, total * dim * sizeof(float),
+                                 cudaMemcpyHostToDevice, q));
     for (int32_t t = 0; t < steps; ++t) {
-        if (next_chunk < nch && static_cast<size_t>(t) ==
-                                    static_cast<size_t>(steps) * next_chunk / nch)
-            SVT_CUDA_TRY(cudaStreamWaitEvent(q, s0->ev_chunk[next_chunk++], 0));
         size_t off = static_cast<size_t>(t) * rows;
         for (int32_t i = 0; i < n_sessions; ++i) {
             svt_session* si = sessions[i];
