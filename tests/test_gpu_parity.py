@@ -1215,3 +1215,53 @@ def test_decode_steps_across_reselect(th, fused):
         tb.run_select()
         if not fused:
             tb.gather(head)
+
+
+@pytest.mark.gpu
+def test_session_batch1_host_counts_edge_cases(th):
+    """Batch-1 prepares compute the plan counts and the out-of-range check on
+    the host (no read-back): empty prompt, a prompt inside T, duplicates,
+    ids 0 and V-1, an empty static set, and bad ids at the first and last
+    position (the reference's first offending id in input order); every
+    plan, count and decoded id equals the oracle, and a failed prepare
+    leaves the session usable for the next one."""
+    from paper_2508_15229_b200 import session
+
+    V, d = 5000, 256
+    rng = np.random.default_rng(0xC0DE)
+    head = th.HeadMatrix.random(V, d, 0x77, storage=th.SVT_F32)
+    W = head.to_host()
+    t_ids = rng.choice(V, 300, replace=False)
+    words = words_from_ids(t_ids, V)
+    empty = words_from_ids(np.array([], np.int64), V)
+    cases = [
+        ("empty prompt", words, np.array([], np.uint32)),
+        ("inside T", words, t_ids[:40].astype(np.uint32)),
+        ("duplicates", words, np.array([7, 7, 9, 7, 9, 11, 11], np.uint32)),
+        ("ends", words, np.array([0, V - 1, 0, V - 1], np.uint32)),
+        ("no static", empty, rng.integers(0, V, 64).astype(np.uint32)),
+        ("random", words, rng.integers(0, V, 500).astype(np.uint32)),
+    ]
+    with session.Session(head, max_batch=1) as s:
+        for name, w, p in cases:
+            s.prepare(w, V, p, np.array([0, len(p)], np.int64))
+            op = orc.select(p, w, V, V)
+            n_act, n_st, n_dyn, pids, _ = s.plans()
+            assert (int(n_act[0]), int(n_st[0]), int(n_dyn[0])) == (
+                len(op.active_ids), op.n_static, op.n_dynamic), name
+            assert np.array_equal(pids, op.active_ids), name
+            if len(op.active_ids):
+                h = rng.uniform(-1, 1, (1, d)).astype(np.float32)
+                got = s.greedy(h)
+                want, _ = orc.greedy_step(W[op.active_ids], h[0], op.active_ids)
+                assert int(got[0]) == want, name
+        for bad_pos in (0, 5):
+            p = rng.integers(0, V, 6).astype(np.uint32)
+            p[bad_pos] = V + bad_pos
+            p[5] = V + 100 if bad_pos == 0 else p[5]
+            with pytest.raises(th.IntegrityError, match=f"input token id {V + bad_pos} out of range"):
+                s.prepare(words, V, p, np.array([0, len(p)], np.int64))
+        p = rng.integers(0, V, 30).astype(np.uint32)
+        s.prepare(words, V, p, np.array([0, len(p)], np.int64))
+        op = orc.select(p, words, V, V)
+        assert np.array_equal(s.plans()[3], op.active_ids)
