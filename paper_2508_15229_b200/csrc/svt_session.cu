@@ -43,6 +43,21 @@ struct svt_session {
     int64_t* d_act_off = nullptr;
     size_t meta_stride = 0;  // cap_batch at the prepare (D2H of the four count arrays)
     cudaEvent_t ev_stage = nullptr;  // after the prepare's H2D out of h_stage
+    // svt_session_decode_host: the hidden states' H2D in chunks on a copy
+    // stream, each step waiting only for its own chunk
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_chunk[8] = {};
+    cudaEvent_t ev_copy_fork = nullptr;
+    // ... and, for batched sessions with pinned host buffers, the whole call
+    // (uploads, every step, read-back) as one CUDA graph, kept while the
+    // sessions' layouts are unchanged (dh_key); the host pointers of its
+    // memcpy nodes are patched per call
+    std::vector<int64_t> dh_key;
+    cudaGraph_t dh_graph = nullptr;  // (alive: its node handles patch dh_exec)
+    cudaGraphExec_t dh_exec = nullptr;
+    std::vector<cudaGraphNode_t> dh_h2d;
+    std::vector<size_t> dh_h2d_off, dh_h2d_bytes;
+    cudaGraphNode_t dh_d2h = nullptr;
     bool stage_busy = false;         // that H2D may still be pending (no sync since)
     std::vector<uint64_t> seen;      // prepare scratch: prompt-id bitmap (kept all-zero)
     std::vector<uint32_t> host_ids;  // ... and the ids it set
@@ -145,6 +160,12 @@ void free_all(svt_session* s) {
     for (void* p : host)
         if (p) cudaFreeHost(p);
     if (s->ev_stage) cudaEventDestroy(s->ev_stage);
+    for (cudaEvent_t e : s->ev_chunk)
+        if (e) cudaEventDestroy(e);
+    if (s->ev_copy_fork) cudaEventDestroy(s->ev_copy_fork);
+    if (s->dh_exec) cudaGraphExecDestroy(s->dh_exec);
+    if (s->dh_graph) cudaGraphDestroy(s->dh_graph);
+    if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
 }
 
 bool is_pinned(const void* p) {
@@ -894,21 +915,157 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
     if (!st) st = grow(&s0->d_multi_ids, &s0->cap_multi_ids, total);
     if (st) return st;
     cudaStream_t q = s0->stream;
-    SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi, h_hidden, total * dim * sizeof(float),
-                                 cudaMemcpyHostToDevice, q));
-    for (int32_t t = 0; t < steps; ++t) {
-        size_t off = static_cast<size_t>(t) * rows;
-        for (int32_t i = 0; i < n_sessions; ++i) {
-            svt_session* si = sessions[i];
-            if (si->batch == 0) continue;
-            st = session_greedy_device(si, s0->d_multi + off * dim, dim, s0->d_multi_ids + off,
-                                       nullptr, SVT_ROWS_HIDDEN_STABLE);
-            if (st) return st;
-            off += static_cast<size_t>(si->batch);
+    // batched sessions: the hidden states go up in (at most 8) chunks of
+    // steps on a copy stream, each step waiting for its own chunk, so the
+    // upload (14.7 MB at cfg2) overlaps the decode. Batch-1 sessions take one
+    // upload: their steps are chained by programmatic launches, which a
+    // chunk's event wait would break (measured 20 us slower per cfg1 step).
+    bool any_rows = false;
+    for (int32_t i = 0; i < n_sessions; ++i) any_rows = any_rows || sessions[i]->rows_mode;
+    if (!s0->copy_stream)
+        SVT_CUDA_TRY(cudaStreamCreateWithFlags(&s0->copy_stream, cudaStreamNonBlocking));
+    if (!s0->ev_copy_fork)
+        SVT_CUDA_TRY(cudaEventCreateWithFlags(&s0->ev_copy_fork, cudaEventDisableTiming));
+    constexpr int32_t kMaxChunks = 8;
+    const int32_t nch = any_rows ? 0 : (steps < kMaxChunks ? steps : kMaxChunks);
+    for (int32_t c = 0; c < nch; ++c)
+        if (!s0->ev_chunk[c])
+            SVT_CUDA_TRY(cudaEventCreateWithFlags(&s0->ev_chunk[c], cudaEventDisableTiming));
+    auto enqueue = [&]() -> svt_status {
+        if (any_rows)
+            SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi, h_hidden, total * dim * sizeof(float),
+                                         cudaMemcpyHostToDevice, q));
+        if (nch) {
+            SVT_CUDA_TRY(cudaEventRecord(s0->ev_copy_fork, q));
+            SVT_CUDA_TRY(cudaStreamWaitEvent(s0->copy_stream, s0->ev_copy_fork, 0));
         }
+        for (int32_t c = 0; c < nch; ++c) {
+            const size_t t0 = static_cast<size_t>(steps) * c / nch;
+            const size_t t1 = static_cast<size_t>(steps) * (c + 1) / nch;
+            SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi + t0 * rows * dim,
+                                         h_hidden + t0 * rows * dim,
+                                         (t1 - t0) * rows * dim * sizeof(float),
+                                         cudaMemcpyHostToDevice, s0->copy_stream));
+            SVT_CUDA_TRY(cudaEventRecord(s0->ev_chunk[c], s0->copy_stream));
+        }
+        int32_t next_chunk = 0;
+        for (int32_t t = 0; t < steps; ++t) {
+            if (next_chunk < nch && static_cast<size_t>(t) ==
+                                        static_cast<size_t>(steps) * next_chunk / nch)
+                SVT_CUDA_TRY(cudaStreamWaitEvent(q, s0->ev_chunk[next_chunk++], 0));
+            size_t off = static_cast<size_t>(t) * rows;
+            for (int32_t i = 0; i < n_sessions; ++i) {
+                svt_session* si = sessions[i];
+                if (si->batch == 0) continue;
+                if (svt_status e = session_greedy_device(si, s0->d_multi + off * dim, dim,
+                                                         s0->d_multi_ids + off, nullptr,
+                                                         SVT_ROWS_HIDDEN_STABLE))
+                    return e;
+                off += static_cast<size_t>(si->batch);
+            }
+        }
+        SVT_CUDA_TRY(cudaMemcpyAsync(h_out_ids, s0->d_multi_ids, total * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, q));
+        return SVT_OK;
+    };
+    const char* gv = getenv("SVT_DECODE_GRAPH");  // 0: always eager
+    const bool graph_ok = !any_rows && !(gv && atoi(gv) == 0) && pinned_cached(s0, h_hidden) &&
+                          pinned_cached(s0, h_out_ids);
+    if (graph_ok) {
+        // everything a captured kernel parameter depends on
+        std::vector<int64_t> key = {steps, static_cast<int64_t>(rows), static_cast<int64_t>(dim),
+                                    reinterpret_cast<int64_t>(s0->d_multi),
+                                    reinterpret_cast<int64_t>(s0->d_multi_ids), n_sessions};
+        for (int32_t i = 0; i < n_sessions; ++i) {
+            const svt_session* si = sessions[i];
+            const int64_t v[] = {reinterpret_cast<int64_t>(si), si->batch, si->max_groups,
+                                 si->split, si->n_st, si->st_groups, si->weights_stable,
+                                 static_cast<int64_t>(si->cap_batch),
+                                 reinterpret_cast<int64_t>(si->d_sub),
+                                 reinterpret_cast<int64_t>(si->d_group_req),
+                                 reinterpret_cast<int64_t>(si->d_active),
+                                 reinterpret_cast<int64_t>(si->d_ws),
+                                 reinterpret_cast<int64_t>(si->d_meta),
+                                 reinterpret_cast<int64_t>(si->d_st_sub),
+                                 reinterpret_cast<int64_t>(si->d_st_ids),
+                                 reinterpret_cast<int64_t>(si->d_dyn_ids),
+                                 reinterpret_cast<int64_t>(si->d_split_meta),
+                                 reinterpret_cast<int64_t>(si->d_split_ws)};
+            key.insert(key.end(), v, v + sizeof(v) / sizeof(v[0]));
+        }
+        if (!s0->dh_exec || key != s0->dh_key) {
+            if (s0->dh_exec) cudaGraphExecDestroy(s0->dh_exec);
+            if (s0->dh_graph) cudaGraphDestroy(s0->dh_graph);
+            s0->dh_exec = nullptr;
+            s0->dh_graph = nullptr;
+            s0->dh_h2d.clear();
+            s0->dh_h2d_off.clear();
+            s0->dh_h2d_bytes.clear();
+            s0->dh_d2h = nullptr;
+            SVT_CUDA_TRY(cudaStreamBeginCapture(q, cudaStreamCaptureModeThreadLocal));
+            const svt_status es = enqueue();
+            cudaGraph_t g = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(q, &g);
+            if (es != SVT_OK || ec != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                if (es) return es;
+                return svt::cuda_status(ec, "decode_host graph capture");
+            }
+            size_t n = 0;
+            cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
+            std::vector<cudaGraphNode_t> nodes(n);
+            if (e == cudaSuccess) e = cudaGraphGetNodes(g, nodes.data(), &n);
+            for (size_t k = 0; e == cudaSuccess && k < n; ++k) {
+                cudaGraphNodeType t;
+                e = cudaGraphNodeGetType(nodes[k], &t);
+                if (e != cudaSuccess || t != cudaGraphNodeTypeMemcpy) continue;
+                cudaMemcpy3DParms mp = {};
+                e = cudaGraphMemcpyNodeGetParams(nodes[k], &mp);
+                if (e != cudaSuccess) break;
+                if (mp.kind == cudaMemcpyDeviceToHost) {
+                    s0->dh_d2h = nodes[k];
+                } else {
+                    s0->dh_h2d.push_back(nodes[k]);
+                    s0->dh_h2d_off.push_back(static_cast<size_t>(
+                        static_cast<const char*>(mp.dstPtr.ptr) -
+                        reinterpret_cast<const char*>(s0->d_multi)));
+                    s0->dh_h2d_bytes.push_back(mp.extent.width);
+                }
+            }
+            if (e == cudaSuccess) e = cudaGraphInstantiate(&s0->dh_exec, g, 0);
+            s0->dh_graph = g;
+            if (e != cudaSuccess || !s0->dh_d2h || s0->dh_h2d.empty()) {
+                if (s0->dh_exec) cudaGraphExecDestroy(s0->dh_exec);
+                cudaGraphDestroy(g);
+                s0->dh_exec = nullptr;
+                s0->dh_graph = nullptr;
+                cudaGetLastError();
+                set_error("decode_host graph: %s", e != cudaSuccess ? cudaGetErrorString(e)
+                                                                    : "memcpy nodes not found");
+                return SVT_ERR_RUNTIME;
+            }
+            s0->dh_key = std::move(key);
+        } else {
+            // replays run the captured flags: the first step after a prepare
+            // is keyed as not weight-stable, later ones as stable
+            for (int32_t i = 0; i < n_sessions; ++i) sessions[i]->weights_stable = true;
+        }
+        for (size_t k = 0; k < s0->dh_h2d.size(); ++k) {
+            const size_t o = s0->dh_h2d_off[k];
+            SVT_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(
+                s0->dh_exec, s0->dh_h2d[k], reinterpret_cast<char*>(s0->d_multi) + o,
+                reinterpret_cast<const char*>(h_hidden) + o, s0->dh_h2d_bytes[k],
+                cudaMemcpyHostToDevice));
+        }
+        SVT_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(s0->dh_exec, s0->dh_d2h, h_out_ids,
+                                                        s0->d_multi_ids,
+                                                        total * sizeof(uint32_t),
+                                                        cudaMemcpyDeviceToHost));
+        SVT_CUDA_TRY(cudaGraphLaunch(s0->dh_exec, q));
+    } else {
+        if (svt_status e = enqueue()) return e;
     }
-    SVT_CUDA_TRY(cudaMemcpyAsync(h_out_ids, s0->d_multi_ids, total * sizeof(uint32_t),
-                                 cudaMemcpyDeviceToHost, q));
     SVT_CUDA_TRY(cudaStreamSynchronize(q));
     for (int32_t i = 0; i < n_sessions; ++i) sessions[i]->stage_busy = false;
     return SVT_OK;

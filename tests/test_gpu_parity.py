@@ -1265,3 +1265,53 @@ def test_session_batch1_host_counts_edge_cases(th):
         s.prepare(words, V, p, np.array([0, len(p)], np.int64))
         op = orc.select(p, words, V, V)
         assert np.array_equal(s.plans()[3], op.active_ids)
+
+
+def test_session_decode_host_graph_batched(th):
+    """svt_session_decode_host over a batched (split) session with pinned
+    host buffers runs as one cached CUDA graph: repeated calls with
+    re-prepares of the same shape and with DIFFERENT pinned hidden / output
+    buffers (the memcpy nodes are re-pointed), then a prepare with other
+    prompt lengths (a new layout: the graph is rebuilt), and a pageable
+    call in between (eager) all return the reference ids."""
+    from paper_2508_15229_b200 import session
+
+    V, d, B, steps = 20000, 256, 12, 5
+    rng = np.random.default_rng(0x6A)
+    head = th.HeadMatrix.random(V, d, 0x6A, storage=th.SVT_BF16)
+    W = head.to_host()
+    words = words_from_ids(rng.choice(V, 400, replace=False), V)
+
+    def prompts_of(lo, hi):
+        return [rng.integers(0, V, int(rng.integers(lo, hi))).astype(np.uint32) for _ in range(B)]
+
+    def want(prompts, hid):
+        plans = [orc.select(p, words, V, V).active_ids for p in prompts]
+        return np.array([[orc.greedy_step(W[plans[b]], hid[t, b], plans[b])[0] for b in range(B)]
+                         for t in range(steps)], np.uint32)
+
+    with session.Session(head, max_batch=B) as s:
+        prompts = prompts_of(20, 120)
+        flat = np.concatenate(prompts)
+        off = np.zeros(B + 1, np.int64)
+        off[1:] = np.cumsum([len(p) for p in prompts])
+        for rnd in range(4):
+            s.prepare(words, V, flat, off)
+            hid = bf16_np(rng.uniform(-1, 1, (steps, B, d)).astype(np.float32))
+            if rnd == 2:  # pageable: the eager path
+                got = session.decode_host([s], hid, steps)
+            else:
+                hp = torch.from_numpy(hid).pin_memory()
+                out = torch.empty((steps, B), dtype=torch.int32).pin_memory()
+                session.decode_host([s], hp, steps, out)
+                got = out.numpy().view(np.uint32)
+            assert np.array_equal(got, want(prompts, hid)), rnd
+        prompts = prompts_of(130, 200)  # other lengths: a new layout
+        flat = np.concatenate(prompts)
+        off[1:] = np.cumsum([len(p) for p in prompts])
+        s.prepare(words, V, flat, off)
+        hid = bf16_np(rng.uniform(-1, 1, (steps, B, d)).astype(np.float32))
+        hp = torch.from_numpy(hid).pin_memory()
+        out = torch.empty((steps, B), dtype=torch.int32).pin_memory()
+        session.decode_host([s], hp, steps, out)
+        assert np.array_equal(out.numpy().view(np.uint32), want(prompts, hid))
