@@ -52,7 +52,7 @@ struct svt_session {
     // (uploads, every step, read-back) as one CUDA graph, kept while the
     // sessions' layouts are unchanged (dh_key); the host pointers of its
     // memcpy nodes are patched per call
-    std::vector<int64_t> dh_key;
+    std::vector<int64_t> dh_key, dh_seen;  // cached layout / the last call's (eager)
     cudaGraph_t dh_graph = nullptr;  // (alive: its node handles patch dh_exec)
     cudaGraphExec_t dh_exec = nullptr;
     std::vector<cudaGraphNode_t> dh_h2d;
@@ -992,6 +992,16 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
                                  reinterpret_cast<int64_t>(si->d_split_meta),
                                  reinterpret_cast<int64_t>(si->d_split_ws)};
             key.insert(key.end(), v, v + sizeof(v) / sizeof(v[0]));
+        }
+        if ((!s0->dh_exec || key != s0->dh_key) && key != s0->dh_seen) {
+            // a layout seen for the first time runs eagerly: capturing pays
+            // off only when calls repeat a layout (then the next call builds
+            // the graph), and varying layouts never pay for captures
+            s0->dh_seen = std::move(key);
+            if (svt_status e = enqueue()) return e;
+            SVT_CUDA_TRY(cudaStreamSynchronize(q));
+            for (int32_t i = 0; i < n_sessions; ++i) sessions[i]->stage_busy = false;
+            return SVT_OK;
         }
         if (!s0->dh_exec || key != s0->dh_key) {
             if (s0->dh_exec) cudaGraphExecDestroy(s0->dh_exec);
