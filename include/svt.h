@@ -708,7 +708,11 @@ svt_stream svt_session_stream(svt_session* s);
  * session's greedy step in order), one D2H of the ids, one synchronisation.
  * h_hidden: [steps][sum of batches][dim] f32; h_out_ids: [steps][sum of
  * batches]. A batch-1 session runs the certified rows kernel (gathered once
- * per prepare); larger batches the split / interleaved decode. */
+ * per prepare); larger batches the split / interleaved decode. Without
+ * batch-1 sessions and with pinned host buffers the call runs as one CUDA
+ * graph (uploads in chunks on a copy stream, every step, the read-back),
+ * captured the second time a layout (buffers, batches, group capacities)
+ * is seen and replayed while it repeats; SVT_DECODE_GRAPH=0 keeps it eager. */
 svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessions,
                                    const float* h_hidden, int32_t steps, uint32_t* h_out_ids);
 
