@@ -928,13 +928,21 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
         SVT_CUDA_TRY(cudaEventCreateWithFlags(&s0->ev_copy_fork, cudaEventDisableTiming));
     constexpr int32_t kMaxChunks = 8;
     const int32_t nch = any_rows ? 0 : (steps < kMaxChunks ? steps : kMaxChunks);
-    for (int32_t c = 0; c < nch; ++c)
+    for (int32_t c = 0; c < (nch > 1 ? nch : 1); ++c)
         if (!s0->ev_chunk[c])
             SVT_CUDA_TRY(cudaEventCreateWithFlags(&s0->ev_chunk[c], cudaEventDisableTiming));
     auto enqueue = [&]() -> svt_status {
-        if (any_rows)
+        if (any_rows) {
+            // nothing queued on the sessions' stream touches the staging
+            // block (the previous call synchronised), so the upload goes on
+            // the copy stream at once and overlaps the tail of the prepares'
+            // selects and row gathers (batch-1 prepares do not synchronise);
+            // the first step waits for it (cfg1: 2.045 -> 2.030 ms per call)
             SVT_CUDA_TRY(cudaMemcpyAsync(s0->d_multi, h_hidden, total * dim * sizeof(float),
-                                         cudaMemcpyHostToDevice, q));
+                                         cudaMemcpyHostToDevice, s0->copy_stream));
+            SVT_CUDA_TRY(cudaEventRecord(s0->ev_chunk[0], s0->copy_stream));
+            SVT_CUDA_TRY(cudaStreamWaitEvent(q, s0->ev_chunk[0], 0));
+        }
         if (nch) {
             SVT_CUDA_TRY(cudaEventRecord(s0->ev_copy_fork, q));
             SVT_CUDA_TRY(cudaStreamWaitEvent(s0->copy_stream, s0->ev_copy_fork, 0));
