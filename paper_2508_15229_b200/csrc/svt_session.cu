@@ -942,6 +942,14 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
                                          cudaMemcpyHostToDevice, s0->copy_stream));
             SVT_CUDA_TRY(cudaEventRecord(s0->ev_chunk[0], s0->copy_stream));
             SVT_CUDA_TRY(cudaStreamWaitEvent(q, s0->ev_chunk[0], 0));
+            // that wait is a full dependency: the first step cannot start
+            // before every kernel queued ahead of it (the prepares' row
+            // gathers) has completed, and every later step follows a decode
+            // step, so no step's rows come from the kernel right before it;
+            // the first token after a prepare also runs the stable-hidden
+            // kernel (SVT_ROWS_WEIGHTS_STABLE)
+            for (int32_t i = 0; i < n_sessions; ++i)
+                if (sessions[i]->rows_mode) sessions[i]->weights_stable = true;
         }
         if (nch) {
             SVT_CUDA_TRY(cudaEventRecord(s0->ev_copy_fork, q));
