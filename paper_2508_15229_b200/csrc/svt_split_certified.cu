@@ -178,6 +178,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1) static_gemm_kernel(const Spli
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    // the first batch of the B operand's hidden-state loads goes out first
+    constexpr int kBatch = 8;
+    float4 x[kBatch][2];
+    auto load_b = [&](int i0) {
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const int i = i0 + threadIdx.x + j * kGemmThreads;
+            const int n = i % kSN, c = i / kSN;
+            const int b = blk * kSN + n;
+            if (i < kSN * (ks / 8) && b < p.B && !(p.dbg_mode & 8)) {
+                const float* h = p.hidden + static_cast<int64_t>(b) * p.ld + sl * ks + c * 8;
+                x[j][0] = __ldg(reinterpret_cast<const float4*>(h));
+                x[j][1] = __ldg(reinterpret_cast<const float4*>(h + 4));
+            } else {
+                x[j][0] = x[j][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    };
+    load_b(0);
     // A: chunk (row r = 32 g + l, piece c) of the slice -> swizzled position;
     // consecutive threads take consecutive lanes (coalesced 512 B)
     const int64_t groups = (p.n_static + 31) / 32;
@@ -200,23 +219,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) static_gemm_kernel(const Spli
     CERT_STAMP(2);
     // B: the block's hidden states split h = hi + lo + r (hi = bf16(h),
     // lo = bf16(h - hi), |r| <= 2^-16 |h|; bf16 x bf16 products are exact in
-    // f32); every load of a batch issued before any is used
-    constexpr int kBatch = 8;
+    // f32); every load of a batch issued before any is used (the first
+    // batch before the A copies, so its latency overlaps their issue)
     for (int i0 = 0; i0 < kSN * nc; i0 += kGemmThreads * kBatch) {
-        float4 x[kBatch][2];
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-            const int i = i0 + threadIdx.x + j * kGemmThreads;
-            const int n = i % kSN, c = i / kSN;
-            const int b = blk * kSN + n;
-            if (i < kSN * nc && b < p.B && !(p.dbg_mode & 8)) {
-                const float* h = p.hidden + static_cast<int64_t>(b) * p.ld + sl * ks + c * 8;
-                x[j][0] = __ldg(reinterpret_cast<const float4*>(h));
-                x[j][1] = __ldg(reinterpret_cast<const float4*>(h + 4));
-            } else {
-                x[j][0] = x[j][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
+        if (i0 > 0) load_b(i0);
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const int i = i0 + threadIdx.x + j * kGemmThreads;
