@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(256)
 certify_kernel(int P, int S, const RowMap map,
                const float* __restrict__ top_val, const uint32_t* __restrict__ top_row,
                const uint8_t* __restrict__ flags, int nsplit, const float* __restrict__ hnorm,
-               const unsigned int* __restrict__ wmax_bits, float c_rel,
+               const unsigned int* __restrict__ wmax_bits, float c_rel, float eta,
                uint32_t* __restrict__ out_ids, float* __restrict__ out_max,
                unsigned int* __restrict__ stats, int64_t* __restrict__ all_list,
                unsigned long long* __restrict__ all_keys, uint2* __restrict__ pairs,
@@ -727,7 +727,8 @@ certify_kernel(int P, int S, const RowMap map,
         float thr = FLT_MAX;
         bool all = false, flg = false;
         if (work) {
-            const float B = __fmul_ru(__fmul_ru(c_rel, hnorm[pos]), __uint_as_float(wmax_bits[s]));
+            const float B = __fadd_ru(
+                __fmul_ru(__fmul_ru(c_rel, hnorm[pos]), __uint_as_float(wmax_bits[s])), eta);
             float top = -FLT_MAX;
             for (int j = 0; j < nsplit; ++j) {
                 top = fmaxf(top, top_val[(pos * nsplit + j) * TOPK]);
@@ -1427,11 +1428,16 @@ svt_status prefill_score_impl(const void* d_hidden, const void* W, int64_t w_row
     if (side->join) SVT_CUDA_TRY(cudaStreamWaitEvent(st, side->join, 0));
     if (p.mode & 16) return SVT_OK;  // profiling: the GEMM alone, no certification
     const double c = (gamma_n(2.0 * dim) + gamma_n(dim)) * 1.001;
+    // absolute slack for underflow, which the relative terms do not cover:
+    // the reference's products and sums may be subnormal (gradual
+    // underflow, <= 2^-149 each) and the tensor core may flush subnormal
+    // products and partial sums (<= 2^-126 each): 2 d + 16 terms of 2^-126
+    const float eta = static_cast<float>((2.0 * dim + 16.0) * 1.1754943508222875e-38);
     const int64_t warps = (npos + 3) / 4;
     const int64_t blocks = (warps + 7) / 8;
     certify_kernel<<<static_cast<int>(blocks < sm_count() * 8 ? blocks : sm_count() * 8), 256, 0,
                      st>>>(positions, sequences, rmap, top_val, top_row,
-                           flags, ns, hnorm, wmax, static_cast<float>(c) * 1.0001f, d_out_ids,
+                           flags, ns, hnorm, wmax, static_cast<float>(c) * 1.0001f, eta, d_out_ids,
                            d_out_max, stats, all_list, all_keys, pairs, rec_list, pos_keys,
                            reinterpret_cast<int32_t*>(ws + L.meta));
     SVT_LAUNCH_CHECK("certify_kernel");

@@ -733,7 +733,11 @@ SplitCertParams make_params(const void* d_static_sub, const uint32_t* d_static_i
     const double c = (gamma_n(static_cast<double>(dim)) + gamma_n(8.0 * p.ks) +
                       gamma_n(static_cast<double>(p.ksplit) + 2.0) + 1.52587890625e-05) * 1.01;
     p.c_rel = static_cast<float>(c) * (1.0f + FLT_EPSILON);
-    p.eta = static_cast<float>((static_cast<double>(dim) * 4.0 + 64.0) * 1.40129846e-45 * 4.0);
+    // + underflow the relative terms do not cover: the tensor core may flush
+    // subnormal products and partial sums, and the slices' reductions
+    // (red.add.f32) flush subnormal operands and results (<= 2^-126 each)
+    p.eta = static_cast<float>((static_cast<double>(dim) * 4.0 + 64.0) * 1.40129846e-45 * 4.0 +
+                               (2.0 * dim + p.ksplit + 8.0) * 1.1754943508222875e-38);
     p.dbg_mode = getenv("SVT_CERT_SKIP") ? atoi(getenv("SVT_CERT_SKIP")) : 0;  // measurement
     return p;
 }
