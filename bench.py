@@ -937,10 +937,13 @@ def run_cfg1(args, torch, dist, world, rank):
         "clocks": clocks,
     }
     if rank == 0 and not args.no_e2e:
-        e2e_v, h2d, d2h, ok, sec = cfg1_e2e(jobs, max(4, args.steps // 2), 2, torch, th,
-                                            session_mod)
+        # host-clocked: the mean over 40+ steps (each ~2 ms) after 5 warm-up
+        # steps; with 10 steps one slow host iteration moved it by up to 10%
+        k_e2e = max(40, 2 * args.steps)
+        e2e_v, h2d, d2h, ok, sec = cfg1_e2e(jobs, k_e2e, 5, torch, th, session_mod)
         result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
                          "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
+                         "timed_steps": k_e2e, "warmup_steps": 5,
                          "api": "svt_session_prepare_host_many (R sessions) + "
                                 "svt_session_decode_host (host buffers)", "ids_match_device_path": ok,
                          "breakdown": getattr(cfg1_e2e, "breakdown", None)}
@@ -1088,9 +1091,10 @@ def run_cfg2(args, torch, dist, world, rank):
     }
     if rank == 0 and not args.no_e2e:
         # host timing: more steps and a warm-up step damp host-side noise
-        e2e_v, h2d, d2h, ok = e2e_session(job, max(4, args.steps // 2), 2, th, torch, session_mod)
+        k_e2e = max(40, 2 * args.steps)
+        e2e_v, h2d, d2h, ok = e2e_session(job, k_e2e, 5, th, torch, session_mod)
         result["e2e"] = {"value": e2e_v * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                         "d2h_bytes_per_step": d2h,
+                         "d2h_bytes_per_step": d2h, "timed_steps": k_e2e, "warmup_steps": 5,
                          "api": "svt_session_prepare_host + svt_session_decode_host (host "
                                 "buffers: the job's hidden states in, its ids out)",
                          "per_step_host_calls_tokens_per_s": getattr(e2e_session, "per_step", None),
