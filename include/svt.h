@@ -708,7 +708,11 @@ svt_stream svt_session_stream(svt_session* s);
  * session's greedy step in order), one D2H of the ids, one synchronisation.
  * h_hidden: [steps][sum of batches][dim] f32; h_out_ids: [steps][sum of
  * batches]. A batch-1 session runs the certified rows kernel (gathered once
- * per prepare); larger batches the split / interleaved decode. Without
+ * per prepare); larger batches the split / interleaved decode. With batch-1
+ * sessions the call is eager: the upload goes on an internal copy stream
+ * (it overlaps prepares still running on the sessions' stream) and the
+ * first step waits for it, so every step, the first after a prepare
+ * included, runs the resident-hidden kernel. Without
  * batch-1 sessions and with pinned host buffers the call runs as one CUDA
  * graph (uploads in chunks on a copy stream, every step, the read-back),
  * captured the second time a layout (buffers, batches, group capacities)
