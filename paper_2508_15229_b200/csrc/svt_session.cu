@@ -942,12 +942,12 @@ svt_status svt_session_decode_host(svt_session* const* sessions, int32_t n_sessi
                                          cudaMemcpyHostToDevice, s0->copy_stream));
             SVT_CUDA_TRY(cudaEventRecord(s0->ev_chunk[0], s0->copy_stream));
             SVT_CUDA_TRY(cudaStreamWaitEvent(q, s0->ev_chunk[0], 0));
-            // that wait is a full dependency: the first step cannot start
-            // before every kernel queued ahead of it (the prepares' row
-            // gathers) has completed, and every later step follows a decode
-            // step, so no step's rows come from the kernel right before it;
-            // the first token after a prepare also runs the stable-hidden
-            // kernel (SVT_ROWS_WEIGHTS_STABLE)
+            // the prepares' row gathers are plain launches that never
+            // trigger their dependents, so the first step starts only once
+            // they have completed (and after this event wait); every later
+            // step follows a decode step. No step's rows come from the
+            // kernel right before it: the first token after a prepare also
+            // runs the stable-hidden kernel (SVT_ROWS_WEIGHTS_STABLE)
             for (int32_t i = 0; i < n_sessions; ++i)
                 if (sessions[i]->rows_mode) sessions[i]->weights_stable = true;
         }
